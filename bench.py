@@ -1,0 +1,425 @@
+#!/usr/bin/env python
+"""HBP SpMV benchmark on B200 (BASELINE.json metric), one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2|cfg1|cfg4|H]
+    python bench.py --impl reference ...      # the reference CPU path (oracle port)
+
+A step is one y = A x (HBP block kernel + combine) over the configured
+matrix, inputs resident in HBM (`value`); `e2e` repeats it through the public
+API with x copied in from pinned host memory and y copied back every step.
+Timing: CUDA events on the launching stream, barrier + synchronize on both
+sides, max over ranks.  The matrix data (>= 1 GB) exceeds L2 (126 MB), so
+no L2 flush is needed between steps; x stays cache-resident by design.
+Multi-GPU (torchrun): each rank owns a row stripe of the global matrix (one
+full-size instance per rank, weak scaling); a single SpMV has no collective.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "HBP SpMV GFLOP/s and % HBM roofline at 1/2/4/8 B200; preprocess ms vs CPU"
+UNIT = "GFLOP/s"
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback (used only if MEASURED_PEAKS.json is absent)
+
+CONFIGS = {
+    # name: (description, generator kwargs, dtype, col_width (None = cols))
+    "cfg2": ("R-MAT scale 24 (16,777,216 rows), edge factor 16, Graph500 (0.57,0.19,0.19,0.05), "
+             "random vertex relabel, duplicates removed, fp32, C=cols R=512 W=32",
+             dict(kind="rmat", scale=24, edge_factor=16), "f32", None),
+    "cfg4": ("uniform 8,388,608^2, Poisson(16) per row, fp32, C=cols R=512 W=32",
+             dict(kind="uniform", rows=8388608, cols=8388608, mean=16.0), "f32", None),
+    "H": ("uniform 6,250,000^2, Poisson(16) per row (~100M nnz), fp32, C=cols R=512 W=32",
+          dict(kind="uniform", rows=6250000, cols=6250000, mean=16.0), "f32", None),
+    "cfg1": ("5-point Laplacian 1024x1024 grid, fp64, C=4096 R=512 W=32",
+             dict(kind="laplacian", n=1024), "f64", 4096),
+}
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [s.strip() for s in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ inputs
+def make_matrix_gpu(cfg_name: str, seed: int, device):
+    import torch
+    import bench_inputs as BI
+    desc, gen, dt, C = CONFIGS[cfg_name]
+    vdt = torch.float32 if dt == "f32" else torch.float64
+    if gen["kind"] == "rmat":
+        rows, cols, rp, col, val = BI.rmat_csr_torch(gen["scale"], gen["edge_factor"], seed,
+                                                     device, vdt)
+    elif gen["kind"] == "uniform":
+        rows, cols, rp, col, val = BI.uniform_csr_torch(gen["rows"], gen["cols"], gen["mean"],
+                                                        seed, device, vdt)
+    else:
+        rows, cols, rp, col, val = BI.laplacian_csr(gen["n"])
+        rp = torch.as_tensor(rp, device=device)
+        col = torch.as_tensor(col, device=device).to(torch.int32)
+        val = torch.as_tensor(val, device=device).to(vdt)
+    return desc, rows, cols, rp, col, val, (C or cols), vdt
+
+
+def make_matrix_cpu_sample(cfg_name: str, seed: int):
+    """A bounded sample of the same workload for the CPU reference path."""
+    import bench_inputs as BI
+    desc, gen, dt, C = CONFIGS[cfg_name]
+    if gen["kind"] == "rmat":
+        scale = int(os.environ.get("HBP_CPU_SCALE", "20"))
+        rows, cols, rp, col, val = BI.rmat_csr_numpy(scale, gen["edge_factor"], seed)
+        sample = f"R-MAT scale {scale} (same generator, edge factor, geometry C=cols)"
+    elif gen["kind"] == "uniform":
+        n = int(os.environ.get("HBP_CPU_ROWS", str(1 << 20)))
+        rng = np.random.default_rng(seed)
+        counts = rng.poisson(gen["mean"], n)
+        r = np.repeat(np.arange(n), counts)
+        c = rng.integers(0, n, r.size)
+        key = np.unique(r * n + c)
+        r, c = key // n, key % n
+        rp = np.concatenate(([0], np.cumsum(np.bincount(r, minlength=n)))).astype(np.int64)
+        rows = cols = n
+        col, val = c, rng.uniform(-1, 1, key.size)
+        sample = f"uniform {n}^2 Poisson({gen['mean']}) rows (same generator family, C=cols)"
+    else:
+        rows, cols, rp, col, val = BI.laplacian_csr(gen["n"])
+        sample = "full matrix"
+    if dt == "f32":
+        val = val.astype(np.float32).astype(np.float64)
+    return rows, cols, rp, col, val, (C or cols), sample
+
+
+# ------------------------------------------------------- CPU reference arm
+def cpu_reference(cfg_name: str, steps: int, warmup: int, seed: int = 0):
+    """The reference's CPU HBP path (oracle port of _kernels.py / engine.py:
+    fixed + ticket worker threads, dense partial zero-fill, combine) on a
+    bounded sample, all host threads.  Returns a dict."""
+    from oracle import oracle as O
+    rows, cols, rp, col, val, C, sample = make_matrix_cpu_sample(cfg_name, seed)
+    R, W = 512, 32
+    t0 = time.perf_counter()
+    grid = O.make_grid(rp, col, rows, cols, C, R, W)
+    t1 = time.perf_counter()
+    params = O.sample_hash_params(grid)
+    t2 = time.perf_counter()
+    perms, _ = O.hash_permutations(grid, params)
+    t3 = time.perf_counter()
+    h = O.build_hbp(rp, col, val, grid, perms)
+    t4 = time.perf_counter()
+    workers = os.cpu_count() or 1
+    plan = O.plan_execution(grid.block_nnz, 0.7, workers)
+    x = np.random.default_rng(0).uniform(-1.0, 1.0, cols)
+    for _ in range(max(1, warmup)):
+        part, _ = O.run_spmv(h, x, plan, workers)
+        O.combine(part, rows, h.ncb)
+    times = []
+    deadline = time.perf_counter() + 30.0
+    for i in range(max(1, steps)):
+        a = time.perf_counter()
+        part, _ = O.run_spmv(h, x, plan, workers)
+        O.combine(part, rows, h.ncb)
+        times.append(time.perf_counter() - a)
+        if time.perf_counter() > deadline and i >= 2:
+            break
+    t = statistics.median(times)
+    nnz = int(rp[-1])
+    return dict(value=2.0 * nnz / t / 1e9, unit=UNIT, cores=workers, kind="port",
+                sample=f"{sample}: {rows} rows, {nnz} nnz, median of {len(times)} SpMV+combine",
+                ms_per_step=t * 1e3, nnz=nnz, rows=rows,
+                preprocess_ms=dict(grid=(t1 - t0) * 1e3, sample=(t2 - t1) * 1e3,
+                                   hash=(t3 - t2) * 1e3, build=(t4 - t3) * 1e3,
+                                   total=(t4 - t0) * 1e3))
+
+
+# ------------------------------------------------------------------ GPU arm
+def _dist():
+    import torch
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws > 1:
+        import torch.distributed as dist
+        lr = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(lr)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
+        return dist, dist.get_rank(), ws, lr
+    torch.cuda.set_device(0)
+    return None, 0, 1, 0
+
+
+def run_gpu(args):
+    import torch
+    import paper_2504_08860_b200 as H
+    from paper_2504_08860_b200 import _lib
+
+    dist, rank, world, local = _dist()
+    dev = torch.device("cuda", local)
+    desc, rows, cols, rp, col, val, C, vdt = make_matrix_gpu(args.config, seed=rank, device=dev)
+    torch.cuda.synchronize()
+    nnz = int(rp[-1].item())
+    cfg = H.PartitionConfig(col_width=C, row_height=512, warp_size=32, fixed_fraction=0.7)
+
+    # ---- preprocessing (timed like cli.py:150-158, GPU stages)
+    csr = H.CsrMatrix(rows, cols, rp, col, val)
+    del col, val
+    pre = {}
+    for rep in range(2):  # first pass warms allocator / module load; report the second
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        grid = H.make_grid(csr, cfg)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        params = H.sample_hash_params(grid, cfg)
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        perms = H.hash_permutations(grid, params)
+        torch.cuda.synchronize()
+        t3 = time.perf_counter()
+        hbp = H.build_hbp(csr, grid, perms, with_add_sign=False, with_zero_row=False)
+        torch.cuda.synchronize()
+        t4 = time.perf_counter()
+        pre = dict(grid=(t1 - t0) * 1e3, sample=(t2 - t1) * 1e3, hash=(t3 - t2) * 1e3,
+                   build=(t4 - t3) * 1e3, total=(t4 - t0) * 1e3)
+        if rep == 0:
+            del hbp, perms, grid
+    op = H.SpmvOperator(hbp)
+    x_host = np.random.default_rng(0).uniform(-1.0, 1.0, cols)  # cli.py:170-171
+    x = torch.as_tensor(x_host, device=dev).to(vdt)
+    y = torch.empty(rows, dtype=vdt, device=dev)
+    stream = torch.cuda.current_stream()
+
+    for _ in range(args.warmup):
+        op(x, y)
+    torch.cuda.synchronize()
+
+    # ---- device-resident timed region
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(K)]
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for i in range(K):
+        ev[i][0].record(stream)
+        op(x, y)
+        ev[i][1].record(stream)
+    end.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    total_ms = start.elapsed_time(end)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    kernel_ms = statistics.mean(step_ms)
+
+    # ---- end to end through the public API with host buffers
+    xh = torch.as_tensor(x_host).to(vdt).pin_memory()
+    yh = torch.empty(rows, dtype=vdt).pin_memory()
+    xd = torch.empty_like(x)
+    for _ in range(max(1, args.warmup)):
+        xd.copy_(xh, non_blocking=True)
+        H.hbp_spmv(hbp, xd)
+        yh.copy_(op(xd, y), non_blocking=True)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(K):
+        xd.copy_(xh, non_blocking=True)
+        yd = H.hbp_spmv(hbp, xd)
+        yh.copy_(yd, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / K
+    esz = 4 if vdt == torch.float32 else 8
+
+    # ---- correctness check (not timed): componentwise vs cuSPARSE fp64
+    A = torch.sparse_csr_tensor(csr.row_ptr, csr.col_idx.to(torch.int64),
+                                csr.values.to(torch.float64), (rows, cols))
+    Aabs = torch.sparse_csr_tensor(csr.row_ptr, csr.col_idx.to(torch.int64),
+                                   csr.values.to(torch.float64).abs(), (rows, cols))
+    x64 = x.to(torch.float64)
+    yref = A @ x64
+    scale = Aabs @ x64.abs()
+    err = (op(x, y).to(torch.float64) - yref).abs()
+    live = scale > 0
+    check = float((err[live] / scale[live]).max().item()) if bool(live.any()) else 0.0
+    zero_ok = bool((err[~live] == 0).all().item())
+    del A, Aabs
+
+    # ---- aggregate over ranks (max time, sum of work)
+    per_step_ms = total_ms / K
+    vals = torch.tensor([per_step_ms, kernel_ms, e2e_ms, float(nnz)], dtype=torch.float64,
+                        device=dev)
+    if dist:
+        mx = vals.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = vals.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        per_step_ms, kernel_ms, e2e_ms = mx[0].item(), mx[1].item(), mx[2].item()
+        total_nnz = sm[3].item()
+    else:
+        total_nnz = float(nnz)
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return None
+
+    gflops = 2.0 * total_nnz / (per_step_ms * 1e-3) / 1e9
+    b_alg = nnz * (esz + 4) + cols * esz + rows * esz  # SURVEY.md §8(d), per rank
+    peak, peak_src = _peaks()
+    achieved = b_alg / (kernel_ms * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        with open(prof) as fh:
+            traffic = json.load(fh).get(args.config, {}).get("dram_bytes_per_launch")
+    out = {
+        "metric": METRIC, "value": round(gflops, 3), "unit": UNIT, "n_gpus": world,
+        "steps": K, "warmup": args.warmup, "ms_per_step": round(per_step_ms, 5),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32" if vdt == torch.float32 else "f64",
+        "data": "synthetic (generated on device, seed = rank)",
+        "config": {"workload": f"{args.config}: {desc}", "rows": rows, "cols": cols, "nnz": nnz,
+                   "nonzero_blocks": hbp.nzb, "col_width": C, "row_height": 512,
+                   "warp_size": 32, "fixed_fraction": 0.7, "workers": op.workers,
+                   "hash_params": [params.a, params.b, params.c, params.d],
+                   "parallelism": f"row stripes x{world} (weak)",
+                   "l2": "inputs larger than L2 (no flush); x reused from L2 by design"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "algorithmic_bytes": b_alg, "peak_source": peak_src,
+                     "kernel": "k_spmv (+ combine/zero launches in the step)"},
+        "e2e": {"value": round(2.0 * total_nnz / (e2e_ms * 1e-3) / 1e9, 3), "unit": UNIT,
+                "h2d_bytes_per_step": cols * esz, "d2h_bytes_per_step": rows * esz},
+        "gpu_launches": K * op.launches_per_call,
+        "clocks": clk,
+        "preprocess_ms": {k: round(v, 3) for k, v in pre.items()},
+        "check": {"max_componentwise_err_vs_cusparse_f64": check, "zero_rows_exact": zero_ok},
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        cb = cpu_reference(args.config, steps=5, warmup=1)
+        out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        out["cpu_baseline"]["preprocess_ms"] = {k: round(v, 1)
+                                                for k, v in cb["preprocess_ms"].items()}
+    if dist:
+        dist.destroy_process_group()
+    return out
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    cb = cpu_reference(args.config, steps=args.steps, warmup=args.warmup)
+    desc = CONFIGS[args.config][0]
+    return {
+        "impl": "reference", "metric": METRIC, "value": round(cb["value"], 4), "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(cb["ms_per_step"], 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (bounded CPU sample of the same workload)",
+        "config": {"workload": f"{args.config}: {desc}", "sample": cb["sample"],
+                   "parallelism": "host threads"},
+        "cpu_baseline": {"value": round(cb["value"], 4), "unit": UNIT, "cores": cb["cores"],
+                         "kind": cb["kind"], "sample": cb["sample"]},
+        "e2e": {"value": round(cb["value"], 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "preprocess_ms": {k: round(v, 1) for k, v in cb["preprocess_ms"].items()},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    out = run_reference(args) if args.impl == "reference" else run_gpu(args)
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,251 @@
+/*
+ * hbp.h -- C ABI of libhbp.so, the sm_100a (B200) implementation of the
+ * Hash-based Partition (HBP) SpMV hot path (arXiv 2504.08860).
+ *
+ * The reference package (`hbp_spmv`, /root/reference/pkg/src/hbp_spmv) binds
+ * its native code through numba-compiled kernels called from Python with
+ * caller-allocated, C-contiguous buffers and no error path inside kernels
+ * (SURVEY.md §8b).  This ABI keeps those conventions on the GPU:
+ *
+ *   - every entry point takes raw DEVICE pointers, 64-bit sizes and a
+ *     cudaStream_t (passed as `hbp_stream_t`, NULL = legacy default stream);
+ *   - nothing allocates: outputs and scratch are caller-provided; functions
+ *     that need CUB scratch take (temp, temp_bytes) and report the size when
+ *     called with temp == NULL (CUB convention);
+ *   - no global mutable state: the work ticket lives in caller memory, so
+ *     calls are re-entrant per stream;
+ *   - return value: HBP_OK, an HBP_E_* code, or a cudaError_t (< 1000).
+ *     hbp_status_string() maps it to the reference's error vocabulary.
+ *
+ * Each function cites the reference interface it replaces (file:line under
+ * /root/reference/pkg/src/hbp_spmv/).  Layout vocabulary:
+ *   - "block"   = one (br, bc) tile of row_height x col_width;
+ *   - "nzb"     = number of NONZERO blocks, listed bc-major (engine.py:86-93);
+ *   - "slot"    = one (block, local row) entry; compact slot arrays hold
+ *                 row_height entries per nonzero block (short last row block
+ *                 padded with zeros);
+ *   - "group"   = warp_size consecutive slots (hbp.py:17-19); compact group
+ *                 arrays hold gpb = row_height / warp_size groups per nonzero
+ *                 block (missing groups of a short block have size 0).
+ */
+#ifndef HBP_H
+#define HBP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void *hbp_stream_t; /* cudaStream_t */
+
+enum {
+    HBP_OK = 0,
+    HBP_E_ARG = 1001,         /* invalid argument ("config", "length", ...) */
+    HBP_E_PERM = 1002,        /* "permutation of block (br, bc) is not a bijection" */
+    HBP_E_DUP = 1003,         /* "duplicate (row, col) entries; canonicalize first" */
+    HBP_E_UNSUPPORTED = 1004, /* geometry outside what the kernels support */
+    HBP_E_FORMAT = 1005       /* structurally invalid HBP arrays */
+};
+
+enum { HBP_F32 = 0, HBP_F64 = 1 };
+
+const char *hbp_status_string(int status);
+int hbp_abi_version(void);
+
+/* Device facts for sizing persistent grids (replaces the worker-count
+ * argument of engine.py:96 / cli.py:59-60 with a device-derived default). */
+int hbp_device_sm_count(int *sms);
+int hbp_spmv_default_workers(int dtype, int64_t warp_size, int64_t *workers);
+
+/* ---------------------------------------------------------------- utils */
+/* CUB device-wide primitives used by the host pipeline (temp == NULL -> size). */
+int hbp_exclusive_sum_i64(const int64_t *in, int64_t *out, int64_t n, void *temp,
+                          size_t *temp_bytes, hbp_stream_t stream);
+int hbp_inclusive_sum_i64(const int64_t *in, int64_t *out, int64_t n, void *temp,
+                          size_t *temp_bytes, hbp_stream_t stream);
+/* Stable LSD radix sort of (u32 key, u32 value) pairs on bits [0, end_bit). */
+int hbp_sort_pairs_u32(const uint32_t *keys_in, uint32_t *keys_out, const uint32_t *vals_in,
+                       uint32_t *vals_out, int64_t n, int end_bit, void *temp,
+                       size_t *temp_bytes, hbp_stream_t stream);
+/* Stable LSD radix sort of (u64 key, u64 value) pairs on bits [0, end_bit). */
+int hbp_sort_pairs_u64(const uint64_t *keys_in, uint64_t *keys_out, const uint64_t *vals_in,
+                       uint64_t *vals_out, int64_t n, int end_bit, void *temp,
+                       size_t *temp_bytes, hbp_stream_t stream);
+
+/* ------------------------------------------------------- formats (COO/CSR) */
+/* formats.py:243-258 coo_to_csr, after the caller sorted keys = row*cols+col
+ * (stable, values carried by the original index `order`):
+ * gathers col/val, rejects duplicates (HBP_E_DUP) and builds row_ptr. */
+int hbp_coo_finish_csr(const uint64_t *sorted_keys, const uint64_t *order, const void *val_in,
+                       int64_t nnz, int64_t rows, int64_t cols, int dtype, int64_t *row_ptr,
+                       int32_t *col_idx, void *val_out, int32_t *dup_flag,
+                       hbp_stream_t stream);
+/* formats.py:87-97 TripletMatrix.canonicalized: given keys sorted stably,
+ * marks run heads (head[i] = 1 if key[i] != key[i-1]) ... */
+int hbp_coo_run_heads(const uint64_t *sorted_keys, int64_t n, int64_t *head,
+                      hbp_stream_t stream);
+/* ... and sums each duplicate run left to right in sorted order (np.add.reduceat). */
+int hbp_coo_reduce_runs(const uint64_t *sorted_keys, const uint64_t *order, const double *val_in,
+                        const int64_t *head_incl, int64_t n, int64_t cols, int64_t *row_out,
+                        int64_t *col_out, double *val_out, hbp_stream_t stream);
+
+/* ----------------------------------------------------- make_grid (compact) */
+/* partition.py:100-127 make_grid, without its dense rows x ncb arrays.
+ * A "run" is the maximal piece of one CSR row inside one column block. */
+int hbp_grid_count_runs(const int64_t *row_ptr, const int32_t *col_idx, int64_t rows,
+                        int64_t cols, int64_t col_width, int64_t *runs_per_row,
+                        hbp_stream_t stream);
+/* Writes every run (bc, row, csr start, count), row-major order, at
+ * run_offset[row] (exclusive prefix of runs_per_row). */
+int hbp_grid_emit_runs(const int64_t *row_ptr, const int32_t *col_idx, int64_t rows,
+                       int64_t cols, int64_t col_width, const int64_t *run_offset,
+                       int64_t nruns, uint32_t *run_bc, uint32_t *run_row, int64_t *run_start,
+                       int32_t *run_count, hbp_stream_t stream);
+/* After the runs are ordered bc-major (order = stable sort by bc, NULL when
+ * ncb == 1), flags the first run of every nonzero block. */
+int hbp_grid_block_heads(const uint32_t *sorted_bc, const uint32_t *order,
+                         const uint32_t *run_row, int64_t nruns, int64_t row_height,
+                         int64_t *head, hbp_stream_t stream);
+/* Scatters runs into the compact per-block slot arrays: blk_br/blk_bc
+ * (nonzero block directory, bc-major), len_local[blk*R + local_row] (the
+ * reference's BlockGrid.row_counts restricted to nonzero blocks) and
+ * start_local (BlockGrid.row_starts).  len_local must be zero-filled. */
+int hbp_grid_fill_slots(const uint32_t *sorted_bc, const uint32_t *order,
+                        const uint32_t *run_row, const int64_t *run_start,
+                        const int32_t *run_count, const int64_t *block_incl, int64_t nruns,
+                        int64_t row_height, int32_t *blk_br, int32_t *blk_bc,
+                        uint32_t *len_local, int64_t *start_local, hbp_stream_t stream);
+/* partition.py:118-124 block_nnz over nonzero blocks. */
+int hbp_block_nnz(const uint32_t *len_local, int64_t nzb, int64_t row_height, int64_t *block_nnz,
+                  hbp_stream_t stream);
+
+/* ------------------------------------------------------- hash reordering */
+/* reorder.py:80-85: row_counts[bc, row] at sampled flat indices
+ * (flat = bc*rows + row), by binary search in the CSR row. */
+int hbp_sample_counts(const int64_t *row_ptr, const int32_t *col_idx, int64_t rows,
+                      int64_t col_width, const int64_t *flat_idx, int64_t k, int32_t *counts,
+                      hbp_stream_t stream);
+/* reorder.py:174-184 hash_permutations -> _kernels.py:62-92
+ * hash_perm_kernel, for nonzero blocks: FCFS linear probing with an
+ * occupancy bitmap (first free slot at or after the preliminary slot,
+ * cyclic), bit-exact with the reference's literal probe loop.
+ * perm[blk*R + slot] = local row; *probes += reference OpCounter.probes. */
+int hbp_hash_perm(const uint32_t *len_local, const int32_t *blk_br, int64_t nzb, int64_t rows,
+                  int64_t row_height, int64_t a, int64_t b, int64_t c, int64_t d,
+                  int64_t bucket_max, uint32_t *perm, unsigned long long *probes,
+                  hbp_stream_t stream);
+/* The permutation every EMPTY block of height n gets (all counts zero):
+ * needed only to expand to the reference's dense output_hash. */
+int hbp_hash_perm_empty(int64_t n, int64_t a, int64_t b, int64_t c, int64_t d,
+                        int64_t bucket_max, uint32_t *perm, hbp_stream_t stream);
+/* reorder.py:187-219 sort_permutations (stable ascending nnz) for nonzero
+ * blocks, and reorder.py:222-225 identity_permutations. */
+int hbp_sort_perm(const uint32_t *len_local, const int32_t *blk_br, int64_t nzb, int64_t rows,
+                  int64_t row_height, uint32_t *perm, hbp_stream_t stream);
+/* Gathers nonzero blocks' slices of a dense [ncb*rows] permutation table and
+ * checks every block (empty ones too) is a bijection (hbp.py:179-181):
+ * *bad = smallest bc-major block index that is not, or -1. */
+int hbp_gather_dense_perm(const uint32_t *dense, int64_t rows, int64_t ncb, int64_t row_height,
+                          const int32_t *blk_br, const int32_t *blk_bc, int64_t nzb,
+                          uint32_t *perm, long long *bad, hbp_stream_t stream);
+/* (`bad` must hold LLONG_MAX on entry; it is atomically lowered.) */
+
+/* ------------------------------------------------------------- build_hbp */
+/* hbp.py:183-185,215: permuted slot lengths, zero_row (nullable) and per
+ * group nnz (group_nnz has nzb*gpb + 1 entries; the last is set to 0 so an
+ * exclusive sum yields group_start with the nnz sentinel).  Checks the
+ * compact permutation is a bijection: *bad = first bad nonzero block or -1. */
+int hbp_slot_lengths(const uint32_t *len_local, const uint32_t *perm, const int32_t *blk_br,
+                     int64_t nzb, int64_t rows, int64_t row_height, int64_t warp_size,
+                     uint32_t *slot_len, int32_t *zero_row, int64_t *group_nnz,
+                     long long *bad, hbp_stream_t stream);
+/* hbp.py:194-213: column-major-within-group emission of col/data and the
+ * add_sign stride chain (nullable), computed from slot lengths. */
+int hbp_emit(const uint32_t *slot_len, const uint32_t *perm, const int64_t *start_local,
+             const int64_t *group_start, const int32_t *blk_br, int64_t nzb, int64_t rows,
+             int64_t row_height, int64_t warp_size, const int32_t *col_idx, const void *values,
+             int dtype, uint32_t *col, void *data, int32_t *add_sign, hbp_stream_t stream);
+/* Per row block, the number of its nonzero blocks (rb_count zero-filled by
+ * the caller; its exclusive sum is rb_ptr, and a stable sort of the block
+ * indices by br lists each row block's blocks in ascending bc). */
+int hbp_row_block_counts(const int32_t *blk_br, int64_t nzb, int64_t *rb_count,
+                         hbp_stream_t stream);
+
+/* Dense (reference-layout) view of the slot and group arrays:
+ * zero_row[ncb*rows], output_hash[ncb*rows], group_start[ncb*gpc+1]
+ * (hbp.py:51-62 HbpMatrix fields).  empty_perm_full / empty_perm_last are
+ * hbp_hash_perm_empty() for heights R and the last block's height. */
+int hbp_expand_reference(const int32_t *blk_br, const int32_t *blk_bc, int64_t nzb, int64_t rows,
+                         int64_t cols, int64_t nnz, int64_t col_width, int64_t row_height,
+                         int64_t warp_size,
+                         const uint32_t *perm, const int32_t *zero_row_c,
+                         const int64_t *group_start_c, const uint32_t *empty_perm_full,
+                         const uint32_t *empty_perm_last, int32_t *zero_row, uint32_t *output_hash,
+                         int64_t *group_start, hbp_stream_t stream);
+
+/* hbp.py:241-315 hbp_to_triplets: follows every slot's add_sign chain over
+ * the reference-layout arrays; row_out[j] = row of element j, seen[j] =
+ * visit count (zero-filled by the caller), *err |= 1 (lane start outside its
+ * group), 2 (column outside its block), 4 (invalid stride), 8 (chain escapes
+ * its group). */
+int hbp_walk_chains(int64_t rows, int64_t cols, int64_t col_width, int64_t row_height,
+                    int64_t warp_size, const int32_t *zero_row, const uint32_t *output_hash,
+                    const int64_t *group_start, const uint32_t *col, const int32_t *add_sign,
+                    int64_t nnz, int64_t *row_out, int32_t *seen, int32_t *err,
+                    hbp_stream_t stream);
+
+/* ------------------------------------------------------------------ SpMV */
+typedef struct {
+    int64_t rows, cols, col_width, row_height, warp_size;
+    int64_t nrb, ncb, nzb, nnz;
+    int32_t dtype; /* HBP_F32 or HBP_F64 (element values, x and y) */
+    int32_t exact; /* 1: reference summation order, bitwise for f64 */
+    const int32_t *blk_br;       /* [nzb] */
+    const int32_t *blk_bc;       /* [nzb] */
+    const uint32_t *slot_len;    /* [nzb*R] permuted in-block row lengths */
+    const uint32_t *perm;        /* [nzb*R] output_hash (slot -> local row) */
+    const int64_t *group_start;  /* [nzb*gpb + 1] */
+    const uint32_t *col;         /* [nnz] global column */
+    const void *data;            /* [nnz] */
+    const int64_t *rb_ptr;       /* [nrb+1] combine lists, ascending bc */
+    const int32_t *rb_blk;       /* [nzb] */
+} hbp_format_t;
+
+typedef struct {
+    int64_t workers;     /* persistent warps (paper: one warp per worker) */
+    int64_t fixed_count; /* engine.py:107 int(f * nzb + 0.5) */
+    uint32_t *ticket;    /* device scratch, 1 word; reset by the call */
+    int32_t *log_worker; /* nullable ExecutionLog (engine.py:71-83) */
+    int8_t *log_kind;
+    int64_t *log_start_ns;
+    int64_t *log_end_ns;
+} hbp_schedule_t;
+
+/* engine.py:179-193 run_spmv -> _run_plan (engine.py:137-176) ->
+ * block_spmv (engine.py:123-134) -> _kernels.py:22-47 hbp_block_kernel.
+ * Fixed contiguous chunks per worker, then an atomic ticket.  Writes either
+ * the compact partial [nzb*R] (per block, indexed by ORIGINAL local row),
+ * or -- when y_direct != NULL and ncb == 1 -- y directly. */
+int hbp_spmv_blocks(const hbp_format_t *f, const hbp_schedule_t *sched, const void *x,
+                    double *partial, void *y_direct, hbp_stream_t stream);
+/* engine.py:196-201 combine over nonzero blocks only, ascending bc
+ * (bitwise equal to the dense combine); rows of row blocks with
+ * no nonzero block get +0.0. */
+int hbp_combine(const hbp_format_t *f, const double *partial, void *y, hbp_stream_t stream);
+/* Zero y for row blocks with no nonzero block (direct mode companion). */
+int hbp_zero_empty_rows(const hbp_format_t *f, void *y, hbp_stream_t stream);
+/* Dense PartialVector view (engine.py:59-68): partial_dense[bc*rows + row]. */
+int hbp_expand_partial(const hbp_format_t *f, const double *partial, double *partial_dense,
+                       hbp_stream_t stream);
+
+/* hbp.py:241-315 hbp_to_triplets: invert the layout (per element row, col,
+ * value) from slot lengths; integrity checks live in the host wrapper. */
+int hbp_to_triplets(const hbp_format_t *f, int64_t *row_out, int64_t *col_out, void *val_out,
+                    hbp_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HBP_H */

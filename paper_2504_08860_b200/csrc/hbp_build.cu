@@ -1,0 +1,810 @@
+// hbp_build.cu -- GPU preprocessing for the HBP format (sm_100a).
+//
+// Replaces the reference's CPU preprocessing:
+//   make_grid          partition.py:100-127   -> count/emit runs, block heads, fill slots
+//   sample_hash_params reorder.py:69-103       -> sampled counts (the (a, c) arithmetic
+//                                                 stays on the host, same numpy calls)
+//   hash_permutations  reorder.py:174-184 / _kernels.py:62-92 -> bitmap FCFS probing
+//   build_hbp          hbp.py:150-238          -> slot lengths, group sizes, emission
+// The reference's arrays are dense in rows x column-blocks; here every
+// per-slot array is compact over NONZERO blocks and
+// hbp_expand_reference() rebuilds the dense view for parity.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <climits>
+
+#include "hbp.h"
+#include "hbp_common.cuh"
+
+using namespace hbp;
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ int64_t rows_in_block(int64_t rows, int64_t R, int64_t br) {
+    int64_t n = rows - br * R;
+    return n < R ? n : R;
+}
+
+// ------------------------------------------------------------- make_grid
+// One warp per CSR row: a run head is the row's first element or an element
+// whose column block differs from its predecessor's (partition.py:109-112).
+__global__ void k_count_runs(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                             int64_t rows, int64_t C, int single_block,
+                             int64_t *__restrict__ out) {
+    int lane = threadIdx.x & 31;
+    int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = warp; r < rows; r += nwarps) {
+        int64_t lo = row_ptr[r], hi = row_ptr[r + 1];
+        if (single_block) {
+            if (lane == 0) out[r] = hi > lo ? 1 : 0;
+            continue;
+        }
+        int64_t cnt = 0;
+        for (int64_t b = lo; b < hi; b += 32) {
+            int64_t j = b + lane;
+            bool head = false;
+            if (j < hi) head = (j == lo) || (col[j] / C != col[j - 1] / C);
+            cnt += __popc(__ballot_sync(0xffffffffu, head));
+        }
+        if (lane == 0) out[r] = cnt;
+    }
+}
+
+__global__ void k_emit_runs(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                            int64_t rows, int64_t C, int single_block,
+                            const int64_t *__restrict__ run_offset, uint32_t *__restrict__ run_bc,
+                            uint32_t *__restrict__ run_row, int64_t *__restrict__ run_start) {
+    int lane = threadIdx.x & 31;
+    int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned lt = (1u << lane) - 1u;
+    for (int64_t r = warp; r < rows; r += nwarps) {
+        int64_t lo = row_ptr[r], hi = row_ptr[r + 1];
+        int64_t off = run_offset[r];
+        if (single_block) {
+            if (lane == 0 && hi > lo) {
+                run_bc[off] = 0;
+                run_row[off] = (uint32_t)r;
+                run_start[off] = lo;
+            }
+            continue;
+        }
+        for (int64_t b = lo; b < hi; b += 32) {
+            int64_t j = b + lane;
+            bool head = false;
+            int32_t bc = 0;
+            if (j < hi) {
+                bc = col[j] / C;
+                head = (j == lo) || (bc != col[j - 1] / C);
+            }
+            unsigned m = __ballot_sync(0xffffffffu, head);
+            if (head) {
+                int64_t i = off + __popc(m & lt);
+                run_bc[i] = (uint32_t)bc;
+                run_row[i] = (uint32_t)r;
+                run_start[i] = j;
+            }
+            off += __popc(m);
+        }
+    }
+}
+
+// count = next run start of the same row (or the row end) - this start
+__global__ void k_run_counts(const int64_t *__restrict__ row_ptr,
+                             const int64_t *__restrict__ run_offset,
+                             const uint32_t *__restrict__ run_row,
+                             const int64_t *__restrict__ run_start, int64_t nruns,
+                             int32_t *__restrict__ run_count) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nruns;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t r = run_row[i];
+        int64_t end = (i + 1 < run_offset[r + 1]) ? run_start[i + 1] : row_ptr[r + 1];
+        run_count[i] = (int32_t)(end - run_start[i]);
+    }
+}
+
+__global__ void k_block_heads(const uint32_t *__restrict__ sbc, const uint32_t *__restrict__ order,
+                              const uint32_t *__restrict__ run_row, int64_t nruns, int64_t R,
+                              int64_t *__restrict__ head) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nruns;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t h = 1;
+        if (i > 0) {
+            uint32_t ri = run_row[order ? order[i] : i];
+            uint32_t rp = run_row[order ? order[i - 1] : i - 1];
+            uint32_t bi = sbc ? sbc[i] : 0, bp = sbc ? sbc[i - 1] : 0;
+            h = (bi != bp) || (ri / R != rp / R);
+        }
+        head[i] = h;
+    }
+}
+
+__global__ void k_fill_slots(const uint32_t *__restrict__ sbc, const uint32_t *__restrict__ order,
+                             const uint32_t *__restrict__ run_row,
+                             const int64_t *__restrict__ run_start,
+                             const int32_t *__restrict__ run_count,
+                             const int64_t *__restrict__ block_incl, int64_t nruns, int64_t R,
+                             int32_t *__restrict__ blk_br, int32_t *__restrict__ blk_bc,
+                             uint32_t *__restrict__ len_local, int64_t *__restrict__ start_local) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nruns;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t src = order ? order[i] : (uint32_t)i;
+        uint32_t r = run_row[src];
+        int64_t blk = block_incl[i] - 1;
+        int64_t br = r / R;
+        if (i == 0 || block_incl[i - 1] != block_incl[i]) {
+            blk_br[blk] = (int32_t)br;
+            blk_bc[blk] = sbc ? (int32_t)sbc[i] : 0;
+        }
+        int64_t s = blk * R + (r - br * R);
+        len_local[s] = (uint32_t)run_count[src];
+        start_local[s] = run_start[src];
+    }
+}
+
+// warp per nonzero block
+__global__ void k_block_nnz(const uint32_t *__restrict__ len_local, int64_t nzb, int64_t R,
+                            int64_t *__restrict__ out) {
+    int lane = threadIdx.x & 31;
+    int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t b = warp; b < nzb; b += nwarps) {
+        unsigned long long s = 0;
+        for (int64_t i = lane; i < R; i += 32) s += len_local[b * R + i];
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) out[b] = (int64_t)s;
+    }
+}
+
+// --------------------------------------------------------- sampled counts
+// reorder.py:80-85 reads row_counts[flat] at numpy-drawn flat indices; the
+// count of row r inside column block bc is found by binary search.
+__device__ __forceinline__ int64_t lower_bound_col(const int32_t *col, int64_t lo, int64_t hi,
+                                                   int64_t v) {
+    while (lo < hi) {
+        int64_t m = (lo + hi) >> 1;
+        if ((int64_t)col[m] < v) lo = m + 1;
+        else hi = m;
+    }
+    return lo;
+}
+
+__global__ void k_sample_counts(const int64_t *__restrict__ row_ptr,
+                                const int32_t *__restrict__ col, int64_t rows, int64_t C,
+                                const int64_t *__restrict__ flat, int64_t k,
+                                int32_t *__restrict__ counts) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t f = flat[i];
+        int64_t bc = f / rows, r = f - bc * rows;
+        int64_t lo = row_ptr[r], hi = row_ptr[r + 1];
+        int64_t a = lower_bound_col(col, lo, hi, bc * C);
+        int64_t b = lower_bound_col(col, a, hi, (bc + 1) * C);
+        counts[i] = (int32_t)(b - a);
+    }
+}
+
+// ------------------------------------------------------------- hash perm
+// One thread per nonzero block; the block's occupancy bitmap lives in shared
+// memory, word w of thread t at [w * blockDim + t] (conflict-free).  Rows
+// claim slots in ascending local-row order; the claimed slot is the first
+// free one at or after the preliminary slot, cyclically -- the same slot the
+// reference's +1 probe loop reaches, and the probes
+// it counts are the cyclic distance (slot - preliminary) mod n.
+__device__ __forceinline__ int64_t prelim_slot(uint32_t len, int64_t r, int64_t n, int64_t a,
+                                               int64_t b, int64_t c, int64_t d, int64_t bmax) {
+    int64_t g = a >= 32 ? 0 : (int64_t)(len >> a);
+    if (g > bmax) g = bmax;
+    return (g * b + (r * c) % d) % n;
+}
+
+template <bool EMPTY>
+__global__ void k_hash_perm(const uint32_t *__restrict__ len_local,
+                            const int32_t *__restrict__ blk_br, int64_t nzb, int64_t rows,
+                            int64_t R, int64_t a, int64_t b, int64_t c, int64_t d, int64_t bmax,
+                            uint32_t *__restrict__ perm, unsigned long long *__restrict__ probes) {
+    extern __shared__ uint32_t bm[];
+    const int T = blockDim.x, t = threadIdx.x;
+    int64_t blk = (int64_t)blockIdx.x * T + t;
+    unsigned long long my_probes = 0;
+    if (blk < nzb) {
+        int64_t n = EMPTY ? rows : rows_in_block(rows, R, blk_br[blk]);
+        int nw = (int)((n + 31) >> 5);
+        for (int w = 0; w < nw; ++w) bm[w * T + t] = 0u;
+        if (n & 31) bm[(nw - 1) * T + t] = ~((1u << (n & 31)) - 1u);  // bits >= n: taken
+        const uint32_t *lens = len_local + blk * R;
+        uint32_t *out = perm + blk * R;
+        for (int64_t r = 0; r < n; ++r) {
+            uint32_t len = EMPTY ? 0u : lens[r];
+            int64_t pos = prelim_slot(len, r, n, a, b, c, d, bmax);
+            int w = (int)(pos >> 5);
+            uint32_t word = bm[w * T + t];
+            uint32_t fr = ~word & (0xffffffffu << (pos & 31));
+            while (!fr) {
+                w = (w + 1 == nw) ? 0 : w + 1;
+                word = bm[w * T + t];
+                fr = ~word;
+            }
+            int bit = __ffs(fr) - 1;
+            bm[w * T + t] = word | (1u << bit);
+            int64_t slot = (int64_t)w * 32 + bit;
+            out[slot] = (uint32_t)r;
+            my_probes += (unsigned long long)(slot >= pos ? slot - pos : slot + n - pos);
+        }
+        if (n < R)
+            for (int64_t s = n; s < R && !EMPTY; ++s) out[s] = 0u;
+    }
+    if (probes) {
+        for (int o = 16; o; o >>= 1) my_probes += __shfl_xor_sync(0xffffffffu, my_probes, o);
+        if ((t & 31) == 0 && my_probes) atomicAdd(probes, my_probes);
+    }
+}
+
+// reorder.py:160-171 sort_permutation: stable ascending nnz; warp per block,
+// rank(r) = #{r' : len[r'] < len[r]} + #{r' < r : len[r'] == len[r]}.
+__global__ void k_sort_perm(const uint32_t *__restrict__ len_local,
+                            const int32_t *__restrict__ blk_br, int64_t nzb, int64_t rows,
+                            int64_t R, uint32_t *__restrict__ perm) {
+    int lane = threadIdx.x & 31;
+    int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t blk = warp; blk < nzb; blk += nwarps) {
+        int64_t n = rows_in_block(rows, R, blk_br[blk]);
+        const uint32_t *lens = len_local + blk * R;
+        for (int64_t r = lane; r < n; r += 32) {
+            uint32_t lr = lens[r];
+            int64_t rank = 0;
+            for (int64_t o = 0; o < n; ++o) {
+                uint32_t lo = lens[o];
+                rank += (lo < lr) || (lo == lr && o < r);
+            }
+            perm[blk * R + rank] = (uint32_t)r;
+        }
+        for (int64_t s = n + lane; s < R; s += 32) perm[blk * R + s] = 0u;
+    }
+}
+
+// Bijection check, warp per block with a per-warp bitmap in shared memory.
+// dense == true: every (br, bc) block of a [ncb*rows] table (hbp.py:179-181);
+// otherwise the compact [nzb*R] table.  *bad = min offending block index.
+__global__ void k_check_perm(const uint32_t *__restrict__ tab, int64_t rows, int64_t R,
+                             int64_t nrb, int64_t nblocks, const int32_t *__restrict__ blk_br,
+                             int dense, long long *__restrict__ bad) {
+    extern __shared__ uint32_t bits[];
+    int lane = threadIdx.x & 31;
+    int wib = threadIdx.x >> 5;
+    int nw = (int)((R + 31) >> 5);
+    uint32_t *my = bits + wib * nw;
+    int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t blk = warp; blk < nblocks; blk += nwarps) {
+        int64_t br, base;
+        if (dense) {
+            int64_t bc = blk / nrb;
+            br = blk - bc * nrb;
+            base = bc * rows + br * R;
+        } else {
+            br = blk_br[blk];
+            base = blk * R;
+        }
+        int64_t n = rows_in_block(rows, R, br);
+        for (int w = lane; w < nw; w += 32) my[w] = 0u;
+        __syncwarp();
+        bool ok = true;
+        for (int64_t s = lane; s < n; s += 32) {
+            uint32_t v = tab[base + s];
+            if (v >= (uint64_t)n) {
+                ok = false;
+            } else {
+                uint32_t old = atomicOr(&my[v >> 5], 1u << (v & 31));
+                if (old & (1u << (v & 31))) ok = false;
+            }
+        }
+        if (!__all_sync(0xffffffffu, ok) && lane == 0) atomicMin(bad, (long long)blk);
+        __syncwarp();
+    }
+}
+
+__global__ void k_gather_perm(const uint32_t *__restrict__ dense, int64_t rows, int64_t R,
+                              const int32_t *__restrict__ blk_br,
+                              const int32_t *__restrict__ blk_bc, int64_t nzb,
+                              uint32_t *__restrict__ perm) {
+    int64_t total = nzb * R;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t blk = i / R, s = i - blk * R;
+        int64_t br = blk_br[blk];
+        int64_t n = rows_in_block(rows, R, br);
+        perm[i] = s < n ? dense[(int64_t)blk_bc[blk] * rows + br * R + s] : 0u;
+    }
+}
+
+// ----------------------------------------------------------- build_hbp
+// One lane-group (segment) per HBP warp group.
+__global__ void k_slot_lengths(const uint32_t *__restrict__ len_local,
+                               const uint32_t *__restrict__ perm,
+                               const int32_t *__restrict__ blk_br, int64_t nzb, int64_t rows,
+                               int64_t R, int W, uint32_t *__restrict__ slot_len,
+                               int32_t *__restrict__ zero_row, int64_t *__restrict__ group_nnz) {
+    Seg sg = make_seg(W);
+    if (sg.idle()) return;
+    const int64_t gpb = R / W;
+    const int64_t ngroups = nzb * gpb;
+    int64_t seg_id = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * sg.spw + sg.seg;
+    int64_t nseg = (((int64_t)gridDim.x * blockDim.x) >> 5) * sg.spw;
+    if (seg_id == 0 && sg.q == 0) group_nnz[ngroups] = 0;
+    for (int64_t gg = seg_id; gg < ngroups; gg += nseg) {
+        int64_t blk = gg / gpb, g = gg - blk * gpb;
+        int64_t n = rows_in_block(rows, R, blk_br[blk]);
+        int64_t slot = g * W + sg.q;
+        bool valid = slot < n;
+        uint32_t len = 0;
+        if (valid) {
+            uint32_t r = perm[blk * R + slot];
+            len = r < (uint32_t)n ? len_local[blk * R + r] : 0u;  // bad tables caught by k_check_perm
+        }
+        slot_len[blk * R + slot] = len;
+        unsigned empt = seg_ballot(sg, valid && len == 0);
+        if (zero_row) {
+            int32_t zr = (valid && len == 0) ? -1 : __popc(empt & ((1u << sg.q) - 1u));
+            zero_row[blk * R + slot] = valid ? zr : -1;
+        }
+        long long tot = seg_add_i64(sg, (long long)len);
+        if (sg.q == 0) group_nnz[gg] = tot;
+    }
+}
+
+// Column-major emission within a group (hbp.py:194-213).  Within a "phase"
+// (a maximal step range with a fixed live-lane set of size k) the element
+// of live lane `rank` at step t sits at base + (t - t0) * k + rank, so all
+// addresses come from the slot lengths.
+template <typename V>
+__global__ void k_emit(const uint32_t *__restrict__ slot_len, const uint32_t *__restrict__ perm,
+                       const int64_t *__restrict__ start_local,
+                       const int64_t *__restrict__ group_start,
+                       const int32_t *__restrict__ blk_br, int64_t nzb, int64_t rows, int64_t R,
+                       int W, const int32_t *__restrict__ col_idx, const V *__restrict__ vals,
+                       uint32_t *__restrict__ col_out, V *__restrict__ data_out,
+                       int32_t *__restrict__ add_out) {
+    __shared__ int64_t tab_src[kThreads / 32][32];
+    __shared__ int32_t tab_nx[kThreads / 32][32];  // rank in the next phase, or -1
+    Seg sg = make_seg(W);
+    if (sg.idle()) return;
+    const int wib = threadIdx.x >> 5;
+    const int64_t gpb = R / W;
+    const int64_t ngroups = nzb * gpb;
+    const unsigned lt = (1u << sg.q) - 1u;
+    int64_t seg_id = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * sg.spw + sg.seg;
+    int64_t nseg = (((int64_t)gridDim.x * blockDim.x) >> 5) * sg.spw;
+    for (int64_t gg = seg_id; gg < ngroups; gg += nseg) {
+        int64_t blk = gg / gpb, g = gg - blk * gpb;
+        int64_t slot = blk * R + g * W + sg.q;
+        uint32_t len = slot_len[slot];
+        int64_t src = len ? start_local[blk * R + perm[slot]] : 0;
+        int64_t base = group_start[gg];
+        uint32_t t0 = 0;
+        bool live = len > 0;
+        unsigned mask = seg_ballot(sg, live);
+        while (mask) {
+            const int k = __popc(mask);
+            const int rank = __popc(mask & lt);
+            const uint32_t t1 = seg_min_u32(sg, live ? len : 0xffffffffu);
+            const bool live_n = len > t1;
+            const unsigned mask_n = seg_ballot(sg, live_n);
+            const int rank_n = __popc(mask_n & lt);
+            const int64_t M = (int64_t)(t1 - t0);
+            if (2 * k >= W || M < 4) {
+                if (live) {
+                    int64_t p = base + rank;
+                    int64_t j = src + t0;
+                    for (int64_t t = 0; t < M; ++t, p += k, ++j) {
+                        col_out[p] = (uint32_t)col_idx[j];
+                        data_out[p] = vals[j];
+                        if (add_out)
+                            add_out[p] = (t + 1 < M) ? k : (live_n ? k + rank_n - rank : -1);
+                    }
+                }
+            } else {
+                // few live lanes over many steps: the segment writes the
+                // phase's positions cooperatively (coalesced)
+                if (live) {
+                    tab_src[wib][sg.shift + rank] = src + t0;
+                    tab_nx[wib][sg.shift + rank] = live_n ? (k + rank_n - rank) : -1;
+                }
+                __syncwarp(sg.mask);
+                const int64_t total = M * k;
+                for (int64_t off = sg.q; off < total; off += W) {
+                    int64_t t = off / k;
+                    int r = (int)(off - t * k);
+                    int64_t j = tab_src[wib][sg.shift + r] + t;
+                    int64_t p = base + off;
+                    col_out[p] = (uint32_t)col_idx[j];
+                    data_out[p] = vals[j];
+                    if (add_out) add_out[p] = (t + 1 < M) ? k : tab_nx[wib][sg.shift + r];
+                }
+                __syncwarp(sg.mask);
+            }
+            base += M * k;
+            t0 = t1;
+            live = live_n;
+            mask = mask_n;
+        }
+    }
+}
+
+__global__ void k_rb_counts(const int32_t *__restrict__ blk_br, int64_t nzb,
+                            int64_t *__restrict__ cnt) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nzb;
+         i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd((unsigned long long *)&cnt[blk_br[i]], 1ull);
+}
+
+// ------------------------------------------------------ dense expansion
+__global__ void k_expand_slots(int64_t rows, int64_t ncb, int64_t R,
+                               const uint32_t *__restrict__ ep_full,
+                               const uint32_t *__restrict__ ep_last,
+                               uint32_t *__restrict__ output_hash, int32_t *__restrict__ zero_row) {
+    int64_t total = ncb * rows;
+    int64_t nrb = (rows + R - 1) / R;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t r = i % rows;
+        int64_t br = r / R, s = r - br * R;
+        bool last_short = (br == nrb - 1) && (rows - br * R) < R;
+        output_hash[i] = last_short ? ep_last[s] : ep_full[s];
+        zero_row[i] = -1;
+    }
+}
+
+__global__ void k_scatter_slots(const int32_t *__restrict__ blk_br,
+                                const int32_t *__restrict__ blk_bc, int64_t nzb, int64_t rows,
+                                int64_t R, const uint32_t *__restrict__ perm,
+                                const int32_t *__restrict__ zr_c,
+                                uint32_t *__restrict__ output_hash, int32_t *__restrict__ zero_row) {
+    int64_t total = nzb * R;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t blk = i / R, s = i - blk * R;
+        int64_t br = blk_br[blk];
+        if (s >= rows_in_block(rows, R, br)) continue;
+        int64_t d = (int64_t)blk_bc[blk] * rows + br * R + s;
+        output_hash[d] = perm[i];
+        zero_row[d] = zr_c[i];
+    }
+}
+
+__global__ void k_expand_groups(const int32_t *__restrict__ blk_br,
+                                const int32_t *__restrict__ blk_bc, int64_t nzb, int64_t nrb,
+                                int64_t ncb, int64_t gpc, int64_t gpb, int64_t nnz,
+                                const int64_t *__restrict__ gs_c, int64_t *__restrict__ gs) {
+    int64_t total = ncb * gpc;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e <= total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        if (e == total) {
+            gs[e] = nnz;
+            continue;
+        }
+        int64_t bc = e / gpc, rem = e - bc * gpc;
+        int64_t br = rem / gpb, g = rem - br * gpb;
+        int64_t key = bc * nrb + br;
+        int64_t lo = 0, hi = nzb;
+        while (lo < hi) {
+            int64_t m = (lo + hi) >> 1;
+            int64_t km = (int64_t)blk_bc[m] * nrb + blk_br[m];
+            if (km < key) lo = m + 1;
+            else hi = m;
+        }
+        int64_t v;
+        if (lo < nzb && (int64_t)blk_bc[lo] * nrb + blk_br[lo] == key) v = gs_c[lo * gpb + g];
+        else v = lo < nzb ? gs_c[lo * gpb] : nnz;
+        gs[e] = v;
+    }
+}
+
+// hbp.py:241-315 hbp_to_triplets: walk every slot's add_sign chain over the
+// reference-layout arrays (dense zero_row / output_hash / group_start), one
+// thread per slot.  err bits: 1 lane start outside its group, 2 column
+// outside the block, 4 invalid stride, 8 chain escapes its group.
+__global__ void k_walk_chains(int64_t rows, int64_t cols, int64_t C, int64_t R, int64_t W,
+                              int64_t ncb, int64_t gpc, const int32_t *__restrict__ zero_row,
+                              const uint32_t *__restrict__ output_hash,
+                              const int64_t *__restrict__ group_start,
+                              const uint32_t *__restrict__ col, const int32_t *__restrict__ add,
+                              int64_t nnz, int64_t *__restrict__ row_out,
+                              int32_t *__restrict__ seen, int32_t *__restrict__ err) {
+    int64_t total = ncb * rows;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t zr = zero_row[i];
+        if (zr < 0) continue;
+        int64_t bc = i / rows, row = i - bc * rows;
+        int64_t br = row / R, s = row - br * R, g = s / W, q = s - g * W;
+        int64_t gb = bc * gpc + br * (R / W) + g;
+        int64_t gs = group_start[gb], ge = group_start[gb + 1];
+        int64_t j = gs + q - zr;
+        if (j < gs || j >= ge || j >= nnz || j < 0) {
+            atomicOr(err, 1);
+            continue;
+        }
+        int64_t out_row = br * R + (int64_t)output_hash[i];
+        int64_t lo = bc * C, hi = lo + C < cols ? lo + C : cols;
+        for (;;) {
+            int64_t c = col[j];
+            if (c < lo || c >= hi) {
+                atomicOr(err, 2);
+                break;
+            }
+            atomicAdd(&seen[j], 1);
+            row_out[j] = out_row;
+            int32_t step = add[j];
+            if (step == 0 || (step < 0 && step != -1)) {
+                atomicOr(err, 4);
+                break;
+            }
+            if (step < 0) break;
+            j += step;
+            if (j >= ge || j >= nnz) {
+                atomicOr(err, 8);
+                break;
+            }
+        }
+    }
+}
+
+}  // namespace
+
+// ====================================================================== ABI
+extern "C" {
+
+int hbp_grid_count_runs(const int64_t *row_ptr, const int32_t *col_idx, int64_t rows,
+                        int64_t cols, int64_t col_width, int64_t *runs_per_row,
+                        hbp_stream_t stream) {
+    if (rows < 1 || col_width < 1) return HBP_E_ARG;
+    k_count_runs<<<grid_for(rows * 32, kThreads), kThreads, 0, as_stream(stream)>>>(
+        row_ptr, col_idx, rows, col_width, col_width >= cols, runs_per_row);
+    HBP_LAUNCH_CHECK();
+    return HBP_OK;
+}
+
+int hbp_grid_emit_runs(const int64_t *row_ptr, const int32_t *col_idx, int64_t rows,
+                       int64_t cols, int64_t col_width, const int64_t *run_offset,
+                       int64_t nruns, uint32_t *run_bc, uint32_t *run_row, int64_t *run_start,
+                       int32_t *run_count, hbp_stream_t stream) {
+    if (rows < 1 || col_width < 1) return HBP_E_ARG;
+    cudaStream_t s = as_stream(stream);
+    k_emit_runs<<<grid_for(rows * 32, kThreads), kThreads, 0, s>>>(
+        row_ptr, col_idx, rows, col_width, col_width >= cols, run_offset, run_bc, run_row,
+        run_start);
+    HBP_LAUNCH_CHECK();
+    if (nruns > 0) {
+        k_run_counts<<<grid_for(nruns, kThreads), kThreads, 0, s>>>(row_ptr, run_offset, run_row,
+                                                                    run_start, nruns, run_count);
+        HBP_LAUNCH_CHECK();
+    }
+    return HBP_OK;
+}
+
+int hbp_grid_block_heads(const uint32_t *sorted_bc, const uint32_t *order,
+                         const uint32_t *run_row, int64_t nruns, int64_t row_height,
+                         int64_t *head, hbp_stream_t stream) {
+    if (nruns <= 0) return HBP_OK;
+    k_block_heads<<<grid_for(nruns, kThreads), kThreads, 0, as_stream(stream)>>>(
+        sorted_bc, order, run_row, nruns, row_height, head);
+    HBP_LAUNCH_CHECK();
+    return HBP_OK;
+}
+
+int hbp_grid_fill_slots(const uint32_t *sorted_bc, const uint32_t *order,
+                        const uint32_t *run_row, const int64_t *run_start,
+                        const int32_t *run_count, const int64_t *block_incl, int64_t nruns,
+                        int64_t row_height, int32_t *blk_br, int32_t *blk_bc,
+                        uint32_t *len_local, int64_t *start_local, hbp_stream_t stream) {
+    if (nruns <= 0) return HBP_OK;
+    k_fill_slots<<<grid_for(nruns, kThreads), kThreads, 0, as_stream(stream)>>>(
+        sorted_bc, order, run_row, run_start, run_count, block_incl, nruns, row_height, blk_br,
+        blk_bc, len_local, start_local);
+    HBP_LAUNCH_CHECK();
+    return HBP_OK;
+}
+
+int hbp_block_nnz(const uint32_t *len_local, int64_t nzb, int64_t row_height, int64_t *block_nnz,
+                  hbp_stream_t stream) {
+    if (nzb <= 0) return HBP_OK;
+    k_block_nnz<<<grid_for(nzb * 32, kThreads), kThreads, 0, as_stream(stream)>>>(
+        len_local, nzb, row_height, block_nnz);
+    HBP_LAUNCH_CHECK();
+    return HBP_OK;
+}
+
+int hbp_sample_counts(const int64_t *row_ptr, const int32_t *col_idx, int64_t rows,
+                      int64_t col_width, const int64_t *flat_idx, int64_t k, int32_t *counts,
+                      hbp_stream_t stream) {
+    if (k <= 0) return HBP_OK;
+    k_sample_counts<<<grid_for(k, kThreads), kThreads, 0, as_stream(stream)>>>(
+        row_ptr, col_idx, rows, col_width, flat_idx, k, counts);
+    HBP_LAUNCH_CHECK();
+    return HBP_OK;
+}
+
+static int hash_launch_shape(int64_t R, int *threads, size_t *smem) {
+    int64_t nw = (R + 31) / 32;
+    int64_t t = 64;
+    while (t > 1 && nw * 4 * t > 48 * 1024) t >>= 1;
+    if (nw * 4 * t > 48 * 1024) return HBP_E_UNSUPPORTED;
+    *threads = (int)t;
+    *smem = (size_t)(nw * 4 * t);
+    return HBP_OK;
+}
+
+int hbp_hash_perm(const uint32_t *len_local, const int32_t *blk_br, int64_t nzb, int64_t rows,
+                  int64_t row_height, int64_t a, int64_t b, int64_t c, int64_t d,
+                  int64_t bucket_max, uint32_t *perm, unsigned long long *probes,
+                  hbp_stream_t stream) {
+    if (b < 1 || d < 1 || a < 0 || row_height < 1) return HBP_E_ARG;
+    if (nzb <= 0) return HBP_OK;
+    int threads;
+    size_t smem;
+    int st = hash_launch_shape(row_height, &threads, &smem);
+    if (st) return st;
+    unsigned grid = (unsigned)((nzb + threads - 1) / threads);
+    k_hash_perm<false><<<grid, threads, smem, as_stream(stream)>>>(
+        len_local, blk_br, nzb, rows, row_height, a, b, c, d, bucket_max, perm, probes);
+    HBP_LAUNCH_CHECK();
+    return HBP_OK;
+}
+
+int hbp_hash_perm_empty(int64_t n, int64_t a, int64_t b, int64_t c, int64_t d,
+                        int64_t bucket_max, uint32_t *perm, hbp_stream_t stream) {
+    if (n < 1 || b < 1 || d < 1) return HBP_E_ARG;
+    int threads;
+    size_t smem;
+    int st = hash_launch_shape(n, &threads, &smem);
+    if (st) return st;
+    // one thread; `rows` carries n, R = n
+    k_hash_perm<true><<<1, 32, (size_t)((n + 31) / 32) * 4 * 32, as_stream(stream)>>>(
+        nullptr, nullptr, 1, n, n, a, b, c, d, bucket_max, perm, nullptr);
+    HBP_LAUNCH_CHECK();
+    return HBP_OK;
+}
+
+int hbp_sort_perm(const uint32_t *len_local, const int32_t *blk_br, int64_t nzb, int64_t rows,
+                  int64_t row_height, uint32_t *perm, hbp_stream_t stream) {
+    if (nzb <= 0) return HBP_OK;
+    k_sort_perm<<<grid_for(nzb * 32, kThreads), kThreads, 0, as_stream(stream)>>>(
+        len_local, blk_br, nzb, rows, row_height, perm);
+    HBP_LAUNCH_CHECK();
+    return HBP_OK;
+}
+
+static int check_perm(const uint32_t *tab, int64_t rows, int64_t R, int64_t nrb, int64_t nblocks,
+                      const int32_t *blk_br, int dense, long long *bad, cudaStream_t s) {
+    if (nblocks <= 0) return HBP_OK;
+    int64_t nw = (R + 31) / 32;
+    int warps = 8;
+    while (warps > 1 && nw * 4 * warps > 48 * 1024) warps >>= 1;
+    if (nw * 4 * warps > 48 * 1024) return HBP_E_UNSUPPORTED;
+    k_check_perm<<<grid_for(nblocks * 32, warps * 32), warps * 32, (size_t)(nw * 4 * warps), s>>>(
+        tab, rows, R, nrb, nblocks, blk_br, dense, bad);
+    HBP_LAUNCH_CHECK();
+    return HBP_OK;
+}
+
+int hbp_gather_dense_perm(const uint32_t *dense, int64_t rows, int64_t ncb, int64_t row_height,
+                          const int32_t *blk_br, const int32_t *blk_bc, int64_t nzb,
+                          uint32_t *perm, long long *bad, hbp_stream_t stream) {
+    cudaStream_t s = as_stream(stream);
+    int64_t nrb = (rows + row_height - 1) / row_height;
+    int st = check_perm(dense, rows, row_height, nrb, ncb * nrb, nullptr, 1, bad, s);
+    if (st) return st;
+    if (nzb > 0) {
+        k_gather_perm<<<grid_for(nzb * row_height, kThreads), kThreads, 0, s>>>(
+            dense, rows, row_height, blk_br, blk_bc, nzb, perm);
+        HBP_LAUNCH_CHECK();
+    }
+    return HBP_OK;
+}
+
+int hbp_slot_lengths(const uint32_t *len_local, const uint32_t *perm, const int32_t *blk_br,
+                     int64_t nzb, int64_t rows, int64_t row_height, int64_t warp_size,
+                     uint32_t *slot_len, int32_t *zero_row, int64_t *group_nnz,
+                     long long *bad, hbp_stream_t stream) {
+    if (warp_size < 1 || warp_size > 32 || row_height % warp_size) return HBP_E_UNSUPPORTED;
+    cudaStream_t s = as_stream(stream);
+    int64_t nrb = (rows + row_height - 1) / row_height;
+    if (bad) {
+        int st = check_perm(perm, rows, row_height, nrb, nzb, blk_br, 0, bad, s);
+        if (st) return st;
+    }
+    int64_t ngroups = nzb * (row_height / warp_size);
+    int64_t spw = 32 / warp_size;
+    int64_t warps = (ngroups + spw - 1) / spw;
+    k_slot_lengths<<<grid_for((warps > 0 ? warps : 1) * 32, kThreads), kThreads, 0, s>>>(
+        len_local, perm, blk_br, nzb, rows, row_height, (int)warp_size, slot_len, zero_row,
+        group_nnz);
+    HBP_LAUNCH_CHECK();
+    return HBP_OK;
+}
+
+int hbp_emit(const uint32_t *slot_len, const uint32_t *perm, const int64_t *start_local,
+             const int64_t *group_start, const int32_t *blk_br, int64_t nzb, int64_t rows,
+             int64_t row_height, int64_t warp_size, const int32_t *col_idx, const void *values,
+             int dtype, uint32_t *col, void *data, int32_t *add_sign, hbp_stream_t stream) {
+    if (warp_size < 1 || warp_size > 32 || row_height % warp_size) return HBP_E_UNSUPPORTED;
+    if (nzb <= 0) return HBP_OK;
+    int64_t ngroups = nzb * (row_height / warp_size);
+    int64_t spw = 32 / warp_size;
+    unsigned grid = grid_for(((ngroups + spw - 1) / spw) * 32, kThreads);
+    cudaStream_t s = as_stream(stream);
+    if (dtype == HBP_F64)
+        k_emit<double><<<grid, kThreads, 0, s>>>(slot_len, perm, start_local, group_start, blk_br,
+                                                 nzb, rows, row_height, (int)warp_size, col_idx,
+                                                 (const double *)values, col, (double *)data,
+                                                 add_sign);
+    else if (dtype == HBP_F32)
+        k_emit<float><<<grid, kThreads, 0, s>>>(slot_len, perm, start_local, group_start, blk_br,
+                                                nzb, rows, row_height, (int)warp_size, col_idx,
+                                                (const float *)values, col, (float *)data,
+                                                add_sign);
+    else
+        return HBP_E_ARG;
+    HBP_LAUNCH_CHECK();
+    return HBP_OK;
+}
+
+int hbp_row_block_counts(const int32_t *blk_br, int64_t nzb, int64_t *rb_count,
+                         hbp_stream_t stream) {
+    if (nzb <= 0) return HBP_OK;
+    k_rb_counts<<<grid_for(nzb, kThreads), kThreads, 0, as_stream(stream)>>>(blk_br, nzb,
+                                                                             rb_count);
+    HBP_LAUNCH_CHECK();
+    return HBP_OK;
+}
+
+int hbp_expand_reference(const int32_t *blk_br, const int32_t *blk_bc, int64_t nzb, int64_t rows,
+                         int64_t cols, int64_t nnz, int64_t col_width, int64_t row_height,
+                         int64_t warp_size, const uint32_t *perm, const int32_t *zero_row_c,
+                         const int64_t *group_start_c, const uint32_t *empty_perm_full,
+                         const uint32_t *empty_perm_last, int32_t *zero_row, uint32_t *output_hash,
+                         int64_t *group_start, hbp_stream_t stream) {
+    if (warp_size < 1 || row_height % warp_size) return HBP_E_ARG;
+    cudaStream_t s = as_stream(stream);
+    int64_t R = row_height, W = warp_size;
+    int64_t nrb = (rows + R - 1) / R, ncb = (cols + col_width - 1) / col_width;
+    int64_t last = rows - (nrb - 1) * R;
+    int64_t gpc = (nrb - 1) * (R / W) + (last + W - 1) / W;
+    k_expand_slots<<<grid_for(ncb * rows, kThreads), kThreads, 0, s>>>(
+        rows, ncb, R, empty_perm_full, empty_perm_last, output_hash, zero_row);
+    HBP_LAUNCH_CHECK();
+    if (nzb > 0) {
+        k_scatter_slots<<<grid_for(nzb * R, kThreads), kThreads, 0, s>>>(
+            blk_br, blk_bc, nzb, rows, R, perm, zero_row_c, output_hash, zero_row);
+        HBP_LAUNCH_CHECK();
+    }
+    k_expand_groups<<<grid_for(ncb * gpc + 1, kThreads), kThreads, 0, s>>>(
+        blk_br, blk_bc, nzb, nrb, ncb, gpc, R / W, nnz, group_start_c, group_start);
+    HBP_LAUNCH_CHECK();
+    return HBP_OK;
+}
+
+int hbp_walk_chains(int64_t rows, int64_t cols, int64_t col_width, int64_t row_height,
+                    int64_t warp_size, const int32_t *zero_row, const uint32_t *output_hash,
+                    const int64_t *group_start, const uint32_t *col, const int32_t *add_sign,
+                    int64_t nnz, int64_t *row_out, int32_t *seen, int32_t *err,
+                    hbp_stream_t stream) {
+    if (warp_size < 1 || row_height % warp_size) return HBP_E_ARG;
+    int64_t R = row_height, W = warp_size;
+    int64_t nrb = (rows + R - 1) / R, ncb = (cols + col_width - 1) / col_width;
+    int64_t last = rows - (nrb - 1) * R;
+    int64_t gpc = (nrb - 1) * (R / W) + (last + W - 1) / W;
+    k_walk_chains<<<grid_for(ncb * rows, kThreads), kThreads, 0, as_stream(stream)>>>(
+        rows, cols, col_width, R, W, ncb, gpc, zero_row, output_hash, group_start, col, add_sign,
+        nnz, row_out, seen, err);
+    HBP_LAUNCH_CHECK();
+    return HBP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,336 @@
+// hbp_spmv.cu -- the HBP SpMV and the combine on sm_100a.
+//
+// Reference path: hbp_spmv (engine.py:228-232) ->
+// plan_execution (engine.py:96-115) -> run_spmv (engine.py:179-193) ->
+// _run_plan (engine.py:137-176: fixed chunks, then a ticket) -> block_spmv
+// (engine.py:123-134) -> hbp_block_kernel (_kernels.py:22-47) -> combine
+// (engine.py:196-201).
+//
+// GPU mapping ("each block being computed by a warp"): one
+// persistent warp per worker; a worker runs its fixed contiguous chunk of
+// nonzero blocks, then claims blocks with an atomic ticket.  Inside a block
+// each W-lane segment owns one HBP group and each lane one slot (= one row).
+// Instead of chasing add_sign (a serial dependent-load chain) the lane
+// derives element addresses from the group's slot lengths: within a phase
+// where k lanes are live, lane `rank` reads base + t*k + rank -- the same
+// elements in the same order, coalesced across the
+// k live lanes, with loads of several steps in flight.  Each row's sum is
+// accumulated in step order, so:
+//   f64: __dmul_rn / __dadd_rn, bitwise identical to the reference;
+//   f32: products are exact in f64, sums in f64, one rounding at the end.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "hbp.h"
+#include "hbp_common.cuh"
+
+using namespace hbp;
+
+namespace {
+
+constexpr int kSpmvThreads = 256;
+constexpr int kSpmvWarps = kSpmvThreads / 32;
+
+template <typename V, bool EXACT>
+__device__ __forceinline__ double fmadd(double acc, V v, V xv) {
+    if (EXACT) return __dadd_rn(acc, __dmul_rn((double)v, (double)xv));
+    return fma((double)v, (double)xv, acc);  // exact product for f32 inputs
+}
+
+// Sum of one slot's elements in step order.  All segment lanes must call it.
+template <typename V, bool EXACT>
+__device__ __forceinline__ double group_dot(const Seg &sg, const uint32_t *__restrict__ col,
+                                            const V *__restrict__ data,
+                                            const V *__restrict__ x, uint32_t len,
+                                            int64_t base, uint64_t pe, uint64_t pl) {
+    const unsigned lt = (1u << sg.q) - 1u;
+    double acc = 0.0;
+    uint32_t t0 = 0;
+    bool live = len > 0;
+    unsigned mask = seg_ballot(sg, live);
+    while (mask) {
+        const int k = __popc(mask);
+        const uint32_t t1 = seg_min_u32(sg, live ? len : 0xffffffffu);
+        if (live) {
+            const int rank = __popc(mask & lt);
+            const uint32_t *cp = col + base + rank;
+            const V *dp = data + base + rank;
+            const uint32_t M = t1 - t0;
+            uint32_t t = 0;
+            for (; t + 4 <= M; t += 4) {
+                uint32_t c0 = ld_stream_u32(cp, pe), c1 = ld_stream_u32(cp + k, pe),
+                         c2 = ld_stream_u32(cp + 2 * k, pe), c3 = ld_stream_u32(cp + 3 * k, pe);
+                V v0 = ld_stream(dp, pe), v1 = ld_stream(dp + k, pe), v2 = ld_stream(dp + 2 * k, pe),
+                  v3 = ld_stream(dp + 3 * k, pe);
+                V x0 = ld_x(x + c0, pl), x1 = ld_x(x + c1, pl), x2 = ld_x(x + c2, pl), x3 = ld_x(x + c3, pl);
+                acc = fmadd<V, EXACT>(acc, v0, x0);
+                acc = fmadd<V, EXACT>(acc, v1, x1);
+                acc = fmadd<V, EXACT>(acc, v2, x2);
+                acc = fmadd<V, EXACT>(acc, v3, x3);
+                cp += 4 * k;
+                dp += 4 * k;
+            }
+            for (; t < M; ++t) {
+                uint32_t c0 = ld_stream_u32(cp, pe);
+                V v0 = ld_stream(dp, pe);
+                acc = fmadd<V, EXACT>(acc, v0, ld_x(x + c0, pl));
+                cp += k;
+                dp += k;
+            }
+        }
+        base += (int64_t)(t1 - t0) * k;
+        t0 = t1;
+        live = len > t0;
+        mask = seg_ballot(sg, live);
+    }
+    return acc;
+}
+
+template <typename V, bool EXACT, bool DIRECT, bool LOG>
+__global__ void __launch_bounds__(kSpmvThreads)
+    k_spmv(const hbp_format_t f, const hbp_schedule_t sch, const V *__restrict__ x,
+           double *__restrict__ partial, V *__restrict__ y) {
+    const int lane = threadIdx.x & 31;
+    const int64_t worker = (int64_t)blockIdx.x * kSpmvWarps + (threadIdx.x >> 5);
+    if (worker >= sch.workers) return;  // whole warps exit together
+    const Seg sg = make_seg((int)f.warp_size);
+    const int64_t R = f.row_height, W = f.warp_size, gpb = R / W;
+    const V *__restrict__ data = (const V *)f.data;
+    const uint64_t pe = policy_evict_first(), pl = policy_evict_last();
+
+    auto run_block = [&](int64_t idx, int8_t kind) {
+        int64_t t_start = 0;
+        if (LOG && lane == 0) t_start = globaltimer_ns();
+        const int64_t br = f.blk_br[idx];
+        int64_t n = f.rows - br * R;
+        if (n > R) n = R;
+        const int64_t ng = (n + W - 1) / W;
+        if (!sg.idle()) {
+            for (int64_t g = sg.seg; g < ng; g += sg.spw) {
+                const int64_t slot = g * W + sg.q;
+                const bool valid = slot < n;
+                const uint32_t len = valid ? f.slot_len[idx * R + slot] : 0u;
+                const double acc = group_dot<V, EXACT>(sg, f.col, data, x, len,
+                                                       f.group_start[idx * gpb + g], pe, pl);
+                if (valid) {
+                    const uint32_t row = f.perm[idx * R + slot];
+                    if (DIRECT) y[br * R + row] = (V)acc;
+                    else partial[idx * R + row] = acc;
+                }
+            }
+        }
+        __syncwarp();
+        if (LOG && lane == 0) {
+            sch.log_start_ns[idx] = t_start;
+            sch.log_end_ns[idx] = globaltimer_ns();
+            sch.log_worker[idx] = (int32_t)worker;
+            sch.log_kind[idx] = kind;
+        }
+    };
+
+    // engine.py:107-115: contiguous chunks, the first `rem` one block longer
+    const int64_t per = sch.fixed_count / sch.workers, rem = sch.fixed_count % sch.workers;
+    const int64_t lo = worker * per + (worker < rem ? worker : rem);
+    const int64_t hi = lo + per + (worker < rem ? 1 : 0);
+    for (int64_t idx = lo; idx < hi; ++idx) run_block(idx, 0);
+    // engine.py:159-165: ticket acquisition over [fixed_count, nzb)
+    for (;;) {
+        uint32_t t = 0;
+        if (lane == 0) t = atomicAdd(sch.ticket, 1u);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        const int64_t idx = sch.fixed_count + (int64_t)t;
+        if (idx >= f.nzb) break;
+        run_block(idx, 1);
+    }
+}
+
+// combine over nonzero blocks, ascending bc (engine.py:196-201)
+template <typename V>
+__global__ void k_combine(const hbp_format_t f, const double *__restrict__ partial,
+                          V *__restrict__ y) {
+    const int64_t R = f.row_height;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < f.rows;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t br = r / R, local = r - br * R;
+        const int64_t lo = f.rb_ptr[br], hi = f.rb_ptr[br + 1];
+        double s = 0.0;
+        if (lo < hi) {
+            s = partial[(int64_t)f.rb_blk[lo] * R + local];
+            for (int64_t i = lo + 1; i < hi; ++i)
+                s = __dadd_rn(s, partial[(int64_t)f.rb_blk[i] * R + local]);
+        }
+        y[r] = (V)s;
+    }
+}
+
+template <typename V>
+__global__ void k_zero_empty(const hbp_format_t f, V *__restrict__ y) {
+    const int64_t R = f.row_height;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < f.rows;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t br = r / R;
+        if (f.rb_ptr[br] == f.rb_ptr[br + 1]) y[r] = (V)0;
+    }
+}
+
+__global__ void k_expand_partial(const hbp_format_t f, const double *__restrict__ partial,
+                                 double *__restrict__ dense) {
+    const int64_t R = f.row_height;
+    const int64_t total = f.nzb * R;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t blk = i / R, s = i - blk * R;
+        const int64_t br = f.blk_br[blk];
+        if (br * R + s >= f.rows) continue;
+        dense[(int64_t)f.blk_bc[blk] * f.rows + br * R + s] = partial[i];
+    }
+}
+
+// hbp.py:241-315: every element's (row, col, value), by position.
+template <typename V>
+__global__ void k_to_triplets(const hbp_format_t f, int64_t *__restrict__ row_out,
+                              int64_t *__restrict__ col_out, V *__restrict__ val_out) {
+    const Seg sg = make_seg((int)f.warp_size);
+    if (sg.idle()) return;
+    const int64_t R = f.row_height, W = f.warp_size, gpb = R / W;
+    const int64_t ngroups = f.nzb * gpb;
+    const unsigned lt = (1u << sg.q) - 1u;
+    const V *data = (const V *)f.data;
+    int64_t seg_id = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * sg.spw + sg.seg;
+    int64_t nseg = (((int64_t)gridDim.x * blockDim.x) >> 5) * sg.spw;
+    for (int64_t gg = seg_id; gg < ngroups; gg += nseg) {
+        const int64_t blk = gg / gpb, g = gg - blk * gpb;
+        const int64_t slot = blk * R + g * W + sg.q;
+        const uint32_t len = f.slot_len[slot];
+        const int64_t row = (int64_t)f.blk_br[blk] * R + (len ? f.perm[slot] : 0);
+        int64_t base = f.group_start[gg];
+        uint32_t t0 = 0;
+        bool live = len > 0;
+        unsigned mask = seg_ballot(sg, live);
+        while (mask) {
+            const int k = __popc(mask);
+            const uint32_t t1 = seg_min_u32(sg, live ? len : 0xffffffffu);
+            if (live) {
+                int64_t p = base + __popc(mask & lt);
+                for (uint32_t t = t0; t < t1; ++t, p += k) {
+                    row_out[p] = row;
+                    col_out[p] = f.col[p];
+                    val_out[p] = data[p];
+                }
+            }
+            base += (int64_t)(t1 - t0) * k;
+            t0 = t1;
+            live = len > t0;
+            mask = seg_ballot(sg, live);
+        }
+    }
+}
+
+template <typename V, bool EXACT, bool DIRECT, bool LOG>
+void launch_spmv(const hbp_format_t *f, const hbp_schedule_t *s, const void *x, double *partial,
+                 void *y, cudaStream_t st) {
+    unsigned grid = (unsigned)((s->workers + kSpmvWarps - 1) / kSpmvWarps);
+    k_spmv<V, EXACT, DIRECT, LOG><<<grid, kSpmvThreads, 0, st>>>(*f, *s, (const V *)x, partial,
+                                                                 (V *)y);
+}
+
+template <typename V, bool EXACT>
+void dispatch_spmv(const hbp_format_t *f, const hbp_schedule_t *s, const void *x,
+                   double *partial, void *y, cudaStream_t st) {
+    const bool direct = y != nullptr, log = s->log_worker != nullptr;
+    if (direct) {
+        if (log) launch_spmv<V, EXACT, true, true>(f, s, x, partial, y, st);
+        else launch_spmv<V, EXACT, true, false>(f, s, x, partial, y, st);
+    } else {
+        if (log) launch_spmv<V, EXACT, false, true>(f, s, x, partial, y, st);
+        else launch_spmv<V, EXACT, false, false>(f, s, x, partial, y, st);
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int hbp_spmv_default_workers(int dtype, int64_t warp_size, int64_t *workers) {
+    int dev = 0, sms = 0, per_sm = 0;
+    HBP_CUDA_TRY(cudaGetDevice(&dev));
+    HBP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (dtype == HBP_F64)
+        HBP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, k_spmv<double, true, true, false>, kSpmvThreads, 0));
+    else
+        HBP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, k_spmv<float, false, true, false>, kSpmvThreads, 0));
+    (void)warp_size;
+    *workers = (int64_t)sms * per_sm * kSpmvWarps;
+    return HBP_OK;
+}
+
+int hbp_spmv_blocks(const hbp_format_t *f, const hbp_schedule_t *s, const void *x,
+                    double *partial, void *y_direct, hbp_stream_t stream) {
+    if (!f || !s || s->workers < 1) return HBP_E_ARG;
+    if (f->warp_size < 1 || f->warp_size > 32 || f->row_height % f->warp_size)
+        return HBP_E_UNSUPPORTED;
+    if (y_direct && f->ncb != 1) return HBP_E_ARG;
+    if (!y_direct && !partial) return HBP_E_ARG;
+    cudaStream_t st = as_stream(stream);
+    HBP_CUDA_TRY(cudaMemsetAsync(s->ticket, 0, sizeof(uint32_t), st));
+    if (f->nzb == 0) return HBP_OK;
+    if (f->dtype == HBP_F64) dispatch_spmv<double, true>(f, s, x, partial, y_direct, st);
+    else if (f->dtype == HBP_F32) dispatch_spmv<float, false>(f, s, x, partial, y_direct, st);
+    else return HBP_E_ARG;
+    HBP_LAUNCH_CHECK();
+    return HBP_OK;
+}
+
+int hbp_combine(const hbp_format_t *f, const double *partial, void *y, hbp_stream_t stream) {
+    if (!f || f->rows < 1) return HBP_E_ARG;
+    cudaStream_t st = as_stream(stream);
+    unsigned grid = grid_for(f->rows, 256);
+    if (f->dtype == HBP_F64) k_combine<double><<<grid, 256, 0, st>>>(*f, partial, (double *)y);
+    else if (f->dtype == HBP_F32) k_combine<float><<<grid, 256, 0, st>>>(*f, partial, (float *)y);
+    else return HBP_E_ARG;
+    HBP_LAUNCH_CHECK();
+    return HBP_OK;
+}
+
+int hbp_zero_empty_rows(const hbp_format_t *f, void *y, hbp_stream_t stream) {
+    if (!f || f->rows < 1) return HBP_E_ARG;
+    cudaStream_t st = as_stream(stream);
+    unsigned grid = grid_for(f->rows, 256);
+    if (f->dtype == HBP_F64) k_zero_empty<double><<<grid, 256, 0, st>>>(*f, (double *)y);
+    else if (f->dtype == HBP_F32) k_zero_empty<float><<<grid, 256, 0, st>>>(*f, (float *)y);
+    else return HBP_E_ARG;
+    HBP_LAUNCH_CHECK();
+    return HBP_OK;
+}
+
+int hbp_expand_partial(const hbp_format_t *f, const double *partial, double *partial_dense,
+                       hbp_stream_t stream) {
+    if (!f) return HBP_E_ARG;
+    cudaStream_t st = as_stream(stream);
+    HBP_CUDA_TRY(cudaMemsetAsync(partial_dense, 0, sizeof(double) * (size_t)(f->ncb * f->rows), st));
+    if (f->nzb == 0) return HBP_OK;
+    k_expand_partial<<<grid_for(f->nzb * f->row_height, 256), 256, 0, st>>>(*f, partial,
+                                                                           partial_dense);
+    HBP_LAUNCH_CHECK();
+    return HBP_OK;
+}
+
+int hbp_to_triplets(const hbp_format_t *f, int64_t *row_out, int64_t *col_out, void *val_out,
+                    hbp_stream_t stream) {
+    if (!f || f->warp_size < 1 || f->warp_size > 32) return HBP_E_ARG;
+    if (f->nzb == 0) return HBP_OK;
+    cudaStream_t st = as_stream(stream);
+    int64_t spw = 32 / f->warp_size;
+    int64_t warps = (f->nzb * (f->row_height / f->warp_size) + spw - 1) / spw;
+    unsigned grid = grid_for(warps * 32, 256);
+    if (f->dtype == HBP_F64)
+        k_to_triplets<double><<<grid, 256, 0, st>>>(*f, row_out, col_out, (double *)val_out);
+    else
+        k_to_triplets<float><<<grid, 256, 0, st>>>(*f, row_out, col_out, (float *)val_out);
+    HBP_LAUNCH_CHECK();
+    return HBP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,269 @@
+"""Two-step SpMV execution on the GPU: scheduled block kernel, then combine.
+
+Mirrors /root/reference/pkg/src/hbp_spmv/engine.py.  A worker is one
+persistent GPU warp; the plan's fixed chunks and the atomic
+ticket over the competitive pool are executed inside ``hbp_spmv_blocks``.
+Each block writes a disjoint slice of the (compact) partial vector and every
+row's sum is schedule-independent, so results are bitwise identical for any
+worker count or fixed fraction (engine.py:1-8).
+
+``SpmvOperator`` is the allocation-free hot path behind ``hbp_spmv``: it
+owns the partial/ticket buffers and can capture SpMV + combine in a CUDA
+graph.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .hbp import HbpMatrix
+from .partition import BlockGrid, PartitionConfig
+
+__all__ = ["ExecutionPlan", "PartialVector", "ExecutionLog", "SpmvOperator", "plan_execution",
+           "block_spmv", "run_spmv", "combine", "hbp_spmv", "KIND_FIXED", "KIND_COMPETITIVE"]
+
+KIND_FIXED = 0
+KIND_COMPETITIVE = 1
+
+
+@dataclass(frozen=True)
+class ExecutionPlan:
+    """engine.py:38-56: nonzero blocks bc-major plus the fixed/competitive split."""
+
+    block_order: np.ndarray
+    fixed_count: int
+    worker_ranges: tuple
+
+    @property
+    def competitive_start(self) -> int:
+        return self.fixed_count
+
+    @property
+    def num_blocks(self) -> int:
+        return len(self.block_order)
+
+    @property
+    def workers(self) -> int:
+        return len(self.worker_ranges)
+
+
+class PartialVector:
+    """engine.py:59-68.  ``compact`` is f64 [nzb * R] (block-major, original
+    local row); ``values`` / ``segment`` give the reference's dense
+    [bc][global row] layout on demand."""
+
+    def __init__(self, hbp: HbpMatrix, compact: torch.Tensor):
+        self.hbp = hbp
+        self.compact = compact
+        self.rows = hbp.rows
+        self.num_col_blocks = hbp.num_col_blocks
+        self._dense = None
+
+    @property
+    def values(self) -> torch.Tensor:
+        if self._dense is None:
+            d = torch.empty(self.num_col_blocks * self.rows, dtype=torch.float64,
+                            device=self.compact.device)
+            f = self.hbp.format_struct()
+            L.call("hbp_expand_partial", ctypes.byref(f), L.P(self.compact), L.P(d), L.stream())
+            self._dense = d
+        return self._dense
+
+    def segment(self, bc: int) -> torch.Tensor:
+        return self.values[bc * self.rows:(bc + 1) * self.rows]
+
+
+@dataclass
+class ExecutionLog:
+    """engine.py:71-83 (times from the GPU %globaltimer, ns)."""
+
+    worker: np.ndarray
+    kind: np.ndarray
+    start_ns: np.ndarray
+    end_ns: np.ndarray
+
+    @classmethod
+    def empty(cls, n: int) -> "ExecutionLog":
+        return cls(np.full(n, -1, np.int32), np.full(n, -1, np.int8),
+                   np.zeros(n, np.int64), np.zeros(n, np.int64))
+
+
+def _block_order(source) -> np.ndarray:
+    """engine.py:86-93: (br, bc) of nonzero blocks in bc-major order."""
+    return np.ascontiguousarray(
+        np.stack([source.blk_br.cpu().numpy(), source.blk_bc.cpu().numpy()], axis=1)
+    ).astype(np.int32).reshape(-1, 2)
+
+
+def default_workers(dtype=torch.float64, warp_size: int = 32) -> int:
+    """Persistent warps that fill the device (all SMs x resident warps)."""
+    return L.default_workers(dtype, warp_size)
+
+
+def plan_execution(source, config: PartitionConfig, workers: int | None) -> ExecutionPlan:
+    """engine.py:96-115.  source is a BlockGrid or an HbpMatrix; workers is the
+    number of persistent GPU warps (None: fill the device)."""
+    if workers is None:
+        workers = default_workers(getattr(source, "dtype", torch.float64), config.warp_size)
+    if workers < 1:
+        raise ValueError("workers must be >= 1")
+    if not isinstance(source, (BlockGrid, HbpMatrix)):
+        raise TypeError("source must be a BlockGrid or an HbpMatrix")
+    order = _block_order(source)
+    n = len(order)
+    fixed = int(config.fixed_fraction * n + 0.5)
+    base, rem = divmod(fixed, workers)
+    ranges, s = [], 0
+    for w in range(workers):
+        size = base + (1 if w < rem else 0)
+        ranges.append((s, s + size))
+        s += size
+    return ExecutionPlan(order, fixed, tuple(ranges))
+
+
+def _as_x(hbp: HbpMatrix, x) -> torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        t = x
+    else:
+        t = torch.as_tensor(np.asarray(x))
+    if tuple(t.shape) != (hbp.cols,):
+        raise ValueError(f"vector length {tuple(t.shape)} != cols {hbp.cols}")
+    return t.to(device=hbp.data.device, dtype=hbp.data.dtype).contiguous()
+
+
+class SpmvOperator:
+    """Preallocated y = A x for one HbpMatrix (the bench / serving hot path).
+
+    direct mode (one column block): the block kernel writes y itself;
+    otherwise the partial (f64, compact) is combined in ascending bc."""
+
+    def __init__(self, hbp: HbpMatrix, workers: int | None = None,
+                 fixed_fraction: float | None = None):
+        self.hbp = hbp
+        dev = hbp.data.device
+        self.workers = workers or default_workers(hbp.dtype, hbp.config.warp_size)
+        f = hbp.config.fixed_fraction if fixed_fraction is None else fixed_fraction
+        self.fixed_count = int(f * hbp.nzb + 0.5)
+        self.ticket = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.direct = hbp.num_col_blocks == 1
+        R = hbp.config.row_height
+        self.partial = None if self.direct else torch.empty(hbp.nzb * R, dtype=torch.float64,
+                                                            device=dev)
+        self.has_empty_row_blocks = bool((hbp.rb_ptr[1:] == hbp.rb_ptr[:-1]).any())
+        self.sched = L.ScheduleT()
+        self.sched.workers = self.workers
+        self.sched.fixed_count = self.fixed_count
+        self.sched.ticket = self.ticket.data_ptr()
+        self.launches_per_call = 1 + (0 if self.direct and not self.has_empty_row_blocks else 1)
+        self._graph = None
+        self._gx = self._gy = None
+
+    def __call__(self, x: torch.Tensor, y: torch.Tensor | None = None) -> torch.Tensor:
+        hbp = self.hbp
+        if y is None:
+            y = torch.empty(hbp.rows, dtype=hbp.dtype, device=hbp.data.device)
+        f = hbp.format_struct()
+        s = L.stream()
+        if self.direct:
+            L.call("hbp_spmv_blocks", ctypes.byref(f), ctypes.byref(self.sched), L.P(x),
+                   L.P(None), L.P(y), s)
+            if self.has_empty_row_blocks:
+                L.call("hbp_zero_empty_rows", ctypes.byref(f), L.P(y), s)
+        else:
+            L.call("hbp_spmv_blocks", ctypes.byref(f), ctypes.byref(self.sched), L.P(x),
+                   L.P(self.partial), L.P(None), s)
+            L.call("hbp_combine", ctypes.byref(f), L.P(self.partial), L.P(y), s)
+        return y
+
+    def capture(self, x: torch.Tensor, y: torch.Tensor) -> "torch.cuda.CUDAGraph":
+        """Capture one SpMV (+combine) on fixed x / y buffers in a CUDA graph."""
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self(x, y)  # warm (library calls have no lazy init, but keep it symmetric)
+        torch.cuda.current_stream().wait_stream(s)
+        with torch.cuda.graph(g):
+            self(x, y)
+        self._graph, self._gx, self._gy = g, x, y
+        return g
+
+
+def block_spmv(hbp: HbpMatrix, block, x, partial: PartialVector) -> None:
+    """engine.py:123-134: run one block into the partial vector."""
+    br, bc = int(block[0]), int(block[1])
+    keys = (hbp.blk_bc.to(torch.int64) * hbp.num_row_blocks + hbp.blk_br).cpu().numpy()
+    k = bc * hbp.num_row_blocks + br
+    i = int(np.searchsorted(keys, k))
+    if i >= keys.size or keys[i] != k:
+        return  # an empty block contributes nothing
+    xd = _as_x(hbp, x)
+    R, gpb = hbp.config.row_height, hbp.config.row_height // hbp.config.warp_size
+    f = L.FormatT.from_buffer_copy(hbp.format_struct())
+    esz4, esz8 = 4, 8
+    f.nzb = 1
+    f.blk_br = hbp.blk_br.data_ptr() + i * esz4
+    f.blk_bc = hbp.blk_bc.data_ptr() + i * esz4
+    f.slot_len = hbp.slot_len.data_ptr() + i * R * esz4
+    f.perm = hbp.perm.data_ptr() + i * R * esz4
+    f.group_start = hbp.group_start_c.data_ptr() + i * gpb * esz8
+    sched = L.ScheduleT()
+    sched.workers, sched.fixed_count = 1, 0
+    ticket = torch.zeros(1, dtype=torch.int32, device=xd.device)
+    sched.ticket = ticket.data_ptr()
+    L.call("hbp_spmv_blocks", ctypes.byref(f), ctypes.byref(sched), L.P(xd),
+           L.c_vp(partial.compact.data_ptr() + i * R * esz8), L.P(None), L.stream())
+    partial._dense = None
+
+
+def run_spmv(hbp: HbpMatrix, x, plan: ExecutionPlan, workers: int):
+    """engine.py:179-193: every planned block once (GPU persistent warps);
+    returns (PartialVector, ExecutionLog)."""
+    if workers != plan.workers:
+        raise ValueError("plan was built for a different worker count")
+    xd = _as_x(hbp, x)
+    dev = xd.device
+    n = plan.num_blocks
+    R = hbp.config.row_height
+    compact = torch.zeros(hbp.nzb * R, dtype=torch.float64, device=dev)
+    lw = torch.full((max(n, 1),), -1, dtype=torch.int32, device=dev)
+    lk = torch.full((max(n, 1),), -1, dtype=torch.int8, device=dev)
+    ls = torch.zeros(max(n, 1), dtype=torch.int64, device=dev)
+    le = torch.zeros(max(n, 1), dtype=torch.int64, device=dev)
+    ticket = torch.zeros(1, dtype=torch.int32, device=dev)
+    sched = L.ScheduleT()
+    sched.workers, sched.fixed_count = workers, plan.fixed_count
+    sched.ticket = ticket.data_ptr()
+    sched.log_worker, sched.log_kind = lw.data_ptr(), lk.data_ptr()
+    sched.log_start_ns, sched.log_end_ns = ls.data_ptr(), le.data_ptr()
+    f = hbp.format_struct()
+    L.call("hbp_spmv_blocks", ctypes.byref(f), ctypes.byref(sched), L.P(xd), L.P(compact),
+           L.P(None), L.stream())
+    log = ExecutionLog(lw[:n].cpu().numpy(), lk[:n].cpu().numpy(), ls[:n].cpu().numpy(),
+                       le[:n].cpu().numpy())
+    return PartialVector(hbp, compact), log
+
+
+def combine(partial: PartialVector) -> torch.Tensor:
+    """engine.py:196-201: sum partials over column blocks, ascending bc."""
+    hbp = partial.hbp
+    y = torch.empty(hbp.rows, dtype=hbp.dtype, device=partial.compact.device)
+    f = hbp.format_struct()
+    L.call("hbp_combine", ctypes.byref(f), L.P(partial.compact), L.P(y), L.stream())
+    return y
+
+
+def hbp_spmv(hbp: HbpMatrix, x, workers: int | None = None) -> torch.Tensor:
+    """engine.py:228-232: plan, run and combine in one call (device tensor y).
+    workers=None fills the device with persistent warps."""
+    xd = _as_x(hbp, x)
+    key = ("op", workers)
+    op = hbp._ops.get(key)
+    if op is None:
+        op = SpmvOperator(hbp, workers)
+        hbp._ops[key] = op
+    return op(xd)

@@ -1,0 +1,498 @@
+"""The HBP format on the GPU: build, reference-layout views, validation, inverse.
+
+Mirrors /root/reference/pkg/src/hbp_spmv/hbp.py.  Element arrays (col, data,
+add_sign) have exactly the reference's layout (bc-major blocks, groups,
+column-major steps within a group).  The slot and group arrays are kept
+compact over nonzero blocks for the kernels; ``zero_row``, ``output_hash``
+and ``group_start`` expose the reference's dense layout (hbp.py:51-62) as
+device tensors built on first access (``hbp_expand_reference``).
+
+Runtime layout (HBM) used by the SpMV kernel:
+    col u32[nnz], data f32|f64[nnz]              streamed once per SpMV
+    slot_len u32[nzb*R], perm u32[nzb*R]         per-slot length / output row
+    group_start_c int64[nzb*gpb + 1]             per-group element base
+    blk_br, blk_bc int32[nzb]                    nonzero block directory
+    rb_ptr int64[nrb+1], rb_blk int32[nzb]       combine lists (ascending bc)
+add_sign is produced for the reference view and the .hbp codec; the kernel
+derives addresses from slot lengths instead of chasing it.
+"""
+from __future__ import annotations
+
+import io
+import struct
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .formats import CsrMatrix, TripletMatrix
+from .partition import (BlockGrid, PartitionConfig, _check_gpu_geometry, groups_in_row_block,
+                        groups_per_col_block, rows_in_row_block)
+from .reorder import BlockPermutations
+
+__all__ = ["HbpMatrix", "HbpFormatError", "build_hbp", "hbp_to_triplets", "serialize_hbp",
+           "deserialize_hbp", "save_hbp", "load_hbp"]
+
+MAGIC = b"HBP1"
+VERSION = 1
+
+
+class HbpFormatError(ValueError):
+    """hbp.py:47-48: malformed .hbp streams or structurally invalid matrices."""
+
+
+class HbpMatrix:
+    """Device-resident HBP matrix (hbp.py:51-135)."""
+
+    def __init__(self, rows: int, cols: int, config: PartitionConfig, grid_shape, *,
+                 col: torch.Tensor, data: torch.Tensor, add_sign: torch.Tensor | None,
+                 blk_br: torch.Tensor, blk_bc: torch.Tensor, slot_len: torch.Tensor,
+                 perm: torch.Tensor, group_start_c: torch.Tensor,
+                 zero_row_c: torch.Tensor | None, rb_ptr: torch.Tensor, rb_blk: torch.Tensor,
+                 permutations=None):
+        self.rows, self.cols, self.config = rows, cols, config
+        self.grid_shape = tuple(grid_shape)
+        self.col, self.data, self._add_sign = col, data, add_sign
+        self.blk_br, self.blk_bc = blk_br, blk_bc
+        self.slot_len, self.perm = slot_len, perm
+        self.group_start_c, self.zero_row_c = group_start_c, zero_row_c
+        self.rb_ptr, self.rb_blk = rb_ptr, rb_blk
+        self.permutations = permutations
+        self._views: dict = {}
+        self._fmt = None
+        self._ops: dict = {}
+
+    # ---- reference attributes
+    @property
+    def nnz(self) -> int:
+        return self.data.numel()
+
+    @property
+    def nzb(self) -> int:
+        return self.blk_br.numel()
+
+    @property
+    def dtype(self) -> torch.dtype:
+        return self.data.dtype
+
+    @property
+    def num_row_blocks(self) -> int:
+        return self.grid_shape[0]
+
+    @property
+    def num_col_blocks(self) -> int:
+        return self.grid_shape[1]
+
+    def rows_in_block(self, br: int) -> int:
+        return rows_in_row_block(self.rows, self.config.row_height, br)
+
+    def groups_in_block(self, br: int) -> int:
+        return groups_in_row_block(self.rows, self.config.row_height, self.config.warp_size, br)
+
+    def slot_base(self, br: int, bc: int) -> int:
+        return bc * self.rows + br * self.config.row_height
+
+    def group_base(self, br: int, bc: int) -> int:
+        per_col = groups_per_col_block(self.rows, self.config.row_height, self.config.warp_size)
+        return bc * per_col + br * (self.config.row_height // self.config.warp_size)
+
+    @property
+    def add_sign(self) -> torch.Tensor:
+        if self._add_sign is None:
+            raise ValueError("this HbpMatrix was built without add_sign")
+        return self._add_sign
+
+    def _expand(self):
+        if "zero_row" in self._views:
+            return
+        R, W, C = self.config.row_height, self.config.warp_size, self.config.col_width
+        nrb, ncb = self.grid_shape
+        dev = self.data.device
+        gpc = groups_per_col_block(self.rows, R, W)
+        zr = torch.empty(ncb * self.rows, dtype=torch.int32, device=dev)
+        oh = torch.empty(ncb * self.rows, dtype=torch.int32, device=dev)
+        gs = torch.empty(ncb * gpc + 1, dtype=torch.int64, device=dev)
+        last = self.rows - (nrb - 1) * R
+        if isinstance(self.permutations, BlockPermutations):
+            ef = torch.as_tensor(self.permutations.empty_block_perm(R).view(np.int32), device=dev)
+            el = torch.as_tensor(self.permutations.empty_block_perm(last).view(np.int32),
+                                 device=dev)
+        else:
+            ef = torch.arange(R, dtype=torch.int32, device=dev)
+            el = torch.arange(last, dtype=torch.int32, device=dev)
+        zrc = self.zero_row_c
+        if zrc is None:
+            raise ValueError("this HbpMatrix was built without zero_row")
+        L.call("hbp_expand_reference", L.P(self.blk_br), L.P(self.blk_bc), L.c_i64(self.nzb),
+               L.c_i64(self.rows), L.c_i64(self.cols), L.c_i64(self.nnz), L.c_i64(C), L.c_i64(R),
+               L.c_i64(W), L.P(self.perm), L.P(zrc), L.P(self.group_start_c), L.P(ef), L.P(el),
+               L.P(zr), L.P(oh), L.P(gs), L.stream())
+        if self.permutations is not None and not isinstance(self.permutations, BlockPermutations):
+            oh = self.permutations  # the caller's dense table, copied like hbp.py:237
+        self._views.update(zero_row=zr, output_hash=oh, group_start=gs)
+
+    @property
+    def zero_row(self) -> torch.Tensor:
+        """int32 [ncb * rows] (reference layout)."""
+        self._expand()
+        return self._views["zero_row"]
+
+    @property
+    def output_hash(self) -> torch.Tensor:
+        """u32 bits in int32 [ncb * rows] (reference layout)."""
+        self._expand()
+        return self._views["output_hash"]
+
+    @property
+    def group_start(self) -> torch.Tensor:
+        """int64 [ncb * gpc + 1] (reference layout)."""
+        self._expand()
+        return self._views["group_start"]
+
+    def block_nnz_matrix(self) -> np.ndarray:
+        """hbp.py:91-100: element count per block, from the compact group starts."""
+        R, W = self.config.row_height, self.config.warp_size
+        gpb = R // W
+        gs = self.group_start_c.view(-1)
+        per = (gs[gpb::gpb] - gs[:-1:gpb])[: self.nzb] if self.nzb else gs[:0]
+        out = np.zeros(self.grid_shape, np.int64)
+        out[self.blk_br.cpu().numpy(), self.blk_bc.cpu().numpy()] = per.cpu().numpy()
+        return out
+
+    def to_reference(self) -> dict:
+        """The six reference arrays as numpy with the reference dtypes."""
+        out = dict(col=self.col.cpu().numpy().view(np.uint32),
+                   data=self.data.to(torch.float64).cpu().numpy(),
+                   zero_row=self.zero_row.cpu().numpy(),
+                   group_start=self.group_start.cpu().numpy(),
+                   output_hash=self.output_hash.cpu().numpy().view(np.uint32))
+        out["add_sign"] = self.add_sign.cpu().numpy() if self._add_sign is not None else None
+        return out
+
+    # ---- kernel descriptor
+    def format_struct(self) -> L.FormatT:
+        if self._fmt is None:
+            f = L.FormatT()
+            f.rows, f.cols = self.rows, self.cols
+            f.col_width, f.row_height = self.config.col_width, self.config.row_height
+            f.warp_size = self.config.warp_size
+            f.nrb, f.ncb = self.grid_shape
+            f.nzb, f.nnz = self.nzb, self.nnz
+            f.dtype = L.dtype_code(self.data.dtype)
+            f.exact = 1
+            for name, t in (("blk_br", self.blk_br), ("blk_bc", self.blk_bc),
+                            ("slot_len", self.slot_len), ("perm", self.perm),
+                            ("group_start", self.group_start_c), ("col", self.col),
+                            ("data", self.data), ("rb_ptr", self.rb_ptr),
+                            ("rb_blk", self.rb_blk)):
+                setattr(f, name, t.data_ptr() if t.numel() else 0)
+            self._fmt = f
+        return self._fmt
+
+    def astype(self, dtype: torch.dtype) -> "HbpMatrix":
+        """Same structure with values in another precision (f64 <-> f32)."""
+        m = HbpMatrix(self.rows, self.cols, self.config, self.grid_shape, col=self.col,
+                      data=self.data.to(dtype), add_sign=self._add_sign, blk_br=self.blk_br,
+                      blk_bc=self.blk_bc, slot_len=self.slot_len, perm=self.perm,
+                      group_start_c=self.group_start_c, zero_row_c=self.zero_row_c,
+                      rb_ptr=self.rb_ptr, rb_blk=self.rb_blk, permutations=self.permutations)
+        m._views = self._views
+        return m
+
+    # ---- validation (hbp.py:102-135) on the reference-layout views
+    def validate_structure(self) -> None:
+        nrb, ncb = self.grid_shape
+        R, W = self.config.row_height, self.config.warp_size
+        if nrb != -(-self.rows // R) or ncb != -(-self.cols // self.config.col_width):
+            raise HbpFormatError("grid shape inconsistent with dimensions")
+        nnz = self.nnz
+        if not (self.col.numel() == self.data.numel()
+                and (self._add_sign is None or self._add_sign.numel() == nnz)):
+            raise HbpFormatError("element array lengths differ")
+        n_slots = ncb * self.rows
+        zr, oh, gs = self.zero_row, self.output_hash, self.group_start
+        if zr.numel() != n_slots or oh.numel() != n_slots:
+            raise HbpFormatError("slot array length mismatch")
+        n_groups = ncb * groups_per_col_block(self.rows, R, W)
+        if gs.numel() != n_groups + 1:
+            raise HbpFormatError("group_start length mismatch")
+        ends = gs[[0, -1]].cpu().tolist()
+        if ends[0] != 0 or ends[1] != nnz:
+            raise HbpFormatError("group_start must span [0, nnz]")
+        if bool((gs[1:] < gs[:-1]).any()):
+            raise HbpFormatError("group_start must be non-decreasing")
+        if self._add_sign is not None and nnz and bool(
+                ((self._add_sign < 1) & (self._add_sign != -1)).any()):
+            raise HbpFormatError("add_sign entries must be >= 1 or -1")
+        bad = torch.full((1,), L.LLONG_MAX, dtype=torch.int64, device=zr.device)
+        L.call("hbp_gather_dense_perm", L.P(oh), L.c_i64(self.rows), L.c_i64(ncb), L.c_i64(R),
+               L.P(None), L.P(None), L.c_i64(0), L.P(None), L.P(bad), L.stream())
+        b = int(bad.item())
+        if b != L.LLONG_MAX:
+            bc, br = divmod(b, nrb)
+            raise HbpFormatError(f"output_hash of block ({br}, {bc}) is not a permutation")
+        # zero_row implied by the empty-slot mask, per W-lane group
+        i = torch.arange(n_slots, device=zr.device)
+        q = (i % self.rows) % R % W
+        is_zero = (zr == -1).to(torch.int64)
+        cs = torch.cumsum(is_zero, 0)
+        g0 = i - q
+        before = cs - is_zero - (cs[g0] - is_zero[g0])
+        expected = torch.where(is_zero.bool(), torch.full_like(before, -1), before)
+        wrong = torch.nonzero(expected != zr.to(torch.int64))
+        if wrong.numel():
+            s = int(wrong[0, 0])
+            bc, r = divmod(s, self.rows)
+            raise HbpFormatError(f"zero_row of block ({r // R}, {bc}) has wrong lane counts")
+
+
+def _bad_block_message(grid_or_hbp, idx: int, dense: bool, nrb: int) -> str:
+    if dense:
+        bc, br = divmod(idx, nrb)
+    else:
+        br = int(grid_or_hbp.blk_br[idx])
+        bc = int(grid_or_hbp.blk_bc[idx])
+    return f"permutation of block ({br}, {bc}) is not a bijection"
+
+
+def build_hbp(csr: CsrMatrix, grid: BlockGrid, permutations, config: PartitionConfig | None = None,
+              *, with_add_sign: bool = True, with_zero_row: bool = True) -> HbpMatrix:
+    """hbp.py:150-238 on the GPU.
+
+    permutations: a ``BlockPermutations`` (from hash_/sort_/identity_permutations)
+    or any dense flat [ncb * rows] slot -> local-row table (numpy or tensor),
+    validated block by block like hbp.py:179-181."""
+    if config is None:
+        config = grid.config
+    elif config != grid.config:
+        raise ValueError("config disagrees with the grid's config")
+    if grid.rows != csr.rows or grid.cols != csr.cols or grid.nnz != csr.nnz:
+        raise ValueError("grid does not describe this matrix")
+    _check_gpu_geometry(config)
+    dev = L.require_cuda()
+    R, W = config.row_height, config.warp_size
+    nrb, ncb, nzb = grid.num_row_blocks, grid.num_col_blocks, grid.nzb
+    gpb = R // W
+    s = L.stream()
+    bad = torch.full((1,), L.LLONG_MAX, dtype=torch.int64, device=dev)
+
+    keep = permutations
+    if isinstance(permutations, BlockPermutations):
+        if permutations.grid is not grid:
+            permutations = np.asarray(permutations)
+        else:
+            perm = permutations.compact
+    if not isinstance(permutations, BlockPermutations):
+        dense = permutations
+        if not isinstance(dense, torch.Tensor):
+            dense = torch.as_tensor(np.ascontiguousarray(np.asarray(dense, np.uint32)).view(np.int32))
+        dense = dense.to(device=dev, dtype=torch.int32).contiguous()
+        if dense.numel() != ncb * grid.rows:
+            raise ValueError("permutation table length mismatch")
+        perm = torch.empty(nzb * R, dtype=torch.int32, device=dev)
+        L.call("hbp_gather_dense_perm", L.P(dense), L.c_i64(grid.rows), L.c_i64(ncb), L.c_i64(R),
+               L.P(grid.blk_br), L.P(grid.blk_bc), L.c_i64(nzb), L.P(perm), L.P(bad), s)
+        b = int(bad.item())
+        if b != L.LLONG_MAX:
+            raise ValueError(_bad_block_message(grid, b, True, nrb))
+        keep = dense
+
+    slot_len = torch.empty(nzb * R, dtype=torch.int32, device=dev)
+    zero_row_c = torch.empty(nzb * R, dtype=torch.int32, device=dev) if with_zero_row else None
+    group_nnz = torch.empty(nzb * gpb + 1, dtype=torch.int64, device=dev)
+    L.call("hbp_slot_lengths", L.P(grid.len_local), L.P(perm), L.P(grid.blk_br), L.c_i64(nzb),
+           L.c_i64(grid.rows), L.c_i64(R), L.c_i64(W), L.P(slot_len), L.P(zero_row_c),
+           L.P(group_nnz), L.P(bad), s)
+    b = int(bad.item())
+    if b != L.LLONG_MAX:
+        raise ValueError(_bad_block_message(grid, b, False, nrb))
+    group_start_c = L.exclusive_sum(group_nnz)
+    if int(group_start_c[-1].item()) != csr.nnz:
+        raise ValueError("emitted element count disagrees with matrix nnz")
+
+    vdt = csr.values.dtype
+    col = torch.empty(csr.nnz, dtype=torch.int32, device=dev)
+    data = torch.empty(csr.nnz, dtype=vdt, device=dev)
+    add = torch.empty(csr.nnz, dtype=torch.int32, device=dev) if with_add_sign else None
+    L.call("hbp_emit", L.P(slot_len), L.P(perm), L.P(grid.start_local), L.P(group_start_c),
+           L.P(grid.blk_br), L.c_i64(nzb), L.c_i64(grid.rows), L.c_i64(R), L.c_i64(W),
+           L.P(csr.col_idx), L.P(csr.values), L.c_int(L.dtype_code(vdt)), L.P(col), L.P(data),
+           L.P(add), s)
+
+    rb_count = torch.zeros(nrb + 1, dtype=torch.int64, device=dev)
+    L.call("hbp_row_block_counts", L.P(grid.blk_br), L.c_i64(nzb), L.P(rb_count), s)
+    rb_ptr = L.exclusive_sum(rb_count)
+    idx = torch.arange(nzb, dtype=torch.int32, device=dev)
+    _, rb_blk = L.sort_pairs_u32(grid.blk_br, idx, max(1, int(nrb - 1).bit_length()))
+    return HbpMatrix(csr.rows, csr.cols, config, (nrb, ncb), col=col, data=data, add_sign=add,
+                     blk_br=grid.blk_br, blk_bc=grid.blk_bc, slot_len=slot_len, perm=perm,
+                     group_start_c=group_start_c, zero_row_c=zero_row_c, rb_ptr=rb_ptr,
+                     rb_blk=rb_blk, permutations=keep)
+
+
+def hbp_to_triplets(hbp: HbpMatrix) -> TripletMatrix:
+    """hbp.py:241-315: invert the layout by walking every add_sign chain on
+    the GPU (over the reference-layout arrays, so corruption is detected the
+    way the reference detects it)."""
+    dev = hbp.data.device
+    nnz = hbp.nnz
+    row = torch.full((nnz,), -1, dtype=torch.int64, device=dev)
+    seen = torch.zeros(max(1, nnz), dtype=torch.int32, device=dev)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    c = hbp.config
+    L.call("hbp_walk_chains", L.c_i64(hbp.rows), L.c_i64(hbp.cols), L.c_i64(c.col_width),
+           L.c_i64(c.row_height), L.c_i64(c.warp_size), L.P(hbp.zero_row), L.P(hbp.output_hash),
+           L.P(hbp.group_start), L.P(hbp.col), L.P(hbp.add_sign), L.c_i64(nnz), L.P(row),
+           L.P(seen), L.P(err), L.stream())
+    e = int(err.item())
+    if e & 1:
+        raise HbpFormatError("lane start offset outside its group region")
+    if e & 2:
+        raise HbpFormatError("element column outside its block's range")
+    if e & 4:
+        raise HbpFormatError("invalid add_sign stride")
+    if e & 8:
+        raise HbpFormatError("stride chain escapes its group region")
+    if nnz:
+        if int(seen.max().item()) > 1:
+            raise HbpFormatError("element visited more than once")
+        if int(seen[:nnz].sum().item()) != nnz:
+            raise HbpFormatError("stride chains do not cover every element")
+    return TripletMatrix(hbp.rows, hbp.cols, row, hbp.col.to(torch.int64) & 0xFFFFFFFF,
+                         hbp.data.clone())
+
+
+# ------------------------------------------------------------ .hbp codec
+_ARRAY_SPECS = (("group_start", "<u8"), ("col", "<u4"), ("data", "<f8"), ("add_sign", "<i4"),
+                ("zero_row", "<i4"), ("output_hash", "<u4"))
+
+
+def serialize_hbp(hbp: HbpMatrix, stream) -> None:
+    """hbp.py:328-339: the .hbp binary layout (little-endian, length-prefixed)."""
+    ref = hbp.to_reference()
+    stream.write(MAGIC)
+    stream.write(struct.pack("<I", VERSION))
+    stream.write(struct.pack("<8Q", hbp.rows, hbp.cols, hbp.nnz, hbp.config.col_width,
+                             hbp.config.row_height, hbp.config.warp_size, hbp.num_row_blocks,
+                             hbp.num_col_blocks))
+    for name, dt in _ARRAY_SPECS:
+        arr = np.ascontiguousarray(ref[name], dtype=dt)
+        stream.write(struct.pack("<Q", arr.size))
+        stream.write(arr.tobytes())
+
+
+def _read_exact(stream, n: int) -> bytes:
+    buf = stream.read(n)
+    if len(buf) != n:
+        raise HbpFormatError(f"truncated stream: wanted {n} bytes, got {len(buf)}")
+    return buf
+
+
+def deserialize_hbp(stream) -> HbpMatrix:
+    """hbp.py:349-381: read a .hbp stream into a device HbpMatrix (compact
+    arrays rebuilt from the dense ones), validating structure."""
+    if _read_exact(stream, 4) != MAGIC:
+        raise HbpFormatError("bad magic; not an .hbp stream")
+    (version,) = struct.unpack("<I", _read_exact(stream, 4))
+    if version != VERSION:
+        raise HbpFormatError(f"unsupported version {version}")
+    rows, cols, nnz, C, R, W, nrb, ncb = struct.unpack("<8Q", _read_exact(stream, 64))
+    arrays = {}
+    for name, dt in _ARRAY_SPECS:
+        (count,) = struct.unpack("<Q", _read_exact(stream, 8))
+        arrays[name] = np.frombuffer(_read_exact(stream, count * np.dtype(dt).itemsize), dtype=dt)
+    try:
+        config = PartitionConfig(col_width=C, row_height=R, warp_size=W)
+    except ValueError as exc:
+        raise HbpFormatError(f"invalid partition config in header: {exc}") from exc
+    if arrays["data"].size != nnz:
+        raise HbpFormatError("element array length disagrees with header nnz")
+    hbp = from_reference(int(rows), int(cols), config, (int(nrb), int(ncb)), **arrays)
+    hbp.validate_structure()
+    return hbp
+
+
+def from_reference(rows, cols, config: PartitionConfig, grid_shape, *, col, data, add_sign,
+                   zero_row, group_start, output_hash, dtype=torch.float64) -> HbpMatrix:
+    """Build the device HbpMatrix from the reference's six dense arrays."""
+    _check_gpu_geometry(config)
+    dev = L.require_cuda()
+    R, W = config.row_height, config.warp_size
+    nrb, ncb = grid_shape
+    gpb = R // W
+    gpc = groups_per_col_block(rows, R, W)
+    gs = np.asarray(group_start, np.int64)
+    # nonzero blocks: their group range spans at least one element
+    bc_i, br_i = np.meshgrid(np.arange(ncb), np.arange(nrb), indexing="ij")
+    bc_i, br_i = bc_i.ravel(), br_i.ravel()
+    first = bc_i * gpc + br_i * gpb
+    ng = np.minimum(R, rows - br_i * R)
+    ng = -(-ng // W)
+    nnz_b = gs[np.minimum(first + ng, gs.size - 1)] - gs[np.minimum(first, gs.size - 1)]
+    nzmask = nnz_b > 0
+    blk_bc = bc_i[nzmask].astype(np.int32)
+    blk_br = br_i[nzmask].astype(np.int32)
+    nzb = blk_br.size
+    oh = np.asarray(output_hash, np.uint32)
+    zr = np.asarray(zero_row, np.int32)
+    perm = np.zeros((nzb, R), np.uint32)
+    zrc = np.full((nzb, R), -1, np.int32)
+    slot_len = np.zeros((nzb, R), np.int64)
+    gsc = np.zeros(nzb * gpb + 1, np.int64)
+    gsc[-1] = gs[-1] if gs.size else 0
+    for i in range(nzb):
+        br, bc = int(blk_br[i]), int(blk_bc[i])
+        n = min(R, rows - br * R)
+        base = bc * rows + br * R
+        perm[i, :n] = oh[base:base + n]
+        zrc[i, :n] = zr[base:base + n]
+        g0 = bc * gpc + br * gpb
+        ngi = -(-n // W)
+        gsc[i * gpb:i * gpb + ngi] = gs[g0:g0 + ngi]
+        gsc[i * gpb + ngi:(i + 1) * gpb] = gs[g0 + ngi]
+        # slot lengths from the add_sign chains
+        add = np.asarray(add_sign)
+        for g in range(ngi):
+            a0, a1 = gs[g0 + g], gs[g0 + g + 1]
+            for q in range(min(W, n - g * W)):
+                z = int(zrc[i, g * W + q])
+                if z < 0:
+                    continue
+                j, k = a0 + q - z, 0
+                while True:
+                    k += 1
+                    st = int(add[j]) if 0 <= j < add.size else -1
+                    if st < 0 or j + st >= a1:
+                        break
+                    j += st
+                slot_len[i, g * W + q] = k
+    t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a), device=dev).to(dt)  # noqa: E731
+    rb_count = np.bincount(blk_br, minlength=nrb + 1).astype(np.int64)
+    rb_ptr = np.concatenate(([0], np.cumsum(rb_count)[:-1]))
+    rb_blk = np.argsort(blk_br, kind="stable").astype(np.int32)
+    return HbpMatrix(rows, cols, config, grid_shape,
+                     col=t(np.asarray(col, np.uint32).view(np.int32), torch.int32),
+                     data=t(np.asarray(data, np.float64), dtype),
+                     add_sign=t(np.asarray(add_sign, np.int32), torch.int32),
+                     blk_br=t(blk_br, torch.int32), blk_bc=t(blk_bc, torch.int32),
+                     slot_len=t(slot_len.astype(np.int32).ravel(), torch.int32),
+                     perm=t(perm.view(np.int32).ravel(), torch.int32),
+                     group_start_c=t(gsc, torch.int64), zero_row_c=t(zrc.ravel(), torch.int32),
+                     rb_ptr=t(rb_ptr, torch.int64), rb_blk=t(rb_blk, torch.int32),
+                     permutations=t(oh.view(np.int32), torch.int32))
+
+
+def save_hbp(hbp: HbpMatrix, path) -> None:
+    with open(path, "wb") as fh:
+        serialize_hbp(hbp, fh)
+
+
+def load_hbp(path) -> HbpMatrix:
+    with open(path, "rb") as fh:
+        return deserialize_hbp(fh)
+
+
+def serialize_bytes(hbp: HbpMatrix) -> bytes:
+    buf = io.BytesIO()
+    serialize_hbp(hbp, buf)
+    return buf.getvalue()
