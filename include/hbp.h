@@ -230,6 +230,26 @@ typedef struct {
  * or -- when y_direct != NULL and ncb == 1 -- y directly. */
 int hbp_spmv_blocks(const hbp_format_t *f, const hbp_schedule_t *sched, const void *x,
                     double *partial, void *y_direct, hbp_stream_t stream);
+/* Element-balanced SpMV (B200 schedule for warp_size == 32): the element
+ * array is cut into `workers` equal ranges, one per persistent warp.  Exact
+ * mode (f64 or fmt->exact) rounds cuts to group boundaries -- every row is
+ * summed in reference order by one lane; otherwise cuts fall on step
+ * boundaries and split groups are combined by the last-arriving warp from
+ * per-warp partials (deterministic, f64 accumulation).  Scratch (fast mode):
+ * part_head/part_tail f64[workers*32], cut_end i64[workers], counters
+ * u32[nzb*gpb] zero-filled once (the kernel leaves them zeroed). */
+typedef struct {
+    int64_t workers;
+    double *part_head;
+    double *part_tail;
+    int64_t *cut_end;
+    uint32_t *counters;
+} hbp_balanced_t;
+
+int hbp_balanced_workers(const hbp_format_t *f, int64_t *workers);
+int hbp_spmv_balanced(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y,
+                      double *partial, hbp_stream_t stream);
+
 /* engine.py:196-201 combine over nonzero blocks only, ascending bc
  * (bitwise equal to the dense combine); rows of row blocks with
  * no nonzero block get +0.0. */

@@ -49,6 +49,12 @@ class ScheduleT(ctypes.Structure):
     ]
 
 
+class BalancedT(ctypes.Structure):
+    """Mirror of hbp_balanced_t."""
+    _fields_ = [("workers", c_i64), ("part_head", c_vp), ("part_tail", c_vp),
+                ("cut_end", c_vp), ("counters", c_vp)]
+
+
 # name -> argtypes (all return int status)
 _SIGS = {
     "hbp_abi_version": [],
@@ -86,6 +92,9 @@ _SIGS = {
                         c_vp, c_vp, c_vp, c_vp],
     "hbp_spmv_blocks": [ctypes.POINTER(FormatT), ctypes.POINTER(ScheduleT), c_vp, c_vp, c_vp,
                         c_vp],
+    "hbp_balanced_workers": [ctypes.POINTER(FormatT), ctypes.POINTER(c_i64)],
+    "hbp_spmv_balanced": [ctypes.POINTER(FormatT), ctypes.POINTER(BalancedT), c_vp, c_vp, c_vp,
+                          c_vp],
     "hbp_combine": [ctypes.POINTER(FormatT), c_vp, c_vp, c_vp],
     "hbp_zero_empty_rows": [ctypes.POINTER(FormatT), c_vp, c_vp],
     "hbp_expand_partial": [ctypes.POINTER(FormatT), c_vp, c_vp, c_vp],

@@ -272,10 +272,10 @@ int hbp_spmv_blocks(const hbp_format_t *f, const hbp_schedule_t *s, const void *
     if (f->warp_size < 1 || f->warp_size > 32 || f->row_height % f->warp_size)
         return HBP_E_UNSUPPORTED;
     if (y_direct && f->ncb != 1) return HBP_E_ARG;
-    if (!y_direct && !partial) return HBP_E_ARG;
     cudaStream_t st = as_stream(stream);
     HBP_CUDA_TRY(cudaMemsetAsync(s->ticket, 0, sizeof(uint32_t), st));
     if (f->nzb == 0) return HBP_OK;
+    if (!y_direct && !partial) return HBP_E_ARG;
     if (f->dtype == HBP_F64) dispatch_spmv<double, true>(f, s, x, partial, y_direct, st);
     else if (f->dtype == HBP_F32) dispatch_spmv<float, false>(f, s, x, partial, y_direct, st);
     else return HBP_E_ARG;

@@ -138,16 +138,46 @@ def _as_x(hbp: HbpMatrix, x) -> torch.Tensor:
 class SpmvOperator:
     """Preallocated y = A x for one HbpMatrix (the bench / serving hot path).
 
-    direct mode (one column block): the block kernel writes y itself;
-    otherwise the partial (f64, compact) is combined in ascending bc."""
+    schedule="balanced" (default when warp_size == 32): the element array is
+    cut into equal ranges, one per persistent warp (hbp_spmv_balanced; exact
+    reference order for f64, step-aligned cuts + deterministic last-arriver
+    combine for f32).  schedule="plan": the reference's fixed + competitive
+    block schedule (hbp_spmv_blocks) with this fixed_fraction.
+    direct mode (one column block): the kernel writes y itself; otherwise the
+    partial (f64, compact) is combined in ascending bc."""
 
     def __init__(self, hbp: HbpMatrix, workers: int | None = None,
-                 fixed_fraction: float | None = None):
+                 fixed_fraction: float | None = None, schedule: str | None = None):
         self.hbp = hbp
         dev = hbp.data.device
-        self.workers = workers or default_workers(hbp.dtype, hbp.config.warp_size)
-        f = hbp.config.fixed_fraction if fixed_fraction is None else fixed_fraction
-        self.fixed_count = int(f * hbp.nzb + 0.5)
+        if schedule is None:
+            schedule = "balanced" if hbp.config.warp_size == 32 else "plan"
+        if schedule == "balanced" and hbp.config.warp_size != 32:
+            raise ValueError("the balanced schedule needs warp_size == 32")
+        self.schedule = schedule
+        f = hbp.format_struct()
+        if schedule == "balanced":
+            if workers is None:
+                w = L.c_i64(0)
+                L.call("hbp_balanced_workers", ctypes.byref(f), ctypes.byref(w))
+                workers = int(w.value)
+            self.workers = max(1, workers)
+            self.bal = L.BalancedT()
+            self.bal.workers = self.workers
+            self._scratch = []
+            if not f.exact:
+                ph = torch.empty(self.workers * 32, dtype=torch.float64, device=dev)
+                pt = torch.empty(self.workers * 32, dtype=torch.float64, device=dev)
+                ce = torch.empty(self.workers, dtype=torch.int64, device=dev)
+                cn = torch.zeros(max(1, hbp.nzb * (hbp.config.row_height // 32)),
+                                 dtype=torch.int32, device=dev)
+                self._scratch = [ph, pt, ce, cn]
+                self.bal.part_head, self.bal.part_tail = ph.data_ptr(), pt.data_ptr()
+                self.bal.cut_end, self.bal.counters = ce.data_ptr(), cn.data_ptr()
+        else:
+            self.workers = workers or default_workers(hbp.dtype, hbp.config.warp_size)
+        fr = hbp.config.fixed_fraction if fixed_fraction is None else fixed_fraction
+        self.fixed_count = int(fr * hbp.nzb + 0.5)
         self.ticket = torch.zeros(1, dtype=torch.int32, device=dev)
         self.direct = hbp.num_col_blocks == 1
         R = hbp.config.row_height
@@ -162,6 +192,14 @@ class SpmvOperator:
         self._graph = None
         self._gx = self._gy = None
 
+    def _blocks(self, f, x, partial, y, s):
+        if self.schedule == "balanced":
+            L.call("hbp_spmv_balanced", ctypes.byref(f), ctypes.byref(self.bal), L.P(x), L.P(y),
+                   L.P(partial), s)
+        else:
+            L.call("hbp_spmv_blocks", ctypes.byref(f), ctypes.byref(self.sched), L.P(x),
+                   L.P(partial), L.P(y), s)
+
     def __call__(self, x: torch.Tensor, y: torch.Tensor | None = None) -> torch.Tensor:
         hbp = self.hbp
         if y is None:
@@ -169,13 +207,11 @@ class SpmvOperator:
         f = hbp.format_struct()
         s = L.stream()
         if self.direct:
-            L.call("hbp_spmv_blocks", ctypes.byref(f), ctypes.byref(self.sched), L.P(x),
-                   L.P(None), L.P(y), s)
+            self._blocks(f, x, None, y, s)
             if self.has_empty_row_blocks:
                 L.call("hbp_zero_empty_rows", ctypes.byref(f), L.P(y), s)
         else:
-            L.call("hbp_spmv_blocks", ctypes.byref(f), ctypes.byref(self.sched), L.P(x),
-                   L.P(self.partial), L.P(None), s)
+            self._blocks(f, x, self.partial, None, s)
             L.call("hbp_combine", ctypes.byref(f), L.P(self.partial), L.P(y), s)
         return y
 

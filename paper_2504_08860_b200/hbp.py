@@ -179,7 +179,7 @@ class HbpMatrix:
             f.nrb, f.ncb = self.grid_shape
             f.nzb, f.nnz = self.nzb, self.nnz
             f.dtype = L.dtype_code(self.data.dtype)
-            f.exact = 1
+            f.exact = 1 if self.data.dtype == torch.float64 else 0
             for name, t in (("blk_br", self.blk_br), ("blk_bc", self.blk_bc),
                             ("slot_len", self.slot_len), ("perm", self.perm),
                             ("group_start", self.group_start_c), ("col", self.col),

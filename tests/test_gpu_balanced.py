@@ -1,0 +1,111 @@
+"""The element-balanced B200 schedule (hbp_spmv_balanced) vs the oracle.
+
+f64: cuts on group boundaries -> bitwise equal to the reference for any
+worker count.  f32: step-aligned cuts + last-arriver combine -> within 1e-5
+componentwise of the reference (fp64 on the fp32-rounded inputs), and
+deterministic run to run.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import golden_names, has_gpu, load_golden
+
+pytestmark = pytest.mark.gpu
+
+if has_gpu():
+    import torch
+    import paper_2504_08860_b200 as H
+    from oracle import oracle as O
+
+W32 = [n for n in golden_names() if load_golden(n)["W"] == 32]
+
+
+def _hbp(rows, cols, r, c, v, C, R=512, W=32, seed=0):
+    cfg = H.PartitionConfig(col_width=C, row_height=R, warp_size=W)
+    csr = H.coo_to_csr(H.TripletMatrix(rows, cols, r, c, v))
+    grid = H.make_grid(csr, cfg)
+    params = H.sample_hash_params(grid, cfg, seed=seed)
+    return H.build_hbp(csr, grid, H.hash_permutations(grid, params))
+
+
+@pytest.mark.parametrize("name", W32)
+@pytest.mark.parametrize("workers", [1, 3, 17, 200, None])
+def test_balanced_matches_golden(name, workers):
+    g = load_golden(name)
+    val = g["trip_val"].astype(np.float32) if g["fp32"] else g["trip_val"]
+    hbp = _hbp(g["rows"], g["cols"], g["trip_row"], g["trip_col"], val, g["C"], g["R"], g["W"],
+               g["seed"])
+    x = g["x"].astype(np.float32) if g["fp32"] else g["x"]
+    op = H.SpmvOperator(hbp, workers=workers, schedule="balanced")
+    y = op(torch.as_tensor(x, device="cuda")).cpu().numpy()
+    if g["fp32"]:
+        err = O.componentwise_error(g["rows"], g["trip_row"], g["trip_col"], g["trip_val"],
+                                    g["x"], y.astype(np.float64))
+        assert err <= 1e-5
+    else:
+        np.testing.assert_array_equal(y, g["y"])
+
+
+def _hot_matrix(seed=3, rows=4096, cols=50000):
+    """Rows of wildly different lengths: a few 20k-40k-element rows among
+    short ones, so groups split across many warps."""
+    rng = np.random.default_rng(seed)
+    lens = rng.poisson(6, rows)
+    hot = rng.choice(rows, 12, replace=False)
+    lens[hot] = rng.integers(20000, 40000, hot.size)
+    lens[rows // 2: rows // 2 + 40] = 900  # one long, fully live group
+    r = np.repeat(np.arange(rows), lens)
+    c = np.concatenate([rng.choice(cols, k, replace=False) for k in lens])
+    v = rng.uniform(-1, 1, r.size)
+    return rows, cols, r, c, v
+
+
+@pytest.mark.parametrize("workers", [2, 9, 64, 333, 1500, None])
+def test_balanced_f32_hot_rows(workers):
+    rows, cols, r, c, v = _hot_matrix()
+    v32 = v.astype(np.float32)
+    x = np.random.default_rng(1).uniform(-1, 1, cols).astype(np.float32)
+    hbp = _hbp(rows, cols, r, c, v32, C=cols)
+    op = H.SpmvOperator(hbp, workers=workers)
+    xd = torch.as_tensor(x, device="cuda")
+    y1 = op(xd).cpu().numpy()
+    y2 = op(xd).cpu().numpy()
+    np.testing.assert_array_equal(y1, y2)  # deterministic (counters self-reset)
+    err = O.componentwise_error(rows, r, c, v32.astype(np.float64), x.astype(np.float64),
+                                y1.astype(np.float64))
+    assert err <= 1e-5
+
+
+@pytest.mark.parametrize("workers", [2, 9, 333, None])
+def test_balanced_f64_hot_rows_bitwise(workers):
+    rows, cols, r, c, v = _hot_matrix(seed=4)
+    x = np.random.default_rng(2).uniform(-1, 1, cols)
+    hbp = _hbp(rows, cols, r, c, v, C=cols)
+    y = H.SpmvOperator(hbp, workers=workers)(torch.as_tensor(x, device="cuda")).cpu().numpy()
+    p = O.pipeline(rows, cols, r, c, v, cols, 512, 32)
+    np.testing.assert_array_equal(y, O.hbp_spmv(p["hbp"], x, workers=4))
+
+
+def test_balanced_multi_column_blocks_f32():
+    rows, cols, r, c, v = _hot_matrix(seed=5, rows=3000, cols=60000)
+    v32 = v.astype(np.float32)
+    x = np.random.default_rng(3).uniform(-1, 1, cols).astype(np.float32)
+    hbp = _hbp(rows, cols, r, c, v32, C=4096)
+    assert hbp.num_col_blocks > 1
+    for workers in (5, 100, None):
+        y = H.SpmvOperator(hbp, workers=workers)(torch.as_tensor(x, device="cuda"))
+        err = O.componentwise_error(rows, r, c, v32.astype(np.float64), x.astype(np.float64),
+                                    y.cpu().numpy().astype(np.float64))
+        assert err <= 1e-5
+
+
+def test_plan_schedule_still_available():
+    rows, cols, r, c, v = _hot_matrix(seed=6, rows=1024, cols=5000)
+    x = np.random.default_rng(4).uniform(-1, 1, cols)
+    hbp = _hbp(rows, cols, r, c, v, C=cols)
+    xd = torch.as_tensor(x, device="cuda")
+    a = H.SpmvOperator(hbp, schedule="plan")(xd).cpu().numpy()
+    b = H.SpmvOperator(hbp, schedule="balanced")(xd).cpu().numpy()
+    np.testing.assert_array_equal(a, b)
