@@ -250,7 +250,7 @@ def run_gpu(args):
                    build=(t4 - t3) * 1e3, total=(t4 - t0) * 1e3)
         if rep == 0:
             del hbp, perms, grid
-    op = H.SpmvOperator(hbp)
+    op = H.SpmvOperator(hbp, schedule=args.schedule)
     x_host = np.random.default_rng(0).uniform(-1.0, 1.0, cols)  # cli.py:170-171
     x = torch.as_tensor(x_host, device=dev).to(vdt)
     y = torch.empty(rows, dtype=vdt, device=dev)
@@ -360,6 +360,7 @@ def run_gpu(args):
         "config": {"workload": f"{args.config}: {desc}", "rows": rows, "cols": cols, "nnz": nnz,
                    "nonzero_blocks": hbp.nzb, "col_width": C, "row_height": 512,
                    "warp_size": 32, "fixed_fraction": 0.7, "workers": op.workers,
+                   "schedule": op.schedule,
                    "hash_params": [params.a, params.b, params.c, params.d],
                    "parallelism": f"row stripes x{world} (weak)",
                    "l2": "inputs larger than L2 (no flush); x reused from L2 by design"},
@@ -414,6 +415,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--schedule", default=None, choices=[None, "stream", "balanced", "plan"])
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     out = run_reference(args) if args.impl == "reference" else run_gpu(args)

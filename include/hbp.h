@@ -247,6 +247,15 @@ typedef struct {
 } hbp_balanced_t;
 
 int hbp_balanced_workers(const hbp_format_t *f, int64_t *workers);
+/* Same slices and combine rule, but each warp streams its slice's col/data
+ * through shared memory with cp.async.bulk (TMA bulk copies, two chunks in
+ * flight), gathers x for a whole chunk at once and sums rows from shared
+ * memory via the group's phase table (hbp_spmv_stream.cu).  Slices are cut
+ * at arbitrary element offsets in fast mode (no cut_end needed).  col and
+ * data must be readable 16 bytes past nnz (the builder pads them). */
+int hbp_stream_workers(const hbp_format_t *f, int64_t *workers);
+int hbp_spmv_stream(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y,
+                    double *partial, hbp_stream_t stream);
 int hbp_spmv_balanced(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y,
                       double *partial, hbp_stream_t stream);
 

@@ -95,6 +95,9 @@ _SIGS = {
     "hbp_balanced_workers": [ctypes.POINTER(FormatT), ctypes.POINTER(c_i64)],
     "hbp_spmv_balanced": [ctypes.POINTER(FormatT), ctypes.POINTER(BalancedT), c_vp, c_vp, c_vp,
                           c_vp],
+    "hbp_stream_workers": [ctypes.POINTER(FormatT), ctypes.POINTER(c_i64)],
+    "hbp_spmv_stream": [ctypes.POINTER(FormatT), ctypes.POINTER(BalancedT), c_vp, c_vp, c_vp,
+                        c_vp],
     "hbp_combine": [ctypes.POINTER(FormatT), c_vp, c_vp, c_vp],
     "hbp_zero_empty_rows": [ctypes.POINTER(FormatT), c_vp, c_vp],
     "hbp_expand_partial": [ctypes.POINTER(FormatT), c_vp, c_vp, c_vp],

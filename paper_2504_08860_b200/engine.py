@@ -138,10 +138,12 @@ def _as_x(hbp: HbpMatrix, x) -> torch.Tensor:
 class SpmvOperator:
     """Preallocated y = A x for one HbpMatrix (the bench / serving hot path).
 
-    schedule="balanced" (default when warp_size == 32): the element array is
-    cut into equal ranges, one per persistent warp (hbp_spmv_balanced; exact
-    reference order for f64, step-aligned cuts + deterministic last-arriver
-    combine for f32).  schedule="plan": the reference's fixed + competitive
+    schedule="stream" (default when warp_size == 32): the element array is
+    cut into equal slices, one per persistent warp, streamed through shared
+    memory with TMA bulk copies (hbp_spmv_stream; exact reference order for
+    f64, deterministic last-arriver combine of cut groups for f32).
+    schedule="balanced": the same slices walked from global memory
+    (hbp_spmv_balanced, step-aligned cuts).  schedule="plan": the reference's fixed + competitive
     block schedule (hbp_spmv_blocks) with this fixed_fraction.
     direct mode (one column block): the kernel writes y itself; otherwise the
     partial (f64, compact) is combined in ascending bc."""
@@ -151,15 +153,15 @@ class SpmvOperator:
         self.hbp = hbp
         dev = hbp.data.device
         if schedule is None:
-            schedule = "balanced" if hbp.config.warp_size == 32 else "plan"
-        if schedule == "balanced" and hbp.config.warp_size != 32:
-            raise ValueError("the balanced schedule needs warp_size == 32")
+            schedule = "stream" if hbp.config.warp_size == 32 else "plan"
+        if schedule in ("balanced", "stream") and hbp.config.warp_size != 32:
+            raise ValueError(f"the {schedule} schedule needs warp_size == 32")
         self.schedule = schedule
         f = hbp.format_struct()
-        if schedule == "balanced":
+        if schedule in ("balanced", "stream"):
             if workers is None:
                 w = L.c_i64(0)
-                L.call("hbp_balanced_workers", ctypes.byref(f), ctypes.byref(w))
+                L.call(f"hbp_{schedule}_workers", ctypes.byref(f), ctypes.byref(w))
                 workers = int(w.value)
             self.workers = max(1, workers)
             self.bal = L.BalancedT()
@@ -193,8 +195,8 @@ class SpmvOperator:
         self._gx = self._gy = None
 
     def _blocks(self, f, x, partial, y, s):
-        if self.schedule == "balanced":
-            L.call("hbp_spmv_balanced", ctypes.byref(f), ctypes.byref(self.bal), L.P(x), L.P(y),
+        if self.schedule in ("balanced", "stream"):
+            L.call(f"hbp_spmv_{self.schedule}", ctypes.byref(f), ctypes.byref(self.bal), L.P(x), L.P(y),
                    L.P(partial), s)
         else:
             L.call("hbp_spmv_blocks", ctypes.byref(f), ctypes.byref(self.sched), L.P(x),

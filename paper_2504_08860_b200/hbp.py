@@ -37,6 +37,14 @@ MAGIC = b"HBP1"
 VERSION = 1
 
 
+def _padded(t: torch.Tensor, pad: int = 16) -> torch.Tensor:
+    """Copy of a 1-D tensor whose storage extends `pad` elements past its end
+    (the streaming kernel's 16-byte bulk copies may read past the last element)."""
+    out = torch.zeros(t.numel() + pad, dtype=t.dtype, device=t.device)
+    out[:t.numel()] = t
+    return out[:t.numel()]
+
+
 class HbpFormatError(ValueError):
     """hbp.py:47-48: malformed .hbp streams or structurally invalid matrices."""
 
@@ -192,7 +200,7 @@ class HbpMatrix:
     def astype(self, dtype: torch.dtype) -> "HbpMatrix":
         """Same structure with values in another precision (f64 <-> f32)."""
         m = HbpMatrix(self.rows, self.cols, self.config, self.grid_shape, col=self.col,
-                      data=self.data.to(dtype), add_sign=self._add_sign, blk_br=self.blk_br,
+                      data=_padded(self.data.to(dtype)), add_sign=self._add_sign, blk_br=self.blk_br,
                       blk_bc=self.blk_bc, slot_len=self.slot_len, perm=self.perm,
                       group_start_c=self.group_start_c, zero_row_c=self.zero_row_c,
                       rb_ptr=self.rb_ptr, rb_blk=self.rb_blk, permutations=self.permutations)
@@ -311,8 +319,10 @@ def build_hbp(csr: CsrMatrix, grid: BlockGrid, permutations, config: PartitionCo
         raise ValueError("emitted element count disagrees with matrix nnz")
 
     vdt = csr.values.dtype
-    col = torch.empty(csr.nnz, dtype=torch.int32, device=dev)
-    data = torch.empty(csr.nnz, dtype=vdt, device=dev)
+    # padded by 16 elements: the streaming kernel's bulk copies may read up
+    # to 15 bytes past the last element
+    col = torch.zeros(csr.nnz + 16, dtype=torch.int32, device=dev)[:csr.nnz]
+    data = torch.zeros(csr.nnz + 16, dtype=vdt, device=dev)[:csr.nnz]
     add = torch.empty(csr.nnz, dtype=torch.int32, device=dev) if with_add_sign else None
     L.call("hbp_emit", L.P(slot_len), L.P(perm), L.P(grid.start_local), L.P(group_start_c),
            L.P(grid.blk_br), L.c_i64(nzb), L.c_i64(grid.rows), L.c_i64(R), L.c_i64(W),
@@ -471,8 +481,8 @@ def from_reference(rows, cols, config: PartitionConfig, grid_shape, *, col, data
     rb_ptr = np.concatenate(([0], np.cumsum(rb_count)[:-1]))
     rb_blk = np.argsort(blk_br, kind="stable").astype(np.int32)
     return HbpMatrix(rows, cols, config, grid_shape,
-                     col=t(np.asarray(col, np.uint32).view(np.int32), torch.int32),
-                     data=t(np.asarray(data, np.float64), dtype),
+                     col=_padded(t(np.asarray(col, np.uint32).view(np.int32), torch.int32)),
+                     data=_padded(t(np.asarray(data, np.float64), dtype)),
                      add_sign=t(np.asarray(add_sign, np.int32), torch.int32),
                      blk_br=t(blk_br, torch.int32), blk_bc=t(blk_bc, torch.int32),
                      slot_len=t(slot_len.astype(np.int32).ravel(), torch.int32),

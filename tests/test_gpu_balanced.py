@@ -32,13 +32,14 @@ def _hbp(rows, cols, r, c, v, C, R=512, W=32, seed=0):
 
 @pytest.mark.parametrize("name", W32)
 @pytest.mark.parametrize("workers", [1, 3, 17, 200, None])
-def test_balanced_matches_golden(name, workers):
+@pytest.mark.parametrize("schedule", ["balanced", "stream"])
+def test_balanced_matches_golden(name, workers, schedule):
     g = load_golden(name)
     val = g["trip_val"].astype(np.float32) if g["fp32"] else g["trip_val"]
     hbp = _hbp(g["rows"], g["cols"], g["trip_row"], g["trip_col"], val, g["C"], g["R"], g["W"],
                g["seed"])
     x = g["x"].astype(np.float32) if g["fp32"] else g["x"]
-    op = H.SpmvOperator(hbp, workers=workers, schedule="balanced")
+    op = H.SpmvOperator(hbp, workers=workers, schedule=schedule)
     y = op(torch.as_tensor(x, device="cuda")).cpu().numpy()
     if g["fp32"]:
         err = O.componentwise_error(g["rows"], g["trip_row"], g["trip_col"], g["trip_val"],
@@ -54,7 +55,7 @@ def _hot_matrix(seed=3, rows=4096, cols=50000):
     rng = np.random.default_rng(seed)
     lens = rng.poisson(6, rows)
     hot = rng.choice(rows, 12, replace=False)
-    lens[hot] = rng.integers(20000, 40000, hot.size)
+    lens[hot] = rng.integers(min(20000, cols // 2), min(40000, cols), hot.size)
     lens[rows // 2: rows // 2 + 40] = 900  # one long, fully live group
     r = np.repeat(np.arange(rows), lens)
     c = np.concatenate([rng.choice(cols, k, replace=False) for k in lens])
@@ -63,12 +64,13 @@ def _hot_matrix(seed=3, rows=4096, cols=50000):
 
 
 @pytest.mark.parametrize("workers", [2, 9, 64, 333, 1500, None])
-def test_balanced_f32_hot_rows(workers):
+@pytest.mark.parametrize("schedule", ["balanced", "stream"])
+def test_balanced_f32_hot_rows(workers, schedule):
     rows, cols, r, c, v = _hot_matrix()
     v32 = v.astype(np.float32)
     x = np.random.default_rng(1).uniform(-1, 1, cols).astype(np.float32)
     hbp = _hbp(rows, cols, r, c, v32, C=cols)
-    op = H.SpmvOperator(hbp, workers=workers)
+    op = H.SpmvOperator(hbp, workers=workers, schedule=schedule)
     xd = torch.as_tensor(x, device="cuda")
     y1 = op(xd).cpu().numpy()
     y2 = op(xd).cpu().numpy()
@@ -79,11 +81,13 @@ def test_balanced_f32_hot_rows(workers):
 
 
 @pytest.mark.parametrize("workers", [2, 9, 333, None])
-def test_balanced_f64_hot_rows_bitwise(workers):
+@pytest.mark.parametrize("schedule", ["balanced", "stream"])
+def test_balanced_f64_hot_rows_bitwise(workers, schedule):
     rows, cols, r, c, v = _hot_matrix(seed=4)
     x = np.random.default_rng(2).uniform(-1, 1, cols)
     hbp = _hbp(rows, cols, r, c, v, C=cols)
-    y = H.SpmvOperator(hbp, workers=workers)(torch.as_tensor(x, device="cuda")).cpu().numpy()
+    y = H.SpmvOperator(hbp, workers=workers, schedule=schedule)(
+        torch.as_tensor(x, device="cuda")).cpu().numpy()
     p = O.pipeline(rows, cols, r, c, v, cols, 512, 32)
     np.testing.assert_array_equal(y, O.hbp_spmv(p["hbp"], x, workers=4))
 
@@ -94,8 +98,10 @@ def test_balanced_multi_column_blocks_f32():
     x = np.random.default_rng(3).uniform(-1, 1, cols).astype(np.float32)
     hbp = _hbp(rows, cols, r, c, v32, C=4096)
     assert hbp.num_col_blocks > 1
-    for workers in (5, 100, None):
-        y = H.SpmvOperator(hbp, workers=workers)(torch.as_tensor(x, device="cuda"))
+    for workers, schedule in ((5, "balanced"), (100, "balanced"), (None, "balanced"),
+                              (5, "stream"), (100, "stream"), (None, "stream")):
+        y = H.SpmvOperator(hbp, workers=workers, schedule=schedule)(
+            torch.as_tensor(x, device="cuda"))
         err = O.componentwise_error(rows, r, c, v32.astype(np.float64), x.astype(np.float64),
                                     y.cpu().numpy().astype(np.float64))
         assert err <= 1e-5
@@ -108,4 +114,6 @@ def test_plan_schedule_still_available():
     xd = torch.as_tensor(x, device="cuda")
     a = H.SpmvOperator(hbp, schedule="plan")(xd).cpu().numpy()
     b = H.SpmvOperator(hbp, schedule="balanced")(xd).cpu().numpy()
+    c = H.SpmvOperator(hbp, schedule="stream")(xd).cpu().numpy()
     np.testing.assert_array_equal(a, b)
+    np.testing.assert_array_equal(a, c)
