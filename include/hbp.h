@@ -74,6 +74,12 @@ int hbp_sort_pairs_u64(const uint64_t *keys_in, uint64_t *keys_out, const uint64
                        uint64_t *vals_out, int64_t n, int end_bit, void *temp,
                        size_t *temp_bytes, hbp_stream_t stream);
 
+/* L2 residency of the gathered x vector (B200: 126 MB L2): persisting
+ * set-aside plus an access-policy window on `stream`. */
+int hbp_l2_persist(const void *base, size_t bytes, float hit_ratio, hbp_stream_t stream);
+int hbp_l2_persist_reset(hbp_stream_t stream);
+int hbp_l2_info(int *l2_bytes, int *max_persist, int *max_window);
+
 /* ------------------------------------------------------- formats (COO/CSR) */
 /* formats.py:243-258 coo_to_csr, after the caller sorted keys = row*cols+col
  * (stable, values carried by the original index `order`):

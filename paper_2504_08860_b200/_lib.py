@@ -98,6 +98,9 @@ _SIGS = {
     "hbp_stream_workers": [ctypes.POINTER(FormatT), ctypes.POINTER(c_i64)],
     "hbp_spmv_stream": [ctypes.POINTER(FormatT), ctypes.POINTER(BalancedT), c_vp, c_vp, c_vp,
                         c_vp],
+    "hbp_l2_persist": [c_vp, ctypes.c_size_t, ctypes.c_float, c_vp],
+    "hbp_l2_persist_reset": [c_vp],
+    "hbp_l2_info": [ctypes.POINTER(c_int), ctypes.POINTER(c_int), ctypes.POINTER(c_int)],
     "hbp_combine": [ctypes.POINTER(FormatT), c_vp, c_vp, c_vp],
     "hbp_zero_empty_rows": [ctypes.POINTER(FormatT), c_vp, c_vp],
     "hbp_expand_partial": [ctypes.POINTER(FormatT), c_vp, c_vp, c_vp],

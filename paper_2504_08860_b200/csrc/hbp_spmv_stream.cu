@@ -87,6 +87,29 @@ __device__ __forceinline__ void fence_mbar_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
+// per live-lane count k (1..32): sub-streams S = largest power of two with
+// k*S <= 32, and the 16-bit reciprocal ceil(2^16/k) (exact lane / k for lane < 32)
+__constant__ int c_streams[33] = {0,  32, 16, 8, 8, 4, 4, 4, 4, 2, 2, 2, 2, 2, 2, 2, 2,
+                                  1,  1,  1,  1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1};
+__constant__ uint32_t c_magic16[33] = {
+    0,    65536, 32768, 21846, 16384, 13108, 10923, 9363, 8192, 7282, 6554,
+    5958, 5462,  5042,  4682,  4370,  4096,  3856,  3641, 3450, 3277, 3121,
+    2979, 2850,  2731,  2622,  2521,  2428,  2341,  2260, 2185, 2115, 2048};
+
+// ceil(2^32 / k): floor(n / k) = (n * m) >> 32 exactly for n < 2^27
+__constant__ uint64_t c_magic32[33] = {
+    0ull,          4294967296ull, 2147483648ull, 1431655766ull, 1073741824ull, 858993460ull,
+    715827883ull,  613566757ull,  536870912ull,  477218589ull,  429496730ull,  390451573ull,
+    357913942ull,  330382100ull,  306783379ull,  286331154ull,  268435456ull,  252645136ull,
+    238609295ull,  226050911ull,  214748365ull,  204522253ull,  195225787ull,  186737709ull,
+    178956971ull,  171798692ull,  165191050ull,  159072863ull,  153391690ull,  148102321ull,
+    143165577ull,  138547333ull,  134217728ull};
+
+// ceil(n / k) for 0 < n < 2^20, 1 <= k <= 32
+__device__ __forceinline__ int32_t ceil_div_small(int32_t n, int k) {
+    return (int32_t)((((uint64_t)(uint32_t)(n + k - 1)) * c_magic32[k]) >> 32);
+}
+
 template <typename V, bool EXACT>
 __device__ __forceinline__ double mul(V v, V xv) {
     if (EXACT) return __dmul_rn((double)v, (double)xv);
@@ -182,7 +205,7 @@ struct Streamer {
 };
 
 template <typename V, bool EXACT, int CH>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 4)
     k_spmv_stream(const hbp_format_t f, const hbp_balanced_t b, const V *__restrict__ x,
                   V *__restrict__ y, double *__restrict__ partial) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -301,21 +324,30 @@ __global__ void __launch_bounds__(kThreads)
                     const int rank = __popc(pm & lt);
                     if (EXACT || k >= 16) {
                         if (live && plo < phi) {
-                            int32_t rel = plo - po - rank;
-                            int32_t t = rel > 0 ? (rel + k - 1) / k : 0;
+                            // first own step at or after plo (plo == po: step 0)
+                            const int32_t rel = plo - po - rank;
+                            const int32_t t = rel > 0 ? ceil_div_small(rel, k) : 0;
                             for (int32_t p = po + t * k + rank; p < phi; p += k)
                                 acc = EXACT ? __dadd_rn(acc, pr[p]) : acc + pr[p];
                         }
                     } else {
-                        int SS = 32 / k;
-                        SS = 1 << (31 - __clz(SS));
-                        const int r = lane % k, s = lane / k;
+                        const int SS = c_streams[k];
+                        const int s = (int)(((uint32_t)lane * c_magic16[k]) >> 16);  // lane / k
+                        const int r = lane - s * k;
                         double v = 0.0;
                         if (s < SS && plo < phi) {
-                            int32_t rel = plo - po - r;
-                            int32_t t = rel > 0 ? (rel + k - 1) / k : 0;
-                            t += ((s - t) % SS + SS) % SS;
-                            for (int32_t p = po + t * k + r; p < phi; p += SS * k) v += pr[p];
+                            const int32_t rel = plo - po - r;
+                            int32_t t = rel > 0 ? ceil_div_small(rel, k) : 0;
+                            t += (s - t) & (SS - 1);  // next step of sub-stream s
+                            const int32_t stride = SS * k;
+                            int32_t p = po + t * k + r;
+                            double v1 = 0.0;
+                            for (; p + stride < phi; p += 2 * stride) {
+                                v += pr[p];
+                                v1 += pr[p + stride];
+                            }
+                            if (p < phi) v += pr[p];
+                            v += v1;
                         }
                         for (int d = SS >> 1; d >= 1; d >>= 1) v += __shfl_down_sync(FULL, v, d * k);
                         const double tot = __shfl_sync(FULL, v, live ? rank : 0);

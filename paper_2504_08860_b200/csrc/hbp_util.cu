@@ -206,3 +206,45 @@ int hbp_coo_reduce_runs(const uint64_t *sorted_keys, const uint64_t *order, cons
 }
 
 }  // extern "C"
+
+extern "C" {
+
+// Keep `bytes` at `base` (the gathered x vector) resident in L2: set aside
+// persisting L2 and attach an access-policy window to `stream`.
+int hbp_l2_persist(const void *base, size_t bytes, float hit_ratio, hbp_stream_t stream) {
+    int dev = 0, max_persist = 0, max_window = 0;
+    HBP_CUDA_TRY(cudaGetDevice(&dev));
+    HBP_CUDA_TRY(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev));
+    HBP_CUDA_TRY(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev));
+    if (max_persist <= 0 || max_window <= 0) return HBP_E_UNSUPPORTED;
+    size_t set_aside = bytes < (size_t)max_persist ? bytes : (size_t)max_persist;
+    HBP_CUDA_TRY(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, set_aside));
+    cudaStreamAttrValue v = {};
+    v.accessPolicyWindow.base_ptr = const_cast<void *>(base);
+    v.accessPolicyWindow.num_bytes = bytes < (size_t)max_window ? bytes : (size_t)max_window;
+    float hr = (float)set_aside / (float)(v.accessPolicyWindow.num_bytes ? v.accessPolicyWindow.num_bytes : 1);
+    v.accessPolicyWindow.hitRatio = hit_ratio < hr ? hit_ratio : hr;
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    HBP_CUDA_TRY(cudaStreamSetAttribute(as_stream(stream), cudaStreamAttributeAccessPolicyWindow, &v));
+    return HBP_OK;
+}
+
+int hbp_l2_persist_reset(hbp_stream_t stream) {
+    cudaStreamAttrValue v = {};
+    v.accessPolicyWindow.num_bytes = 0;
+    HBP_CUDA_TRY(cudaStreamSetAttribute(as_stream(stream), cudaStreamAttributeAccessPolicyWindow, &v));
+    HBP_CUDA_TRY(cudaCtxResetPersistingL2Cache());
+    return HBP_OK;
+}
+
+int hbp_l2_info(int *l2_bytes, int *max_persist, int *max_window) {
+    int dev = 0;
+    HBP_CUDA_TRY(cudaGetDevice(&dev));
+    HBP_CUDA_TRY(cudaDeviceGetAttribute(l2_bytes, cudaDevAttrL2CacheSize, dev));
+    HBP_CUDA_TRY(cudaDeviceGetAttribute(max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev));
+    HBP_CUDA_TRY(cudaDeviceGetAttribute(max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev));
+    return HBP_OK;
+}
+
+}  // extern "C"

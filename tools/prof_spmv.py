@@ -19,6 +19,7 @@ ap.add_argument("--config", default="cfg2")
 ap.add_argument("--schedule", default=None)
 ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--workers", type=int, default=None)
+ap.add_argument("--persist", action="store_true")
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 desc, rows, cols, rp, col, val, C, vdt = bench.make_matrix_gpu(a.config, 0, dev)
@@ -30,6 +31,9 @@ hbp = H.build_hbp(csr, grid, H.hash_permutations(grid, H.sample_hash_params(grid
 op = H.SpmvOperator(hbp, workers=a.workers, schedule=a.schedule)
 x = torch.as_tensor(np.random.default_rng(0).uniform(-1, 1, cols), device=dev).to(vdt)
 y = torch.empty(rows, dtype=vdt, device=dev)
+if a.persist:
+    from paper_2504_08860_b200 import _lib as L
+    L.call("hbp_l2_persist", L.P(x), x.numel() * x.element_size(), 1.0, L.stream())
 for _ in range(a.iters):
     op(x, y)
 torch.cuda.synchronize()
