@@ -26,6 +26,7 @@
 //      (atomic) adds the pieces in slice order (deterministic).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "hbp.h"
 #include "hbp_common.cuh"
@@ -204,8 +205,8 @@ struct Streamer {
     }
 };
 
-template <typename V, bool EXACT, int CH>
-__global__ void __launch_bounds__(kThreads, 4)
+template <typename V, bool EXACT, int CH, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
     k_spmv_stream(const hbp_format_t f, const hbp_balanced_t b, const V *__restrict__ x,
                   V *__restrict__ y, double *__restrict__ partial) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -402,31 +403,62 @@ __global__ void __launch_bounds__(kThreads, 4)
     }
 }
 
-template <typename V, bool EXACT, int CH>
+template <typename V, bool EXACT, int CH, int MINB>
 int launch(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y,
            double *partial, cudaStream_t st) {
     const size_t smem = sizeof(WarpSmem<V, CH>) * kWarps;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_spmv_stream<V, EXACT, CH>,
+        cudaFuncSetAttribute(k_spmv_stream<V, EXACT, CH, MINB>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
     unsigned grid = (unsigned)((b->workers + kWarps - 1) / kWarps);
-    k_spmv_stream<V, EXACT, CH><<<grid, kThreads, smem, st>>>(*f, *b, (const V *)x, (V *)y,
-                                                                partial);
+    k_spmv_stream<V, EXACT, CH, MINB><<<grid, kThreads, smem, st>>>(*f, *b, (const V *)x,
+                                                                      (V *)y, partial);
     return (int)cudaGetLastError();
 }
 
-constexpr int kCH = 256;
+template <typename V, bool EXACT, int CH, int MINB>
+int occupancy_of(int *per_sm) {
+    const size_t smem = sizeof(WarpSmem<V, CH>) * kWarps;
+    cudaFuncSetAttribute(k_spmv_stream<V, EXACT, CH, MINB>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        per_sm, k_spmv_stream<V, EXACT, CH, MINB>, kThreads, smem);
+}
+
+// Tile / occupancy variants (chunk CH, min CTAs per SM), chosen with the
+// environment variable HBP_STREAM_VARIANT for sweeps; 0 is the default.
+constexpr int kVariants = 5;
+int variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("HBP_STREAM_VARIANT");
+        v = e ? atoi(e) : 0;
+        if (v < 0 || v >= kVariants) v = 0;
+    }
+    return v;
+}
+
+#define HBP_STREAM_VARIANTS(FN, V, EXACT, ...)          \
+    switch (variant()) {                                 \
+        case 1: return FN<V, EXACT, 256, 4>(__VA_ARGS__); \
+        case 2: return FN<V, EXACT, 128, 4>(__VA_ARGS__); \
+        case 3: return FN<V, EXACT, 512, 2>(__VA_ARGS__); \
+        case 4: return FN<V, EXACT, 128, 6>(__VA_ARGS__); \
+        default: return FN<V, EXACT, 256, 3>(__VA_ARGS__); \
+    }
 
 template <typename V, bool EXACT>
 int occupancy(int *per_sm) {
-    const size_t smem = sizeof(WarpSmem<V, kCH>) * kWarps;
-    cudaFuncSetAttribute(k_spmv_stream<V, EXACT, kCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_spmv_stream<V, EXACT, kCH>,
-                                                              kThreads, smem);
+    HBP_STREAM_VARIANTS(occupancy_of, V, EXACT, per_sm)
+}
+
+template <typename V, bool EXACT>
+int run(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y, double *partial,
+        cudaStream_t st) {
+    HBP_STREAM_VARIANTS(launch, V, EXACT, f, b, x, y, partial, st)
 }
 
 }  // namespace
@@ -460,11 +492,11 @@ int hbp_spmv_stream(const hbp_format_t *f, const hbp_balanced_t *b, const void *
     if (!exact && (!b->part_head || !b->part_tail || !b->counters)) return HBP_E_ARG;
     cudaStream_t st = as_stream(stream);
     if (f->dtype == HBP_F64)
-        return exact ? launch<double, true, kCH>(f, b, x, y, partial, st)
-                     : launch<double, false, kCH>(f, b, x, y, partial, st);
+        return exact ? run<double, true>(f, b, x, y, partial, st)
+                     : run<double, false>(f, b, x, y, partial, st);
     if (f->dtype == HBP_F32)
-        return exact ? launch<float, true, kCH>(f, b, x, y, partial, st)
-                     : launch<float, false, kCH>(f, b, x, y, partial, st);
+        return exact ? run<float, true>(f, b, x, y, partial, st)
+                     : run<float, false>(f, b, x, y, partial, st);
     return HBP_E_ARG;
 }
 
