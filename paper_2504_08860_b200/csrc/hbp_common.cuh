@@ -124,6 +124,20 @@ __device__ __forceinline__ double ld_x(const double *p, uint64_t pol) {
     return v;
 }
 
+// x gathers that do not allocate L1 lines (L2 evict-last policy kept)
+__device__ __forceinline__ float ld_x_na(const float *p, uint64_t pol) {
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;"
+                 : "=f"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ double ld_x_na(const double *p, uint64_t pol) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+                 : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
 __device__ __forceinline__ int64_t globaltimer_ns() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

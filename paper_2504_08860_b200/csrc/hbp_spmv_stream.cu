@@ -144,7 +144,7 @@ __device__ __forceinline__ int64_t cut_at(int64_t w, int64_t E, int64_t Nw) {
     return (int64_t)((__int128)w * E / Nw);
 }
 
-template <typename V, bool EXACT, int CH>
+template <typename V, bool EXACT, int CH, bool XNA>
 struct Streamer {
     const hbp_format_t &f;
     WarpSmem<V, CH> &S;
@@ -193,7 +193,7 @@ struct Streamer {
             cl[u] = i < n ? S.col[buf][offc + i] : 0u;
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) xv[u] = ld_x(x + cl[u], pl);
+        for (int u = 0; u < U; ++u) xv[u] = XNA ? ld_x_na(x + cl[u], pl) : ld_x(x + cl[u], pl);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int i = lane + 32 * u;
@@ -205,7 +205,7 @@ struct Streamer {
     }
 };
 
-template <typename V, bool EXACT, int CH, int MINB>
+template <typename V, bool EXACT, int CH, int MINB, bool XNA>
 __global__ void __launch_bounds__(kThreads, MINB)
     k_spmv_stream(const hbp_format_t f, const hbp_balanced_t b, const V *__restrict__ x,
                   V *__restrict__ y, double *__restrict__ partial) {
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
     const uint32_t *__restrict__ slot_len = (const uint32_t *)f.slot_len;
     const uint32_t *__restrict__ permp = (const uint32_t *)f.perm;
 
-    Streamer<V, EXACT, CH> st{f, S, x};
+    Streamer<V, EXACT, CH, XNA> st{f, S, x};
     st.lane = lane;
     st.pe = policy_evict_first();
     st.pl = policy_evict_last();
@@ -403,34 +403,34 @@ __global__ void __launch_bounds__(kThreads, MINB)
     }
 }
 
-template <typename V, bool EXACT, int CH, int MINB>
+template <typename V, bool EXACT, int CH, int MINB, bool XNA>
 int launch(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y,
            double *partial, cudaStream_t st) {
     const size_t smem = sizeof(WarpSmem<V, CH>) * kWarps;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_spmv_stream<V, EXACT, CH, MINB>,
+        cudaFuncSetAttribute(k_spmv_stream<V, EXACT, CH, MINB, XNA>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
     unsigned grid = (unsigned)((b->workers + kWarps - 1) / kWarps);
-    k_spmv_stream<V, EXACT, CH, MINB><<<grid, kThreads, smem, st>>>(*f, *b, (const V *)x,
+    k_spmv_stream<V, EXACT, CH, MINB, XNA><<<grid, kThreads, smem, st>>>(*f, *b, (const V *)x,
                                                                       (V *)y, partial);
     return (int)cudaGetLastError();
 }
 
-template <typename V, bool EXACT, int CH, int MINB>
+template <typename V, bool EXACT, int CH, int MINB, bool XNA>
 int occupancy_of(int *per_sm) {
     const size_t smem = sizeof(WarpSmem<V, CH>) * kWarps;
-    cudaFuncSetAttribute(k_spmv_stream<V, EXACT, CH, MINB>,
+    cudaFuncSetAttribute(k_spmv_stream<V, EXACT, CH, MINB, XNA>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        per_sm, k_spmv_stream<V, EXACT, CH, MINB>, kThreads, smem);
+        per_sm, k_spmv_stream<V, EXACT, CH, MINB, XNA>, kThreads, smem);
 }
 
 // Tile / occupancy variants (chunk CH, min CTAs per SM), chosen with the
 // environment variable HBP_STREAM_VARIANT for sweeps; 0 is the default.
-constexpr int kVariants = 5;
+constexpr int kVariants = 9;
 int variant() {
     static int v = -1;
     if (v < 0) {
@@ -443,11 +443,15 @@ int variant() {
 
 #define HBP_STREAM_VARIANTS(FN, V, EXACT, ...)          \
     switch (variant()) {                                 \
-        case 1: return FN<V, EXACT, 256, 4>(__VA_ARGS__); \
-        case 2: return FN<V, EXACT, 128, 4>(__VA_ARGS__); \
-        case 3: return FN<V, EXACT, 512, 2>(__VA_ARGS__); \
-        case 4: return FN<V, EXACT, 128, 6>(__VA_ARGS__); \
-        default: return FN<V, EXACT, 256, 3>(__VA_ARGS__); \
+        case 1: return FN<V, EXACT, 256, 4, false>(__VA_ARGS__); \
+        case 5: return FN<V, EXACT, 256, 3, true>(__VA_ARGS__); \
+        case 6: return FN<V, EXACT, 256, 4, true>(__VA_ARGS__); \
+        case 7: return FN<V, EXACT, 128, 4, true>(__VA_ARGS__); \
+        case 8: return FN<V, EXACT, 512, 2, true>(__VA_ARGS__); \
+        case 2: return FN<V, EXACT, 128, 4, false>(__VA_ARGS__); \
+        case 3: return FN<V, EXACT, 512, 2, false>(__VA_ARGS__); \
+        case 4: return FN<V, EXACT, 128, 6, false>(__VA_ARGS__); \
+        default: return FN<V, EXACT, 256, 3, false>(__VA_ARGS__); \
     }
 
 template <typename V, bool EXACT>
