@@ -155,8 +155,14 @@ struct Streamer {
     // current chunk window
     int64_t cur = -1, a = 0, bnd = 0;
 
+    // chunk c covers elements [base + c*CH, min(base + (c+1)*CH, c_hi)),
+    // base = c_lo rounded down to 4 elements (16-byte aligned for col and
+    // data); elements before c_lo belong to the previous slice and are
+    // gathered but never summed.
+    int64_t base;
+
     __device__ void chunk_bounds(int64_t c, int64_t &ca, int64_t &cb) const {
-        ca = c_lo + c * CH;
+        ca = base + c * CH;
         cb = ca + CH < c_hi ? ca + CH : c_hi;
     }
 
@@ -164,40 +170,62 @@ struct Streamer {
         int64_t ca, cb;
         chunk_bounds(c, ca, cb);
         const int buf = (int)(c & 1);
-        const int64_t ac = ca & ~(int64_t)3;
-        const uint32_t bc = (uint32_t)(((cb - ac) * 4 + 15) & ~(int64_t)15);
-        constexpr int64_t VA = 16 / sizeof(V);
-        const int64_t av = ca & ~(VA - 1);
-        const uint32_t bv = (uint32_t)(((cb - av) * (int64_t)sizeof(V) + 15) & ~(int64_t)15);
+        const uint32_t bc = (uint32_t)(((cb - ca) * 4 + 15) & ~(int64_t)15);
+        const uint32_t bv = (uint32_t)(((cb - ca) * (int64_t)sizeof(V) + 15) & ~(int64_t)15);
         mbar_expect_tx(&S.mbar[buf], bc + bv);
-        bulk_g2s(S.col[buf], f.col + ac, bc, &S.mbar[buf], pe);
-        bulk_g2s(S.val[buf], (const V *)f.data + av, bv, &S.mbar[buf], pe);
+        bulk_g2s(S.col[buf], f.col + ca, bc, &S.mbar[buf], pe);
+        bulk_g2s(S.val[buf], (const V *)f.data + ca, bv, &S.mbar[buf], pe);
     }
 
-    // make chunk c the current one: wait, gather x, products -> S.prod
+    // make chunk c the current one: wait, gather x, products -> S.prod.
+    // Chunks are 16-byte aligned in element space (a = base + c*CH), so each
+    // lane reads 4 consecutive cols / values with one vector LDS.
     __device__ void prepare(int64_t c) {
         chunk_bounds(c, a, bnd);
         cur = c;
         const int buf = (int)(c & 1);
         mbar_wait(&S.mbar[buf], (uint32_t)((c >> 1) & 1));
-        constexpr int64_t VA = 16 / sizeof(V);
-        const int offc = (int)(a - (a & ~(int64_t)3));
-        const int offv = (int)(a - (a & ~(VA - 1)));
         const int n = (int)(bnd - a);
-        constexpr int U = CH / 32;
-        uint32_t cl[U];
-        V xv[U];
+        constexpr int U = CH / 128;
+        uint4 cl[U];
+        V xv[U][4];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int i = lane + 32 * u;
-            cl[u] = i < n ? S.col[buf][offc + i] : 0u;
+            const int i = 4 * lane + 128 * u;
+            cl[u] = *reinterpret_cast<const uint4 *>(&S.col[buf][i]);
+            if (i + 3 >= n) {  // tail of the last chunk: never gather past the slice
+                if (i >= n) cl[u].x = 0u;
+                if (i + 1 >= n) cl[u].y = 0u;
+                if (i + 2 >= n) cl[u].z = 0u;
+                cl[u].w = 0u;
+            }
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) xv[u] = XNA ? ld_x_na(x + cl[u], pl) : ld_x(x + cl[u], pl);
+        for (int u = 0; u < U; ++u) {
+            const uint32_t cc[4] = {cl[u].x, cl[u].y, cl[u].z, cl[u].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                xv[u][e] = XNA ? ld_x_na(x + cc[e], pl) : ld_x(x + cc[e], pl);
+        }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int i = lane + 32 * u;
-            if (i < n) S.prod[i] = mul<V, EXACT>(S.val[buf][offv + i], xv[u]);
+            const int i = 4 * lane + 128 * u;
+            V vv[4];
+            if (sizeof(V) == 4) {
+                const float4 t = *reinterpret_cast<const float4 *>(&S.val[buf][i]);
+                vv[0] = t.x, vv[1] = t.y, vv[2] = t.z, vv[3] = t.w;
+            } else {
+                const double2 t0 = *reinterpret_cast<const double2 *>(&S.val[buf][i]);
+                const double2 t1 = *reinterpret_cast<const double2 *>(&S.val[buf][i + 2]);
+                vv[0] = t0.x, vv[1] = t0.y, vv[2] = t1.x, vv[3] = t1.y;
+            }
+            double2 p0, p1;
+            p0.x = mul<V, EXACT>(vv[0], xv[u][0]);
+            p0.y = mul<V, EXACT>(vv[1], xv[u][1]);
+            p1.x = mul<V, EXACT>(vv[2], xv[u][2]);
+            p1.y = mul<V, EXACT>(vv[3], xv[u][3]);
+            *reinterpret_cast<double2 *>(&S.prod[i]) = p0;
+            *reinterpret_cast<double2 *>(&S.prod[i + 2]) = p1;
         }
         fence_proxy_async();  // generic reads of this buffer precede the next bulk write
         __syncwarp();
@@ -242,7 +270,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
     }
     st.c_lo = c_lo;
     st.c_hi = c_hi;
-    st.nchunks = (c_hi - c_lo + CH - 1) / CH;
+    st.base = c_lo & ~(int64_t)3;
+    st.nchunks = c_hi > c_lo ? (c_hi - st.base + CH - 1) / CH : 0;
 
     if (lane == 0) {
         mbar_init(&S.mbar[0], 1);
@@ -323,12 +352,16 @@ __global__ void __launch_bounds__(kThreads, MINB)
                     const unsigned pm = S.ph_mask[j];
                     const bool live = (pm >> lane) & 1u;
                     const int rank = __popc(pm & lt);
-                    if (EXACT || k >= 16) {
+                    // lane-serial unless the phase is long with few live lanes
+                    if (EXACT || k >= 16 || pn - po <= 8 * k) {
                         if (live && plo < phi) {
                             // first own step at or after plo (plo == po: step 0)
-                            const int32_t rel = plo - po - rank;
-                            const int32_t t = rel > 0 ? ceil_div_small(rel, k) : 0;
-                            for (int32_t p = po + t * k + rank; p < phi; p += k)
+                            int32_t p = po + rank;
+                            if (plo != po) {
+                                const int32_t rel = plo - p;
+                                if (rel > 0) p += ceil_div_small(rel, k) * k;
+                            }
+                            for (; p < phi; p += k)
                                 acc = EXACT ? __dadd_rn(acc, pr[p]) : acc + pr[p];
                         }
                     } else {
@@ -444,14 +477,14 @@ int variant() {
 #define HBP_STREAM_VARIANTS(FN, V, EXACT, ...)          \
     switch (variant()) {                                 \
         case 1: return FN<V, EXACT, 256, 4, false>(__VA_ARGS__); \
-        case 5: return FN<V, EXACT, 256, 3, true>(__VA_ARGS__); \
+        case 5: return FN<V, EXACT, 256, 3, false>(__VA_ARGS__); \
         case 6: return FN<V, EXACT, 256, 4, true>(__VA_ARGS__); \
         case 7: return FN<V, EXACT, 128, 4, true>(__VA_ARGS__); \
         case 8: return FN<V, EXACT, 512, 2, true>(__VA_ARGS__); \
         case 2: return FN<V, EXACT, 128, 4, false>(__VA_ARGS__); \
         case 3: return FN<V, EXACT, 512, 2, false>(__VA_ARGS__); \
         case 4: return FN<V, EXACT, 128, 6, false>(__VA_ARGS__); \
-        default: return FN<V, EXACT, 256, 3, false>(__VA_ARGS__); \
+        default: return FN<V, EXACT, 256, 3, true>(__VA_ARGS__); \
     }
 
 template <typename V, bool EXACT>
