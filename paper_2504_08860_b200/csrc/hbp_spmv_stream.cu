@@ -1,29 +1,34 @@
 // hbp_spmv_stream.cu -- TMA-streamed, element-balanced HBP SpMV (W = 32).
 //
-// Why: in the HBP layout a group's elements are step-major (all lanes' first
-// elements, then the second ...).  On skewed matrices a group has ~10
+// Why: in the HBP layout a group's elements are step-major (all live lanes'
+// t-th elements, then the (t+1)-th ...).  On skewed matrices a group has ~10
 // "phases" (step ranges with a fixed live-lane set) and few live lanes, so a
-// lane-per-row walk over global memory pays two dependent DRAM round trips
-// (col, then x) per phase.  Here memory and the irregular walk are decoupled:
+// lane-per-row walk over global memory pays dependent DRAM round trips (col,
+// then x) per phase.  Here memory and the irregular walk are decoupled:
 //
 //   1. each persistent warp owns an equal slice [c_lo, c_hi) of the element
 //      array (exact mode: slice ends rounded up to group boundaries);
-//   2. lane 0 streams the slice's col/data through shared memory in chunks of
-//      CH elements with cp.async.bulk (TMA bulk copies, mbarrier completion),
-//      two chunks in flight;
-//   3. per chunk the warp gathers x for all CH elements at once (CH/32
-//      independent loads per lane) and stores the products (f64) in shared
-//      memory;
-//   4. the group's phase table (offset, live count k, live mask, steps) is
-//      built once per group from the 32 slot lengths with ballots, and the
-//      products are summed per row from shared memory:
-//        exact (f64): each lane adds its own elements in step order --
-//                     bitwise identical to the reference (_kernels.py:41-46);
-//        fast  (f32 data, f64 sums): phases with k < 16 live lanes use
-//                     S = 32/k sub-streams per lane and a shuffle tree.
+//   2. lane 0 streams the slice's col/data into a shared-memory ring of NB
+//      chunks of CH elements with cp.async.bulk (TMA bulk copies completing
+//      on per-slot mbarriers), NB-2 chunks ahead of the walk;
+//   3. per chunk the warp gathers x for all CH elements at once and writes
+//      the products in place of the values (f32 data: f32 products, exact
+//      f64 data: __dmul_rn products), so the ring always holds the products
+//      of the two chunks the walk can touch;
+//   4. the group's phase table (offset, steps, live mask) is built from the
+//      32 slot lengths with ballots; the walk then runs
+//        - a step-uniform loop while >= KT lanes are live (exact mode: all
+//          steps): every live lane adds its element of the step, phase
+//          changes only reload (k, mask, rank) -- each row is summed in
+//          step order, bitwise identical to _kernels.py:41-46 for f64;
+//        - (fast mode) per remaining phase: short ones lane-serially, long
+//          ones with S = 32/k sub-streams per live lane and a shuffle tree;
 //   5. a group cut by a slice boundary (fast mode only) leaves per-lane
 //      partials; the warp whose piece completes the group's element count
-//      (atomic) adds the pieces in slice order (deterministic).
+//      (atomic) adds the pieces in slice order -- deterministic.
+//
+// Precision (fast mode): f32 products (relative error <= 2^-24 each) summed
+// in f64, one rounding to f32: componentwise error <= ~1.2e-7 |A||x|.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -38,16 +43,16 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr unsigned FULL = 0xffffffffu;
+constexpr int NB = 4;  // ring slots (chunks)
 
 template <typename V, int CH>
 struct __align__(16) WarpSmem {
-    uint32_t col[2][CH + 8];
-    V val[2][CH + 8];
-    double prod[CH];
+    uint32_t col[NB * CH];
+    V val[NB * CH];  // values, then products in place
     int32_t ph_off[33];
-    int32_t ph_k[32];
+    int32_t ph_t1[32];
     uint32_t ph_mask[32];
-    uint64_t mbar[2];
+    uint64_t mbar[NB];
 };
 
 // ---- PTX helpers: mbarrier + bulk async copy (sm_90+ / sm_100a) ------------
@@ -89,14 +94,13 @@ __device__ __forceinline__ void fence_mbar_init() {
 }
 
 // per live-lane count k (1..32): sub-streams S = largest power of two with
-// k*S <= 32, and the 16-bit reciprocal ceil(2^16/k) (exact lane / k for lane < 32)
+// k*S <= 32, and ceil(2^16/k) (exact lane / k for lane < 32)
 __constant__ int c_streams[33] = {0,  32, 16, 8, 8, 4, 4, 4, 4, 2, 2, 2, 2, 2, 2, 2, 2,
                                   1,  1,  1,  1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1};
 __constant__ uint32_t c_magic16[33] = {
     0,    65536, 32768, 21846, 16384, 13108, 10923, 9363, 8192, 7282, 6554,
     5958, 5462,  5042,  4682,  4370,  4096,  3856,  3641, 3450, 3277, 3121,
     2979, 2850,  2731,  2622,  2521,  2428,  2341,  2260, 2185, 2115, 2048};
-
 // ceil(2^32 / k): floor(n / k) = (n * m) >> 32 exactly for n < 2^27
 __constant__ uint64_t c_magic32[33] = {
     0ull,          4294967296ull, 2147483648ull, 1431655766ull, 1073741824ull, 858993460ull,
@@ -106,15 +110,9 @@ __constant__ uint64_t c_magic32[33] = {
     178956971ull,  171798692ull,  165191050ull,  159072863ull,  153391690ull,  148102321ull,
     143165577ull,  138547333ull,  134217728ull};
 
-// ceil(n / k) for 0 < n < 2^20, 1 <= k <= 32
-__device__ __forceinline__ int32_t ceil_div_small(int32_t n, int k) {
-    return (int32_t)((((uint64_t)(uint32_t)(n + k - 1)) * c_magic32[k]) >> 32);
-}
-
-template <typename V, bool EXACT>
-__device__ __forceinline__ double mul(V v, V xv) {
-    if (EXACT) return __dmul_rn((double)v, (double)xv);
-    return (double)v * (double)xv;  // exact for f32 inputs
+__device__ __forceinline__ int64_t div_small(int64_t n, int k) {  // n >= 0, 1 <= k <= 32
+    if (n < (1 << 26)) return (int64_t)(((uint64_t)n * c_magic32[k]) >> 32);
+    return n / k;
 }
 
 // largest g in [0, n] with gs[g] <= e
@@ -144,60 +142,67 @@ __device__ __forceinline__ int64_t cut_at(int64_t w, int64_t E, int64_t Nw) {
     return (int64_t)((__int128)w * E / Nw);
 }
 
+template <typename V, bool EXACT>
+__device__ __forceinline__ V product(V v, V xv) {
+    if (EXACT) return (V)__dmul_rn((double)v, (double)xv);
+    return v * xv;
+}
+
 template <typename V, bool EXACT, int CH, bool XNA>
-struct Streamer {
+struct Ring {
+    static constexpr int RMASK = NB * CH - 1;
     const hbp_format_t &f;
     WarpSmem<V, CH> &S;
     const V *__restrict__ x;
-    int64_t c_lo, c_hi, nchunks;
+    int64_t c_lo, c_hi, base, nchunks;
+    int64_t ready = -1;   // highest prepared chunk
+    int64_t issued = 0;   // chunks whose bulk copy was issued
+    int64_t res_hi = 0;   // products resident for positions < res_hi
     int lane;
     uint64_t pe, pl;
-    // current chunk window
-    int64_t cur = -1, a = 0, bnd = 0;
 
-    // chunk c covers elements [base + c*CH, min(base + (c+1)*CH, c_hi)),
-    // base = c_lo rounded down to 4 elements (16-byte aligned for col and
-    // data); elements before c_lo belong to the previous slice and are
-    // gathered but never summed.
-    int64_t base;
+    __device__ __forceinline__ int64_t chunk_start(int64_t c) const { return base + c * CH; }
 
-    __device__ void chunk_bounds(int64_t c, int64_t &ca, int64_t &cb) const {
-        ca = base + c * CH;
-        cb = ca + CH < c_hi ? ca + CH : c_hi;
+    __device__ void issue_upto(int64_t last) {  // lane 0
+        for (; issued <= last && issued < nchunks; ++issued) {
+            const int64_t ca = chunk_start(issued);
+            const int64_t cb = ca + CH < c_hi ? ca + CH : c_hi;
+            const int slot = (int)(issued % NB);
+            const uint32_t bc = (uint32_t)(((cb - ca) * 4 + 15) & ~(int64_t)15);
+            const uint32_t bv = (uint32_t)(((cb - ca) * (int64_t)sizeof(V) + 15) & ~(int64_t)15);
+            mbar_expect_tx(&S.mbar[slot], bc + bv);
+            bulk_g2s(&S.col[slot * CH], f.col + ca, bc, &S.mbar[slot], pe);
+            bulk_g2s(&S.val[slot * CH], (const V *)f.data + ca, bv, &S.mbar[slot], pe);
+        }
     }
 
-    __device__ void issue(int64_t c) {  // lane 0 only
-        int64_t ca, cb;
-        chunk_bounds(c, ca, cb);
-        const int buf = (int)(c & 1);
-        const uint32_t bc = (uint32_t)(((cb - ca) * 4 + 15) & ~(int64_t)15);
-        const uint32_t bv = (uint32_t)(((cb - ca) * (int64_t)sizeof(V) + 15) & ~(int64_t)15);
-        mbar_expect_tx(&S.mbar[buf], bc + bv);
-        bulk_g2s(S.col[buf], f.col + ca, bc, &S.mbar[buf], pe);
-        bulk_g2s(S.val[buf], (const V *)f.data + ca, bv, &S.mbar[buf], pe);
-    }
-
-    // make chunk c the current one: wait, gather x, products -> S.prod.
-    // Chunks are 16-byte aligned in element space (a = base + c*CH), so each
-    // lane reads 4 consecutive cols / values with one vector LDS.
+    // wait for chunk c's bytes, gather x, overwrite its values with products
     __device__ void prepare(int64_t c) {
-        chunk_bounds(c, a, bnd);
-        cur = c;
-        const int buf = (int)(c & 1);
-        mbar_wait(&S.mbar[buf], (uint32_t)((c >> 1) & 1));
-        const int n = (int)(bnd - a);
+        const int slot = (int)(c % NB);
+        mbar_wait(&S.mbar[slot], (uint32_t)((c / NB) & 1));
+        const int64_t ca = chunk_start(c);
+        const int n = (int)((ca + CH < c_hi ? ca + CH : c_hi) - ca);
         constexpr int U = CH / 128;
         uint4 cl[U];
+        V vv[U][4];
         V xv[U][4];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int i = 4 * lane + 128 * u;
-            cl[u] = *reinterpret_cast<const uint4 *>(&S.col[buf][i]);
-            if (i + 3 >= n) {  // tail of the last chunk: never gather past the slice
+            cl[u] = *reinterpret_cast<const uint4 *>(&S.col[slot * CH + i]);
+            if (i + 3 >= n) {  // never gather past the slice
                 if (i >= n) cl[u].x = 0u;
                 if (i + 1 >= n) cl[u].y = 0u;
                 if (i + 2 >= n) cl[u].z = 0u;
                 cl[u].w = 0u;
+            }
+            if (sizeof(V) == 4) {
+                const float4 t = *reinterpret_cast<const float4 *>(&S.val[slot * CH + i]);
+                vv[u][0] = t.x, vv[u][1] = t.y, vv[u][2] = t.z, vv[u][3] = t.w;
+            } else {
+                const double2 t0 = *reinterpret_cast<const double2 *>(&S.val[slot * CH + i]);
+                const double2 t1 = *reinterpret_cast<const double2 *>(&S.val[slot * CH + i + 2]);
+                vv[u][0] = t0.x, vv[u][1] = t0.y, vv[u][2] = t1.x, vv[u][3] = t1.y;
             }
         }
 #pragma unroll
@@ -210,26 +215,34 @@ struct Streamer {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int i = 4 * lane + 128 * u;
-            V vv[4];
+            V p[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) p[e] = product<V, EXACT>(vv[u][e], xv[u][e]);
             if (sizeof(V) == 4) {
-                const float4 t = *reinterpret_cast<const float4 *>(&S.val[buf][i]);
-                vv[0] = t.x, vv[1] = t.y, vv[2] = t.z, vv[3] = t.w;
+                *reinterpret_cast<float4 *>(&S.val[slot * CH + i]) =
+                    make_float4((float)p[0], (float)p[1], (float)p[2], (float)p[3]);
             } else {
-                const double2 t0 = *reinterpret_cast<const double2 *>(&S.val[buf][i]);
-                const double2 t1 = *reinterpret_cast<const double2 *>(&S.val[buf][i + 2]);
-                vv[0] = t0.x, vv[1] = t0.y, vv[2] = t1.x, vv[3] = t1.y;
+                *reinterpret_cast<double2 *>(&S.val[slot * CH + i]) =
+                    make_double2((double)p[0], (double)p[1]);
+                *reinterpret_cast<double2 *>(&S.val[slot * CH + i + 2]) =
+                    make_double2((double)p[2], (double)p[3]);
             }
-            double2 p0, p1;
-            p0.x = mul<V, EXACT>(vv[0], xv[u][0]);
-            p0.y = mul<V, EXACT>(vv[1], xv[u][1]);
-            p1.x = mul<V, EXACT>(vv[2], xv[u][2]);
-            p1.y = mul<V, EXACT>(vv[3], xv[u][3]);
-            *reinterpret_cast<double2 *>(&S.prod[i]) = p0;
-            *reinterpret_cast<double2 *>(&S.prod[i + 2]) = p1;
         }
-        fence_proxy_async();  // generic reads of this buffer precede the next bulk write
+        fence_proxy_async();  // our generic accesses precede later bulk writes of the ring
         __syncwarp();
-        if (lane == 0 && c + 2 < nchunks) issue(c + 2);
+        ready = c;
+        res_hi = ca + n;
+        // slots of chunks < c - 1 are free: keep NB - 2 chunks in flight
+        if (lane == 0) issue_upto(c + NB - 2);
+    }
+
+    // make positions < need resident (warp-uniform call)
+    __device__ __forceinline__ void ensure(int64_t need) {
+        while (need > res_hi && ready + 1 < nchunks) prepare(ready + 1);
+    }
+
+    __device__ __forceinline__ double at(int64_t P) const {
+        return (double)S.val[(int)((P - base) & RMASK)];
     }
 };
 
@@ -237,6 +250,7 @@ template <typename V, bool EXACT, int CH, int MINB, bool XNA>
 __global__ void __launch_bounds__(kThreads, MINB)
     k_spmv_stream(const hbp_format_t f, const hbp_balanced_t b, const V *__restrict__ x,
                   V *__restrict__ y, double *__restrict__ partial) {
+    constexpr int KT = 8;  // fast mode: lanes live below which phases go cooperative
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
@@ -252,10 +266,10 @@ __global__ void __launch_bounds__(kThreads, MINB)
     const uint32_t *__restrict__ slot_len = (const uint32_t *)f.slot_len;
     const uint32_t *__restrict__ permp = (const uint32_t *)f.perm;
 
-    Streamer<V, EXACT, CH, XNA> st{f, S, x};
-    st.lane = lane;
-    st.pe = policy_evict_first();
-    st.pl = policy_evict_last();
+    Ring<V, EXACT, CH, XNA> ring{f, S, x};
+    ring.lane = lane;
+    ring.pe = policy_evict_first();
+    ring.pl = policy_evict_last();
 
     int64_t c_lo = cut_at(w, E, Nw), c_hi = cut_at(w + 1, E, Nw);
     if (EXACT) {  // round slice ends up to group boundaries
@@ -268,21 +282,18 @@ __global__ void __launch_bounds__(kThreads, MINB)
             if (gs[g] != c_hi) c_hi = gs[g + 1];
         }
     }
-    st.c_lo = c_lo;
-    st.c_hi = c_hi;
-    st.base = c_lo & ~(int64_t)3;
-    st.nchunks = c_hi > c_lo ? (c_hi - st.base + CH - 1) / CH : 0;
+    ring.c_lo = c_lo;
+    ring.c_hi = c_hi;
+    ring.base = c_lo & ~(int64_t)3;
+    ring.res_hi = ring.base;
+    ring.nchunks = c_hi > c_lo ? (c_hi - ring.base + CH - 1) / CH : 0;
 
     if (lane == 0) {
-        mbar_init(&S.mbar[0], 1);
-        mbar_init(&S.mbar[1], 1);
+        for (int i = 0; i < NB; ++i) mbar_init(&S.mbar[i], 1);
         fence_mbar_init();
     }
     __syncwarp();
-    if (lane == 0) {
-        if (st.nchunks > 0) st.issue(0);
-        if (st.nchunks > 1) st.issue(1);
-    }
+    if (lane == 0) ring.issue_upto(NB - 2);
 
     int64_t g = upper_group(gs, ngroups, c_lo);
     if (!(g < ngroups && gs[g] < c_lo)) g = lower_group(gs, ngroups, c_lo);
@@ -309,7 +320,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
 
         double acc = 0.0;
         if (lo < hi) {
-            // ---- phase table of the group
+            // ---- phase table: ph_off[j] (group offset of phase j), ph_t1[j]
+            // (its end step), ph_mask[j] (live lanes)
             int nph = 0;
             {
                 uint32_t t0 = 0;
@@ -321,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
                     const uint32_t t1 = __reduce_min_sync(FULL, live ? len : 0xffffffffu);
                     if (lane == nph) {
                         S.ph_off[nph] = off;
-                        S.ph_k[nph] = k;
+                        S.ph_t1[nph] = (int32_t)t1;
                         S.ph_mask[nph] = mask;
                     }
                     off += (int32_t)(t1 - t0) * k;
@@ -333,64 +345,82 @@ __global__ void __launch_bounds__(kThreads, MINB)
                 if (lane == 0) S.ph_off[nph] = off;
                 __syncwarp();
             }
-            // phase containing group-relative offset lo - g0
-            int j = 0;
+            // ---- start: phase j and step t containing group offset lo - g0
             const int32_t o_lo = (int32_t)(lo - g0);
+            int j = 0;
             while (j + 1 < nph && S.ph_off[j + 1] <= o_lo) ++j;
+            unsigned pm = S.ph_mask[j];
+            int k = __popc(pm);
+            int32_t t0j = j ? S.ph_t1[j - 1] : 0;
+            int32_t t = t0j + (int32_t)div_small(o_lo - S.ph_off[j], k);
+            int32_t t1 = S.ph_t1[j];
+            int64_t pb = g0 + S.ph_off[j] + (int64_t)(t - t0j) * k;  // first position of step t
+            bool live = (pm >> lane) & 1u;
+            int rank = __popc(pm & lt);
 
-            int64_t pos = lo;
-            while (pos < hi) {
-                if (pos >= st.bnd) st.prepare(st.cur + 1);
-                const int64_t seg_end = hi < st.bnd ? hi : st.bnd;
-                const int32_t wa = (int32_t)(pos - g0), wb = (int32_t)(seg_end - g0);
-                const double *pr = S.prod + (g0 - st.a);  // pr[o] = product at group offset o
-                // walk phases overlapping [wa, wb)
-                for (;;) {
-                    const int32_t po = S.ph_off[j], pn = S.ph_off[j + 1];
-                    const int32_t plo = wa > po ? wa : po, phi = wb < pn ? wb : pn;
-                    const int k = S.ph_k[j];
-                    const unsigned pm = S.ph_mask[j];
-                    const bool live = (pm >> lane) & 1u;
-                    const int rank = __popc(pm & lt);
-                    // lane-serial unless the phase is long with few live lanes
-                    if (EXACT || k >= 16 || pn - po <= 8 * k) {
-                        if (live && plo < phi) {
-                            // first own step at or after plo (plo == po: step 0)
-                            int32_t p = po + rank;
-                            if (plo != po) {
-                                const int32_t rel = plo - p;
-                                if (rel > 0) p += ceil_div_small(rel, k) * k;
-                            }
-                            for (; p < phi; p += k)
-                                acc = EXACT ? __dadd_rn(acc, pr[p]) : acc + pr[p];
-                        }
-                    } else {
+            // ---- step-uniform lane walk while enough lanes are live
+            while (pb < hi && (EXACT || k >= KT)) {
+                ring.ensure(pb + k);
+                const int64_t P = pb + rank;
+                if (live && P >= lo && P < hi) {
+                    const double v = ring.at(P);
+                    acc = EXACT ? __dadd_rn(acc, v) : acc + v;
+                }
+                pb += k;
+                if (++t == t1) {
+                    if (++j == nph) break;
+                    pm = S.ph_mask[j];
+                    k = __popc(pm);
+                    t1 = S.ph_t1[j];
+                    live = (pm >> lane) & 1u;
+                    rank = __popc(pm & lt);
+                }
+            }
+            // ---- fast mode: remaining phases have few live lanes
+            if (!EXACT) {
+                while (pb < hi && j < nph) {
+                    // steps of this phase inside [.., hi)
+                    int32_t steps = t1 - t;
+                    const int64_t lim = hi - pb;  // > 0
+                    if ((int64_t)steps * k > lim) steps = (int32_t)div_small(lim + k - 1, k);
+                    // a step cut by the slice start is handled lane-serially first
+                    if (steps > 8 && pb >= lo) {
                         const int SS = c_streams[k];
                         const int s = (int)(((uint32_t)lane * c_magic16[k]) >> 16);  // lane / k
                         const int r = lane - s * k;
+                        const int32_t stride = SS * k;
+                        const int64_t pend = pb + (int64_t)steps * k;
                         double v = 0.0;
-                        if (s < SS && plo < phi) {
-                            const int32_t rel = plo - po - r;
-                            int32_t t = rel > 0 ? ceil_div_small(rel, k) : 0;
-                            t += (s - t) & (SS - 1);  // next step of sub-stream s
-                            const int32_t stride = SS * k;
-                            int32_t p = po + t * k + r;
-                            double v1 = 0.0;
-                            for (; p + stride < phi; p += 2 * stride) {
-                                v += pr[p];
-                                v1 += pr[p + stride];
-                            }
-                            if (p < phi) v += pr[p];
-                            v += v1;
+                        for (int64_t q = pb; q < pend; q += stride) {  // one iteration = SS steps
+                            ring.ensure(q + stride < pend ? q + stride : pend);
+                            const int64_t P = q + s * k + r;
+                            if (s < SS && P < pend && P < hi) v += ring.at(P);
                         }
-                        for (int d = SS >> 1; d >= 1; d >>= 1) v += __shfl_down_sync(FULL, v, d * k);
+                        for (int d = SS >> 1; d >= 1; d >>= 1)
+                            v += __shfl_down_sync(FULL, v, d * k);
                         const double tot = __shfl_sync(FULL, v, live ? rank : 0);
                         if (live) acc += tot;
+                        pb = pend;
+                        t += steps;
+                    } else {
+                        const int32_t n1 = steps > 8 ? 1 : steps;
+                        for (int32_t i = 0; i < n1; ++i) {
+                            ring.ensure(pb + k);
+                            const int64_t P = pb + rank;
+                            if (live && P >= lo && P < hi) acc += ring.at(P);
+                            pb += k;
+                        }
+                        t += n1;
                     }
-                    if (pn <= wb && j + 1 < nph) ++j;
-                    else break;
+                    if (t == t1) {
+                        if (++j == nph) break;
+                        pm = S.ph_mask[j];
+                        k = __popc(pm);
+                        t1 = S.ph_t1[j];
+                        live = (pm >> lane) & 1u;
+                        rank = __popc(pm & lt);
+                    }
                 }
-                pos = seg_end;
             }
         }
 
@@ -447,8 +477,8 @@ int launch(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *
         attr = true;
     }
     unsigned grid = (unsigned)((b->workers + kWarps - 1) / kWarps);
-    k_spmv_stream<V, EXACT, CH, MINB, XNA><<<grid, kThreads, smem, st>>>(*f, *b, (const V *)x,
-                                                                      (V *)y, partial);
+    k_spmv_stream<V, EXACT, CH, MINB, XNA><<<grid, kThreads, smem, st>>>(
+        *f, *b, (const V *)x, (V *)y, partial);
     return (int)cudaGetLastError();
 }
 
@@ -461,9 +491,9 @@ int occupancy_of(int *per_sm) {
         per_sm, k_spmv_stream<V, EXACT, CH, MINB, XNA>, kThreads, smem);
 }
 
-// Tile / occupancy variants (chunk CH, min CTAs per SM), chosen with the
-// environment variable HBP_STREAM_VARIANT for sweeps; 0 is the default.
-constexpr int kVariants = 9;
+// Tile / occupancy variants (chunk CH, min CTAs per SM, L1 policy of the x
+// gathers), chosen with HBP_STREAM_VARIANT for sweeps; 0 is the default.
+constexpr int kVariants = 5;
 int variant() {
     static int v = -1;
     if (v < 0) {
@@ -474,17 +504,13 @@ int variant() {
     return v;
 }
 
-#define HBP_STREAM_VARIANTS(FN, V, EXACT, ...)          \
-    switch (variant()) {                                 \
-        case 1: return FN<V, EXACT, 256, 4, false>(__VA_ARGS__); \
-        case 5: return FN<V, EXACT, 256, 3, false>(__VA_ARGS__); \
-        case 6: return FN<V, EXACT, 256, 4, true>(__VA_ARGS__); \
-        case 7: return FN<V, EXACT, 128, 4, true>(__VA_ARGS__); \
-        case 8: return FN<V, EXACT, 512, 2, true>(__VA_ARGS__); \
-        case 2: return FN<V, EXACT, 128, 4, false>(__VA_ARGS__); \
-        case 3: return FN<V, EXACT, 512, 2, false>(__VA_ARGS__); \
-        case 4: return FN<V, EXACT, 128, 6, false>(__VA_ARGS__); \
-        default: return FN<V, EXACT, 256, 3, true>(__VA_ARGS__); \
+#define HBP_STREAM_VARIANTS(FN, V, EXACT, ...)                   \
+    switch (variant()) {                                          \
+        case 1: return FN<V, EXACT, 128, 4, true>(__VA_ARGS__);  \
+        case 2: return FN<V, EXACT, 256, 3, true>(__VA_ARGS__);  \
+        case 3: return FN<V, EXACT, 128, 3, false>(__VA_ARGS__); \
+        case 4: return FN<V, EXACT, 128, 2, true>(__VA_ARGS__);  \
+        default: return FN<V, EXACT, 128, 3, true>(__VA_ARGS__); \
     }
 
 template <typename V, bool EXACT>
@@ -509,8 +535,10 @@ int hbp_stream_workers(const hbp_format_t *f, int64_t *workers) {
     HBP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const bool exact = f->exact != 0 || f->dtype == HBP_F64;
     int rc;
-    if (f->dtype == HBP_F64) rc = exact ? occupancy<double, true>(&per_sm) : occupancy<double, false>(&per_sm);
-    else rc = exact ? occupancy<float, true>(&per_sm) : occupancy<float, false>(&per_sm);
+    if (f->dtype == HBP_F64)
+        rc = exact ? occupancy<double, true>(&per_sm) : occupancy<double, false>(&per_sm);
+    else
+        rc = exact ? occupancy<float, true>(&per_sm) : occupancy<float, false>(&per_sm);
     if (rc) return rc;
     int64_t wmax = (int64_t)sms * per_sm * kWarps;
     int64_t wcap = f->nnz / 1024;
