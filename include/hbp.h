@@ -217,7 +217,18 @@ typedef struct {
     const void *data;            /* [nnz] */
     const int64_t *rb_ptr;       /* [nrb+1] combine lists, ascending bc */
     const int32_t *rb_blk;       /* [nzb] */
+    const int64_t *phase_ptr;    /* [nzb*gpb + 1] phase stream index (W = 32), nullable */
+    const void *phases;          /* uint2 (live mask, group offset) per phase, nullable */
 } hbp_format_t;
+
+/* Phase stream (runtime index used by hbp_spmv_stream, W = 32): a group's
+ * phases are its maximal step ranges with a fixed live-lane set; phase j is
+ * (live mask, element offset within the group).  nph[ngroups] is set to 0
+ * so an exclusive sum of nph gives phase_ptr. */
+int hbp_phase_counts(const uint32_t *slot_len, int64_t ngroups, int64_t *nph,
+                     hbp_stream_t stream);
+int hbp_phase_emit(const uint32_t *slot_len, int64_t ngroups, const int64_t *phase_ptr,
+                   void *phases, hbp_stream_t stream);
 
 typedef struct {
     int64_t workers;     /* persistent warps (paper: one warp per worker) */

@@ -38,6 +38,7 @@ class FormatT(ctypes.Structure):
         ("dtype", ctypes.c_int32), ("exact", ctypes.c_int32),
         ("blk_br", c_vp), ("blk_bc", c_vp), ("slot_len", c_vp), ("perm", c_vp),
         ("group_start", c_vp), ("col", c_vp), ("data", c_vp), ("rb_ptr", c_vp), ("rb_blk", c_vp),
+        ("phase_ptr", c_vp), ("phases", c_vp),
     ]
 
 
@@ -86,6 +87,8 @@ _SIGS = {
     "hbp_emit": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_int,
                  c_vp, c_vp, c_vp, c_vp],
     "hbp_row_block_counts": [c_vp, c_i64, c_vp, c_vp],
+    "hbp_phase_counts": [c_vp, c_i64, c_vp, c_vp],
+    "hbp_phase_emit": [c_vp, c_i64, c_vp, c_vp, c_vp],
     "hbp_expand_reference": [c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp,
                              c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
     "hbp_walk_chains": [c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64,

@@ -436,6 +436,51 @@ __global__ void k_emit(const uint32_t *__restrict__ slot_len, const uint32_t *__
     }
 }
 
+// ---- phase stream (runtime index for the streaming SpMV, W = 32) --------
+// A group's "phases" are its maximal step ranges with a fixed live-lane set
+// (one per distinct nonzero slot length).  Phase j is stored as
+// (live mask, group-relative element offset); k = popc(mask), its step count
+// is (next offset - offset) / k.  Warp per group.
+__global__ void k_phase_counts(const uint32_t *__restrict__ slot_len, int64_t ngroups,
+                               int64_t *__restrict__ nph) {
+    const int lane = threadIdx.x & 31;
+    int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t g = warp; g < ngroups; g += nwarps) {
+        const uint32_t len = slot_len[g * 32 + lane];
+        // distinct nonzero lengths: lane counts if no lower lane has the same length
+        const unsigned same = __match_any_sync(0xffffffffu, len);
+        const bool first = len > 0 && (same & ((1u << lane) - 1u)) == 0u;
+        const int n = __popc(__ballot_sync(0xffffffffu, first));
+        if (lane == 0) nph[g] = n;
+    }
+    if (warp == 0 && lane == 0) nph[ngroups] = 0;
+}
+
+__global__ void k_phase_emit(const uint32_t *__restrict__ slot_len, int64_t ngroups,
+                             const int64_t *__restrict__ phase_ptr, uint2 *__restrict__ phases) {
+    const int lane = threadIdx.x & 31;
+    int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t g = warp; g < ngroups; g += nwarps) {
+        const uint32_t len = slot_len[g * 32 + lane];
+        uint2 *out = phases + phase_ptr[g];
+        uint32_t t0 = 0, off = 0;
+        int j = 0;
+        bool live = len > 0;
+        unsigned mask = __ballot_sync(0xffffffffu, live);
+        while (mask) {
+            const uint32_t t1 = __reduce_min_sync(0xffffffffu, live ? len : 0xffffffffu);
+            if (lane == (j & 31)) out[j] = make_uint2(mask, off);
+            off += (t1 - t0) * (uint32_t)__popc(mask);
+            ++j;
+            t0 = t1;
+            live = len > t0;
+            mask = __ballot_sync(0xffffffffu, live);
+        }
+    }
+}
+
 __global__ void k_rb_counts(const int32_t *__restrict__ blk_br, int64_t nzb,
                             int64_t *__restrict__ cnt) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nzb;
@@ -751,6 +796,24 @@ int hbp_emit(const uint32_t *slot_len, const uint32_t *perm, const int64_t *star
                                                 add_sign);
     else
         return HBP_E_ARG;
+    HBP_LAUNCH_CHECK();
+    return HBP_OK;
+}
+
+int hbp_phase_counts(const uint32_t *slot_len, int64_t ngroups, int64_t *nph,
+                     hbp_stream_t stream) {
+    if (ngroups < 0) return HBP_E_ARG;
+    k_phase_counts<<<grid_for((ngroups + 1) * 32, kThreads), kThreads, 0, as_stream(stream)>>>(
+        slot_len, ngroups, nph);
+    HBP_LAUNCH_CHECK();
+    return HBP_OK;
+}
+
+int hbp_phase_emit(const uint32_t *slot_len, int64_t ngroups, const int64_t *phase_ptr,
+                   void *phases, hbp_stream_t stream) {
+    if (ngroups <= 0) return HBP_OK;
+    k_phase_emit<<<grid_for(ngroups * 32, kThreads), kThreads, 0, as_stream(stream)>>>(
+        slot_len, ngroups, phase_ptr, (uint2 *)phases);
     HBP_LAUNCH_CHECK();
     return HBP_OK;
 }

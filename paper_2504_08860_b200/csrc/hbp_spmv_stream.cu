@@ -10,19 +10,21 @@
 //      array (exact mode: slice ends rounded up to group boundaries);
 //   2. lane 0 streams the slice's col/data into a shared-memory ring of NB
 //      chunks of CH elements with cp.async.bulk (TMA bulk copies completing
-//      on per-slot mbarriers), NB-2 chunks ahead of the walk;
-//   3. per chunk the warp gathers x for all CH elements at once and writes
-//      the products in place of the values (f32 data: f32 products, exact
-//      f64 data: __dmul_rn products), so the ring always holds the products
-//      of the two chunks the walk can touch;
-//   4. the group's phase table (offset, steps, live mask) is built from the
-//      32 slot lengths with ballots; the walk then runs
+//      on per-slot mbarriers), NB-3 chunks ahead of the walk;
+//   3. the x gathers of chunk c+1 are issued (registers) before the walk of
+//      chunk c needs them; when the walk reaches chunk c+1 the products are
+//      written over its values (f32 data: f32 products; exact f64 data:
+//      __dmul_rn products), so products of the chunks the walk can touch are
+//      always resident;
+//   4. each group's phases come precomputed from the phase stream (live mask
+//      and element offset per phase, hbp_phase_emit); the walk runs
 //        - a step-uniform loop while >= KT lanes are live (exact mode: all
-//          steps): every live lane adds its element of the step, phase
-//          changes only reload (k, mask, rank) -- each row is summed in
-//          step order, bitwise identical to _kernels.py:41-46 for f64;
-//        - (fast mode) per remaining phase: short ones lane-serially, long
-//          ones with S = 32/k sub-streams per live lane and a shuffle tree;
+//          steps): every live lane adds its element of the step -- each row
+//          is summed in step order, bitwise identical to _kernels.py:41-46
+//          for f64;
+//        - (fast mode) the remaining few-lane phases: short ones lane by
+//          lane, long ones with S = 32/k sub-streams per live lane and a
+//          shuffle tree;
 //   5. a group cut by a slice boundary (fast mode only) leaves per-lane
 //      partials; the warp whose piece completes the group's element count
 //      (atomic) adds the pieces in slice order -- deterministic.
@@ -43,15 +45,13 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int NB = 4;  // ring slots (chunks)
 
-template <typename V, int CH>
+template <typename V, int CH, int NB>
 struct __align__(16) WarpSmem {
     uint32_t col[NB * CH];
     V val[NB * CH];  // values, then products in place
+    uint32_t ph_mask[33];
     int32_t ph_off[33];
-    int32_t ph_t1[32];
-    uint32_t ph_mask[32];
     uint64_t mbar[NB];
 };
 
@@ -110,8 +110,8 @@ __constant__ uint64_t c_magic32[33] = {
     178956971ull,  171798692ull,  165191050ull,  159072863ull,  153391690ull,  148102321ull,
     143165577ull,  138547333ull,  134217728ull};
 
-__device__ __forceinline__ int64_t div_small(int64_t n, int k) {  // n >= 0, 1 <= k <= 32
-    if (n < (1 << 26)) return (int64_t)(((uint64_t)n * c_magic32[k]) >> 32);
+__device__ __forceinline__ int32_t div_small(int32_t n, int k) {  // 0 <= n < 2^30
+    if (n < (1 << 26)) return (int32_t)(((uint64_t)(uint32_t)n * c_magic32[k]) >> 32);
     return n / k;
 }
 
@@ -148,113 +148,109 @@ __device__ __forceinline__ V product(V v, V xv) {
     return v * xv;
 }
 
-template <typename V, bool EXACT, int CH, bool XNA>
+// Streams one warp's slice through the shared-memory ring.  All positions
+// are 32-bit offsets relative to `base` (slice start rounded down to 16 B).
+template <typename V, bool EXACT, int CH, int NB, bool XNA>
 struct Ring {
     static constexpr int RMASK = NB * CH - 1;
+    static constexpr int EPL = CH / 32;  // elements per lane per chunk
     const hbp_format_t &f;
-    WarpSmem<V, CH> &S;
+    WarpSmem<V, CH, NB> &S;
     const V *__restrict__ x;
-    int64_t c_lo, c_hi, base, nchunks;
-    int64_t ready = -1;   // highest prepared chunk
-    int64_t issued = 0;   // chunks whose bulk copy was issued
-    int64_t res_hi = 0;   // products resident for positions < res_hi
+    int64_t base;
+    int32_t len32;        // c_hi - base
+    int32_t nchunks;
+    int32_t ready = -1;   // chunks <= ready hold products
+    int32_t pending = -1; // chunk whose x gathers are in flight
+    int32_t issued = 0;   // bulk copies issued (lane 0)
+    int32_t res32 = 0;    // products resident for offsets < res32
     int lane;
     uint64_t pe, pl;
+    V xr[EPL];            // gathered x of the pending chunk
 
-    __device__ __forceinline__ int64_t chunk_start(int64_t c) const { return base + c * CH; }
-
-    __device__ void issue_upto(int64_t last) {  // lane 0
+    __device__ void issue_upto(int32_t last) {  // lane 0
         for (; issued <= last && issued < nchunks; ++issued) {
-            const int64_t ca = chunk_start(issued);
-            const int64_t cb = ca + CH < c_hi ? ca + CH : c_hi;
-            const int slot = (int)(issued % NB);
-            const uint32_t bc = (uint32_t)(((cb - ca) * 4 + 15) & ~(int64_t)15);
-            const uint32_t bv = (uint32_t)(((cb - ca) * (int64_t)sizeof(V) + 15) & ~(int64_t)15);
+            const int32_t ca = issued * CH;
+            const int32_t n = (ca + CH < len32 ? ca + CH : len32) - ca;
+            const int slot = issued % NB;
+            const uint32_t bc = (uint32_t)((n * 4 + 15) & ~15);
+            const uint32_t bv = (uint32_t)((n * (int)sizeof(V) + 15) & ~15);
             mbar_expect_tx(&S.mbar[slot], bc + bv);
-            bulk_g2s(&S.col[slot * CH], f.col + ca, bc, &S.mbar[slot], pe);
-            bulk_g2s(&S.val[slot * CH], (const V *)f.data + ca, bv, &S.mbar[slot], pe);
+            bulk_g2s(&S.col[slot * CH], f.col + base + ca, bc, &S.mbar[slot], pe);
+            bulk_g2s(&S.val[slot * CH], (const V *)f.data + base + ca, bv, &S.mbar[slot], pe);
         }
     }
 
-    // wait for chunk c's bytes, gather x, overwrite its values with products
-    __device__ void prepare(int64_t c) {
-        const int slot = (int)(c % NB);
+    // chunk c: wait for its bytes, issue its x gathers into xr
+    __device__ __forceinline__ void start(int32_t c) {
+        const int slot = c % NB;
         mbar_wait(&S.mbar[slot], (uint32_t)((c / NB) & 1));
-        const int64_t ca = chunk_start(c);
-        const int n = (int)((ca + CH < c_hi ? ca + CH : c_hi) - ca);
-        constexpr int U = CH / 128;
-        uint4 cl[U];
-        V vv[U][4];
-        V xv[U][4];
+        const int32_t n = (c * CH + CH < len32 ? c * CH + CH : len32) - c * CH;
+        uint32_t cc[EPL];
+        if constexpr (EPL == 4) {
+            const uint4 t = *reinterpret_cast<const uint4 *>(&S.col[slot * CH + 4 * lane]);
+            cc[0] = t.x, cc[1] = t.y, cc[2] = t.z, cc[3] = t.w;
+        } else if constexpr (EPL == 2) {
+            const uint2 t = *reinterpret_cast<const uint2 *>(&S.col[slot * CH + 2 * lane]);
+            cc[0] = t.x, cc[1] = t.y;
+        } else {
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int i = 4 * lane + 128 * u;
-            cl[u] = *reinterpret_cast<const uint4 *>(&S.col[slot * CH + i]);
-            if (i + 3 >= n) {  // never gather past the slice
-                if (i >= n) cl[u].x = 0u;
-                if (i + 1 >= n) cl[u].y = 0u;
-                if (i + 2 >= n) cl[u].z = 0u;
-                cl[u].w = 0u;
-            }
-            if (sizeof(V) == 4) {
-                const float4 t = *reinterpret_cast<const float4 *>(&S.val[slot * CH + i]);
-                vv[u][0] = t.x, vv[u][1] = t.y, vv[u][2] = t.z, vv[u][3] = t.w;
-            } else {
-                const double2 t0 = *reinterpret_cast<const double2 *>(&S.val[slot * CH + i]);
-                const double2 t1 = *reinterpret_cast<const double2 *>(&S.val[slot * CH + i + 2]);
-                vv[u][0] = t0.x, vv[u][1] = t0.y, vv[u][2] = t1.x, vv[u][3] = t1.y;
+            for (int e = 0; e < EPL; e += 4) {
+                const uint4 t =
+                    *reinterpret_cast<const uint4 *>(&S.col[slot * CH + EPL * lane + e]);
+                cc[e] = t.x, cc[e + 1] = t.y, cc[e + 2] = t.z, cc[e + 3] = t.w;
             }
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t cc[4] = {cl[u].x, cl[u].y, cl[u].z, cl[u].w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-                xv[u][e] = XNA ? ld_x_na(x + cc[e], pl) : ld_x(x + cc[e], pl);
+        for (int e = 0; e < EPL; ++e) {
+            if (EPL * lane + e >= n) cc[e] = 0u;  // never gather past the slice
+            xr[e] = XNA ? ld_x_na(x + cc[e], pl) : ld_x(x + cc[e], pl);
         }
+        pending = c;
+    }
+
+    // pending chunk: values -> products (in place)
+    __device__ __forceinline__ void finish() {
+        const int c = pending;
+        const int slot = c % NB;
+        V *v = &S.val[slot * CH + EPL * lane];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int i = 4 * lane + 128 * u;
-            V p[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) p[e] = product<V, EXACT>(vv[u][e], xv[u][e]);
-            if (sizeof(V) == 4) {
-                *reinterpret_cast<float4 *>(&S.val[slot * CH + i]) =
-                    make_float4((float)p[0], (float)p[1], (float)p[2], (float)p[3]);
-            } else {
-                *reinterpret_cast<double2 *>(&S.val[slot * CH + i]) =
-                    make_double2((double)p[0], (double)p[1]);
-                *reinterpret_cast<double2 *>(&S.val[slot * CH + i + 2]) =
-                    make_double2((double)p[2], (double)p[3]);
-            }
-        }
-        fence_proxy_async();  // our generic accesses precede later bulk writes of the ring
-        __syncwarp();
+        for (int e = 0; e < EPL; ++e) v[e] = product<V, EXACT>(v[e], xr[e]);
         ready = c;
-        res_hi = ca + n;
-        // slots of chunks < c - 1 are free: keep NB - 2 chunks in flight
-        if (lane == 0) issue_upto(c + NB - 2);
+        res32 = (c * CH + CH < len32 ? c * CH + CH : len32);
+        pending = -1;
     }
 
-    // make positions < need resident (warp-uniform call)
-    __device__ __forceinline__ void ensure(int64_t need) {
-        while (need > res_hi && ready + 1 < nchunks) prepare(ready + 1);
+    // make offsets < need resident (warp-uniform); refills the ring
+    __device__ __forceinline__ void advance(int32_t need) {
+        while (need > res32) {
+            if (pending < 0) {
+                if (ready + 1 >= nchunks) return;
+                start(ready + 1);
+            }
+            __syncwarp();  // the walk's reads of the oldest slot are done
+            finish();
+            fence_proxy_async();  // generic ring accesses precede later bulk writes
+            __syncwarp();
+            if (ready + 1 < nchunks) start(ready + 1);
+            // slots of chunks <= ready - 2 are free (the walk may still read
+            // ready - 1 for a step straddling the boundary)
+            if (lane == 0) issue_upto(ready + NB - 2);
+        }
     }
 
-    __device__ __forceinline__ double at(int64_t P) const {
-        return (double)S.val[(int)((P - base) & RMASK)];
-    }
+    __device__ __forceinline__ double at(int32_t o) const { return (double)S.val[o & RMASK]; }
 };
 
-template <typename V, bool EXACT, int CH, int MINB, bool XNA>
+template <typename V, bool EXACT, int CH, int NB, int MINB, bool XNA>
 __global__ void __launch_bounds__(kThreads, MINB)
     k_spmv_stream(const hbp_format_t f, const hbp_balanced_t b, const V *__restrict__ x,
                   V *__restrict__ y, double *__restrict__ partial) {
-    constexpr int KT = 8;  // fast mode: lanes live below which phases go cooperative
+    constexpr int KT = 8;  // fast mode: fewer live lanes -> per-phase processing
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
-    WarpSmem<V, CH> &S = reinterpret_cast<WarpSmem<V, CH> *>(smem_raw)[wib];
+    WarpSmem<V, CH, NB> &S = reinterpret_cast<WarpSmem<V, CH, NB> *>(smem_raw)[wib];
     const int64_t w = (int64_t)blockIdx.x * kWarps + wib;
     const int64_t Nw = b.workers;
     if (w >= Nw) return;
@@ -263,10 +259,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
     const int64_t ngroups = f.nzb * gpb;
     const int64_t E = f.nnz;
     const int64_t *__restrict__ gs = f.group_start;
-    const uint32_t *__restrict__ slot_len = (const uint32_t *)f.slot_len;
+    const int64_t *__restrict__ pptr = f.phase_ptr;
+    const uint2 *__restrict__ phs = (const uint2 *)f.phases;
     const uint32_t *__restrict__ permp = (const uint32_t *)f.perm;
 
-    Ring<V, EXACT, CH, XNA> ring{f, S, x};
+    Ring<V, EXACT, CH, NB, XNA> ring{f, S, x};
     ring.lane = lane;
     ring.pe = policy_evict_first();
     ring.pl = policy_evict_last();
@@ -282,37 +279,43 @@ __global__ void __launch_bounds__(kThreads, MINB)
             if (gs[g] != c_hi) c_hi = gs[g + 1];
         }
     }
-    ring.c_lo = c_lo;
-    ring.c_hi = c_hi;
-    ring.base = c_lo & ~(int64_t)3;
-    ring.res_hi = ring.base;
-    ring.nchunks = c_hi > c_lo ? (c_hi - ring.base + CH - 1) / CH : 0;
+    const int64_t base = c_lo & ~(int64_t)3;
+    ring.base = base;
+    ring.len32 = (int32_t)(c_hi - base);
+    ring.nchunks = c_hi > c_lo ? (ring.len32 + CH - 1) / CH : 0;
 
     if (lane == 0) {
         for (int i = 0; i < NB; ++i) mbar_init(&S.mbar[i], 1);
         fence_mbar_init();
     }
     __syncwarp();
-    if (lane == 0) ring.issue_upto(NB - 2);
+    if (lane == 0) ring.issue_upto(NB - 3);
 
     int64_t g = upper_group(gs, ngroups, c_lo);
     if (!(g < ngroups && gs[g] < c_lo)) g = lower_group(gs, ngroups, c_lo);
     const bool last_warp = (w == Nw - 1);
 
-    // prefetched metadata of group g
+    // prefetched metadata of group g: element range, output rows, phases
     int64_t gs0 = g < ngroups ? gs[g] : E;
     int64_t gs1 = g < ngroups ? gs[g + 1] : E;
-    uint32_t len_n = g < ngroups ? slot_len[g * 32 + lane] : 0u;
     uint32_t perm_n = g < ngroups ? permp[g * 32 + lane] : 0u;
+    int64_t pp0 = g < ngroups ? pptr[g] : 0;
+    int64_t pp1 = g < ngroups ? pptr[g + 1] : 0;
+    uint2 ph_n = make_uint2(0u, 0u);
+    if (g < ngroups && lane < pp1 - pp0) ph_n = phs[pp0 + lane];
 
     for (; g < ngroups && (gs0 < c_hi || last_warp); ++g) {
-        const uint32_t len = len_n, row_local = perm_n;
+        const uint32_t row_local = perm_n;
         const int64_t g0 = gs0, g1 = gs1;
+        const int np = (int)(pp1 - pp0);
+        const uint2 ph = ph_n;
         if (g + 1 < ngroups) {  // prefetch the next group's metadata
             gs0 = g1;
             gs1 = gs[g + 2];
-            len_n = slot_len[(g + 1) * 32 + lane];
             perm_n = permp[(g + 1) * 32 + lane];
+            pp0 = pp1;
+            pp1 = pptr[g + 2];
+            ph_n = lane < pp1 - pp0 ? phs[pp0 + lane] : make_uint2(0u, 0u);
         }
         const int64_t lo = g0 > c_lo ? g0 : c_lo;
         const int64_t hi = g1 < c_hi ? g1 : c_hi;
@@ -320,106 +323,93 @@ __global__ void __launch_bounds__(kThreads, MINB)
 
         double acc = 0.0;
         if (lo < hi) {
-            // ---- phase table: ph_off[j] (group offset of phase j), ph_t1[j]
-            // (its end step), ph_mask[j] (live lanes)
-            int nph = 0;
-            {
-                uint32_t t0 = 0;
-                int32_t off = 0;
-                bool live = len > 0;
-                unsigned mask = __ballot_sync(FULL, live);
-                while (mask) {
-                    const int k = __popc(mask);
-                    const uint32_t t1 = __reduce_min_sync(FULL, live ? len : 0xffffffffu);
-                    if (lane == nph) {
-                        S.ph_off[nph] = off;
-                        S.ph_t1[nph] = (int32_t)t1;
-                        S.ph_mask[nph] = mask;
-                    }
-                    off += (int32_t)(t1 - t0) * k;
-                    ++nph;
-                    t0 = t1;
-                    live = len > t0;
-                    mask = __ballot_sync(FULL, live);
-                }
-                if (lane == 0) S.ph_off[nph] = off;
-                __syncwarp();
+            __syncwarp();  // previous group's table reads are done
+            if (lane < np) {
+                S.ph_mask[lane] = ph.x;
+                S.ph_off[lane] = (int32_t)ph.y;
             }
-            // ---- start: phase j and step t containing group offset lo - g0
-            const int32_t o_lo = (int32_t)(lo - g0);
+            if (lane == 0) S.ph_off[np] = (int32_t)(g1 - g0);
+            __syncwarp();
+            const int32_t gb = (int32_t)(g0 - base);  // group start, ring offset (may be < 0)
+            const int32_t lo_r = (int32_t)(lo - base), hi_r = (int32_t)(hi - base);
+            // start: phase j and step t containing lo
+            const int32_t o_lo = lo_r - gb;
             int j = 0;
-            while (j + 1 < nph && S.ph_off[j + 1] <= o_lo) ++j;
+            while (j + 1 < np && S.ph_off[j + 1] <= o_lo) ++j;
             unsigned pm = S.ph_mask[j];
             int k = __popc(pm);
-            int32_t t0j = j ? S.ph_t1[j - 1] : 0;
-            int32_t t = t0j + (int32_t)div_small(o_lo - S.ph_off[j], k);
-            int32_t t1 = S.ph_t1[j];
-            int64_t pb = g0 + S.ph_off[j] + (int64_t)(t - t0j) * k;  // first position of step t
+            int32_t pend_j = gb + S.ph_off[j + 1];  // ring offset where phase j ends
+            int32_t pb = gb + S.ph_off[j] + div_small(o_lo - S.ph_off[j], k) * k;
             bool live = (pm >> lane) & 1u;
             int rank = __popc(pm & lt);
 
-            // ---- step-uniform lane walk while enough lanes are live
-            while (pb < hi && (EXACT || k >= KT)) {
-                ring.ensure(pb + k);
-                const int64_t P = pb + rank;
-                if (live && P >= lo && P < hi) {
-                    const double v = ring.at(P);
-                    acc = EXACT ? __dadd_rn(acc, v) : acc + v;
+            // ---- step-uniform lane walk (exact: all phases; fast: k >= KT)
+            while (pb < hi_r && (EXACT || k >= KT)) {
+                const int32_t stop = pend_j < hi_r ? pend_j : hi_r;
+                if (!piece) {
+                    for (; pb < stop; pb += k) {
+                        if (pb + k > ring.res32) ring.advance(pb + k);
+                        if (live) {
+                            const double v = ring.at(pb + rank);
+                            acc = EXACT ? __dadd_rn(acc, v) : acc + v;
+                        }
+                    }
+                } else {
+                    for (; pb < stop; pb += k) {
+                        if (pb + k > ring.res32) ring.advance(pb + k < hi_r ? pb + k : hi_r);
+                        const int32_t P = pb + rank;
+                        if (live && P >= lo_r && P < hi_r) {
+                            const double v = ring.at(P);
+                            acc = EXACT ? __dadd_rn(acc, v) : acc + v;
+                        }
+                    }
                 }
-                pb += k;
-                if (++t == t1) {
-                    if (++j == nph) break;
-                    pm = S.ph_mask[j];
-                    k = __popc(pm);
-                    t1 = S.ph_t1[j];
-                    live = (pm >> lane) & 1u;
-                    rank = __popc(pm & lt);
-                }
+                if (pb < pend_j) break;  // reached hi inside the phase
+                if (++j == np) break;
+                pm = S.ph_mask[j];
+                k = __popc(pm);
+                pend_j = gb + S.ph_off[j + 1];
+                live = (pm >> lane) & 1u;
+                rank = __popc(pm & lt);
             }
-            // ---- fast mode: remaining phases have few live lanes
+            // ---- fast mode: phases with few live lanes
             if (!EXACT) {
-                while (pb < hi && j < nph) {
-                    // steps of this phase inside [.., hi)
-                    int32_t steps = t1 - t;
-                    const int64_t lim = hi - pb;  // > 0
-                    if ((int64_t)steps * k > lim) steps = (int32_t)div_small(lim + k - 1, k);
-                    // a step cut by the slice start is handled lane-serially first
-                    if (steps > 8 && pb >= lo) {
+                while (pb < hi_r && j < np) {
+                    const int32_t stop = pend_j < hi_r ? pend_j : hi_r;
+                    if (stop - pb > 8 * k && pb >= lo_r) {
                         const int SS = c_streams[k];
                         const int s = (int)(((uint32_t)lane * c_magic16[k]) >> 16);  // lane / k
                         const int r = lane - s * k;
                         const int32_t stride = SS * k;
-                        const int64_t pend = pb + (int64_t)steps * k;
                         double v = 0.0;
-                        for (int64_t q = pb; q < pend; q += stride) {  // one iteration = SS steps
-                            ring.ensure(q + stride < pend ? q + stride : pend);
-                            const int64_t P = q + s * k + r;
-                            if (s < SS && P < pend && P < hi) v += ring.at(P);
+                        for (int32_t q = pb; q < stop; q += stride) {  // SS steps per pass
+                            const int32_t need = q + stride < stop ? q + stride : stop;
+                            if (need > ring.res32) ring.advance(need);
+                            const int32_t P = q + s * k + r;
+                            if (s < SS && P < stop) v += ring.at(P);
                         }
                         for (int d = SS >> 1; d >= 1; d >>= 1)
                             v += __shfl_down_sync(FULL, v, d * k);
                         const double tot = __shfl_sync(FULL, v, live ? rank : 0);
                         if (live) acc += tot;
-                        pb = pend;
-                        t += steps;
+                        pb = stop;
                     } else {
-                        const int32_t n1 = steps > 8 ? 1 : steps;
-                        for (int32_t i = 0; i < n1; ++i) {
-                            ring.ensure(pb + k);
-                            const int64_t P = pb + rank;
-                            if (live && P >= lo && P < hi) acc += ring.at(P);
-                            pb += k;
+                        // short phase (or a step cut by the slice start): lane by lane
+                        const int32_t stop1 = stop - pb > 8 * k ? pb + k : stop;
+                        for (; pb < stop1; pb += k) {
+                            if (pb + k > ring.res32) ring.advance(pb + k < hi_r ? pb + k : hi_r);
+                            const int32_t P = pb + rank;
+                            if (live && P >= lo_r && P < hi_r) acc += ring.at(P);
                         }
-                        t += n1;
+                        if (pb < pend_j && stop1 != stop) continue;  // rest of this phase
                     }
-                    if (t == t1) {
-                        if (++j == nph) break;
-                        pm = S.ph_mask[j];
-                        k = __popc(pm);
-                        t1 = S.ph_t1[j];
-                        live = (pm >> lane) & 1u;
-                        rank = __popc(pm & lt);
-                    }
+                    if (pb < pend_j) break;  // reached hi inside the phase
+                    if (++j == np) break;
+                    pm = S.ph_mask[j];
+                    k = __popc(pm);
+                    pend_j = gb + S.ph_off[j + 1];
+                    live = (pm >> lane) & 1u;
+                    rank = __popc(pm & lt);
                 }
             }
         }
@@ -466,34 +456,34 @@ __global__ void __launch_bounds__(kThreads, MINB)
     }
 }
 
-template <typename V, bool EXACT, int CH, int MINB, bool XNA>
+template <typename V, bool EXACT, int CH, int NB, int MINB, bool XNA>
 int launch(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y,
            double *partial, cudaStream_t st) {
-    const size_t smem = sizeof(WarpSmem<V, CH>) * kWarps;
+    const size_t smem = sizeof(WarpSmem<V, CH, NB>) * kWarps;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_spmv_stream<V, EXACT, CH, MINB, XNA>,
+        cudaFuncSetAttribute(k_spmv_stream<V, EXACT, CH, NB, MINB, XNA>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
     unsigned grid = (unsigned)((b->workers + kWarps - 1) / kWarps);
-    k_spmv_stream<V, EXACT, CH, MINB, XNA><<<grid, kThreads, smem, st>>>(
+    k_spmv_stream<V, EXACT, CH, NB, MINB, XNA><<<grid, kThreads, smem, st>>>(
         *f, *b, (const V *)x, (V *)y, partial);
     return (int)cudaGetLastError();
 }
 
-template <typename V, bool EXACT, int CH, int MINB, bool XNA>
+template <typename V, bool EXACT, int CH, int NB, int MINB, bool XNA>
 int occupancy_of(int *per_sm) {
-    const size_t smem = sizeof(WarpSmem<V, CH>) * kWarps;
-    cudaFuncSetAttribute(k_spmv_stream<V, EXACT, CH, MINB, XNA>,
+    const size_t smem = sizeof(WarpSmem<V, CH, NB>) * kWarps;
+    cudaFuncSetAttribute(k_spmv_stream<V, EXACT, CH, NB, MINB, XNA>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        per_sm, k_spmv_stream<V, EXACT, CH, MINB, XNA>, kThreads, smem);
+        per_sm, k_spmv_stream<V, EXACT, CH, NB, MINB, XNA>, kThreads, smem);
 }
 
-// Tile / occupancy variants (chunk CH, min CTAs per SM, L1 policy of the x
-// gathers), chosen with HBP_STREAM_VARIANT for sweeps; 0 is the default.
-constexpr int kVariants = 5;
+// Tile / occupancy variants (chunk CH, ring slots NB, min CTAs per SM),
+// chosen with HBP_STREAM_VARIANT for sweeps; 0 is the default.
+constexpr int kVariants = 4;
 int variant() {
     static int v = -1;
     if (v < 0) {
@@ -504,13 +494,14 @@ int variant() {
     return v;
 }
 
-#define HBP_STREAM_VARIANTS(FN, V, EXACT, ...)                   \
-    switch (variant()) {                                          \
-        case 1: return FN<V, EXACT, 128, 4, true>(__VA_ARGS__);  \
-        case 2: return FN<V, EXACT, 256, 3, true>(__VA_ARGS__);  \
-        case 3: return FN<V, EXACT, 128, 3, false>(__VA_ARGS__); \
-        case 4: return FN<V, EXACT, 128, 2, true>(__VA_ARGS__);  \
-        default: return FN<V, EXACT, 128, 3, true>(__VA_ARGS__); \
+#define HBP_STREAM_VARIANTS(FN, V, EXACT, ...)                          \
+    switch (variant()) {                                                 \
+        case 1: return FN<V, EXACT, 64, 8, 4, true>(__VA_ARGS__);       \
+        case 2: return FN<V, EXACT, 128, 4, 3, true>(__VA_ARGS__);      \
+        case 3: return FN<V, EXACT, 256, 4, 2, true>(__VA_ARGS__);      \
+        default:                                                         \
+            if (sizeof(V) == 8) return FN<V, EXACT, 128, 4, 3, true>(__VA_ARGS__); \
+            return FN<V, EXACT, 128, 8, 3, true>(__VA_ARGS__);           \
     }
 
 template <typename V, bool EXACT>
@@ -551,8 +542,11 @@ int hbp_spmv_stream(const hbp_format_t *f, const hbp_balanced_t *b, const void *
                     double *partial, hbp_stream_t stream) {
     if (!f || !b || b->workers < 1) return HBP_E_ARG;
     if (f->warp_size != 32 || f->row_height % 32) return HBP_E_UNSUPPORTED;
+    if (!f->phases || !f->phase_ptr) return HBP_E_ARG;  // hbp_phase_emit first
     if (!partial && (!y || f->ncb != 1)) return HBP_E_ARG;
     if (f->nzb == 0) return HBP_OK;
+    // slices are addressed with 32-bit offsets
+    if ((f->nnz + b->workers - 1) / b->workers > (int64_t)1 << 30) return HBP_E_UNSUPPORTED;
     const bool exact = f->exact != 0 || f->dtype == HBP_F64;
     if (!exact && (!b->part_head || !b->part_tail || !b->counters)) return HBP_E_ARG;
     cudaStream_t st = as_stream(stream);

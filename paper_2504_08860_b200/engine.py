@@ -157,6 +157,8 @@ class SpmvOperator:
         if schedule in ("balanced", "stream") and hbp.config.warp_size != 32:
             raise ValueError(f"the {schedule} schedule needs warp_size == 32")
         self.schedule = schedule
+        if schedule == "stream":
+            hbp.ensure_phases()
         f = hbp.format_struct()
         if schedule in ("balanced", "stream"):
             if workers is None:

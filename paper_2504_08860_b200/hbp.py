@@ -66,9 +66,33 @@ class HbpMatrix:
         self.group_start_c, self.zero_row_c = group_start_c, zero_row_c
         self.rb_ptr, self.rb_blk = rb_ptr, rb_blk
         self.permutations = permutations
+        self.phase_ptr = None
+        self.phases = None
         self._views: dict = {}
         self._fmt = None
         self._ops: dict = {}
+
+    def ensure_phases(self) -> None:
+        """Build the phase stream (runtime index of hbp_spmv_stream, W = 32):
+        per group its (live mask, element offset) phases, ~9 per group on
+        R-MAT, 8 bytes each (include/hbp.h hbp_phase_counts/emit)."""
+        if self.phases is not None:
+            return
+        if self.config.warp_size != 32:
+            raise ValueError("the phase stream needs warp_size == 32")
+        dev = self.data.device
+        ng = self.nzb * (self.config.row_height // 32)
+        nph = torch.empty(ng + 1, dtype=torch.int64, device=dev)
+        L.call("hbp_phase_counts", L.P(self.slot_len), L.c_i64(ng), L.P(nph), L.stream())
+        ptr = L.exclusive_sum(nph)
+        total = int(ptr[-1].item())
+        phases = torch.zeros(max(1, total) * 2, dtype=torch.int32, device=dev)
+        L.call("hbp_phase_emit", L.P(self.slot_len), L.c_i64(ng), L.P(ptr), L.P(phases),
+               L.stream())
+        self.phase_ptr, self.phases = ptr, phases
+        if self._fmt is not None:
+            self._fmt.phase_ptr = ptr.data_ptr()
+            self._fmt.phases = phases.data_ptr()
 
     # ---- reference attributes
     @property
@@ -194,6 +218,9 @@ class HbpMatrix:
                             ("data", self.data), ("rb_ptr", self.rb_ptr),
                             ("rb_blk", self.rb_blk)):
                 setattr(f, name, t.data_ptr() if t.numel() else 0)
+            if self.phases is not None:
+                f.phase_ptr = self.phase_ptr.data_ptr()
+                f.phases = self.phases.data_ptr()
             self._fmt = f
         return self._fmt
 
