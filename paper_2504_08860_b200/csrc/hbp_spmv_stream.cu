@@ -483,7 +483,7 @@ int occupancy_of(int *per_sm) {
 
 // Tile / occupancy variants (chunk CH, ring slots NB, min CTAs per SM),
 // chosen with HBP_STREAM_VARIANT for sweeps; 0 is the default.
-constexpr int kVariants = 4;
+constexpr int kVariants = 8;
 int variant() {
     static int v = -1;
     if (v < 0) {
@@ -494,14 +494,16 @@ int variant() {
     return v;
 }
 
-#define HBP_STREAM_VARIANTS(FN, V, EXACT, ...)                          \
-    switch (variant()) {                                                 \
-        case 1: return FN<V, EXACT, 64, 8, 4, true>(__VA_ARGS__);       \
-        case 2: return FN<V, EXACT, 128, 4, 3, true>(__VA_ARGS__);      \
-        case 3: return FN<V, EXACT, 256, 4, 2, true>(__VA_ARGS__);      \
-        default:                                                         \
-            if (sizeof(V) == 8) return FN<V, EXACT, 128, 4, 3, true>(__VA_ARGS__); \
-            return FN<V, EXACT, 128, 8, 3, true>(__VA_ARGS__);           \
+#define HBP_STREAM_VARIANTS(FN, V, EXACT, ...)                     \
+    switch (variant()) {                                            \
+        case 1: return FN<V, EXACT, 64, 8, 4, true>(__VA_ARGS__);  \
+        case 2: return FN<V, EXACT, 128, 8, 3, true>(__VA_ARGS__); \
+        case 3: return FN<V, EXACT, 256, 4, 2, true>(__VA_ARGS__); \
+        case 4: return FN<V, EXACT, 128, 8, 2, true>(__VA_ARGS__); \
+        case 5: return FN<V, EXACT, 128, 4, 4, true>(__VA_ARGS__); \
+        case 6: return FN<V, EXACT, 64, 8, 3, true>(__VA_ARGS__);  \
+        case 7: return FN<V, EXACT, 128, 4, 3, false>(__VA_ARGS__); \
+        default: return FN<V, EXACT, 128, 4, 3, true>(__VA_ARGS__); \
     }
 
 template <typename V, bool EXACT>
