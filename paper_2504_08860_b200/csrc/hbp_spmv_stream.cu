@@ -343,74 +343,86 @@ __global__ void __launch_bounds__(kThreads, MINB)
             bool live = (pm >> lane) & 1u;
             int rank = __popc(pm & lt);
 
-            // ---- step-uniform lane walk (exact: all phases; fast: k >= KT)
-            while (pb < hi_r && (EXACT || k >= KT)) {
+            // ---- walk phase by phase.  Steps are summed lane by lane (each
+            // lane its own row, in step order); in fast mode long phases with
+            // fewer than KT live lanes use S = 32/k sub-streams per lane.
+            // Residency checks sit in the outer loops; inner loops only load.
+            const V *__restrict__ rv = S.val;
+            constexpr int RM = NB * CH - 1;
+            for (;;) {
                 const int32_t stop = pend_j < hi_r ? pend_j : hi_r;
-                if (!piece) {
-                    for (; pb < stop; pb += k) {
-                        if (pb + k > ring.res32) ring.advance(pb + k);
-                        if (live) {
-                            const double v = ring.at(pb + rank);
-                            acc = EXACT ? __dadd_rn(acc, v) : acc + v;
+                if (pb < lo_r) {
+                    // a step cut by the slice start (fast-mode pieces only)
+                    if (pb + k > ring.res32) ring.advance(pb + k < hi_r ? pb + k : hi_r);
+                    const int32_t P = pb + rank;
+                    if (live && P >= lo_r && P < hi_r) acc += (double)rv[P & RM];
+                    pb += k;
+                    if (pb < stop) continue;  // rest of this phase
+                } else if (!EXACT && k < KT && stop - pb > 8 * k) {
+                    const int SS = c_streams[k];
+                    const int s = (int)(((uint32_t)lane * c_magic16[k]) >> 16);  // lane / k
+                    const int32_t stride = SS * k;
+                    const bool act = s < SS;
+                    const int32_t off_l = s * k + (lane - s * k);  // = lane for active lanes
+                    double v0 = 0.0, v1 = 0.0;
+                    int32_t q = pb;
+                    while (q < stop) {
+                        const int32_t need = q + stride < stop ? q + stride : stop;
+                        if (need > ring.res32) ring.advance(need);
+                        if (q + stride > stop) {  // last, partial pass
+                            const int32_t P = q + off_l;
+                            if (act && P < stop) v0 += (double)rv[P & RM];
+                            q = stop;
+                            break;
                         }
+                        const int32_t lim = stop < ring.res32 ? stop : ring.res32;
+                        const int32_t npass = div_small(lim - q - stride, stride) + 1;
+                        if (act) {
+                            int32_t p = q + off_l;
+                            int32_t i = 0;
+                            for (; i + 2 <= npass; i += 2, p += 2 * stride) {
+                                v0 += (double)rv[p & RM];
+                                v1 += (double)rv[(p + stride) & RM];
+                            }
+                            if (i < npass) v0 += (double)rv[p & RM];
+                        }
+                        q += npass * stride;
                     }
+                    double v = v0 + v1;
+                    for (int d = SS >> 1; d >= 1; d >>= 1) v += __shfl_down_sync(FULL, v, d * k);
+                    const double tot = __shfl_sync(FULL, v, live ? rank : 0);
+                    if (live) acc += tot;
+                    pb = stop;
                 } else {
-                    for (; pb < stop; pb += k) {
+                    while (pb < stop) {
                         if (pb + k > ring.res32) ring.advance(pb + k < hi_r ? pb + k : hi_r);
-                        const int32_t P = pb + rank;
-                        if (live && P >= lo_r && P < hi_r) {
-                            const double v = ring.at(P);
-                            acc = EXACT ? __dadd_rn(acc, v) : acc + v;
+                        const int32_t lim = stop < ring.res32 ? stop : ring.res32;
+                        const int32_t nsteps = lim - pb >= k ? div_small(lim - pb, k) : 0;
+                        if (nsteps == 0) {  // last step cut by the slice end
+                            const int32_t P = pb + rank;
+                            if (live && P < hi_r) {
+                                const double v = (double)rv[P & RM];
+                                acc = EXACT ? __dadd_rn(acc, v) : acc + v;
+                            }
+                            pb += k;
+                            break;
                         }
+                        if (live) {
+                            int32_t p = pb + rank;
+                            for (int32_t i = 0; i < nsteps; ++i, p += k) {
+                                const double v = (double)rv[p & RM];
+                                acc = EXACT ? __dadd_rn(acc, v) : acc + v;
+                            }
+                        }
+                        pb += nsteps * k;
                     }
                 }
-                if (pb < pend_j) break;  // reached hi inside the phase
-                if (++j == np) break;
+                if (pb < pend_j || ++j == np) break;  // reached hi, or the group's end
                 pm = S.ph_mask[j];
                 k = __popc(pm);
                 pend_j = gb + S.ph_off[j + 1];
                 live = (pm >> lane) & 1u;
                 rank = __popc(pm & lt);
-            }
-            // ---- fast mode: phases with few live lanes
-            if (!EXACT) {
-                while (pb < hi_r && j < np) {
-                    const int32_t stop = pend_j < hi_r ? pend_j : hi_r;
-                    if (stop - pb > 8 * k && pb >= lo_r) {
-                        const int SS = c_streams[k];
-                        const int s = (int)(((uint32_t)lane * c_magic16[k]) >> 16);  // lane / k
-                        const int r = lane - s * k;
-                        const int32_t stride = SS * k;
-                        double v = 0.0;
-                        for (int32_t q = pb; q < stop; q += stride) {  // SS steps per pass
-                            const int32_t need = q + stride < stop ? q + stride : stop;
-                            if (need > ring.res32) ring.advance(need);
-                            const int32_t P = q + s * k + r;
-                            if (s < SS && P < stop) v += ring.at(P);
-                        }
-                        for (int d = SS >> 1; d >= 1; d >>= 1)
-                            v += __shfl_down_sync(FULL, v, d * k);
-                        const double tot = __shfl_sync(FULL, v, live ? rank : 0);
-                        if (live) acc += tot;
-                        pb = stop;
-                    } else {
-                        // short phase (or a step cut by the slice start): lane by lane
-                        const int32_t stop1 = stop - pb > 8 * k ? pb + k : stop;
-                        for (; pb < stop1; pb += k) {
-                            if (pb + k > ring.res32) ring.advance(pb + k < hi_r ? pb + k : hi_r);
-                            const int32_t P = pb + rank;
-                            if (live && P >= lo_r && P < hi_r) acc += ring.at(P);
-                        }
-                        if (pb < pend_j && stop1 != stop) continue;  // rest of this phase
-                    }
-                    if (pb < pend_j) break;  // reached hi inside the phase
-                    if (++j == np) break;
-                    pm = S.ph_mask[j];
-                    k = __popc(pm);
-                    pend_j = gb + S.ph_off[j + 1];
-                    live = (pm >> lane) & 1u;
-                    rank = __popc(pm & lt);
-                }
             }
         }
 
