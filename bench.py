@@ -237,7 +237,17 @@ def run_gpu(args):
         grid = H.make_grid(csr, cfg)
         torch.cuda.synchronize()
         t1 = time.perf_counter()
-        params = H.sample_hash_params(grid, cfg)
+        if dist:
+            # this rank's rows are a stripe of the stacked global matrix; (a, c)
+            # come from the global sample (stripes.sample_hash_params_global)
+            from paper_2504_08860_b200.reorder import _grid_counts_at
+            from paper_2504_08860_b200.stripes import Stripe, sample_hash_params_global
+            stripe = Stripe(rank, 0, 0, rank * rows, (rank + 1) * rows)
+            params = sample_hash_params_global(lambda flat: _grid_counts_at(grid, flat), stripe,
+                                               world * rows, grid.num_col_blocks, 512,
+                                               device=dev)
+        else:
+            params = H.sample_hash_params(grid, cfg)
         torch.cuda.synchronize()
         t2 = time.perf_counter()
         perms = H.hash_permutations(grid, params)
