@@ -151,20 +151,19 @@ struct Pipe {
     V b_x[U][4];
     V b_val[U][4];
 
+    int32_t a_off;  // chunk offset of stage A (its elements past len32 are masked at use)
+
+    // issue chunk c's col/data loads; the registers are not touched until
+    // a_to_b() (a consumer here would stall on the loads right away)
     __device__ __forceinline__ void load_a(int32_t c) {
+        a_off = c * CH;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int32_t o = c * CH + 128 * u + 4 * lane;
-            if (c < nchunks && o < len32) {
+            if (o < len32) {
                 const uint4 t = ld_stream_v4(col + o, pe);
                 a_col[u][0] = t.x, a_col[u][1] = t.y, a_col[u][2] = t.z, a_col[u][3] = t.w;
                 ld_vals4(data + o, pe, a_val[u]);
-#pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    if (o + e >= len32) a_col[u][e] = 0u;  // never gather past the slice
-            } else {
-#pragma unroll
-                for (int e = 0; e < 4; ++e) a_col[u][e] = 0u, a_val[u][e] = (V)0;
             }
         }
     }
@@ -173,8 +172,11 @@ struct Pipe {
         for (int u = 0; u < U; ++u)
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                b_x[u][e] = XNA ? ld_x_na(x + a_col[u][e], pl) : ld_x(x + a_col[u][e], pl);
-                b_val[u][e] = a_val[u][e];
+                // never gather past the slice (tail of the last chunk)
+                const bool in = a_off + 128 * u + 4 * lane + e < len32;
+                const uint32_t cc = in ? a_col[u][e] : 0u;
+                b_x[u][e] = XNA ? ld_x_na(x + cc, pl) : ld_x(x + cc, pl);
+                b_val[u][e] = in ? a_val[u][e] : (V)0;
             }
     }
     __device__ __forceinline__ void init(int32_t len, const int64_t base) {
