@@ -481,8 +481,8 @@ int variant() {
         case 1: return FN<V, EXACT, 256, 2, 3, true>(__VA_ARGS__);  \
         case 2: return FN<V, EXACT, 256, 2, 2, true>(__VA_ARGS__);  \
         case 3: return FN<V, EXACT, 128, 2, 4, true>(__VA_ARGS__);  \
-        case 4: return FN<V, EXACT, 256, 2, 3, false>(__VA_ARGS__); \
-        case 5: return FN<V, EXACT, 512, 2, 2, true>(__VA_ARGS__);  \
+        case 4: return FN<V, EXACT, 128, 2, 3, false>(__VA_ARGS__); \
+        case 5: return FN<V, EXACT, 128, 2, 4, false>(__VA_ARGS__);  \
         default: return FN<V, EXACT, 128, 2, 3, true>(__VA_ARGS__); \
     }
 
