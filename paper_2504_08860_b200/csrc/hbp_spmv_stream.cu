@@ -1,4 +1,4 @@
-// hbp_spmv_stream.cu -- streamed, element-balanced HBP SpMV (W = 32).
+// hbp_spmv_stream.cu -- TMA-streamed, element-balanced HBP SpMV (W = 32).
 //
 // Why: in the HBP layout a group's elements are step-major (all live lanes'
 // t-th elements, then the (t+1)-th ...).  On skewed matrices a group has ~10
@@ -8,22 +8,23 @@
 //
 //   1. each persistent warp owns an equal slice [c_lo, c_hi) of the element
 //      array (exact mode: slice ends rounded up to group boundaries);
-//   2. the slice streams through a three-stage register pipeline in chunks
-//      of CH elements (CH/32 per lane, 16-byte streaming loads): chunk c+2's
-//      col/data loads and chunk c+1's x gathers are in flight while the walk
-//      reads chunk c;
-//   3. products (f32 data: f32 products; exact f64 data: __dmul_rn) go to a
-//      small shared-memory ring of NB = 2 chunks (the walk touches at most
-//      the current and the previous chunk); only products live in shared
-//      memory, which keeps most of the SM's 256 KB as L1 -- the L1 capacity
-//      bounds how many x gathers can be outstanding (measured: kernels with
-//      > ~190 KB of shared memory per SM ran 2x slower);
+//   2. lane 0 streams the slice's col/data into a shared-memory ring of NB
+//      chunks of CH elements with cp.async.bulk (TMA bulk copies completing
+//      on per-slot mbarriers), NB-3 chunks ahead of the walk;
+//   3. the x gathers of chunk c+1 are issued (registers) before the walk of
+//      chunk c needs them; when the walk reaches chunk c+1 the products are
+//      written over its values (f32 data: f32 products; exact f64 data:
+//      __dmul_rn products), so products of the chunks the walk can touch are
+//      always resident;
 //   4. each group's phases come precomputed from the phase stream (live mask
-//      and element offset per phase, hbp_phase_emit); the walk sums
-//        - lane by lane in step order (exact mode always): each row in the
-//          reference's order, bitwise identical to _kernels.py:41-46 for f64;
-//        - (fast mode) long phases with fewer than KT live lanes with
-//          S = 32/k sub-streams per live lane and a shuffle tree;
+//      and element offset per phase, hbp_phase_emit); the walk runs
+//        - a step-uniform loop while >= KT lanes are live (exact mode: all
+//          steps): every live lane adds its element of the step -- each row
+//          is summed in step order, bitwise identical to _kernels.py:41-46
+//          for f64;
+//        - (fast mode) the remaining few-lane phases: short ones lane by
+//          lane, long ones with S = 32/k sub-streams per live lane and a
+//          shuffle tree;
 //   5. a group cut by a slice boundary (fast mode only) leaves per-lane
 //      partials; the warp whose piece completes the group's element count
 //      (atomic) adds the pieces in slice order -- deterministic.
@@ -47,10 +48,50 @@ constexpr unsigned FULL = 0xffffffffu;
 
 template <typename V, int CH, int NB>
 struct __align__(16) WarpSmem {
-    V prod[NB * CH];  // product ring
+    uint32_t col[NB * CH];
+    V val[NB * CH];  // values, then products in place
     uint32_t ph_mask[33];
     int32_t ph_off[33];
+    uint64_t mbar[NB];
 };
+
+// ---- PTX helpers: mbarrier + bulk async copy (sm_90+ / sm_100a) ------------
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *m, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(m)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *m, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(m)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *m, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_addr(m)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
+                                         uint64_t *m, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(m)), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
 
 // per live-lane count k (1..32): sub-streams S = largest power of two with
 // k*S <= 32, and ceil(2^16/k) (exact lane / k for lane < 32)
@@ -107,121 +148,105 @@ __device__ __forceinline__ V product(V v, V xv) {
     return v * xv;
 }
 
-// 16-byte streaming loads (read once: no L1 allocation, L2 evict-first)
-__device__ __forceinline__ uint4 ld_stream_v4(const uint32_t *p, uint64_t pol) {
-    uint4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "l"(p), "l"(pol));
-    return v;
-}
-__device__ __forceinline__ void ld_vals4(const float *p, uint64_t pol, float (&o)[4]) {
-    uint4 v = ld_stream_v4(reinterpret_cast<const uint32_t *>(p), pol);
-    o[0] = __uint_as_float(v.x), o[1] = __uint_as_float(v.y);
-    o[2] = __uint_as_float(v.z), o[3] = __uint_as_float(v.w);
-}
-__device__ __forceinline__ void ld_vals4(const double *p, uint64_t pol, double (&o)[4]) {
-    uint4 a = ld_stream_v4(reinterpret_cast<const uint32_t *>(p), pol);
-    uint4 b = ld_stream_v4(reinterpret_cast<const uint32_t *>(p + 2), pol);
-    o[0] = __hiloint2double(a.y, a.x), o[1] = __hiloint2double(a.w, a.z);
-    o[2] = __hiloint2double(b.y, b.x), o[3] = __hiloint2double(b.w, b.z);
-}
-
-// Streams one warp's slice through the register pipeline into the product
-// ring.  Positions are 32-bit offsets relative to `base` (slice start rounded
-// down to 4 elements, 16-byte aligned).  Lane l owns chunk elements
-// [4*l + 128*u, +4) for u < CH/128.
+// Streams one warp's slice through the shared-memory ring.  All positions
+// are 32-bit offsets relative to `base` (slice start rounded down to 16 B).
 template <typename V, bool EXACT, int CH, int NB, bool XNA>
-struct Pipe {
+struct Ring {
     static constexpr int RMASK = NB * CH - 1;
-    static constexpr int U = CH / 128;
-    const uint32_t *__restrict__ col;
-    const V *__restrict__ data;
+    static constexpr int EPL = CH / 32;  // elements per lane per chunk
+    const hbp_format_t &f;
+    WarpSmem<V, CH, NB> &S;
     const V *__restrict__ x;
-    V *prod;              // this warp's ring
+    int64_t base;
     int32_t len32;        // c_hi - base
     int32_t nchunks;
-    int32_t ready = -1;   // chunks <= ready have products in the ring
+    int32_t ready = -1;   // chunks <= ready hold products
+    int32_t pending = -1; // chunk whose x gathers are in flight
+    int32_t issued = 0;   // bulk copies issued (lane 0)
     int32_t res32 = 0;    // products resident for offsets < res32
     int lane;
     uint64_t pe, pl;
-    // stage A: col/data of chunk ready+2;  stage B: x gathers of chunk ready+1
-    uint32_t a_col[U][4];
-    V a_val[U][4];
-    V b_x[U][4];
-    V b_val[U][4];
+    V xr[EPL];            // gathered x of the pending chunk
 
-    int32_t a_off;  // chunk offset of stage A (its elements past len32 are masked at use)
-
-    // issue chunk c's col/data loads; the registers are not touched until
-    // a_to_b() (a consumer here would stall on the loads right away)
-    __device__ __forceinline__ void load_a(int32_t c) {
-        a_off = c * CH;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int32_t o = c * CH + 128 * u + 4 * lane;
-            if (o < len32) {
-                const uint4 t = ld_stream_v4(col + o, pe);
-                a_col[u][0] = t.x, a_col[u][1] = t.y, a_col[u][2] = t.z, a_col[u][3] = t.w;
-                ld_vals4(data + o, pe, a_val[u]);
-            }
+    __device__ void issue_upto(int32_t last) {  // lane 0
+        for (; issued <= last && issued < nchunks; ++issued) {
+            const int32_t ca = issued * CH;
+            const int32_t n = (ca + CH < len32 ? ca + CH : len32) - ca;
+            const int slot = issued % NB;
+            const uint32_t bc = (uint32_t)((n * 4 + 15) & ~15);
+            const uint32_t bv = (uint32_t)((n * (int)sizeof(V) + 15) & ~15);
+            mbar_expect_tx(&S.mbar[slot], bc + bv);
+            bulk_g2s(&S.col[slot * CH], f.col + base + ca, bc, &S.mbar[slot], pe);
+            bulk_g2s(&S.val[slot * CH], (const V *)f.data + base + ca, bv, &S.mbar[slot], pe);
         }
     }
-    __device__ __forceinline__ void a_to_b() {
+
+    // chunk c: wait for its bytes, issue its x gathers into xr
+    __device__ __forceinline__ void start(int32_t c) {
+        const int slot = c % NB;
+        mbar_wait(&S.mbar[slot], (uint32_t)((c / NB) & 1));
+        const int32_t n = (c * CH + CH < len32 ? c * CH + CH : len32) - c * CH;
+        uint32_t cc[EPL];
+        if constexpr (EPL == 4) {
+            const uint4 t = *reinterpret_cast<const uint4 *>(&S.col[slot * CH + 4 * lane]);
+            cc[0] = t.x, cc[1] = t.y, cc[2] = t.z, cc[3] = t.w;
+        } else if constexpr (EPL == 2) {
+            const uint2 t = *reinterpret_cast<const uint2 *>(&S.col[slot * CH + 2 * lane]);
+            cc[0] = t.x, cc[1] = t.y;
+        } else {
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                // never gather past the slice (tail of the last chunk)
-                const bool in = a_off + 128 * u + 4 * lane + e < len32;
-                const uint32_t cc = in ? a_col[u][e] : 0u;
-                b_x[u][e] = XNA ? ld_x_na(x + cc, pl) : ld_x(x + cc, pl);
-                b_val[u][e] = in ? a_val[u][e] : (V)0;
-            }
-    }
-    __device__ __forceinline__ void init(int32_t len, const int64_t base) {
-        len32 = len;
-        nchunks = (len + CH - 1) / CH;
-        load_a(0);
-        a_to_b();
-        load_a(1);
-    }
-    // finish chunk ready+1 into the ring, advance the pipeline by one chunk
-    __device__ __forceinline__ void step() {
-        const int32_t c = ready + 1;
-        V *dst = prod + (c * CH) % (NB * CH);
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            V p[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) p[e] = product<V, EXACT>(b_val[u][e], b_x[u][e]);
-            if (sizeof(V) == 4) {
-                *reinterpret_cast<float4 *>(dst + 128 * u + 4 * lane) =
-                    make_float4((float)p[0], (float)p[1], (float)p[2], (float)p[3]);
-            } else {
-                *reinterpret_cast<double2 *>(dst + 128 * u + 4 * lane) =
-                    make_double2((double)p[0], (double)p[1]);
-                *reinterpret_cast<double2 *>(dst + 128 * u + 4 * lane + 2) =
-                    make_double2((double)p[2], (double)p[3]);
+            for (int e = 0; e < EPL; e += 4) {
+                const uint4 t =
+                    *reinterpret_cast<const uint4 *>(&S.col[slot * CH + EPL * lane + e]);
+                cc[e] = t.x, cc[e + 1] = t.y, cc[e + 2] = t.z, cc[e + 3] = t.w;
             }
         }
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) {
+            if (EPL * lane + e >= n) cc[e] = 0u;  // never gather past the slice
+            xr[e] = XNA ? ld_x_na(x + cc[e], pl) : ld_x(x + cc[e], pl);
+        }
+        pending = c;
+    }
+
+    // pending chunk: values -> products (in place)
+    __device__ __forceinline__ void finish() {
+        const int c = pending;
+        const int slot = c % NB;
+        V *v = &S.val[slot * CH + EPL * lane];
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) v[e] = product<V, EXACT>(v[e], xr[e]);
         ready = c;
-        res32 = (c + 1) * CH < len32 ? (c + 1) * CH : len32;
-        a_to_b();
-        load_a(c + 2);
-        __syncwarp();  // ring writes visible to the walk
+        res32 = (c * CH + CH < len32 ? c * CH + CH : len32);
+        pending = -1;
     }
-    // make offsets < need resident (warp-uniform call)
+
+    // make offsets < need resident (warp-uniform); refills the ring
     __device__ __forceinline__ void advance(int32_t need) {
-        while (need > res32 && ready + 1 < nchunks) step();
+        while (need > res32) {
+            if (pending < 0) {
+                if (ready + 1 >= nchunks) return;
+                start(ready + 1);
+            }
+            __syncwarp();  // the walk's reads of the oldest slot are done
+            finish();
+            fence_proxy_async();  // generic ring accesses precede later bulk writes
+            __syncwarp();
+            if (ready + 1 < nchunks) start(ready + 1);
+            // slots of chunks <= ready - 2 are free (the walk may still read
+            // ready - 1 for a step straddling the boundary)
+            if (lane == 0) issue_upto(ready + NB - 2);
+        }
     }
+
+    __device__ __forceinline__ double at(int32_t o) const { return (double)S.val[o & RMASK]; }
 };
 
 template <typename V, bool EXACT, int CH, int NB, int MINB, bool XNA>
 __global__ void __launch_bounds__(kThreads, MINB)
     k_spmv_stream(const hbp_format_t f, const hbp_balanced_t b, const V *__restrict__ x,
                   V *__restrict__ y, double *__restrict__ partial) {
-    constexpr int KT = 8;  // fast mode: fewer live lanes -> cooperative long phases
+    constexpr int KT = 8;  // fast mode: fewer live lanes -> per-phase processing
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
@@ -238,6 +263,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
     const uint2 *__restrict__ phs = (const uint2 *)f.phases;
     const uint32_t *__restrict__ permp = (const uint32_t *)f.perm;
 
+    Ring<V, EXACT, CH, NB, XNA> ring{f, S, x};
+    ring.lane = lane;
+    ring.pe = policy_evict_first();
+    ring.pl = policy_evict_last();
+
     int64_t c_lo = cut_at(w, E, Nw), c_hi = cut_at(w + 1, E, Nw);
     if (EXACT) {  // round slice ends up to group boundaries
         if (c_lo > 0 && c_lo < E) {
@@ -250,16 +280,16 @@ __global__ void __launch_bounds__(kThreads, MINB)
         }
     }
     const int64_t base = c_lo & ~(int64_t)3;
+    ring.base = base;
+    ring.len32 = (int32_t)(c_hi - base);
+    ring.nchunks = c_hi > c_lo ? (ring.len32 + CH - 1) / CH : 0;
 
-    Pipe<V, EXACT, CH, NB, XNA> pipe;
-    pipe.col = f.col + base;
-    pipe.data = (const V *)f.data + base;
-    pipe.x = x;
-    pipe.prod = S.prod;
-    pipe.lane = lane;
-    pipe.pe = policy_evict_first();
-    pipe.pl = policy_evict_last();
-    pipe.init(c_hi > c_lo ? (int32_t)(c_hi - base) : 0, base);
+    if (lane == 0) {
+        for (int i = 0; i < NB; ++i) mbar_init(&S.mbar[i], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    if (lane == 0) ring.issue_upto(NB - 3);
 
     int64_t g = upper_group(gs, ngroups, c_lo);
     if (!(g < ngroups && gs[g] < c_lo)) g = lower_group(gs, ngroups, c_lo);
@@ -273,9 +303,6 @@ __global__ void __launch_bounds__(kThreads, MINB)
     int64_t pp1 = g < ngroups ? pptr[g + 1] : 0;
     uint2 ph_n = make_uint2(0u, 0u);
     if (g < ngroups && lane < pp1 - pp0) ph_n = phs[pp0 + lane];
-
-    constexpr int RM = NB * CH - 1;
-    const V *rv = S.prod;
 
     for (; g < ngroups && (gs0 < c_hi || last_warp); ++g) {
         const uint32_t row_local = perm_n;
@@ -305,7 +332,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
             __syncwarp();
             const int32_t gb = (int32_t)(g0 - base);  // group start, ring offset (may be < 0)
             const int32_t lo_r = (int32_t)(lo - base), hi_r = (int32_t)(hi - base);
-            // start: phase j and step containing lo
+            // start: phase j and step t containing lo
             const int32_t o_lo = lo_r - gb;
             int j = 0;
             while (j + 1 < np && S.ph_off[j + 1] <= o_lo) ++j;
@@ -316,83 +343,74 @@ __global__ void __launch_bounds__(kThreads, MINB)
             bool live = (pm >> lane) & 1u;
             int rank = __popc(pm & lt);
 
-            // ---- walk phase by phase.  Steps are summed lane by lane (each
-            // lane its own row, in step order); in fast mode long phases with
-            // fewer than KT live lanes use S = 32/k sub-streams per lane.
-            // Residency checks sit in the outer loops; inner loops only load.
-            for (;;) {
+            // ---- step-uniform lane walk (exact: all phases; fast: k >= KT)
+            while (pb < hi_r && (EXACT || k >= KT)) {
                 const int32_t stop = pend_j < hi_r ? pend_j : hi_r;
-                if (pb < lo_r) {
-                    // a step cut by the slice start (fast-mode pieces only)
-                    if (pb + k > pipe.res32) pipe.advance(pb + k < hi_r ? pb + k : hi_r);
-                    const int32_t P = pb + rank;
-                    if (live && P >= lo_r && P < hi_r) acc += (double)rv[P & RM];
-                    pb += k;
-                    if (pb < stop) continue;  // rest of this phase
-                } else if (!EXACT && k < KT && stop - pb > 8 * k) {
-                    const int SS = c_streams[k];
-                    const int s = (int)(((uint32_t)lane * c_magic16[k]) >> 16);  // lane / k
-                    const int32_t stride = SS * k;
-                    const bool act = s < SS;
-                    double v0 = 0.0, v1 = 0.0;
-                    int32_t q = pb;
-                    while (q < stop) {
-                        const int32_t need = q + stride < stop ? q + stride : stop;
-                        if (need > pipe.res32) pipe.advance(need);
-                        if (q + stride > stop) {  // last, partial pass
-                            const int32_t P = q + lane;
-                            if (act && P < stop) v0 += (double)rv[P & RM];
-                            q = stop;
-                            break;
-                        }
-                        const int32_t lim = stop < pipe.res32 ? stop : pipe.res32;
-                        const int32_t npass = div_small(lim - q - stride, stride) + 1;
-                        if (act) {
-                            int32_t p = q + lane;
-                            int32_t i = 0;
-                            for (; i + 2 <= npass; i += 2, p += 2 * stride) {
-                                v0 += (double)rv[p & RM];
-                                v1 += (double)rv[(p + stride) & RM];
-                            }
-                            if (i < npass) v0 += (double)rv[p & RM];
-                        }
-                        q += npass * stride;
-                    }
-                    double v = v0 + v1;
-                    for (int d = SS >> 1; d >= 1; d >>= 1) v += __shfl_down_sync(FULL, v, d * k);
-                    const double tot = __shfl_sync(FULL, v, live ? rank : 0);
-                    if (live) acc += tot;
-                    pb = stop;
-                } else {
-                    while (pb < stop) {
-                        if (pb + k > pipe.res32) pipe.advance(pb + k < hi_r ? pb + k : hi_r);
-                        const int32_t lim = stop < pipe.res32 ? stop : pipe.res32;
-                        const int32_t nsteps = lim - pb >= k ? div_small(lim - pb, k) : 0;
-                        if (nsteps == 0) {  // last step cut by the slice end
-                            const int32_t P = pb + rank;
-                            if (live && P < hi_r) {
-                                const double v = (double)rv[P & RM];
-                                acc = EXACT ? __dadd_rn(acc, v) : acc + v;
-                            }
-                            pb += k;
-                            break;
-                        }
+                if (!piece) {
+                    for (; pb < stop; pb += k) {
+                        if (pb + k > ring.res32) ring.advance(pb + k);
                         if (live) {
-                            int32_t p = pb + rank;
-                            for (int32_t i = 0; i < nsteps; ++i, p += k) {
-                                const double v = (double)rv[p & RM];
-                                acc = EXACT ? __dadd_rn(acc, v) : acc + v;
-                            }
+                            const double v = ring.at(pb + rank);
+                            acc = EXACT ? __dadd_rn(acc, v) : acc + v;
                         }
-                        pb += nsteps * k;
+                    }
+                } else {
+                    for (; pb < stop; pb += k) {
+                        if (pb + k > ring.res32) ring.advance(pb + k < hi_r ? pb + k : hi_r);
+                        const int32_t P = pb + rank;
+                        if (live && P >= lo_r && P < hi_r) {
+                            const double v = ring.at(P);
+                            acc = EXACT ? __dadd_rn(acc, v) : acc + v;
+                        }
                     }
                 }
-                if (pb < pend_j || ++j == np) break;  // reached hi, or the group's end
+                if (pb < pend_j) break;  // reached hi inside the phase
+                if (++j == np) break;
                 pm = S.ph_mask[j];
                 k = __popc(pm);
                 pend_j = gb + S.ph_off[j + 1];
                 live = (pm >> lane) & 1u;
                 rank = __popc(pm & lt);
+            }
+            // ---- fast mode: phases with few live lanes
+            if (!EXACT) {
+                while (pb < hi_r && j < np) {
+                    const int32_t stop = pend_j < hi_r ? pend_j : hi_r;
+                    if (stop - pb > 8 * k && pb >= lo_r) {
+                        const int SS = c_streams[k];
+                        const int s = (int)(((uint32_t)lane * c_magic16[k]) >> 16);  // lane / k
+                        const int r = lane - s * k;
+                        const int32_t stride = SS * k;
+                        double v = 0.0;
+                        for (int32_t q = pb; q < stop; q += stride) {  // SS steps per pass
+                            const int32_t need = q + stride < stop ? q + stride : stop;
+                            if (need > ring.res32) ring.advance(need);
+                            const int32_t P = q + s * k + r;
+                            if (s < SS && P < stop) v += ring.at(P);
+                        }
+                        for (int d = SS >> 1; d >= 1; d >>= 1)
+                            v += __shfl_down_sync(FULL, v, d * k);
+                        const double tot = __shfl_sync(FULL, v, live ? rank : 0);
+                        if (live) acc += tot;
+                        pb = stop;
+                    } else {
+                        // short phase (or a step cut by the slice start): lane by lane
+                        const int32_t stop1 = stop - pb > 8 * k ? pb + k : stop;
+                        for (; pb < stop1; pb += k) {
+                            if (pb + k > ring.res32) ring.advance(pb + k < hi_r ? pb + k : hi_r);
+                            const int32_t P = pb + rank;
+                            if (live && P >= lo_r && P < hi_r) acc += ring.at(P);
+                        }
+                        if (pb < pend_j && stop1 != stop) continue;  // rest of this phase
+                    }
+                    if (pb < pend_j) break;  // reached hi inside the phase
+                    if (++j == np) break;
+                    pm = S.ph_mask[j];
+                    k = __popc(pm);
+                    pend_j = gb + S.ph_off[j + 1];
+                    live = (pm >> lane) & 1u;
+                    rank = __popc(pm & lt);
+                }
             }
         }
 
@@ -463,9 +481,9 @@ int occupancy_of(int *per_sm) {
         per_sm, k_spmv_stream<V, EXACT, CH, NB, MINB, XNA>, kThreads, smem);
 }
 
-// Tile / occupancy variants (chunk CH, ring slots NB, min CTAs per SM, L1
-// policy of the x gathers), chosen with HBP_STREAM_VARIANT for sweeps.
-constexpr int kVariants = 6;
+// Tile / occupancy variants (chunk CH, ring slots NB, min CTAs per SM),
+// chosen with HBP_STREAM_VARIANT for sweeps; 0 is the default.
+constexpr int kVariants = 8;
 int variant() {
     static int v = -1;
     if (v < 0) {
@@ -476,14 +494,16 @@ int variant() {
     return v;
 }
 
-#define HBP_STREAM_VARIANTS(FN, V, EXACT, ...)                      \
-    switch (variant()) {                                             \
-        case 1: return FN<V, EXACT, 256, 2, 3, true>(__VA_ARGS__);  \
-        case 2: return FN<V, EXACT, 256, 2, 2, true>(__VA_ARGS__);  \
-        case 3: return FN<V, EXACT, 128, 2, 4, true>(__VA_ARGS__);  \
-        case 4: return FN<V, EXACT, 128, 2, 3, false>(__VA_ARGS__); \
-        case 5: return FN<V, EXACT, 128, 2, 4, false>(__VA_ARGS__);  \
-        default: return FN<V, EXACT, 128, 2, 3, true>(__VA_ARGS__); \
+#define HBP_STREAM_VARIANTS(FN, V, EXACT, ...)                     \
+    switch (variant()) {                                            \
+        case 1: return FN<V, EXACT, 64, 8, 4, true>(__VA_ARGS__);  \
+        case 2: return FN<V, EXACT, 128, 8, 3, true>(__VA_ARGS__); \
+        case 3: return FN<V, EXACT, 256, 4, 2, true>(__VA_ARGS__); \
+        case 4: return FN<V, EXACT, 128, 8, 2, true>(__VA_ARGS__); \
+        case 5: return FN<V, EXACT, 128, 4, 4, true>(__VA_ARGS__); \
+        case 6: return FN<V, EXACT, 64, 8, 3, true>(__VA_ARGS__);  \
+        case 7: return FN<V, EXACT, 128, 4, 3, false>(__VA_ARGS__); \
+        default: return FN<V, EXACT, 128, 4, 3, true>(__VA_ARGS__); \
     }
 
 template <typename V, bool EXACT>
