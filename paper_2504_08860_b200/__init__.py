@@ -21,14 +21,14 @@ from .reorder import (BUCKET_MAX, BlockPermutations, HashParams, OpCounter,
                       sort_permutation, sort_permutations)
 from .hbp import (HbpFormatError, HbpMatrix, build_hbp, deserialize_hbp, hbp_to_triplets,
                   load_hbp, save_hbp, serialize_hbp)
-from .engine import (ExecutionLog, ExecutionPlan, PartialVector, SpmvOperator, block_spmv,
+from .engine import (ExecutionLog, ExecutionPlan, HostPipeline, PartialVector, SpmvOperator, block_spmv,
                      combine, hbp_spmv, plan_execution, run_spmv)
 
 __version__ = "0.1.0"
 
 __all__ = [
     "BUCKET_MAX", "BlockGrid", "BlockPermutations", "CsrMatrix", "ExecutionLog",
-    "ExecutionPlan", "HashParams", "HbpFormatError", "HbpMatrix", "OpCounter", "PartialVector",
+    "ExecutionPlan", "HashParams", "HostPipeline", "HbpFormatError", "HbpMatrix", "OpCounter", "PartialVector",
     "PartitionConfig", "SpmvOperator", "TripletMatrix", "block_rows_of", "block_spmv",
     "build_block_permutation", "build_hbp", "combine", "coo_to_csr", "csr_to_triplets",
     "deserialize_hbp", "hash_permutations", "hash_slot", "hbp_spmv", "hbp_to_triplets",

@@ -233,6 +233,42 @@ class SpmvOperator:
         return g
 
 
+class HostPipeline:
+    """End-to-end y_i = A x_i for a sequence of HOST vectors (pinned memory):
+    the H2D copy of x_i, the SpMV and the D2H copy of y_i run on `depth`
+    CUDA streams in rotation, so the PCIe copies of one vector overlap the
+    SpMV of its neighbours.  Each stream owns its SpmvOperator (scratch is
+    never shared between concurrent launches)."""
+
+    def __init__(self, hbp: HbpMatrix, depth: int = 2, **op_kwargs):
+        dev = hbp.data.device
+        self.hbp = hbp
+        self.depth = depth
+        self.streams = [torch.cuda.Stream(device=dev) for _ in range(depth)]
+        self.ops = [SpmvOperator(hbp, **op_kwargs) for _ in range(depth)]
+        self.xd = [torch.empty(hbp.cols, dtype=hbp.dtype, device=dev) for _ in range(depth)]
+        self.yd = [torch.empty(hbp.rows, dtype=hbp.dtype, device=dev) for _ in range(depth)]
+
+    @property
+    def launches_per_call(self) -> int:
+        return self.ops[0].launches_per_call
+
+    def run(self, xs_host, ys_host) -> None:
+        """Enqueue every (x_i -> y_i); ordered after the current stream's work.
+        The caller synchronizes (or waits on the current stream)."""
+        cur = torch.cuda.current_stream()
+        for s in self.streams:
+            s.wait_stream(cur)
+        for i, (xh, yh) in enumerate(zip(xs_host, ys_host)):
+            j = i % self.depth
+            with torch.cuda.stream(self.streams[j]):
+                self.xd[j].copy_(xh, non_blocking=True)
+                self.ops[j](self.xd[j], self.yd[j])
+                yh.copy_(self.yd[j], non_blocking=True)
+        for s in self.streams:
+            cur.wait_stream(s)
+
+
 def block_spmv(hbp: HbpMatrix, block, x, partial: PartialVector) -> None:
     """engine.py:123-134: run one block into the partial vector."""
     br, bc = int(block[0]), int(block[1])
