@@ -48,8 +48,8 @@ constexpr unsigned FULL = 0xffffffffu;
 
 template <typename V, int CH, int NB>
 struct __align__(16) WarpSmem {
-    uint32_t col[NB * CH];  // f32: columns, then the f32 products in place
-    V val[sizeof(V) == 4 ? 4 : NB * CH];  // f64: values, then products in place
+    uint32_t col[NB * CH];
+    V val[NB * CH];  // values, then products in place
     uint32_t ph_mask[33];
     int32_t ph_off[33];
     uint64_t mbar[NB];
@@ -166,9 +166,7 @@ struct Ring {
     int32_t res32 = 0;    // products resident for offsets < res32
     int lane;
     uint64_t pe, pl;
-    static constexpr bool COMPACT = sizeof(V) == 4;  // f32: only columns go through TMA
     V xr[EPL];            // gathered x of the pending chunk
-    V vr[EPL];            // f32: its values (16-byte streaming loads)
 
     __device__ void issue_upto(int32_t last) {  // lane 0
         for (; issued <= last && issued < nchunks; ++issued) {
@@ -177,10 +175,9 @@ struct Ring {
             const int slot = issued % NB;
             const uint32_t bc = (uint32_t)((n * 4 + 15) & ~15);
             const uint32_t bv = (uint32_t)((n * (int)sizeof(V) + 15) & ~15);
-            mbar_expect_tx(&S.mbar[slot], COMPACT ? bc : bc + bv);
+            mbar_expect_tx(&S.mbar[slot], bc + bv);
             bulk_g2s(&S.col[slot * CH], f.col + base + ca, bc, &S.mbar[slot], pe);
-            if (!COMPACT)
-                bulk_g2s(&S.val[slot * CH], (const V *)f.data + base + ca, bv, &S.mbar[slot], pe);
+            bulk_g2s(&S.val[slot * CH], (const V *)f.data + base + ca, bv, &S.mbar[slot], pe);
         }
     }
 
@@ -209,22 +206,6 @@ struct Ring {
             if (EPL * lane + e >= n) cc[e] = 0u;  // never gather past the slice
             xr[e] = XNA ? ld_x_na(x + cc[e], pl) : ld_x(x + cc[e], pl);
         }
-        if constexpr (COMPACT) {
-            if (EPL * lane < n) {  // reads stay inside the 16-element padding
-                const uint32_t *src =
-                    reinterpret_cast<const uint32_t *>((const V *)f.data + base) + c * CH + EPL * lane;
-#pragma unroll
-                for (int e = 0; e < EPL; e += 4) {
-                    uint4 t;
-                    asm volatile(
-                        "ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-                        : "=r"(t.x), "=r"(t.y), "=r"(t.z), "=r"(t.w)
-                        : "l"(src + e), "l"(pe));
-                    vr[e] = __uint_as_float(t.x), vr[e + 1] = __uint_as_float(t.y);
-                    vr[e + 2] = __uint_as_float(t.z), vr[e + 3] = __uint_as_float(t.w);
-                }
-            }
-        }
         pending = c;
     }
 
@@ -232,19 +213,9 @@ struct Ring {
     __device__ __forceinline__ void finish() {
         const int c = pending;
         const int slot = c % NB;
-        if constexpr (COMPACT) {
-            uint32_t *dst = &S.col[slot * CH + EPL * lane];
+        V *v = &S.val[slot * CH + EPL * lane];
 #pragma unroll
-            for (int e = 0; e < EPL; e += 4)
-                *reinterpret_cast<uint4 *>(dst + e) = make_uint4(
-                    __float_as_uint((float)(vr[e] * xr[e])), __float_as_uint((float)(vr[e + 1] * xr[e + 1])),
-                    __float_as_uint((float)(vr[e + 2] * xr[e + 2])),
-                    __float_as_uint((float)(vr[e + 3] * xr[e + 3])));
-        } else {
-            V *v = &S.val[slot * CH + EPL * lane];
-#pragma unroll
-            for (int e = 0; e < EPL; ++e) v[e] = product<V, EXACT>(v[e], xr[e]);
-        }
+        for (int e = 0; e < EPL; ++e) v[e] = product<V, EXACT>(v[e], xr[e]);
         ready = c;
         res32 = (c * CH + CH < len32 ? c * CH + CH : len32);
         pending = -1;
@@ -268,10 +239,7 @@ struct Ring {
         }
     }
 
-    __device__ __forceinline__ double at(int32_t o) const {
-        if constexpr (COMPACT) return (double)__uint_as_float(S.col[o & RMASK]);
-        else return (double)S.val[o & RMASK];
-    }
+    __device__ __forceinline__ double at(int32_t o) const { return (double)S.val[o & RMASK]; }
 };
 
 template <typename V, bool EXACT, int CH, int NB, int MINB, bool XNA>
@@ -515,7 +483,7 @@ int occupancy_of(int *per_sm) {
 
 // Tile / occupancy variants (chunk CH, ring slots NB, min CTAs per SM),
 // chosen with HBP_STREAM_VARIANT for sweeps; 0 is the default.
-constexpr int kVariants = 5;
+constexpr int kVariants = 8;
 int variant() {
     static int v = -1;
     if (v < 0) {
@@ -526,15 +494,16 @@ int variant() {
     return v;
 }
 
-#define HBP_STREAM_VARIANTS(FN, V, EXACT, ...)                      \
-    switch (variant()) {                                             \
-        case 1: return FN<V, EXACT, 128, 4, 3, true>(__VA_ARGS__);  \
-        case 2: return FN<V, EXACT, 256, 4, 4, true>(__VA_ARGS__);  \
-        case 3: return FN<V, EXACT, 512, 4, 2, true>(__VA_ARGS__);  \
-        case 4: return FN<V, EXACT, 256, 4, 3, false>(__VA_ARGS__); \
-        default:                                                     \
-            if (sizeof(V) == 8) return FN<V, EXACT, 128, 4, 3, true>(__VA_ARGS__); \
-            return FN<V, EXACT, 256, 4, 3, true>(__VA_ARGS__);       \
+#define HBP_STREAM_VARIANTS(FN, V, EXACT, ...)                     \
+    switch (variant()) {                                            \
+        case 1: return FN<V, EXACT, 64, 8, 4, true>(__VA_ARGS__);  \
+        case 2: return FN<V, EXACT, 128, 8, 3, true>(__VA_ARGS__); \
+        case 3: return FN<V, EXACT, 256, 4, 2, true>(__VA_ARGS__); \
+        case 4: return FN<V, EXACT, 128, 8, 2, true>(__VA_ARGS__); \
+        case 5: return FN<V, EXACT, 128, 4, 4, true>(__VA_ARGS__); \
+        case 6: return FN<V, EXACT, 64, 8, 3, true>(__VA_ARGS__);  \
+        case 7: return FN<V, EXACT, 128, 4, 3, false>(__VA_ARGS__); \
+        default: return FN<V, EXACT, 128, 4, 3, true>(__VA_ARGS__); \
     }
 
 template <typename V, bool EXACT>
