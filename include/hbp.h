@@ -191,6 +191,20 @@ int hbp_expand_reference(const int32_t *blk_br, const int32_t *blk_bc, int64_t n
                          const uint32_t *empty_perm_last, int32_t *zero_row, uint32_t *output_hash,
                          int64_t *group_start, hbp_stream_t stream);
 
+/* ----------------------------------------------- the paper's baselines */
+/* formats.py:266-273 csr_spmv -> _kernels.py:13-19 csr_kernel (PAPER Alg. 1):
+ * one thread per row, left to right, unfused (f64 bitwise with the
+ * reference; f32 values accumulate in f64). */
+int hbp_csr_spmv(const int64_t *row_ptr, const int32_t *col_idx, const void *values, int dtype,
+                 int64_t rows, const void *x, void *y, hbp_stream_t stream);
+/* engine.py:204-225 block2d_spmv_baseline -> _kernels.py:50-59
+ * block2d_kernel: each nonzero block's row runs in CSR order into the
+ * compact partial [nzb*R] (combine with hbp_combine). */
+int hbp_block2d_spmv(const uint32_t *len_local, const int64_t *start_local, const int32_t *blk_br,
+                     int64_t nzb, int64_t rows, int64_t row_height, const int32_t *col_idx,
+                     const void *values, int dtype, const void *x, double *partial,
+                     hbp_stream_t stream);
+
 /* hbp.py:241-315 hbp_to_triplets: follows every slot's add_sign chain over
  * the reference-layout arrays; row_out[j] = row of element j, seen[j] =
  * visit count (zero-filled by the caller), *err |= 1 (lane start outside its

@@ -342,3 +342,23 @@ void orc_combine(const double *partial, int64_t rows, int64_t ncb,
         for (int64_t i = 0; i < rows; ++i) out[i] += seg[i];
     }
 }
+
+/* _kernels.py:50-59 block2d_kernel (engine.py:204-225): per block row, its
+ * run in CSR order, into partial[bc*rows + row]; blocks in bc-major order. */
+void orc_block2d(const int64_t *col_idx, const double *values, const int32_t *row_counts,
+                 const int64_t *row_starts, const int64_t *block_nnz, int64_t rows,
+                 int64_t R, int64_t nrb, int64_t ncb, const double *x, double *partial) {
+    memset(partial, 0, sizeof(double) * (size_t)(ncb * rows));
+    for (int64_t bc = 0; bc < ncb; ++bc)
+        for (int64_t br = 0; br < nrb; ++br) {
+            if (block_nnz[br * ncb + bc] == 0) continue;
+            int64_t r0 = br * R, n = rows - r0 < R ? rows - r0 : R;
+            for (int64_t r = 0; r < n; ++r) {
+                int64_t gr = r0 + r, j = row_starts[bc * rows + gr];
+                double s = 0.0;
+                for (int64_t k = 0; k < row_counts[bc * rows + gr]; ++k)
+                    s += values[j + k] * x[col_idx[j + k]];
+                partial[bc * rows + gr] = s;
+            }
+        }
+}

@@ -449,3 +449,16 @@ def pipeline(rows, cols, row, col, val, C, R, W, seed=0, sample_size=4096, quant
     h = build_hbp(row_ptr, col_idx, values, grid, perms)
     return dict(row_ptr=row_ptr, col_idx=col_idx, values=values, grid=grid,
                 params=params, perms=perms, probes=probes, hbp=h)
+
+
+def block2d_spmv_baseline(row_ptr, col_idx, values, grid: DenseGrid, x):
+    """engine.py:204-225 -> _kernels.py:50-59 (C restatement) + combine."""
+    partial = np.empty(grid.ncb * grid.rows)
+    lib().orc_block2d(_p(np.ascontiguousarray(col_idx, np.int64)),
+                      _p(np.ascontiguousarray(values, np.float64)),
+                      _p(np.ascontiguousarray(grid.row_counts, np.int32)),
+                      _p(np.ascontiguousarray(grid.row_starts, np.int64)),
+                      _p(np.ascontiguousarray(grid.block_nnz, np.int64)), I64(grid.rows),
+                      I64(grid.R), I64(grid.nrb), I64(grid.ncb),
+                      _p(np.ascontiguousarray(x, np.float64)), _p(partial))
+    return combine(partial, grid.rows, grid.ncb)

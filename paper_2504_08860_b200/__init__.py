@@ -13,7 +13,7 @@ Every step runs as hand-written sm_100a CUDA kernels in libhbp.so (C ABI:
 include/hbp.h); arrays are device-resident torch tensors.  There is no CPU
 fallback.
 """
-from .formats import CsrMatrix, TripletMatrix, coo_to_csr, csr_to_triplets
+from .formats import CsrMatrix, TripletMatrix, coo_to_csr, csr_spmv, csr_to_triplets
 from .partition import BlockGrid, PartitionConfig, block_rows_of, make_grid
 from .reorder import (BUCKET_MAX, BlockPermutations, HashParams, OpCounter,
                       build_block_permutation, hash_permutations, hash_slot,
@@ -21,15 +21,17 @@ from .reorder import (BUCKET_MAX, BlockPermutations, HashParams, OpCounter,
                       sort_permutation, sort_permutations)
 from .hbp import (HbpFormatError, HbpMatrix, build_hbp, deserialize_hbp, hbp_to_triplets,
                   load_hbp, save_hbp, serialize_hbp)
-from .engine import (ExecutionLog, ExecutionPlan, HostPipeline, PartialVector, SpmvOperator, block_spmv,
-                     combine, hbp_spmv, plan_execution, run_spmv)
+from .engine import (ExecutionLog, ExecutionPlan, HostPipeline, PartialVector, SpmvOperator,
+                     block2d_spmv_baseline, block_spmv, combine, hbp_spmv, plan_execution,
+                     run_spmv)
 
 __version__ = "0.1.0"
 
 __all__ = [
     "BUCKET_MAX", "BlockGrid", "BlockPermutations", "CsrMatrix", "ExecutionLog",
     "ExecutionPlan", "HashParams", "HostPipeline", "HbpFormatError", "HbpMatrix", "OpCounter", "PartialVector",
-    "PartitionConfig", "SpmvOperator", "TripletMatrix", "block_rows_of", "block_spmv",
+    "PartitionConfig", "SpmvOperator", "TripletMatrix", "block2d_spmv_baseline", "block_rows_of",
+    "block_spmv", "csr_spmv",
     "build_block_permutation", "build_hbp", "combine", "coo_to_csr", "csr_to_triplets",
     "deserialize_hbp", "hash_permutations", "hash_slot", "hbp_spmv", "hbp_to_triplets",
     "identity_permutations", "load_hbp", "make_grid", "perm_for_block", "plan_execution",

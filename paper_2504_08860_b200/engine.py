@@ -333,6 +333,43 @@ def combine(partial: PartialVector) -> torch.Tensor:
     return y
 
 
+def block2d_spmv_baseline(csr, grid: BlockGrid, x, workers: int = 1) -> torch.Tensor:
+    """engine.py:204-225: plain 2D-partitioned SpMV (no reordering, no
+    interleaving) through the same partial + combine machinery; a warp per
+    nonzero block, a lane per row (hbp_block2d_spmv + hbp_combine).
+    `workers` is accepted for signature parity (the GPU grid fills the device)."""
+    from .hbp import row_block_lists
+    if workers < 1:
+        raise ValueError("workers must be >= 1")
+    if isinstance(x, torch.Tensor):
+        xt = x
+    else:
+        xt = torch.as_tensor(np.asarray(x))
+    if tuple(xt.shape) != (csr.cols,):
+        raise ValueError(f"vector length {tuple(xt.shape)} != cols {csr.cols}")
+    dev = csr.values.device
+    xt = xt.to(device=dev, dtype=csr.values.dtype).contiguous()
+    R = grid.config.row_height
+    partial = torch.empty(max(1, grid.nzb * R), dtype=torch.float64, device=dev)
+    L.call("hbp_block2d_spmv", L.P(grid.len_local), L.P(grid.start_local), L.P(grid.blk_br),
+           L.c_i64(grid.nzb), L.c_i64(grid.rows), L.c_i64(R), L.P(csr.col_idx),
+           L.P(csr.values), L.c_int(L.dtype_code(csr.values.dtype)), L.P(xt), L.P(partial),
+           L.stream())
+    key = "rb_lists"
+    if key not in grid._cache:
+        grid._cache[key] = row_block_lists(grid.blk_br, grid.num_row_blocks)
+    rb_ptr, rb_blk = grid._cache[key]
+    f = L.FormatT()
+    f.rows, f.cols, f.col_width, f.row_height = grid.rows, grid.cols, grid.config.col_width, R
+    f.warp_size, f.nrb, f.ncb, f.nzb = grid.config.warp_size, grid.num_row_blocks, \
+        grid.num_col_blocks, grid.nzb
+    f.dtype = L.dtype_code(csr.values.dtype)
+    f.rb_ptr, f.rb_blk = rb_ptr.data_ptr(), (rb_blk.data_ptr() if rb_blk.numel() else 0)
+    y = torch.empty(grid.rows, dtype=csr.values.dtype, device=dev)
+    L.call("hbp_combine", ctypes.byref(f), L.P(partial), L.P(y), L.stream())
+    return y
+
+
 def hbp_spmv(hbp: HbpMatrix, x, workers: int | None = None) -> torch.Tensor:
     """engine.py:228-232: plan, run and combine in one call (device tensor y).
     workers=None fills the device with persistent warps."""

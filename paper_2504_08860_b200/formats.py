@@ -155,6 +155,23 @@ def coo_to_csr(matrix: TripletMatrix) -> CsrMatrix:
     return CsrMatrix(matrix.rows, matrix.cols, row_ptr, col, val)
 
 
+def csr_spmv(csr: CsrMatrix, x) -> torch.Tensor:
+    """formats.py:266-273 / _kernels.py:13-19 (PAPER Alg. 1) on the GPU: one
+    thread per row, left to right in storage order (hbp_csr_spmv)."""
+    if isinstance(x, torch.Tensor):
+        xt = x
+    else:
+        xt = torch.as_tensor(np.asarray(x))
+    if tuple(xt.shape) != (csr.cols,):
+        raise ValueError(f"vector length {tuple(xt.shape)} != cols {csr.cols}")
+    xt = xt.to(device=csr.values.device, dtype=csr.values.dtype).contiguous()
+    y = torch.empty(csr.rows, dtype=csr.values.dtype, device=csr.values.device)
+    L.call("hbp_csr_spmv", L.P(csr.row_ptr), L.P(csr.col_idx), L.P(csr.values),
+           L.c_int(L.dtype_code(csr.values.dtype)), L.c_i64(csr.rows), L.P(xt), L.P(y),
+           L.stream())
+    return y
+
+
 def csr_to_triplets(csr: CsrMatrix) -> TripletMatrix:
     """formats.py:261-263."""
     counts = csr.row_ptr[1:] - csr.row_ptr[:-1]

@@ -356,15 +356,25 @@ def build_hbp(csr: CsrMatrix, grid: BlockGrid, permutations, config: PartitionCo
            L.P(csr.col_idx), L.P(csr.values), L.c_int(L.dtype_code(vdt)), L.P(col), L.P(data),
            L.P(add), s)
 
-    rb_count = torch.zeros(nrb + 1, dtype=torch.int64, device=dev)
-    L.call("hbp_row_block_counts", L.P(grid.blk_br), L.c_i64(nzb), L.P(rb_count), s)
-    rb_ptr = L.exclusive_sum(rb_count)
-    idx = torch.arange(nzb, dtype=torch.int32, device=dev)
-    _, rb_blk = L.sort_pairs_u32(grid.blk_br, idx, max(1, int(nrb - 1).bit_length()))
+    rb_ptr, rb_blk = row_block_lists(grid.blk_br, nrb)
     return HbpMatrix(csr.rows, csr.cols, config, (nrb, ncb), col=col, data=data, add_sign=add,
                      blk_br=grid.blk_br, blk_bc=grid.blk_bc, slot_len=slot_len, perm=perm,
                      group_start_c=group_start_c, zero_row_c=zero_row_c, rb_ptr=rb_ptr,
                      rb_blk=rb_blk, permutations=keep)
+
+
+def row_block_lists(blk_br: torch.Tensor, nrb: int):
+    """Combine lists: rb_ptr[br] .. rb_ptr[br+1] index rb_blk, the nonzero
+    blocks of row block br in ascending bc (stable sort of the bc-major
+    directory by br)."""
+    dev = blk_br.device
+    nzb = blk_br.numel()
+    rb_count = torch.zeros(nrb + 1, dtype=torch.int64, device=dev)
+    L.call("hbp_row_block_counts", L.P(blk_br), L.c_i64(nzb), L.P(rb_count), L.stream())
+    rb_ptr = L.exclusive_sum(rb_count)
+    idx = torch.arange(nzb, dtype=torch.int32, device=dev)
+    _, rb_blk = L.sort_pairs_u32(blk_br, idx, max(1, int(nrb - 1).bit_length()))
+    return rb_ptr, rb_blk
 
 
 def hbp_to_triplets(hbp: HbpMatrix) -> TripletMatrix:

@@ -138,6 +138,8 @@ def run_case(h, name, trip, cfg, ordering, seed):
     partial, log = h.run_spmv(hbp, x, plan, workers)
     y = h.combine(partial)
     sort_perms = h.sort_permutations(grid)
+    y_csr = h.csr_spmv(csr, x)
+    y_2d = h.block2d_spmv_baseline(csr, grid, x, workers=2)
     return dict(
         name=np.array(name), fp32=np.array(fp32), ordering=np.array(ordering),
         rows=np.array(trip.rows), cols=np.array(trip.cols),
@@ -153,7 +155,7 @@ def run_case(h, name, trip, cfg, ordering, seed):
         group_start=hbp.group_start, output_hash=hbp.output_hash,
         block_order=plan.block_order, fixed_count=np.array(plan.fixed_count),
         worker_ranges=np.array(plan.worker_ranges, np.int64).reshape(-1, 2),
-        workers=np.array(workers), x=x, partial=partial.values, y=y,
+        workers=np.array(workers), x=x, partial=partial.values, y=y, y_csr=y_csr, y_2d=y_2d,
     )
 
 

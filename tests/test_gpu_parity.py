@@ -169,3 +169,21 @@ def test_codec_byte_identical(name, tmp_path):
     np.testing.assert_array_equal(_np(y), g["y"])
     if name == "kat_eye8":
         assert len(raw) == 448  # test_hbp.py:224-232
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_baselines_bitwise(name):
+    """GPU csr_spmv / block2d_spmv_baseline vs the reference's (f64 bitwise)."""
+    g = load_golden(name)
+    cfg = _cfg(g)
+    csr = H.coo_to_csr(_trip(g))
+    grid = H.make_grid(csr, cfg)
+    x = g["x"].astype(np.float32) if g["fp32"] else g["x"]
+    y_csr = _np(H.csr_spmv(csr, x))
+    y_2d = _np(H.block2d_spmv_baseline(csr, grid, x, workers=2))
+    if g["fp32"]:
+        assert _fp32_err(g, y_csr) <= FP32_TOL
+        assert _fp32_err(g, y_2d) <= FP32_TOL
+    else:
+        np.testing.assert_array_equal(y_csr, g["y_csr"])
+        np.testing.assert_array_equal(y_2d, g["y_2d"])

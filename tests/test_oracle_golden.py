@@ -118,3 +118,13 @@ def test_shift_follows_quantile():
 def test_duplicates_rejected():
     with pytest.raises(ValueError, match="duplicate"):
         O.coo_to_csr(2, 2, [0, 0], [1, 1], [1.0, 2.0])
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_oracle_baselines(name):
+    """csr_spmv and block2d_spmv_baseline (the paper's comparison kernels)."""
+    g = load_golden(name)
+    rp, ci, vals = O.coo_to_csr(g["rows"], g["cols"], g["trip_row"], g["trip_col"], g["trip_val"])
+    np.testing.assert_array_equal(O.csr_spmv(rp, ci, vals, g["x"]), g["y_csr"])
+    grid = O.make_grid(rp, ci, g["rows"], g["cols"], g["C"], g["R"], g["W"])
+    np.testing.assert_array_equal(O.block2d_spmv_baseline(rp, ci, vals, grid, g["x"]), g["y_2d"])
