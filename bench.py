@@ -330,7 +330,34 @@ def run_gpu(args):
     live = scale > 0
     check = float((err[live] / scale[live]).max().item()) if bool(live.any()) else 0.0
     zero_ok = bool((err[~live] == 0).all().item())
-    del A, Aabs
+    del A, Aabs, yref, scale, err, live, x64
+
+    # ---- the paper's comparison kernels on the same matrix and device (not
+    # part of `value`): CSR Alg. 1 (thread per row), plain 2D blocks (warp per
+    # block, no reordering) and cuSPARSE (torch CSR @ x) as a library anchor
+    baselines = None
+    if not args.no_baselines:
+        def _time(fn, iters=5):
+            fn()
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(iters):
+                fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            return a.elapsed_time(b) / iters
+        Acs = torch.sparse_csr_tensor(csr.row_ptr, csr.col_idx.to(torch.int64), csr.values,
+                                      (rows, cols))
+        bl = {"csr_alg1_ms": _time(lambda: H.csr_spmv(csr, x)),
+              "block2d_ms": _time(lambda: H.block2d_spmv_baseline(csr, grid, x)),
+              "cusparse_ms": _time(lambda: Acs @ x)}
+        del Acs
+        baselines = {k: round(v, 4) for k, v in bl.items()}
+        baselines["hbp_ms"] = round(kernel_ms, 4)
+        for k, name in (("csr_alg1_ms", "csr"), ("block2d_ms", "2d"), ("cusparse_ms", "cusparse")):
+            baselines[f"speedup_vs_{name}"] = round(bl[k] / kernel_ms, 3)
 
     # ---- aggregate over ranks (max time, sum of work)
     per_step_ms = total_ms / K
@@ -388,6 +415,8 @@ def run_gpu(args):
         "check": {"max_componentwise_err_vs_cusparse_f64": check, "zero_rows_exact": zero_ok,
                   "e2e_y_equals_device_y": e2e_ok},
     }
+    if baselines is not None:
+        out["baselines_same_gpu"] = baselines
     if world == 1 and not args.no_cpu_baseline:
         cb = cpu_reference(args.config, steps=5, warmup=1)
         out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
@@ -428,6 +457,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-baselines", action="store_true",
+                    help="skip the CSR / 2D / cuSPARSE comparison timings")
     ap.add_argument("--schedule", default=None, choices=[None, "stream", "balanced", "plan"])
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)

@@ -17,14 +17,15 @@
 //      __dmul_rn products), so products of the chunks the walk can touch are
 //      always resident;
 //   4. each group's phases come precomputed from the phase stream (live mask
-//      and element offset per phase, hbp_phase_emit); the walk runs
-//        - a step-uniform loop while >= KT lanes are live (exact mode: all
-//          steps): every live lane adds its element of the step -- each row
-//          is summed in step order, bitwise identical to _kernels.py:41-46
-//          for f64;
-//        - (fast mode) the remaining few-lane phases: short ones lane by
-//          lane, long ones with S = 32/k sub-streams per live lane and a
-//          shuffle tree;
+//      and element offset per phase, hbp_phase_emit), one phase per lane
+//      register; the walk is
+//        - exact mode: a step-uniform loop, every live lane adds its element
+//          of the step -- each row is summed in step order, bitwise identical
+//          to _kernels.py:41-46 for f64;
+//        - fast mode: per phase of k live lanes, passes of S*k consecutive
+//          elements (S = floor(32/k)); lane i always meets rank i mod k, keeps
+//          a register sum over the phase, and one shuffle tree per phase
+//          folds the S sums of each rank into the row owner's accumulator;
 //   5. a group cut by a slice boundary (fast mode only) leaves per-lane
 //      partials; the warp whose piece completes the group's element count
 //      (atomic) adds the pieces in slice order -- deterministic.
@@ -93,10 +94,13 @@ __device__ __forceinline__ void fence_mbar_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
-// per live-lane count k (1..32): sub-streams S = largest power of two with
-// k*S <= 32, and ceil(2^16/k) (exact lane / k for lane < 32)
-__constant__ int c_streams[33] = {0,  32, 16, 8, 8, 4, 4, 4, 4, 2, 2, 2, 2, 2, 2, 2, 2,
-                                  1,  1,  1,  1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1};
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// ceil(2^16 / k): floor(n / k) = (n * m) >> 16 exactly for n <= 32
 __constant__ uint32_t c_magic16[33] = {
     0,    65536, 32768, 21846, 16384, 13108, 10923, 9363, 8192, 7282, 6554,
     5958, 5462,  5042,  4682,  4370,  4096,  3856,  3641, 3450, 3277, 3121,
@@ -152,68 +156,61 @@ __device__ __forceinline__ V product(V v, V xv) {
 // are 32-bit offsets relative to `base` (slice start rounded down to 16 B).
 template <typename V, bool EXACT, int CH, int NB, bool XNA>
 struct Ring {
+    static_assert((NB & (NB - 1)) == 0 && (CH & (CH - 1)) == 0, "NB, CH: powers of two");
     static constexpr int RMASK = NB * CH - 1;
     static constexpr int EPL = CH / 32;  // elements per lane per chunk
-    const hbp_format_t &f;
     WarpSmem<V, CH, NB> &S;
     const V *__restrict__ x;
-    int64_t base;
-    int32_t len32;        // c_hi - base
+    const uint32_t *colg;  // f.col + base
+    const V *valg;         // f.data + base
+    int32_t len32;         // c_hi - base
     int32_t nchunks;
-    int32_t ready = -1;   // chunks <= ready hold products
-    int32_t pending = -1; // chunk whose x gathers are in flight
-    int32_t issued = 0;   // bulk copies issued (lane 0)
-    int32_t res32 = 0;    // products resident for offsets < res32
+    int32_t ready = -1;    // chunks <= ready hold products
+    int32_t pending = -1;  // chunk whose x gathers are in flight
+    int32_t res32 = 0;     // products resident for offsets < res32
     int lane;
     uint64_t pe, pl;
-    V xr[EPL];            // gathered x of the pending chunk
+    V xr[EPL];             // gathered x of the pending chunk
 
-    __device__ void issue_upto(int32_t last) {  // lane 0
-        for (; issued <= last && issued < nchunks; ++issued) {
-            const int32_t ca = issued * CH;
-            const int32_t n = (ca + CH < len32 ? ca + CH : len32) - ca;
-            const int slot = issued % NB;
-            const uint32_t bc = (uint32_t)((n * 4 + 15) & ~15);
-            const uint32_t bv = (uint32_t)((n * (int)sizeof(V) + 15) & ~15);
-            mbar_expect_tx(&S.mbar[slot], bc + bv);
-            bulk_g2s(&S.col[slot * CH], f.col + base + ca, bc, &S.mbar[slot], pe);
-            bulk_g2s(&S.val[slot * CH], (const V *)f.data + base + ca, bv, &S.mbar[slot], pe);
+    // lane 0: bulk-copy chunk c (< nchunks) into its slot
+    __device__ __forceinline__ void issue(int32_t c) {
+        const int slot = c & (NB - 1);
+        uint32_t bc = CH * 4, bv = CH * (uint32_t)sizeof(V);
+        if (c == nchunks - 1) {
+            const int32_t n = len32 - c * CH;
+            bc = (uint32_t)((n * 4 + 15) & ~15);
+            bv = (uint32_t)((n * (int)sizeof(V) + 15) & ~15);
         }
+        mbar_expect_tx(&S.mbar[slot], bc + bv);
+        bulk_g2s(&S.col[slot * CH], colg + (int64_t)c * CH, bc, &S.mbar[slot], pe);
+        bulk_g2s(&S.val[slot * CH], valg + (int64_t)c * CH, bv, &S.mbar[slot], pe);
     }
 
     // chunk c: wait for its bytes, issue its x gathers into xr
     __device__ __forceinline__ void start(int32_t c) {
-        const int slot = c % NB;
+        const int slot = c & (NB - 1);
         mbar_wait(&S.mbar[slot], (uint32_t)((c / NB) & 1));
-        const int32_t n = (c * CH + CH < len32 ? c * CH + CH : len32) - c * CH;
         uint32_t cc[EPL];
-        if constexpr (EPL == 4) {
-            const uint4 t = *reinterpret_cast<const uint4 *>(&S.col[slot * CH + 4 * lane]);
-            cc[0] = t.x, cc[1] = t.y, cc[2] = t.z, cc[3] = t.w;
-        } else if constexpr (EPL == 2) {
-            const uint2 t = *reinterpret_cast<const uint2 *>(&S.col[slot * CH + 2 * lane]);
-            cc[0] = t.x, cc[1] = t.y;
-        } else {
 #pragma unroll
-            for (int e = 0; e < EPL; e += 4) {
-                const uint4 t =
-                    *reinterpret_cast<const uint4 *>(&S.col[slot * CH + EPL * lane + e]);
-                cc[e] = t.x, cc[e + 1] = t.y, cc[e + 2] = t.z, cc[e + 3] = t.w;
-            }
+        for (int e = 0; e < EPL; e += 4) {
+            const uint4 t = *reinterpret_cast<const uint4 *>(&S.col[slot * CH + EPL * lane + e]);
+            cc[e] = t.x, cc[e + 1] = t.y, cc[e + 2] = t.z, cc[e + 3] = t.w;
+        }
+        if (c == nchunks - 1) {  // never gather past the slice
+            const int32_t n = len32 - c * CH;
+#pragma unroll
+            for (int e = 0; e < EPL; ++e)
+                if (EPL * lane + e >= n) cc[e] = 0u;
         }
 #pragma unroll
-        for (int e = 0; e < EPL; ++e) {
-            if (EPL * lane + e >= n) cc[e] = 0u;  // never gather past the slice
-            xr[e] = XNA ? ld_x_na(x + cc[e], pl) : ld_x(x + cc[e], pl);
-        }
+        for (int e = 0; e < EPL; ++e) xr[e] = XNA ? ld_x_na(x + cc[e], pl) : ld_x(x + cc[e], pl);
         pending = c;
     }
 
     // pending chunk: values -> products (in place)
     __device__ __forceinline__ void finish() {
         const int c = pending;
-        const int slot = c % NB;
-        V *v = &S.val[slot * CH + EPL * lane];
+        V *v = &S.val[(c & (NB - 1)) * CH + EPL * lane];
 #pragma unroll
         for (int e = 0; e < EPL; ++e) v[e] = product<V, EXACT>(v[e], xr[e]);
         ready = c;
@@ -233,20 +230,107 @@ struct Ring {
             fence_proxy_async();  // generic ring accesses precede later bulk writes
             __syncwarp();
             if (ready + 1 < nchunks) start(ready + 1);
-            // slots of chunks <= ready - 2 are free (the walk may still read
+            // the slot of chunk ready - 2 is free (the walk may still read
             // ready - 1 for a step straddling the boundary)
-            if (lane == 0) issue_upto(ready + NB - 2);
+            if (lane == 0 && ready + NB - 2 < nchunks) issue(ready + NB - 2);
         }
     }
 
     __device__ __forceinline__ double at(int32_t o) const { return (double)S.val[o & RMASK]; }
 };
 
-template <typename V, bool EXACT, int CH, int NB, int MINB, bool XNA>
+// Fast-mode walk of one group (or the piece [lo_r, hi_r) of it).  Phase j's
+// live mask and start offset sit in lane j's `ph`.  Per phase of k live lanes:
+//   - k < KT and more than LMIN steps: passes of stride = S*k consecutive
+//     elements (S = floor(32/k)); lane i takes element q + i, whose rank is
+//     i mod k in every pass, so each lane keeps one register sum for the phase;
+//     a deterministic shuffle tree folds the S sums of a rank and the row's
+//     owner lane takes its rank's total;
+//   - otherwise step by step: each live lane adds its element of the step.
+template <bool PIECE, int KT, int LMIN, class RingT>
+__device__ __forceinline__ double walk_fast(RingT &ring, const uint2 ph, const int np,
+                                            const int32_t gb, const int32_t gend,
+                                            const int32_t lo_r, const int32_t hi_r,
+                                            const int lane) {
+    double acc = 0.0;
+    int j = 0;
+    if (PIECE)  // phase containing lo
+        j = __popc(__ballot_sync(FULL, lane < np && (int32_t)ph.y <= lo_r - gb)) - 1;
+    int32_t ps = gb + (int32_t)__shfl_sync(FULL, ph.y, j);
+    for (;;) {
+        const unsigned pm = __shfl_sync(FULL, ph.x, j);
+        const int32_t pe_o = (int32_t)__shfl_sync(FULL, ph.y, (j + 1) & 31);
+        const int32_t pe = gb + (j + 1 < np ? pe_o : gend);
+        const int k = __popc(pm);
+        const int32_t stop = PIECE ? (pe < hi_r ? pe : hi_r) : pe;
+        if (k < KT && pe - ps > LMIN * k) {
+            const uint32_t mk = c_magic16[k];
+            const int SS = (int)((32u * mk) >> 16);  // floor(32 / k)
+            const int32_t stride = SS * k;
+            int32_t q = ps;
+            if (PIECE && lo_r > ps) q = ps + ((lo_r - ps) / stride) * stride;
+            const bool act = lane < stride;
+            double v0 = 0.0, v1 = 0.0;
+            for (; q < stop; q += 2 * stride) {
+                const int32_t q2 = q + stride;
+                const int32_t need = q2 + stride < stop ? q2 + stride : stop;
+                if (need > ring.res32) ring.advance(need);
+                const int32_t P0 = q + lane, P1 = q2 + lane;
+                if (act && P0 < stop && (!PIECE || P0 >= lo_r)) v0 += ring.at(P0);
+                if (act && P1 < stop && (!PIECE || P1 >= lo_r)) v1 += ring.at(P1);
+            }
+            double v = v0 + v1;
+            if (SS > 1) {
+                const int s = (int)(((uint32_t)lane * mk) >> 16);  // lane / k
+                for (int d = 1; d < SS; d <<= 1) {
+                    const double o = __shfl_down_sync(FULL, v, d * k);
+                    if ((s & (2 * d - 1)) == 0 && s + d < SS) v += o;
+                }
+            }
+            const double tot = __shfl_sync(FULL, v, __popc(pm & lanemask_lt()));
+            if ((pm >> lane) & 1u) acc += tot;
+        } else if (!PIECE) {
+            // whole phase, steps end exactly at pe: bound checks merged with
+            // the residency limit, two steps per iteration
+            const bool live = (pm >> lane) & 1u;
+            const int32_t P0 = ps + __popc(pm & lanemask_lt());
+            int32_t pb = 0;  // element offset of the step within the phase
+            const int32_t plen = pe - ps;
+            for (;;) {
+                int32_t lim = ring.res32 - ps;
+                lim = lim < plen ? lim : plen;
+                for (; pb + 2 * k <= lim; pb += 2 * k) {
+                    if (live) acc += ring.at(P0 + pb) + ring.at(P0 + pb + k);
+                }
+                if (pb + k <= lim) {
+                    if (live) acc += ring.at(P0 + pb);
+                    pb += k;
+                }
+                if (pb >= plen) break;
+                ring.advance(ps + pb + k);
+            }
+        } else {
+            const bool live = (pm >> lane) & 1u;
+            const int32_t rank = __popc(pm & lanemask_lt());
+            int32_t pb = ps;
+            if (lo_r > ps) pb = ps + div_small(lo_r - ps, k) * k;
+            for (; pb < stop; pb += k) {
+                const int32_t need = pb + k < stop ? pb + k : stop;
+                if (need > ring.res32) ring.advance(need);
+                const int32_t P = pb + rank;
+                if (live && P < stop && P >= lo_r) acc += ring.at(P);
+            }
+        }
+        if ((PIECE && stop < pe) || ++j == np) break;  // reached hi, or the group's end
+        ps = pe;
+    }
+    return acc;
+}
+
+template <typename V, bool EXACT, int CH, int NB, int MINB, bool XNA, int KT, int LMIN>
 __global__ void __launch_bounds__(kThreads, MINB)
     k_spmv_stream(const hbp_format_t f, const hbp_balanced_t b, const V *__restrict__ x,
                   V *__restrict__ y, double *__restrict__ partial) {
-    constexpr int KT = 8;  // fast mode: fewer live lanes -> per-phase processing
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
@@ -254,19 +338,13 @@ __global__ void __launch_bounds__(kThreads, MINB)
     const int64_t w = (int64_t)blockIdx.x * kWarps + wib;
     const int64_t Nw = b.workers;
     if (w >= Nw) return;
-    const unsigned lt = (1u << lane) - 1u;
-    const int64_t R = f.row_height, gpb = R / 32;
+    const int32_t R = (int32_t)f.row_height, gpb = R / 32;
     const int64_t ngroups = f.nzb * gpb;
     const int64_t E = f.nnz;
     const int64_t *__restrict__ gs = f.group_start;
     const int64_t *__restrict__ pptr = f.phase_ptr;
     const uint2 *__restrict__ phs = (const uint2 *)f.phases;
     const uint32_t *__restrict__ permp = (const uint32_t *)f.perm;
-
-    Ring<V, EXACT, CH, NB, XNA> ring{f, S, x};
-    ring.lane = lane;
-    ring.pe = policy_evict_first();
-    ring.pl = policy_evict_last();
 
     int64_t c_lo = cut_at(w, E, Nw), c_hi = cut_at(w + 1, E, Nw);
     if (EXACT) {  // round slice ends up to group boundaries
@@ -280,153 +358,124 @@ __global__ void __launch_bounds__(kThreads, MINB)
         }
     }
     const int64_t base = c_lo & ~(int64_t)3;
-    ring.base = base;
-    ring.len32 = (int32_t)(c_hi - base);
-    ring.nchunks = c_hi > c_lo ? (ring.len32 + CH - 1) / CH : 0;
+    Ring<V, EXACT, CH, NB, XNA> ring{S, x, f.col + base, (const V *)f.data + base};
+    ring.lane = lane;
+    ring.pe = policy_evict_first();
+    ring.pl = policy_evict_last();
+    const int32_t len32 = (int32_t)(c_hi - base);
+    const int32_t lo_s = (int32_t)(c_lo - base);  // slice start (0..3)
+    ring.len32 = len32;
+    ring.nchunks = c_hi > c_lo ? (len32 + CH - 1) / CH : 0;
 
     if (lane == 0) {
         for (int i = 0; i < NB; ++i) mbar_init(&S.mbar[i], 1);
         fence_mbar_init();
+        for (int c = 0; c <= NB - 3 && c < ring.nchunks; ++c) ring.issue(c);
     }
     __syncwarp();
-    if (lane == 0) ring.issue_upto(NB - 3);
 
     int64_t g = upper_group(gs, ngroups, c_lo);
     if (!(g < ngroups && gs[g] < c_lo)) g = lower_group(gs, ngroups, c_lo);
     const bool last_warp = (w == Nw - 1);
+    // output position of group g: nonzero block blk, group gi within it
+    int32_t blk = (int32_t)(g / gpb), gi = (int32_t)(g - (int64_t)blk * gpb);
+    int32_t rows_left = 0;  // rows of block blk (<= R)
+    V *yb = nullptr;
+    double *pb_out = nullptr;
+    auto enter_block = [&]() {
+        if (blk < f.nzb) {
+            const int64_t br = f.blk_br[blk];
+            const int64_t left = f.rows - br * R;
+            rows_left = (int32_t)(left < R ? left : R);
+            yb = y + br * R;
+            pb_out = partial ? partial + (int64_t)blk * R : nullptr;
+        }
+    };
+    enter_block();
 
-    // prefetched metadata of group g: element range, output rows, phases
-    int64_t gs0 = g < ngroups ? gs[g] : E;
-    int64_t gs1 = g < ngroups ? gs[g + 1] : E;
+    // prefetched metadata of group g: element range (base-relative), output
+    // rows, phases
+    int32_t gr0 = g < ngroups ? (int32_t)(gs[g] - base) : len32;
+    int32_t gr1 = g < ngroups ? (int32_t)(gs[g + 1] - base) : len32;
     uint32_t perm_n = g < ngroups ? permp[g * 32 + lane] : 0u;
     int64_t pp0 = g < ngroups ? pptr[g] : 0;
     int64_t pp1 = g < ngroups ? pptr[g + 1] : 0;
     uint2 ph_n = make_uint2(0u, 0u);
     if (g < ngroups && lane < pp1 - pp0) ph_n = phs[pp0 + lane];
 
-    for (; g < ngroups && (gs0 < c_hi || last_warp); ++g) {
+    for (; g < ngroups && (gr0 < len32 || last_warp); ++g) {
         const uint32_t row_local = perm_n;
-        const int64_t g0 = gs0, g1 = gs1;
+        const int32_t g0 = gr0, g1 = gr1;
         const int np = (int)(pp1 - pp0);
         const uint2 ph = ph_n;
         if (g + 1 < ngroups) {  // prefetch the next group's metadata
-            gs0 = g1;
-            gs1 = gs[g + 2];
+            gr0 = g1;
+            gr1 = (int32_t)(gs[g + 2] - base);
             perm_n = permp[(g + 1) * 32 + lane];
             pp0 = pp1;
             pp1 = pptr[g + 2];
             ph_n = lane < pp1 - pp0 ? phs[pp0 + lane] : make_uint2(0u, 0u);
         }
-        const int64_t lo = g0 > c_lo ? g0 : c_lo;
-        const int64_t hi = g1 < c_hi ? g1 : c_hi;
+        const int32_t lo = g0 > lo_s ? g0 : lo_s;
+        const int32_t hi = g1 < len32 ? g1 : len32;
         const bool piece = (lo > g0) || (hi < g1);
 
         double acc = 0.0;
-        if (lo < hi) {
+        if (!EXACT && lo < hi) {
+            acc = piece ? walk_fast<true, KT, LMIN>(ring, ph, np, g0, g1 - g0, lo, hi, lane)
+                        : walk_fast<false, KT, LMIN>(ring, ph, np, g0, g1 - g0, lo, hi, lane);
+        } else if (lo < hi) {
             __syncwarp();  // previous group's table reads are done
             if (lane < np) {
                 S.ph_mask[lane] = ph.x;
                 S.ph_off[lane] = (int32_t)ph.y;
             }
-            if (lane == 0) S.ph_off[np] = (int32_t)(g1 - g0);
+            if (lane == 0) S.ph_off[np] = g1 - g0;
             __syncwarp();
-            const int32_t gb = (int32_t)(g0 - base);  // group start, ring offset (may be < 0)
-            const int32_t lo_r = (int32_t)(lo - base), hi_r = (int32_t)(hi - base);
-            // start: phase j and step t containing lo
-            const int32_t o_lo = lo_r - gb;
+            const unsigned lt = lanemask_lt();
+            // exact mode: whole groups only (slices end on group boundaries)
             int j = 0;
-            while (j + 1 < np && S.ph_off[j + 1] <= o_lo) ++j;
-            unsigned pm = S.ph_mask[j];
+            unsigned pm = S.ph_mask[0];
             int k = __popc(pm);
-            int32_t pend_j = gb + S.ph_off[j + 1];  // ring offset where phase j ends
-            int32_t pb = gb + S.ph_off[j] + div_small(o_lo - S.ph_off[j], k) * k;
+            int32_t pend_j = g0 + S.ph_off[1];  // ring offset where phase j ends
+            int32_t pb = g0;
             bool live = (pm >> lane) & 1u;
             int rank = __popc(pm & lt);
 
-            // ---- step-uniform lane walk (exact: all phases; fast: k >= KT)
-            while (pb < hi_r && (EXACT || k >= KT)) {
-                const int32_t stop = pend_j < hi_r ? pend_j : hi_r;
-                if (!piece) {
-                    for (; pb < stop; pb += k) {
-                        if (pb + k > ring.res32) ring.advance(pb + k);
-                        if (live) {
-                            const double v = ring.at(pb + rank);
-                            acc = EXACT ? __dadd_rn(acc, v) : acc + v;
-                        }
-                    }
-                } else {
-                    for (; pb < stop; pb += k) {
-                        if (pb + k > ring.res32) ring.advance(pb + k < hi_r ? pb + k : hi_r);
-                        const int32_t P = pb + rank;
-                        if (live && P >= lo_r && P < hi_r) {
-                            const double v = ring.at(P);
-                            acc = EXACT ? __dadd_rn(acc, v) : acc + v;
-                        }
-                    }
+            // ---- exact mode: step-uniform lane walk, each row in step order
+            while (pb < hi) {
+                for (; pb < pend_j; pb += k) {
+                    if (pb + k > ring.res32) ring.advance(pb + k);
+                    if (live) acc = __dadd_rn(acc, ring.at(pb + rank));
                 }
-                if (pb < pend_j) break;  // reached hi inside the phase
                 if (++j == np) break;
                 pm = S.ph_mask[j];
                 k = __popc(pm);
-                pend_j = gb + S.ph_off[j + 1];
+                pend_j = g0 + S.ph_off[j + 1];
                 live = (pm >> lane) & 1u;
                 rank = __popc(pm & lt);
-            }
-            // ---- fast mode: phases with few live lanes
-            if (!EXACT) {
-                while (pb < hi_r && j < np) {
-                    const int32_t stop = pend_j < hi_r ? pend_j : hi_r;
-                    if (stop - pb > 8 * k && pb >= lo_r) {
-                        const int SS = c_streams[k];
-                        const int s = (int)(((uint32_t)lane * c_magic16[k]) >> 16);  // lane / k
-                        const int r = lane - s * k;
-                        const int32_t stride = SS * k;
-                        double v = 0.0;
-                        for (int32_t q = pb; q < stop; q += stride) {  // SS steps per pass
-                            const int32_t need = q + stride < stop ? q + stride : stop;
-                            if (need > ring.res32) ring.advance(need);
-                            const int32_t P = q + s * k + r;
-                            if (s < SS && P < stop) v += ring.at(P);
-                        }
-                        for (int d = SS >> 1; d >= 1; d >>= 1)
-                            v += __shfl_down_sync(FULL, v, d * k);
-                        const double tot = __shfl_sync(FULL, v, live ? rank : 0);
-                        if (live) acc += tot;
-                        pb = stop;
-                    } else {
-                        // short phase (or a step cut by the slice start): lane by lane
-                        const int32_t stop1 = stop - pb > 8 * k ? pb + k : stop;
-                        for (; pb < stop1; pb += k) {
-                            if (pb + k > ring.res32) ring.advance(pb + k < hi_r ? pb + k : hi_r);
-                            const int32_t P = pb + rank;
-                            if (live && P >= lo_r && P < hi_r) acc += ring.at(P);
-                        }
-                        if (pb < pend_j && stop1 != stop) continue;  // rest of this phase
-                    }
-                    if (pb < pend_j) break;  // reached hi inside the phase
-                    if (++j == np) break;
-                    pm = S.ph_mask[j];
-                    k = __popc(pm);
-                    pend_j = gb + S.ph_off[j + 1];
-                    live = (pm >> lane) & 1u;
-                    rank = __popc(pm & lt);
-                }
             }
         }
 
         // ---- outputs
-        const int64_t blk = g / gpb;
-        const int64_t local = (g - blk * gpb) * 32 + lane;
-        const int64_t br = f.blk_br[blk];
-        const bool valid = local < f.rows - br * R;
+        const int32_t gi_now = gi;
+        const bool valid = gi_now * 32 + lane < rows_left;
+        V *const yb_now = yb;
+        double *const pb_now = pb_out;
+        if (++gi == gpb) {
+            gi = 0;
+            ++blk;
+            enter_block();
+        }
         if (!piece) {
             if (valid) {
-                if (partial) partial[blk * R + row_local] = acc;
-                else y[br * R + row_local] = (V)acc;
+                if (pb_now) pb_now[row_local] = acc;
+                else yb_now[row_local] = (V)acc;
             }
             continue;
         }
         // fast mode only: a piece of a group cut by slice boundaries
+        const int64_t ga0 = base + g0, ga1 = base + g1;  // absolute element range
         double *slotp = (lo > g0) ? b.part_head + w * 32 : b.part_tail + w * 32;
         __stcg(slotp + lane, acc);
         __threadfence();
@@ -440,45 +489,45 @@ __global__ void __launch_bounds__(kThreads, MINB)
         done = __shfl_sync(FULL, done, 0);
         if (!done) continue;
         __threadfence();
-        int64_t wa = (int64_t)((__int128)g0 * Nw / E);
-        while (wa + 1 < Nw && cut_at(wa + 1, E, Nw) <= g0) ++wa;
-        while (wa > 0 && cut_at(wa, E, Nw) > g0) --wa;
+        int64_t wa = (int64_t)((__int128)ga0 * Nw / E);
+        while (wa + 1 < Nw && cut_at(wa + 1, E, Nw) <= ga0) ++wa;
+        while (wa > 0 && cut_at(wa, E, Nw) > ga0) --wa;
         double s = __ldcg(b.part_tail + wa * 32 + lane);
         for (int64_t v = wa + 1; v < Nw; ++v) {
             s += __ldcg(b.part_head + v * 32 + lane);
-            if (cut_at(v + 1, E, Nw) >= g1) break;
+            if (cut_at(v + 1, E, Nw) >= ga1) break;
         }
         if (valid) {
-            if (partial) partial[blk * R + row_local] = s;
-            else y[br * R + row_local] = (V)s;
+            if (pb_now) pb_now[row_local] = s;
+            else yb_now[row_local] = (V)s;
         }
         if (lane == 0) b.counters[g] = 0u;
     }
 }
 
-template <typename V, bool EXACT, int CH, int NB, int MINB, bool XNA>
+template <typename V, bool EXACT, int CH, int NB, int MINB, bool XNA, int KT, int LMIN>
 int launch(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y,
            double *partial, cudaStream_t st) {
     const size_t smem = sizeof(WarpSmem<V, CH, NB>) * kWarps;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_spmv_stream<V, EXACT, CH, NB, MINB, XNA>,
+        cudaFuncSetAttribute(k_spmv_stream<V, EXACT, CH, NB, MINB, XNA, KT, LMIN>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
     unsigned grid = (unsigned)((b->workers + kWarps - 1) / kWarps);
-    k_spmv_stream<V, EXACT, CH, NB, MINB, XNA><<<grid, kThreads, smem, st>>>(
+    k_spmv_stream<V, EXACT, CH, NB, MINB, XNA, KT, LMIN><<<grid, kThreads, smem, st>>>(
         *f, *b, (const V *)x, (V *)y, partial);
     return (int)cudaGetLastError();
 }
 
-template <typename V, bool EXACT, int CH, int NB, int MINB, bool XNA>
+template <typename V, bool EXACT, int CH, int NB, int MINB, bool XNA, int KT, int LMIN>
 int occupancy_of(int *per_sm) {
     const size_t smem = sizeof(WarpSmem<V, CH, NB>) * kWarps;
-    cudaFuncSetAttribute(k_spmv_stream<V, EXACT, CH, NB, MINB, XNA>,
+    cudaFuncSetAttribute(k_spmv_stream<V, EXACT, CH, NB, MINB, XNA, KT, LMIN>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        per_sm, k_spmv_stream<V, EXACT, CH, NB, MINB, XNA>, kThreads, smem);
+        per_sm, k_spmv_stream<V, EXACT, CH, NB, MINB, XNA, KT, LMIN>, kThreads, smem);
 }
 
 // Tile / occupancy variants (chunk CH, ring slots NB, min CTAs per SM),
@@ -494,16 +543,16 @@ int variant() {
     return v;
 }
 
-#define HBP_STREAM_VARIANTS(FN, V, EXACT, ...)                     \
-    switch (variant()) {                                            \
-        case 1: return FN<V, EXACT, 64, 8, 4, true>(__VA_ARGS__);  \
-        case 2: return FN<V, EXACT, 128, 8, 3, true>(__VA_ARGS__); \
-        case 3: return FN<V, EXACT, 256, 4, 2, true>(__VA_ARGS__); \
-        case 4: return FN<V, EXACT, 128, 8, 2, true>(__VA_ARGS__); \
-        case 5: return FN<V, EXACT, 128, 4, 4, true>(__VA_ARGS__); \
-        case 6: return FN<V, EXACT, 64, 8, 3, true>(__VA_ARGS__);  \
-        case 7: return FN<V, EXACT, 128, 4, 3, false>(__VA_ARGS__); \
-        default: return FN<V, EXACT, 128, 4, 3, true>(__VA_ARGS__); \
+#define HBP_STREAM_VARIANTS(FN, V, EXACT, ...)                                \
+    switch (variant()) {                                                       \
+        case 1: return FN<V, EXACT, 128, 4, 3, true, 33, 0>(__VA_ARGS__);     \
+        case 2: return FN<V, EXACT, 128, 4, 3, true, 0, 0>(__VA_ARGS__);      \
+        case 3: return FN<V, EXACT, 128, 4, 3, true, 4, 4>(__VA_ARGS__);      \
+        case 4: return FN<V, EXACT, 128, 4, 3, true, 8, 8>(__VA_ARGS__);      \
+        case 5: return FN<V, EXACT, 128, 4, 3, true, 16, 2>(__VA_ARGS__);     \
+        case 6: return FN<V, EXACT, 128, 4, 3, true, 8, 2>(__VA_ARGS__);      \
+        case 7: return FN<V, EXACT, 128, 4, 3, true, 8, 16>(__VA_ARGS__);     \
+        default: return FN<V, EXACT, 128, 4, 3, true, 12, 4>(__VA_ARGS__);    \
     }
 
 template <typename V, bool EXACT>

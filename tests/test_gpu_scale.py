@@ -1,0 +1,107 @@
+"""Parity at larger sizes (GPU): the full oracle pipeline where the dense
+reference layout is affordable, otherwise per-block spot checks and
+size-independent properties.
+
+- Laplacian 512^2 (262,144 rows, C = 4096, R = 512, W = 32, f64): every
+  reference array and y bitwise (the cfg1 geometry at 1/4 size).
+- R-MAT scale 18 with hot rows, f32, C = cols: hash permutations of sampled
+  blocks vs the oracle's per-block FCFS probing, zero_row/group sizes from
+  the compact arrays, y within 1e-5 componentwise of the fp64 oracle on the
+  fp32-rounded inputs, and the inverse walk reproduces the matrix.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import has_gpu
+
+pytestmark = pytest.mark.gpu
+
+if has_gpu():
+    import torch
+    import paper_2504_08860_b200 as H
+    from oracle import oracle as O
+    import bench_inputs as BI
+
+
+def test_laplacian_512_default_geometry_bitwise():
+    rows, cols, rp, ci, v = BI.laplacian_csr(512)
+    C, R, W = 4096, 512, 32
+    r = np.repeat(np.arange(rows), np.diff(rp))
+    p = O.pipeline(rows, cols, r, ci, v, C, R, W)
+    cfg = H.PartitionConfig(col_width=C, row_height=R, warp_size=W)
+    csr = H.CsrMatrix(rows, cols, rp, ci, v)
+    grid = H.make_grid(csr, cfg)
+    params = H.sample_hash_params(grid, cfg)
+    assert (params.a, params.b, params.c, params.d) == tuple(p["params"])
+    ctr = H.OpCounter()
+    hbp = H.build_hbp(csr, grid, H.hash_permutations(grid, params, counter=ctr))
+    assert ctr.probes == p["probes"]
+    ref = hbp.to_reference()
+    for k in ("col", "add_sign", "zero_row", "group_start", "output_hash"):
+        np.testing.assert_array_equal(ref[k], getattr(p["hbp"], k), err_msg=k)
+    x = np.random.default_rng(0).uniform(-1, 1, cols)
+    want = O.hbp_spmv(p["hbp"], x, workers=8)
+    for schedule in ("stream", "balanced", "plan"):
+        y = H.SpmvOperator(hbp, schedule=schedule)(torch.as_tensor(x, device="cuda"))
+        np.testing.assert_array_equal(y.cpu().numpy(), want, err_msg=schedule)
+
+
+@pytest.fixture(scope="module")
+def rmat18():
+    rows, cols, rp, ci, v = BI.rmat_csr_numpy(18, 16, seed=7)
+    v32 = v.astype(np.float32)
+    cfg = H.PartitionConfig(col_width=cols)
+    csr = H.CsrMatrix(rows, cols, rp, ci, v32)
+    grid = H.make_grid(csr, cfg)
+    params = H.sample_hash_params(grid, cfg)
+    perms = H.hash_permutations(grid, params)
+    hbp = H.build_hbp(csr, grid, perms)
+    return dict(rows=rows, cols=cols, rp=rp, ci=ci, v=v32.astype(np.float64), cfg=cfg, csr=csr,
+                grid=grid, params=params, perms=perms, hbp=hbp)
+
+
+def test_rmat_block_permutations_match_oracle(rmat18):
+    m = rmat18
+    g, p = m["grid"], m["params"]
+    rng = np.random.default_rng(1)
+    lens = np.diff(m["rp"])
+    R = g.config.row_height
+    for br in rng.choice(g.num_row_blocks, 40, replace=False):
+        br = int(br)
+        n = g.rows_in_block(br)
+        want, _ = O.hash_perm_block(lens[br * R:br * R + n], p.a, p.b, p.c, p.d)
+        got = np.asarray(H.perm_for_block(m["perms"], g, br, 0))
+        np.testing.assert_array_equal(got, want)
+
+
+def test_rmat_spmv_f32_within_tolerance_all_schedules(rmat18):
+    m = rmat18
+    x = np.random.default_rng(2).uniform(-1, 1, m["cols"]).astype(np.float32)
+    r = np.repeat(np.arange(m["rows"]), np.diff(m["rp"]))
+    for schedule in ("stream", "balanced", "plan"):
+        y = H.SpmvOperator(m["hbp"], schedule=schedule)(torch.as_tensor(x, device="cuda"))
+        err = O.componentwise_error(m["rows"], r, m["ci"], m["v"], x.astype(np.float64),
+                                    y.cpu().numpy().astype(np.float64))
+        assert err <= 1e-5, (schedule, err)
+
+
+def test_rmat_inverse_walk_reproduces_matrix(rmat18):
+    m = rmat18
+    back = H.hbp_to_triplets(m["hbp"]).canonicalized()
+    r, c, v = back.to_numpy()
+    np.testing.assert_array_equal(np.concatenate(([0], np.cumsum(np.bincount(r, minlength=m["rows"])))),
+                                  m["rp"])
+    np.testing.assert_array_equal(c, m["ci"])
+    np.testing.assert_array_equal(v, m["v"])
+
+
+def test_rmat_csr_and_2d_baselines(rmat18):
+    m = rmat18
+    x = np.random.default_rng(3).uniform(-1, 1, m["cols"]).astype(np.float32)
+    want = O.csr_spmv(m["rp"], m["ci"], m["v"], x.astype(np.float64))
+    y = H.csr_spmv(m["csr"], x).cpu().numpy().astype(np.float64)
+    np.testing.assert_array_equal(y, want.astype(np.float32).astype(np.float64))
+    y2 = H.block2d_spmv_baseline(m["csr"], m["grid"], x).cpu().numpy().astype(np.float64)
+    np.testing.assert_array_equal(y2, want.astype(np.float32).astype(np.float64))
