@@ -54,6 +54,13 @@ struct __align__(16) WarpSmem {
     uint32_t ph_mask[33];
     int32_t ph_off[33];
     uint64_t mbar[NB];
+    // cold ring state, touched once per chunk (kept out of registers)
+    const uint32_t *colg;  // f.col + base
+    const V *valg;         // f.data + base
+    int32_t len32;         // c_hi - base
+    int32_t nchunks;
+    int32_t ready;         // chunks <= ready hold products
+    int32_t pending;       // chunk whose x gathers are in flight (-1: none)
 };
 
 // ---- PTX helpers: mbarrier + bulk async copy (sm_90+ / sm_100a) ------------
@@ -154,6 +161,8 @@ __device__ __forceinline__ V product(V v, V xv) {
 
 // Streams one warp's slice through the shared-memory ring.  All positions
 // are 32-bit offsets relative to `base` (slice start rounded down to 16 B).
+// Only res32 and the in-flight gathers live in registers; the rest of the
+// ring state sits in the warp's shared block and is read once per chunk.
 template <typename V, bool EXACT, int CH, int NB, bool XNA>
 struct Ring {
     static_assert((NB & (NB - 1)) == 0 && (CH & (CH - 1)) == 0, "NB, CH: powers of two");
@@ -161,19 +170,12 @@ struct Ring {
     static constexpr int EPL = CH / 32;  // elements per lane per chunk
     WarpSmem<V, CH, NB> &S;
     const V *__restrict__ x;
-    const uint32_t *colg;  // f.col + base
-    const V *valg;         // f.data + base
-    int32_t len32;         // c_hi - base
-    int32_t nchunks;
-    int32_t ready = -1;    // chunks <= ready hold products
-    int32_t pending = -1;  // chunk whose x gathers are in flight
-    int32_t res32 = 0;     // products resident for offsets < res32
+    int32_t res32 = 0;  // products resident for offsets < res32
     int lane;
-    uint64_t pe, pl;
-    V xr[EPL];             // gathered x of the pending chunk
+    V xr[EPL];          // gathered x of the pending chunk
 
     // lane 0: bulk-copy chunk c (< nchunks) into its slot
-    __device__ __forceinline__ void issue(int32_t c) {
+    __device__ __forceinline__ void issue(int32_t c, int32_t nchunks, int32_t len32) {
         const int slot = c & (NB - 1);
         uint32_t bc = CH * 4, bv = CH * (uint32_t)sizeof(V);
         if (c == nchunks - 1) {
@@ -181,13 +183,14 @@ struct Ring {
             bc = (uint32_t)((n * 4 + 15) & ~15);
             bv = (uint32_t)((n * (int)sizeof(V) + 15) & ~15);
         }
+        const uint64_t pe = policy_evict_first();
         mbar_expect_tx(&S.mbar[slot], bc + bv);
-        bulk_g2s(&S.col[slot * CH], colg + (int64_t)c * CH, bc, &S.mbar[slot], pe);
-        bulk_g2s(&S.val[slot * CH], valg + (int64_t)c * CH, bv, &S.mbar[slot], pe);
+        bulk_g2s(&S.col[slot * CH], S.colg + (int64_t)c * CH, bc, &S.mbar[slot], pe);
+        bulk_g2s(&S.val[slot * CH], S.valg + (int64_t)c * CH, bv, &S.mbar[slot], pe);
     }
 
     // chunk c: wait for its bytes, issue its x gathers into xr
-    __device__ __forceinline__ void start(int32_t c) {
+    __device__ __forceinline__ void start(int32_t c, int32_t nchunks, int32_t len32) {
         const int slot = c & (NB - 1);
         mbar_wait(&S.mbar[slot], (uint32_t)((c / NB) & 1));
         uint32_t cc[EPL];
@@ -202,38 +205,50 @@ struct Ring {
             for (int e = 0; e < EPL; ++e)
                 if (EPL * lane + e >= n) cc[e] = 0u;
         }
+        const uint64_t pl = policy_evict_last();
 #pragma unroll
         for (int e = 0; e < EPL; ++e) xr[e] = XNA ? ld_x_na(x + cc[e], pl) : ld_x(x + cc[e], pl);
-        pending = c;
     }
 
-    // pending chunk: values -> products (in place)
-    __device__ __forceinline__ void finish() {
-        const int c = pending;
+    // chunk c (pending): values -> products (in place)
+    __device__ __forceinline__ void finish(int32_t c) {
         V *v = &S.val[(c & (NB - 1)) * CH + EPL * lane];
 #pragma unroll
         for (int e = 0; e < EPL; ++e) v[e] = product<V, EXACT>(v[e], xr[e]);
-        ready = c;
-        res32 = (c * CH + CH < len32 ? c * CH + CH : len32);
-        pending = -1;
     }
 
     // make offsets < need resident (warp-uniform); refills the ring
     __device__ __forceinline__ void advance(int32_t need) {
+        if (need <= res32) return;
+        const int32_t nchunks = S.nchunks, len32 = S.len32;
+        int32_t ready = S.ready, pending = S.pending;
         while (need > res32) {
             if (pending < 0) {
-                if (ready + 1 >= nchunks) return;
-                start(ready + 1);
+                if (ready + 1 >= nchunks) break;
+                start(ready + 1, nchunks, len32);
+                pending = ready + 1;
             }
             __syncwarp();  // the walk's reads of the oldest slot are done
-            finish();
+            finish(pending);
+            ready = pending;
+            pending = -1;
+            res32 = (ready * CH + CH < len32 ? ready * CH + CH : len32);
             fence_proxy_async();  // generic ring accesses precede later bulk writes
             __syncwarp();
-            if (ready + 1 < nchunks) start(ready + 1);
+            if (ready + 1 < nchunks) {
+                start(ready + 1, nchunks, len32);
+                pending = ready + 1;
+            }
             // the slot of chunk ready - 2 is free (the walk may still read
             // ready - 1 for a step straddling the boundary)
-            if (lane == 0 && ready + NB - 2 < nchunks) issue(ready + NB - 2);
+            if (lane == 0 && ready + NB - 2 < nchunks) issue(ready + NB - 2, nchunks, len32);
         }
+        __syncwarp();
+        if (lane == 0) {
+            S.ready = ready;
+            S.pending = pending;
+        }
+        __syncwarp();
     }
 
     __device__ __forceinline__ double at(int32_t o) const { return (double)S.val[o & RMASK]; }
@@ -358,19 +373,21 @@ __global__ void __launch_bounds__(kThreads, MINB)
         }
     }
     const int64_t base = c_lo & ~(int64_t)3;
-    Ring<V, EXACT, CH, NB, XNA> ring{S, x, f.col + base, (const V *)f.data + base};
+    Ring<V, EXACT, CH, NB, XNA> ring{S, x};
     ring.lane = lane;
-    ring.pe = policy_evict_first();
-    ring.pl = policy_evict_last();
     const int32_t len32 = (int32_t)(c_hi - base);
     const int32_t lo_s = (int32_t)(c_lo - base);  // slice start (0..3)
-    ring.len32 = len32;
-    ring.nchunks = c_hi > c_lo ? (len32 + CH - 1) / CH : 0;
-
     if (lane == 0) {
+        const int32_t nchunks = c_hi > c_lo ? (len32 + CH - 1) / CH : 0;
+        S.colg = f.col + base;
+        S.valg = (const V *)f.data + base;
+        S.len32 = len32;
+        S.nchunks = nchunks;
+        S.ready = -1;
+        S.pending = -1;
         for (int i = 0; i < NB; ++i) mbar_init(&S.mbar[i], 1);
         fence_mbar_init();
-        for (int c = 0; c <= NB - 3 && c < ring.nchunks; ++c) ring.issue(c);
+        for (int c = 0; c <= NB - 3 && c < nchunks; ++c) ring.issue(c, nchunks, len32);
     }
     __syncwarp();
 
