@@ -205,6 +205,18 @@ int hbp_block2d_spmv(const uint32_t *len_local, const int64_t *start_local, cons
                      const void *values, int dtype, const void *x, double *partial,
                      hbp_stream_t stream);
 
+/* metrics.py:26-79 group_stats (GroupStats.from_lanes) over the nonzero
+ * blocks: per lane group g = bc*groups_per_col + br*(R/W) + gi, the lane
+ * counts in slot order (perm: compact slot -> local row tables [nzb*R], or
+ * NULL for the unordered grid) into lanes[g*W + q], and mean / population
+ * std_dev (numpy pairwise float64, bitwise) / max / utilization.  Groups of
+ * empty blocks are not written (caller initialises 0, 0, 0, 1.0). */
+int hbp_group_stats(const int32_t *blk_br, const int32_t *blk_bc, int64_t nzb,
+                    const int32_t *len_local, const uint32_t *perm, int64_t rows,
+                    int64_t row_height, int64_t warp_size, int64_t groups_per_col,
+                    int32_t *lanes, double *mean, double *std_dev, int32_t *max_nnz,
+                    double *utilization, hbp_stream_t stream);
+
 /* hbp.py:241-315 hbp_to_triplets: follows every slot's add_sign chain over
  * the reference-layout arrays; row_out[j] = row of element j, seen[j] =
  * visit count (zero-filled by the caller), *err |= 1 (lane start outside its

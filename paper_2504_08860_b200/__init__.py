@@ -13,7 +13,11 @@ Every step runs as hand-written sm_100a CUDA kernels in libhbp.so (C ABI:
 include/hbp.h); arrays are device-resident torch tensors.  There is no CPU
 fallback.
 """
-from .formats import CsrMatrix, TripletMatrix, coo_to_csr, csr_spmv, csr_to_triplets
+from .formats import (CsrMatrix, TripletMatrix, coo_to_csr, csr_spmv, csr_to_triplets,
+                      dense_oracle_spmv, to_dense)
+from .mtx import (MatrixMarketError, MatrixMarketHeader, expand_symmetric, load_mtx,
+                  parse_matrix_market, save_mtx, write_matrix_market)
+from .synth import SyntheticSpec, generate
 from .partition import BlockGrid, PartitionConfig, block_rows_of, make_grid
 from .reorder import (BUCKET_MAX, BlockPermutations, HashParams, OpCounter,
                       build_block_permutation, hash_permutations, hash_slot,
@@ -24,6 +28,8 @@ from .hbp import (HbpFormatError, HbpMatrix, build_hbp, deserialize_hbp, hbp_to_
 from .engine import (ExecutionLog, ExecutionPlan, HostPipeline, PartialVector, SpmvOperator,
                      block2d_spmv_baseline, block_spmv, combine, hbp_spmv, plan_execution,
                      run_spmv)
+from .metrics import (BenchReport, GroupStats, GroupStatsTable, Timing, gflops, group_stats,
+                      group_stats_csv, mean_group_std, reduction_summary, time_kernel)
 
 __version__ = "0.1.0"
 
@@ -37,4 +43,9 @@ __all__ = [
     "identity_permutations", "load_hbp", "make_grid", "perm_for_block", "plan_execution",
     "run_spmv", "sample_hash_params", "save_hbp", "serialize_hbp", "sort_permutation",
     "sort_permutations",
+    "MatrixMarketError", "MatrixMarketHeader", "expand_symmetric", "load_mtx",
+    "parse_matrix_market", "save_mtx", "write_matrix_market", "dense_oracle_spmv", "to_dense",
+    "SyntheticSpec", "generate",
+    "BenchReport", "GroupStats", "GroupStatsTable", "Timing", "gflops", "group_stats",
+    "group_stats_csv", "mean_group_std", "reduction_summary", "time_kernel",
 ]

@@ -90,6 +90,8 @@ _SIGS = {
     "hbp_csr_spmv": [c_vp, c_vp, c_vp, c_int, c_i64, c_vp, c_vp, c_vp],
     "hbp_block2d_spmv": [c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_int, c_vp, c_vp,
                          c_vp],
+    "hbp_group_stats": [c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp,
+                        c_vp, c_vp, c_vp, c_vp],
     "hbp_phase_counts": [c_vp, c_i64, c_vp, c_vp],
     "hbp_phase_emit": [c_vp, c_i64, c_vp, c_vp, c_vp],
     "hbp_expand_reference": [c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp,

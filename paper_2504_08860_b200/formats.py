@@ -18,7 +18,8 @@ import torch
 
 from . import _lib as L
 
-__all__ = ["TripletMatrix", "CsrMatrix", "coo_to_csr", "csr_to_triplets", "as_device_values"]
+__all__ = ["TripletMatrix", "CsrMatrix", "coo_to_csr", "csr_to_triplets", "as_device_values",
+           "csr_spmv", "dense_oracle_spmv", "to_dense"]
 
 
 def _dev(a, dtype: torch.dtype) -> torch.Tensor:
@@ -177,3 +178,31 @@ def csr_to_triplets(csr: CsrMatrix) -> TripletMatrix:
     counts = csr.row_ptr[1:] - csr.row_ptr[:-1]
     row = torch.repeat_interleave(torch.arange(csr.rows, device=counts.device), counts)
     return TripletMatrix(csr.rows, csr.cols, row, csr.col_idx.to(torch.int64), csr.values.clone())
+
+
+def _host_triplets(matrix):
+    if isinstance(matrix, TripletMatrix):
+        return matrix.to_numpy()
+    return (np.asarray(matrix.row, np.int64), np.asarray(matrix.col, np.int64),
+            np.asarray(matrix.val, np.float64))
+
+
+def dense_oracle_spmv(matrix: TripletMatrix, x) -> np.ndarray:
+    """formats.py:276-284: brute-force y = A x in entry order (np.add.at),
+    independent of every kernel; a host verification utility like the
+    reference's, not an SpMV path of this package."""
+    x = np.asarray(x.cpu() if isinstance(x, torch.Tensor) else x, dtype=np.float64)
+    if x.shape != (matrix.cols,):
+        raise ValueError(f"vector length {x.shape} != cols {matrix.cols}")
+    r, c, v = _host_triplets(matrix)
+    y = np.zeros(matrix.rows, dtype=np.float64)
+    np.add.at(y, r, v * x[c])
+    return y
+
+
+def to_dense(matrix: TripletMatrix) -> np.ndarray:
+    """formats.py:287-290 (host array, duplicates summed in entry order)."""
+    r, c, v = _host_triplets(matrix)
+    dense = np.zeros((matrix.rows, matrix.cols), dtype=np.float64)
+    np.add.at(dense, (r, c), v)
+    return dense
