@@ -110,6 +110,29 @@ def banded_csr(n: int, half_band: int = 32, step: int = 2, seed: int = 0):
     return n, n, row_ptr, col, rng.uniform(-1.0, 1.0, col.size)
 
 
+def banded_csr_torch(n: int, device, value_dtype, half_band: int = 32, step: int = 2,
+                     seed: int = 0):
+    """GPU twin of banded_csr (same structure; values from torch's generator):
+    nnz = 33 n - 544 for the default band."""
+    import torch
+    offs = torch.arange(-half_band, half_band + 1, step, device=device)
+    r = torch.arange(n, device=device)
+    first = torch.clamp(((-r - offs.min()) + step - 1) // step, min=0)   # first valid diagonal
+    last = torch.clamp((n - 1 - r - offs.min()) // step, max=offs.numel() - 1)
+    counts = (last - first + 1).clamp(min=0)
+    row_ptr = torch.zeros(n + 1, dtype=torch.int64, device=device)
+    row_ptr[1:] = torch.cumsum(counts, 0)
+    nnz = int(row_ptr[-1].item())
+    row = torch.repeat_interleave(r, counts)
+    k = torch.arange(nnz, device=device) - row_ptr[row]
+    col = (row + offs.min() + (first[row] + k) * step).to(torch.int32)
+    del row, k
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    val = torch.rand(nnz, generator=g, device=device, dtype=torch.float64) * 2 - 1
+    return n, n, row_ptr, col, val.to(value_dtype)
+
+
 def uniform_csr_torch(rows: int, cols: int, mean: float, seed: int, device, value_dtype):
     """Poisson(mean) entries per row, uniform distinct columns (duplicates
     drawn with replacement are removed), values uniform(-1, 1)."""
