@@ -30,8 +30,10 @@
 //      partials; the warp whose piece completes the group's element count
 //      (atomic) adds the pieces in slice order -- deterministic.
 //
-// Precision (fast mode): f32 products (relative error <= 2^-24 each) summed
-// in f64, one rounding to f32: componentwise error <= ~1.2e-7 |A||x|.
+// Precision (fast mode): f32 products (relative error <= u = 2^-24 each),
+// consecutive pairs of a row's products added in f32 (one more rounding of
+// at most u of the pair's magnitude), everything else summed in f64, one
+// final rounding to f32: componentwise error <= ~3u |A||x| (1.8e-7).
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -47,9 +49,17 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr unsigned FULL = 0xffffffffu;
 
+// Column slots: a chunk's columns are needed only until its gathers are
+// issued; while chunk ready+1 is started, chunks up to ready+NB-2 are in
+// flight, so NB-2 slots (rounded up to a power of two, >= 2) suffice.
+template <int NB>
+struct ColSlots {
+    static constexpr int value = NB <= 4 ? 2 : (NB <= 6 ? 4 : NB);
+};
+
 template <typename V, int CH, int NB>
 struct __align__(16) WarpSmem {
-    uint32_t col[NB * CH];
+    uint32_t col[ColSlots<NB>::value * CH];
     V val[NB * CH];  // values, then products in place
     uint32_t ph_mask[33];
     int32_t ph_off[33];
@@ -61,6 +71,8 @@ struct __align__(16) WarpSmem {
     int32_t nchunks;
     int32_t ready;         // chunks <= ready hold products
     int32_t pending;       // chunk whose x gathers are in flight (-1: none)
+    uint64_t pol_stream;   // L2 evict-first policy (element stream)
+    uint64_t pol_x;        // L2 evict-last policy (x gathers)
 };
 
 // ---- PTX helpers: mbarrier + bulk async copy (sm_90+ / sm_100a) ------------
@@ -168,6 +180,7 @@ struct Ring {
     static_assert((NB & (NB - 1)) == 0 && (CH & (CH - 1)) == 0, "NB, CH: powers of two");
     static constexpr int RMASK = NB * CH - 1;
     static constexpr int EPL = CH / 32;  // elements per lane per chunk
+    static constexpr int NCOL = ColSlots<NB>::value;
     WarpSmem<V, CH, NB> &S;
     const V *__restrict__ x;
     int32_t res32 = 0;  // products resident for offsets < res32
@@ -183,9 +196,9 @@ struct Ring {
             bc = (uint32_t)((n * 4 + 15) & ~15);
             bv = (uint32_t)((n * (int)sizeof(V) + 15) & ~15);
         }
-        const uint64_t pe = policy_evict_first();
+        const uint64_t pe = S.pol_stream;
         mbar_expect_tx(&S.mbar[slot], bc + bv);
-        bulk_g2s(&S.col[slot * CH], S.colg + (int64_t)c * CH, bc, &S.mbar[slot], pe);
+        bulk_g2s(&S.col[(c & (NCOL - 1)) * CH], S.colg + (int64_t)c * CH, bc, &S.mbar[slot], pe);
         bulk_g2s(&S.val[slot * CH], S.valg + (int64_t)c * CH, bv, &S.mbar[slot], pe);
     }
 
@@ -194,10 +207,19 @@ struct Ring {
         const int slot = c & (NB - 1);
         mbar_wait(&S.mbar[slot], (uint32_t)((c / NB) & 1));
         uint32_t cc[EPL];
+        const uint32_t *cs = &S.col[(c & (NCOL - 1)) * CH + EPL * lane];
+        if constexpr (EPL % 4 == 0) {
 #pragma unroll
-        for (int e = 0; e < EPL; e += 4) {
-            const uint4 t = *reinterpret_cast<const uint4 *>(&S.col[slot * CH + EPL * lane + e]);
-            cc[e] = t.x, cc[e + 1] = t.y, cc[e + 2] = t.z, cc[e + 3] = t.w;
+            for (int e = 0; e < EPL; e += 4) {
+                const uint4 t = *reinterpret_cast<const uint4 *>(cs + e);
+                cc[e] = t.x, cc[e + 1] = t.y, cc[e + 2] = t.z, cc[e + 3] = t.w;
+            }
+        } else if constexpr (EPL == 2) {
+            const uint2 t = *reinterpret_cast<const uint2 *>(cs);
+            cc[0] = t.x, cc[1] = t.y;
+        } else {
+#pragma unroll
+            for (int e = 0; e < EPL; ++e) cc[e] = cs[e];
         }
         if (c == nchunks - 1) {  // never gather past the slice
             const int32_t n = len32 - c * CH;
@@ -205,7 +227,7 @@ struct Ring {
             for (int e = 0; e < EPL; ++e)
                 if (EPL * lane + e >= n) cc[e] = 0u;
         }
-        const uint64_t pl = policy_evict_last();
+        const uint64_t pl = S.pol_x;
 #pragma unroll
         for (int e = 0; e < EPL; ++e) xr[e] = XNA ? ld_x_na(x + cc[e], pl) : ld_x(x + cc[e], pl);
     }
@@ -213,8 +235,33 @@ struct Ring {
     // chunk c (pending): values -> products (in place)
     __device__ __forceinline__ void finish(int32_t c) {
         V *v = &S.val[(c & (NB - 1)) * CH + EPL * lane];
+        if constexpr (sizeof(V) == 4 && EPL % 4 == 0) {
 #pragma unroll
-        for (int e = 0; e < EPL; ++e) v[e] = product<V, EXACT>(v[e], xr[e]);
+            for (int e = 0; e < EPL; e += 4) {
+                float4 t = *reinterpret_cast<float4 *>(v + e);
+                t.x = (float)product<V, EXACT>((V)t.x, xr[e]);
+                t.y = (float)product<V, EXACT>((V)t.y, xr[e + 1]);
+                t.z = (float)product<V, EXACT>((V)t.z, xr[e + 2]);
+                t.w = (float)product<V, EXACT>((V)t.w, xr[e + 3]);
+                *reinterpret_cast<float4 *>(v + e) = t;
+            }
+        } else if constexpr (sizeof(V) == 4 && EPL == 2) {
+            float2 t = *reinterpret_cast<float2 *>(v);
+            t.x = (float)product<V, EXACT>((V)t.x, xr[0]);
+            t.y = (float)product<V, EXACT>((V)t.y, xr[1]);
+            *reinterpret_cast<float2 *>(v) = t;
+        } else if constexpr (sizeof(V) == 8 && EPL % 2 == 0) {
+#pragma unroll
+            for (int e = 0; e < EPL; e += 2) {
+                double2 t = *reinterpret_cast<double2 *>(v + e);
+                t.x = (double)product<V, EXACT>((V)t.x, xr[e]);
+                t.y = (double)product<V, EXACT>((V)t.y, xr[e + 1]);
+                *reinterpret_cast<double2 *>(v + e) = t;
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < EPL; ++e) v[e] = product<V, EXACT>(v[e], xr[e]);
+        }
     }
 
     // make offsets < need resident (warp-uniform); refills the ring
@@ -252,6 +299,11 @@ struct Ring {
     }
 
     __device__ __forceinline__ double at(int32_t o) const { return (double)S.val[o & RMASK]; }
+    __device__ __forceinline__ V raw(int32_t o) const { return S.val[o & RMASK]; }
+    // two products added in the value type (f32: one extra rounding), then widened
+    __device__ __forceinline__ double at2(int32_t o1, int32_t o2) const {
+        return (double)(S.val[o1 & RMASK] + S.val[o2 & RMASK]);
+    }
 };
 
 // Fast-mode walk of one group (or the piece [lo_r, hi_r) of it).  Phase j's
@@ -291,8 +343,12 @@ __device__ __forceinline__ double walk_fast(RingT &ring, const uint2 ph, const i
                 const int32_t need = q2 + stride < stop ? q2 + stride : stop;
                 if (need > ring.res32) ring.advance(need);
                 const int32_t P0 = q + lane, P1 = q2 + lane;
-                if (act && P0 < stop && (!PIECE || P0 >= lo_r)) v0 += ring.at(P0);
-                if (act && P1 < stop && (!PIECE || P1 >= lo_r)) v1 += ring.at(P1);
+                if (!PIECE && P1 < stop) {
+                    if (act) v0 += ring.at2(P0, P1);
+                } else {
+                    if (act && P0 < stop && (!PIECE || P0 >= lo_r)) v0 += ring.at(P0);
+                    if (act && P1 < stop && (!PIECE || P1 >= lo_r)) v1 += ring.at(P1);
+                }
             }
             double v = v0 + v1;
             if (SS > 1) {
@@ -315,7 +371,7 @@ __device__ __forceinline__ double walk_fast(RingT &ring, const uint2 ph, const i
                 int32_t lim = ring.res32 - ps;
                 lim = lim < plen ? lim : plen;
                 for (; pb + 2 * k <= lim; pb += 2 * k) {
-                    if (live) acc += ring.at(P0 + pb) + ring.at(P0 + pb + k);
+                    if (live) acc += ring.at2(P0 + pb, P0 + pb + k);
                 }
                 if (pb + k <= lim) {
                     if (live) acc += ring.at(P0 + pb);
@@ -385,6 +441,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
         S.nchunks = nchunks;
         S.ready = -1;
         S.pending = -1;
+        S.pol_stream = policy_evict_first();
+        S.pol_x = policy_evict_last();
         for (int i = 0; i < NB; ++i) mbar_init(&S.mbar[i], 1);
         fence_mbar_init();
         for (int c = 0; c <= NB - 3 && c < nchunks; ++c) ring.issue(c, nchunks, len32);
@@ -522,14 +580,33 @@ __global__ void __launch_bounds__(kThreads, MINB)
     }
 }
 
+// Shared memory per SM is kept to what MINB CTAs need: the rest of the
+// 256 KB unified L1/shared array stays L1, which stages the in-flight x
+// gathers (measured: more shared memory -> fewer gathers in flight -> slower).
+// HBP_CARVEOUT (percent of the maximum shared capacity) overrides.
+template <class K>
+void set_attributes(K kernel, size_t smem, int minb) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int pct = -1;
+    if (const char *e = getenv("HBP_CARVEOUT")) pct = atoi(e);
+    if (pct < 0) {
+        int dev = 0, max_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&max_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+        const size_t need = (smem + 1024) * (size_t)minb;  // + per-CTA reservation
+        pct = max_sm > 0 ? (int)((need * 100 + max_sm - 1) / max_sm) : 100;
+        if (pct > 100) pct = 100;
+    }
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+}
+
 template <typename V, bool EXACT, int CH, int NB, int MINB, bool XNA, int KT, int LMIN>
 int launch(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y,
            double *partial, cudaStream_t st) {
     const size_t smem = sizeof(WarpSmem<V, CH, NB>) * kWarps;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_spmv_stream<V, EXACT, CH, NB, MINB, XNA, KT, LMIN>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        set_attributes(k_spmv_stream<V, EXACT, CH, NB, MINB, XNA, KT, LMIN>, smem, MINB);
         attr = true;
     }
     unsigned grid = (unsigned)((b->workers + kWarps - 1) / kWarps);
@@ -541,8 +618,7 @@ int launch(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *
 template <typename V, bool EXACT, int CH, int NB, int MINB, bool XNA, int KT, int LMIN>
 int occupancy_of(int *per_sm) {
     const size_t smem = sizeof(WarpSmem<V, CH, NB>) * kWarps;
-    cudaFuncSetAttribute(k_spmv_stream<V, EXACT, CH, NB, MINB, XNA, KT, LMIN>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set_attributes(k_spmv_stream<V, EXACT, CH, NB, MINB, XNA, KT, LMIN>, smem, MINB);
     return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(
         per_sm, k_spmv_stream<V, EXACT, CH, NB, MINB, XNA, KT, LMIN>, kThreads, smem);
 }
@@ -562,9 +638,9 @@ int variant() {
 
 #define HBP_STREAM_VARIANTS(FN, V, EXACT, ...)                                \
     switch (variant()) {                                                       \
-        case 1: return FN<V, EXACT, 128, 4, 3, true, 33, 0>(__VA_ARGS__);     \
-        case 2: return FN<V, EXACT, 128, 4, 3, true, 0, 0>(__VA_ARGS__);      \
-        case 3: return FN<V, EXACT, 128, 4, 3, true, 4, 4>(__VA_ARGS__);      \
+        case 1: return FN<V, EXACT, 64, 4, 3, true, 12, 4>(__VA_ARGS__);      \
+        case 2: return FN<V, EXACT, 128, 4, 3, false, 12, 4>(__VA_ARGS__);    \
+        case 3: return FN<V, EXACT, 128, 4, 2, true, 12, 4>(__VA_ARGS__);     \
         case 4: return FN<V, EXACT, 128, 4, 3, true, 8, 8>(__VA_ARGS__);      \
         case 5: return FN<V, EXACT, 128, 4, 3, true, 16, 2>(__VA_ARGS__);     \
         case 6: return FN<V, EXACT, 128, 4, 3, true, 8, 2>(__VA_ARGS__);      \
