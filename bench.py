@@ -544,9 +544,9 @@ def run_gpu(args):
         "e2e": {"value": round(2.0 * total_nnz / (e2e_ms * 1e-3) / 1e9, 3), "unit": UNIT,
                 "h2d_bytes_per_step": cols * esz, "d2h_bytes_per_step": rows * esz,
                 "ms_per_step": round(e2e_ms, 4),
-                "how": ("HostPipeline: pinned x H2D, SpMV, y D2H per step"
+                "how": ("HostPipeline (copy-in / compute / copy-out streams): pinned x H2D, SpMV, y D2H per step"
                         + (" (one step at a time, L2 flushed)" if flush
-                           else " on 2 rotating streams"))},
+                           else ", double-buffered"))},
         "gpu_launches": K * launches_step,
         "clocks": clk,
         "preprocess_ms": {k: round(v, 3) for k, v in pre.items()},

@@ -234,38 +234,61 @@ class SpmvOperator:
 
 
 class HostPipeline:
-    """End-to-end y_i = A x_i for a sequence of HOST vectors (pinned memory):
-    the H2D copy of x_i, the SpMV and the D2H copy of y_i run on `depth`
-    CUDA streams in rotation, so the PCIe copies of one vector overlap the
-    SpMV of its neighbours.  Each stream owns its SpmvOperator (scratch is
-    never shared between concurrent launches)."""
+    """End-to-end y_i = A x_i for a sequence of HOST vectors (pinned memory).
+
+    Three streams: copy-in (H2D of x_i into device buffer i mod depth),
+    compute (the SpMV, one SpmvOperator) and copy-out (D2H of y_i), ordered
+    by events, so H2D(x_{i+1}), SpMV_i and D2H(y_{i-1}) run concurrently on
+    the two copy engines and the SMs.  A buffer is rewritten only after the
+    work that read it finished (SpMV_{i-depth} for x, D2H_{i-depth} for y)."""
 
     def __init__(self, hbp: HbpMatrix, depth: int = 2, **op_kwargs):
         dev = hbp.data.device
         self.hbp = hbp
-        self.depth = depth
-        self.streams = [torch.cuda.Stream(device=dev) for _ in range(depth)]
-        self.ops = [SpmvOperator(hbp, **op_kwargs) for _ in range(depth)]
-        self.xd = [torch.empty(hbp.cols, dtype=hbp.dtype, device=dev) for _ in range(depth)]
-        self.yd = [torch.empty(hbp.rows, dtype=hbp.dtype, device=dev) for _ in range(depth)]
+        self.depth = max(1, depth)
+        self.s_in = torch.cuda.Stream(device=dev)
+        self.s_comp = torch.cuda.Stream(device=dev)
+        self.s_out = torch.cuda.Stream(device=dev)
+        self.op = SpmvOperator(hbp, **op_kwargs)
+        self.xd = [torch.empty(hbp.cols, dtype=hbp.dtype, device=dev) for _ in range(self.depth)]
+        self.yd = [torch.empty(hbp.rows, dtype=hbp.dtype, device=dev) for _ in range(self.depth)]
 
     @property
     def launches_per_call(self) -> int:
-        return self.ops[0].launches_per_call
+        return self.op.launches_per_call
 
     def run(self, xs_host, ys_host) -> None:
         """Enqueue every (x_i -> y_i); ordered after the current stream's work.
         The caller synchronizes (or waits on the current stream)."""
         cur = torch.cuda.current_stream()
-        for s in self.streams:
+        D = self.depth
+        for s in (self.s_in, self.s_comp, self.s_out):
             s.wait_stream(cur)
+        x_free = [None] * D   # event: SpMV that last read xd[j] finished
+        y_free = [None] * D   # event: D2H that last read yd[j] finished
         for i, (xh, yh) in enumerate(zip(xs_host, ys_host)):
-            j = i % self.depth
-            with torch.cuda.stream(self.streams[j]):
+            j = i % D
+            if x_free[j] is not None:
+                self.s_in.wait_event(x_free[j])
+            with torch.cuda.stream(self.s_in):
                 self.xd[j].copy_(xh, non_blocking=True)
-                self.ops[j](self.xd[j], self.yd[j])
+            x_ready = torch.cuda.Event()
+            x_ready.record(self.s_in)
+            self.s_comp.wait_event(x_ready)
+            if y_free[j] is not None:
+                self.s_comp.wait_event(y_free[j])
+            with torch.cuda.stream(self.s_comp):
+                self.op(self.xd[j], self.yd[j])
+            done = torch.cuda.Event()
+            done.record(self.s_comp)
+            x_free[j] = done
+            self.s_out.wait_event(done)
+            with torch.cuda.stream(self.s_out):
                 yh.copy_(self.yd[j], non_blocking=True)
-        for s in self.streams:
+            out = torch.cuda.Event()
+            out.record(self.s_out)
+            y_free[j] = out
+        for s in (self.s_in, self.s_comp, self.s_out):
             cur.wait_stream(s)
 
 

@@ -1,0 +1,42 @@
+"""HostPipeline (end-to-end path with host buffers): every y_i equals the
+device-resident SpMV of x_i, for any pipeline depth and sequence length."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import has_gpu
+
+pytestmark = pytest.mark.gpu
+
+if has_gpu():
+    import torch
+    import paper_2504_08860_b200 as H
+
+
+@pytest.mark.parametrize("depth", [1, 2, 3])
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_pipeline_matches_device_spmv(depth, dtype):
+    rng = np.random.default_rng(depth)
+    rows, cols = 5000, 7000
+    lens = rng.poisson(9, rows)
+    lens[rng.choice(rows, 5, replace=False)] = 3000
+    r = np.repeat(np.arange(rows), lens)
+    c = np.concatenate([rng.choice(cols, k, replace=False) for k in lens])
+    v = rng.uniform(-1, 1, r.size)
+    if dtype == "f32":
+        v = v.astype(np.float32)
+    cfg = H.PartitionConfig(col_width=cols if dtype == "f32" else 1024)
+    csr = H.coo_to_csr(H.TripletMatrix(rows, cols, r, c, v))
+    grid = H.make_grid(csr, cfg)
+    hbp = H.build_hbp(csr, grid, H.hash_permutations(grid, H.sample_hash_params(grid, cfg)))
+    tdt = torch.float32 if dtype == "f32" else torch.float64
+    xs = [torch.as_tensor(rng.uniform(-1, 1, cols)).to(tdt).pin_memory() for _ in range(7)]
+    ys = [torch.empty(rows, dtype=tdt).pin_memory() for _ in range(7)]
+    pipe = H.HostPipeline(hbp, depth=depth)
+    pipe.run(xs, ys)
+    torch.cuda.synchronize()
+    op = H.SpmvOperator(hbp)
+    for xh, yh in zip(xs, ys):
+        want = op(xh.cuda()).cpu()
+        assert torch.equal(yh, want)
