@@ -436,6 +436,100 @@ __global__ void k_emit(const uint32_t *__restrict__ slot_len, const uint32_t *__
     }
 }
 
+// Element-balanced emission for W = 32.  k_emit gives a warp whole groups,
+// so the few groups holding hot rows serialise the tail (measured: 23 % of
+// warps active on R-MAT).  Here warp w owns the output range
+// [w E / N, (w+1) E / N), enters the group and phase containing its start,
+// and writes every phase it overlaps cooperatively: 32 consecutive output
+// positions per pass (coalesced stores); position off of a phase with k
+// live lanes is step t = off / k of rank r = off mod k, read from the rank's
+// source row (a shared-memory table built at phase entry).
+__constant__ uint32_t c_emit_magic[33] = {
+    0u,          0u,          2147483648u, 1431655766u, 1073741824u, 858993460u,  715827883u,
+    613566757u,  536870912u,  477218589u,  429496730u,  390451573u,  357913942u,  330382100u,
+    306783379u,  286331154u,  268435456u,  252645136u,  238609295u,  226050911u,  214748365u,
+    204522253u,  195225787u,  186737709u,  178956971u,  171798692u,  165191050u,  159072863u,
+    153391690u,  148102321u,  143165577u,  138547333u,  134217728u};
+
+__device__ __forceinline__ int64_t div_k(int64_t n, int k) {  // n >= 0, 1 <= k <= 32
+    if (k == 1) return n;
+    if (n < (1 << 26)) return (int64_t)(((uint64_t)n * c_emit_magic[k]) >> 32);
+    return n / k;
+}
+
+template <typename V>
+__global__ void __launch_bounds__(kThreads)
+    k_emit_sliced(const uint32_t *__restrict__ slot_len, const uint32_t *__restrict__ perm,
+                  const int64_t *__restrict__ start_local, const int64_t *__restrict__ gs,
+                  int64_t nzb, int64_t R, const int32_t *__restrict__ col_idx,
+                  const V *__restrict__ vals, uint32_t *__restrict__ col_out,
+                  V *__restrict__ data_out, int32_t *__restrict__ add_out) {
+    __shared__ int64_t tab_src[kThreads / 32][32];
+    __shared__ int32_t tab_nx[kThreads / 32][32];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const int64_t gpb = R / 32, ngroups = nzb * gpb;
+    const int64_t E = gs[ngroups];
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t lo = (int64_t)((__int128)w * E / nw), hi = (int64_t)((__int128)(w + 1) * E / nw);
+    if (lo >= hi) return;
+    // group containing lo: largest g with gs[g] <= lo
+    int64_t a = 0, b = ngroups;
+    while (b - a > 1) {
+        const int64_t m = (a + b) >> 1;
+        if (gs[m] <= lo) a = m;
+        else b = m;
+    }
+    for (int64_t g = a; g < ngroups; ++g) {
+        const int64_t g0 = gs[g], g1 = gs[g + 1];
+        if (g0 >= hi) break;
+        if (g1 <= lo) continue;
+        const int64_t blk = g / gpb;
+        const int64_t slot = blk * R + (g - blk * gpb) * 32 + lane;
+        const uint32_t len = slot_len[slot];
+        const int64_t src = len ? start_local[blk * R + perm[slot]] : 0;
+        int64_t pbase = g0;
+        uint32_t t0 = 0;
+        bool live = len > 0;
+        unsigned mask = __ballot_sync(0xffffffffu, live);
+        while (mask) {
+            const int k = __popc(mask);
+            const int rank = __popc(mask & lt);
+            const uint32_t t1 = __reduce_min_sync(0xffffffffu, live ? len : 0xffffffffu);
+            const bool live_n = len > t1;
+            const unsigned mask_n = __ballot_sync(0xffffffffu, live_n);
+            const int rank_n = __popc(mask_n & lt);
+            const int64_t M = (int64_t)(t1 - t0);
+            const int64_t pend = pbase + M * k;
+            if (pend > lo) {
+                __syncwarp();
+                if (live) {
+                    tab_src[wib][rank] = src + t0;
+                    tab_nx[wib][rank] = live_n ? (k + rank_n - rank) : -1;
+                }
+                __syncwarp();
+                const int64_t o0 = (lo > pbase ? lo : pbase) - pbase;
+                const int64_t o1 = (hi < pend ? hi : pend) - pbase;
+                for (int64_t off = o0 + lane; off < o1; off += 32) {
+                    const int64_t t = div_k(off, k);
+                    const int r = (int)(off - t * k);
+                    const int64_t j = tab_src[wib][r] + t;
+                    const int64_t p = pbase + off;
+                    col_out[p] = (uint32_t)__ldg(col_idx + j);
+                    data_out[p] = __ldg(vals + j);
+                    if (add_out) add_out[p] = (t + 1 < M) ? k : tab_nx[wib][r];
+                }
+                if (pend >= hi) return;
+            }
+            pbase = pend;
+            t0 = t1;
+            live = live_n;
+            mask = mask_n;
+        }
+    }
+}
+
 // ---- phase stream (runtime index for the streaming SpMV, W = 32) --------
 // A group's "phases" are its maximal step ranges with a fixed live-lane set
 // (one per distinct nonzero slot length).  Phase j is stored as
@@ -784,6 +878,24 @@ int hbp_emit(const uint32_t *slot_len, const uint32_t *perm, const int64_t *star
     int64_t spw = 32 / warp_size;
     unsigned grid = grid_for(((ngroups + spw - 1) / spw) * 32, kThreads);
     cudaStream_t s = as_stream(stream);
+    if (warp_size == 32) {  // element-balanced emission
+        int dev = 0, sms = 0;
+        HBP_CUDA_TRY(cudaGetDevice(&dev));
+        HBP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        const unsigned g2 = (unsigned)sms * 8;  // 64 warps per SM
+        if (dtype == HBP_F64)
+            k_emit_sliced<double><<<g2, kThreads, 0, s>>>(
+                slot_len, perm, start_local, group_start, nzb, row_height, col_idx,
+                (const double *)values, col, (double *)data, add_sign);
+        else if (dtype == HBP_F32)
+            k_emit_sliced<float><<<g2, kThreads, 0, s>>>(
+                slot_len, perm, start_local, group_start, nzb, row_height, col_idx,
+                (const float *)values, col, (float *)data, add_sign);
+        else
+            return HBP_E_ARG;
+        HBP_LAUNCH_CHECK();
+        return HBP_OK;
+    }
     if (dtype == HBP_F64)
         k_emit<double><<<grid, kThreads, 0, s>>>(slot_len, perm, start_local, group_start, blk_br,
                                                  nzb, rows, row_height, (int)warp_size, col_idx,
