@@ -276,6 +276,9 @@ def run_gpu(args):
     rows = stripe.rows if strong else rows_g
     nnz = int(rp[-1].item())
     cfg = H.PartitionConfig(col_width=C, row_height=R, warp_size=32, fixed_fraction=0.7)
+    hot_arg = {"auto": None, "off": False, "on": True}.get(args.hot)
+    if hot_arg is None and args.hot != "auto":
+        hot_arg = int(args.hot)
 
     # ---- preprocessing (timed like cli.py:150-158, GPU stages)
     csr = H.CsrMatrix(rows, cols, rp, col, val)
@@ -306,11 +309,14 @@ def run_gpu(args):
         hbp = H.build_hbp(csr, grid, perms, with_add_sign=False, with_zero_row=False)
         torch.cuda.synchronize()
         t4 = time.perf_counter()
+        # runtime operator: phase stream + hot-column staging (hbp_hot.cu)
+        op = H.SpmvOperator(hbp, schedule=args.schedule, hot=hot_arg)
+        torch.cuda.synchronize()
+        t5 = time.perf_counter()
         pre = dict(grid=(t1 - t0) * 1e3, sample=(t2 - t1) * 1e3, hash=(t3 - t2) * 1e3,
-                   build=(t4 - t3) * 1e3, total=(t4 - t0) * 1e3)
+                   build=(t4 - t3) * 1e3, operator=(t5 - t4) * 1e3, total=(t5 - t0) * 1e3)
         if rep == 0:
-            del hbp, perms, grid
-    op = H.SpmvOperator(hbp, schedule=args.schedule)
+            del op, hbp, perms, grid
     esz = 4 if vdt == torch.float32 else 8
     x_host = np.random.default_rng(0).uniform(-1.0, 1.0, cols)  # cli.py:170-171
     stream = torch.cuda.current_stream()
@@ -405,7 +411,7 @@ def run_gpu(args):
     # x_i H2D, SpMV, y_i D2H on 2 rotating streams; every step moves its own
     # x in and y out).  With an L2 flush, steps run one at a time instead.
     depth = 1 if flush else 2
-    pipe = H.HostPipeline(hbp, depth=depth, schedule=args.schedule)
+    pipe = H.HostPipeline(hbp, depth=depth, schedule=args.schedule, hot=hot_arg)
     xh = torch.as_tensor(x_host).to(vdt).pin_memory()
     yhs = [torch.empty(rows, dtype=vdt).pin_memory() for _ in range(depth)]
     nw = max(depth, args.warmup)
@@ -528,6 +534,8 @@ def run_gpu(args):
                    "nonzero_blocks": hbp.nzb, "col_width": C, "row_height": R,
                    "warp_size": 32, "fixed_fraction": 0.7, "workers": op.workers,
                    "schedule": op.schedule,
+                   "hot_columns": op.hot.n_hot if op.hot is not None else 0,
+                   "hot_share": round(op.hot.share, 4) if op.hot is not None else 0.0,
                    "hash_params": [params.a, params.b, params.c, params.d],
                    "step": ("power iteration: SpMV + ||y|| all-reduce + y all-gather"
                             if iterated else "SpMV (+ combine when ncb > 1)"),
@@ -539,8 +547,8 @@ def run_gpu(args):
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                      "algorithmic_bytes": b_alg, "peak_source": peak_src,
                      "kernel_ms": round(spmv_ms, 5),
-                     "kernel": f"k_spmv_{op.schedule}" + ("" if launches_step == 1
-                                                          else " (+ combine/zero launch)")},
+                     "kernel": f"k_spmv_{op.schedule}" + (" (+ hot-column gather)" if op.hot is not None else "")
+                     + ("" if launches_step == 1 + (op.hot is not None) else " (+ combine/zero launch)")},
         "e2e": {"value": round(2.0 * total_nnz / (e2e_ms * 1e-3) / 1e9, 3), "unit": UNIT,
                 "h2d_bytes_per_step": cols * esz, "d2h_bytes_per_step": rows * esz,
                 "ms_per_step": round(e2e_ms, 4),
@@ -608,6 +616,8 @@ def main():
     ap.add_argument("--no-baselines", action="store_true",
                     help="skip the CSR / 2D / cuSPARSE comparison timings")
     ap.add_argument("--schedule", default=None, choices=[None, "stream", "balanced", "plan"])
+    ap.add_argument("--hot", default="auto",
+                    help="hot-column x staging: auto (>= 10%% of nnz), on, off, or a column count")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     out = run_reference(args) if args.impl == "reference" else run_gpu(args)

@@ -244,8 +244,14 @@ typedef struct {
     const int64_t *rb_ptr;       /* [nrb+1] combine lists, ascending bc */
     const int32_t *rb_blk;       /* [nzb] */
     const int64_t *phase_ptr;    /* [nzb*gpb + 1] phase stream index (W = 32), nullable */
-    const void *phases;          /* uint2 (live mask, group offset) per phase, nullable */
+    const void *phases;          /* uint2 (live mask, group offset) per phase (+32 pad), nullable */
+    /* Hot-column staging (hbp_spmv_stream only; all nullable / 0 = off):
+     * scol[e] = HBP_HOT_FLAG | s when col[e] == hot_cols[s], else col[e]. */
+    const uint32_t *scol;        /* [nnz] (+16 pad) staged column stream */
+    const uint32_t *hot_cols;    /* [n_hot] global column of hot slot s */
+    int64_t n_hot;               /* multiple of 4, see hbp_hot_capacity */
 } hbp_format_t;
+#define HBP_HOT_FLAG 0x80000000u
 
 /* Phase stream (runtime index used by hbp_spmv_stream, W = 32): a group's
  * phases are its maximal step ranges with a fixed live-lane set; phase j is
@@ -287,6 +293,7 @@ typedef struct {
     double *part_tail;
     int64_t *cut_end;
     uint32_t *counters;
+    void *x_hot; /* [n_hot] scratch for hot-column staging (x at hot_cols) */
 } hbp_balanced_t;
 
 int hbp_balanced_workers(const hbp_format_t *f, int64_t *workers);
@@ -299,6 +306,26 @@ int hbp_balanced_workers(const hbp_format_t *f, int64_t *workers);
 int hbp_stream_workers(const hbp_format_t *f, int64_t *workers);
 int hbp_spmv_stream(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y,
                     double *partial, hbp_stream_t stream);
+/* Hot-column staging for power-law column degrees (R-MAT): the n_hot
+ * columns with the most nonzeros have their x entries copied into every
+ * SM's shared memory at the start of hbp_spmv_stream, so their gathers are
+ * shared-memory loads instead of L1->L2 sector requests (the bound of a
+ * random-gather SpMV).  Results are unchanged: the same x
+ * values are multiplied in the same order.  Not a reference interface; the
+ * reference reads x[col] directly (_kernels.py:41-46).
+ *   hbp_col_degree:  deg[c] += #{e : col[e] == c} (deg zero-filled).
+ *   hbp_hot_capacity: largest n_hot the stream kernel can stage for dtype.
+ *   hbp_hot_slots:   slot_of[hot_cols[s]] = s (slot_of filled with -1).
+ *   hbp_hot_remap:   scol[e] = slot_of[col[e]] >= 0 ? HBP_HOT_FLAG | slot : col[e].
+ *   hbp_hot_gather:  x_hot[s] = x[hot_cols[s]] (run inside hbp_spmv_stream). */
+int hbp_col_degree(const uint32_t *col, int64_t nnz, uint32_t *deg, hbp_stream_t stream);
+int hbp_hot_capacity(int dtype, int64_t *n_hot_max);
+int hbp_hot_slots(const uint32_t *hot_cols, int64_t n_hot, int32_t *slot_of,
+                  hbp_stream_t stream);
+int hbp_hot_remap(const uint32_t *col, int64_t nnz, const int32_t *slot_of, uint32_t *scol,
+                  hbp_stream_t stream);
+int hbp_hot_gather(const void *x, int dtype, const uint32_t *hot_cols, int64_t n_hot,
+                   void *x_hot, hbp_stream_t stream);
 int hbp_spmv_balanced(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y,
                       double *partial, hbp_stream_t stream);
 

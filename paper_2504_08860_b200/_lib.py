@@ -39,6 +39,7 @@ class FormatT(ctypes.Structure):
         ("blk_br", c_vp), ("blk_bc", c_vp), ("slot_len", c_vp), ("perm", c_vp),
         ("group_start", c_vp), ("col", c_vp), ("data", c_vp), ("rb_ptr", c_vp), ("rb_blk", c_vp),
         ("phase_ptr", c_vp), ("phases", c_vp),
+        ("scol", c_vp), ("hot_cols", c_vp), ("n_hot", c_i64),
     ]
 
 
@@ -53,7 +54,7 @@ class ScheduleT(ctypes.Structure):
 class BalancedT(ctypes.Structure):
     """Mirror of hbp_balanced_t."""
     _fields_ = [("workers", c_i64), ("part_head", c_vp), ("part_tail", c_vp),
-                ("cut_end", c_vp), ("counters", c_vp)]
+                ("cut_end", c_vp), ("counters", c_vp), ("x_hot", c_vp)]
 
 
 # name -> argtypes (all return int status)
@@ -106,6 +107,11 @@ _SIGS = {
     "hbp_stream_workers": [ctypes.POINTER(FormatT), ctypes.POINTER(c_i64)],
     "hbp_spmv_stream": [ctypes.POINTER(FormatT), ctypes.POINTER(BalancedT), c_vp, c_vp, c_vp,
                         c_vp],
+    "hbp_col_degree": [c_vp, c_i64, c_vp, c_vp],
+    "hbp_hot_capacity": [c_int, ctypes.POINTER(c_i64)],
+    "hbp_hot_slots": [c_vp, c_i64, c_vp, c_vp],
+    "hbp_hot_remap": [c_vp, c_i64, c_vp, c_vp, c_vp],
+    "hbp_hot_gather": [c_vp, c_int, c_vp, c_i64, c_vp, c_vp],
     "hbp_l2_persist": [c_vp, ctypes.c_size_t, ctypes.c_float, c_vp],
     "hbp_l2_persist_reset": [c_vp],
     "hbp_l2_info": [ctypes.POINTER(c_int), ctypes.POINTER(c_int), ctypes.POINTER(c_int)],

@@ -16,8 +16,8 @@ ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libhbp.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-         "--expt-relaxed-constexpr", "-Xptxas", "-v"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+         "--expt-relaxed-constexpr", "-Xptxas", "-v"]  # + -c / -shared per step
 
 
 def sources():
@@ -36,17 +36,34 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(p) <= t for p in deps())
 
 
+def _compile(src: str, obj: str) -> subprocess.CompletedProcess:
+    cmd = [NVCC, *ARCH, *FLAGS, "-c", "-I", os.path.join(ROOT, "include"), "-o", obj, src]
+    return subprocess.run(cmd, capture_output=True, text=True)
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    """One nvcc per translation unit (in parallel), then one shared link."""
     if not force and up_to_date():
         return LIB
-    cmd = [NVCC, *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp",
-           *sources()]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    from concurrent.futures import ThreadPoolExecutor
+
+    odir = os.path.join(PKG, "build")
+    os.makedirs(odir, exist_ok=True)
+    srcs = sources()
+    objs = [os.path.join(odir, os.path.basename(s)[:-3] + ".o") for s in srcs]
+    with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(_compile, srcs, objs))
+    for r in results:
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("nvcc failed building libhbp.so")
+        if verbose:
+            sys.stderr.write(r.stderr)
+    link = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", LIB + ".tmp", *objs]
+    res = subprocess.run(link, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libhbp.so")
-    if verbose:
-        sys.stderr.write(res.stderr)
+        raise RuntimeError("nvcc failed linking libhbp.so")
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -45,21 +45,26 @@ using namespace hbp;
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
 constexpr unsigned FULL = 0xffffffffu;
+// Hot-column staging (hbp_hot.cu): one 768-thread CTA per SM holds one copy
+// of x at the hot columns after the warps' rings; shared memory per SM is
+// capped at kHotBudget so L1 keeps room to stage the remaining x gathers.
+constexpr int kHotThreads = 768;
+constexpr size_t kHotBudgetDefault = 131 * 1024;  // -> 132 KB carveout (sweep: r01_hot_sweep)
 
 // Column slots: a chunk's columns are needed only until its gathers are
 // issued; while chunk ready+1 is started, chunks up to ready+NB-2 are in
 // flight, so NB-2 slots (rounded up to a power of two, >= 2) suffice.
-template <int NB>
+// With asynchronous gathers (GD > 0, f32) the slot keeps the chunk's columns
+// until they are replaced by the gathered x, so every chunk has its own slot.
+template <int NB, int GD>
 struct ColSlots {
-    static constexpr int value = NB <= 4 ? 2 : (NB <= 6 ? 4 : NB);
+    static constexpr int value = GD > 0 ? NB : (NB <= 4 ? 2 : (NB <= 6 ? 4 : NB));
 };
 
-template <typename V, int CH, int NB>
+template <typename V, int CH, int NB, int GD = 0>
 struct __align__(16) WarpSmem {
-    uint32_t col[ColSlots<NB>::value * CH];
+    uint32_t col[ColSlots<NB, GD>::value * CH];  // columns, then x (GD > 0)
     V val[NB * CH];  // values, then products in place
     uint32_t ph_mask[33];
     int32_t ph_off[33];
@@ -70,7 +75,7 @@ struct __align__(16) WarpSmem {
     int32_t len32;         // c_hi - base
     int32_t nchunks;
     int32_t ready;         // chunks <= ready hold products
-    int32_t pending;       // chunk whose x gathers are in flight (-1: none)
+    int32_t pending;       // chunk whose x gathers are in flight (-1: none; GD = 0)
     uint64_t pol_stream;   // L2 evict-first policy (element stream)
     uint64_t pol_x;        // L2 evict-last policy (x gathers)
 };
@@ -111,6 +116,21 @@ __device__ __forceinline__ void fence_proxy_async() {
 }
 __device__ __forceinline__ void fence_mbar_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// 4-byte asynchronous global -> shared copy (LDGSTS): the x gather lands in
+// shared memory without a destination register or scoreboard, so the walk
+// never waits on it implicitly; completion per thread via commit/wait_group.
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void *src, uint64_t pol) {
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;" ::"r"(dst),
+                 "l"(src), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -175,17 +195,46 @@ __device__ __forceinline__ V product(V v, V xv) {
 // are 32-bit offsets relative to `base` (slice start rounded down to 16 B).
 // Only res32 and the in-flight gathers live in registers; the rest of the
 // ring state sits in the warp's shared block and is read once per chunk.
-template <typename V, bool EXACT, int CH, int NB, bool XNA>
+// x gather of a staged column: HBP_HOT_FLAG | s reads the CTA's shared copy
+// of x at hot slot s, anything else x[c] from global memory (no L1 line).
+__device__ __forceinline__ float ld_x_staged(const float *x, uint32_t hot_base, uint32_t c,
+                                             uint64_t pol) {
+    float v;
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "setp.lt.s32 p, %3, 0;\n"
+        "@p ld.shared.f32 %0, [%4];\n"
+        "@!p ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;\n}"
+        : "=f"(v)
+        : "l"(x + c), "l"(pol), "r"(c), "r"(hot_base + ((c & 0x7fffffffu) << 2)));
+    return v;
+}
+__device__ __forceinline__ double ld_x_staged(const double *x, uint32_t hot_base, uint32_t c,
+                                              uint64_t pol) {
+    double v;
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "setp.lt.s32 p, %3, 0;\n"
+        "@p ld.shared.f64 %0, [%4];\n"
+        "@!p ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;\n}"
+        : "=d"(v)
+        : "l"(x + c), "l"(pol), "r"(c), "r"(hot_base + ((c & 0x7fffffffu) << 3)));
+    return v;
+}
+
+template <typename V, bool EXACT, int CH, int NB, bool XNA, bool HOT, int GD>
 struct Ring {
     static_assert((NB & (NB - 1)) == 0 && (CH & (CH - 1)) == 0, "NB, CH: powers of two");
+    static_assert(GD == 0 || (sizeof(V) == 4 && GD < NB - 2), "async gathers: f32, GD < NB-2");
     static constexpr int RMASK = NB * CH - 1;
     static constexpr int EPL = CH / 32;  // elements per lane per chunk
-    static constexpr int NCOL = ColSlots<NB>::value;
-    WarpSmem<V, CH, NB> &S;
+    static constexpr int NCOL = ColSlots<NB, GD>::value;
+    WarpSmem<V, CH, NB, GD> &S;
     const V *__restrict__ x;
+    uint32_t hot_base = 0;  // shared address of the staged x (HOT)
     int32_t res32 = 0;  // products resident for offsets < res32
     int lane;
-    V xr[EPL];          // gathered x of the pending chunk
+    V xr[GD > 0 ? 1 : EPL];  // gathered x of the pending chunk (GD = 0)
 
     // lane 0: bulk-copy chunk c (< nchunks) into its slot
     __device__ __forceinline__ void issue(int32_t c, int32_t nchunks, int32_t len32) {
@@ -228,12 +277,55 @@ struct Ring {
                 if (EPL * lane + e >= n) cc[e] = 0u;
         }
         const uint64_t pl = S.pol_x;
+        if constexpr (GD > 0) {  // x replaces the columns in the slot
+            const uint32_t dst = smem_addr(cs);
 #pragma unroll
-        for (int e = 0; e < EPL; ++e) xr[e] = XNA ? ld_x_na(x + cc[e], pl) : ld_x(x + cc[e], pl);
+            for (int e = 0; e < EPL; ++e) {
+                if (HOT && (int32_t)cc[e] < 0) {
+                    float hv;
+                    asm volatile("ld.shared.f32 %0, [%1];"
+                                 : "=f"(hv)
+                                 : "r"(hot_base + ((cc[e] & 0x7fffffffu) << 2)));
+                    reinterpret_cast<float *>(const_cast<uint32_t *>(cs))[e] = hv;
+                } else {
+                    cp_async4(dst + 4 * e, x + cc[e], pl);
+                }
+            }
+            cp_async_commit();
+        } else {
+#pragma unroll
+            for (int e = 0; e < EPL; ++e) {
+                if constexpr (HOT) xr[e] = ld_x_staged(x, hot_base, cc[e], pl);
+                else xr[e] = XNA ? ld_x_na(x + cc[e], pl) : ld_x(x + cc[e], pl);
+            }
+        }
     }
 
     // chunk c (pending): values -> products (in place)
     __device__ __forceinline__ void finish(int32_t c) {
+        if constexpr (GD > 0) {  // this lane's gathers of chunk c are the oldest group
+            cp_async_wait<GD - 1>();
+            float *v = reinterpret_cast<float *>(&S.val[(c & (NB - 1)) * CH + EPL * lane]);
+            const float *xs = reinterpret_cast<const float *>(&S.col[(c & (NB - 1)) * CH + EPL * lane]);
+            if constexpr (EPL % 4 == 0) {
+#pragma unroll
+                for (int e = 0; e < EPL; e += 4) {
+                    float4 t = *reinterpret_cast<float4 *>(v + e);
+                    const float4 u = *reinterpret_cast<const float4 *>(xs + e);
+                    t.x *= u.x, t.y *= u.y, t.z *= u.z, t.w *= u.w;
+                    *reinterpret_cast<float4 *>(v + e) = t;
+                }
+            } else if constexpr (EPL == 2) {
+                float2 t = *reinterpret_cast<float2 *>(v);
+                const float2 u = *reinterpret_cast<const float2 *>(xs);
+                t.x *= u.x, t.y *= u.y;
+                *reinterpret_cast<float2 *>(v) = t;
+            } else {
+#pragma unroll
+                for (int e = 0; e < EPL; ++e) v[e] *= xs[e];
+            }
+            return;
+        }
         V *v = &S.val[(c & (NB - 1)) * CH + EPL * lane];
         if constexpr (sizeof(V) == 4 && EPL % 4 == 0) {
 #pragma unroll
@@ -265,9 +357,39 @@ struct Ring {
     }
 
     // make offsets < need resident (warp-uniform); refills the ring
+    // GD > 0: chunks ready+1 .. ready+GD have gathers in flight (one commit
+    // group each; empty groups past the end keep the count uniform)
+    __device__ __forceinline__ void prime(int32_t nchunks, int32_t len32) {
+        if constexpr (GD > 0) {
+#pragma unroll
+            for (int c = 0; c < GD; ++c) {
+                if (c < nchunks) start(c, nchunks, len32);
+                else cp_async_commit();
+            }
+        }
+    }
+
     __device__ __forceinline__ void advance(int32_t need) {
         if (need <= res32) return;
         const int32_t nchunks = S.nchunks, len32 = S.len32;
+        if constexpr (GD > 0) {
+            int32_t ready = S.ready;
+            while (need > res32 && ready + 1 < nchunks) {
+                finish(ready + 1);  // own elements only: no cross-lane dependency
+                ++ready;
+                res32 = (ready * CH + CH < len32 ? ready * CH + CH : len32);
+                fence_proxy_async();  // ring accesses precede later bulk writes
+                __syncwarp();         // products visible; walk reads of old slots done
+                // the slot of chunk ready - 2 is free (the walk may still read
+                // ready - 1 for a step straddling the boundary)
+                if (lane == 0 && ready + NB - 2 < nchunks) issue(ready + NB - 2, nchunks, len32);
+                if (ready + GD < nchunks) start(ready + GD, nchunks, len32);
+                else cp_async_commit();
+            }
+            if (lane == 0) S.ready = ready;
+            __syncwarp();
+            return;
+        }
         int32_t ready = S.ready, pending = S.pending;
         while (need > res32) {
             if (pending < 0) {
@@ -398,14 +520,24 @@ __device__ __forceinline__ double walk_fast(RingT &ring, const uint2 ph, const i
     return acc;
 }
 
-template <typename V, bool EXACT, int CH, int NB, int MINB, bool XNA, int KT, int LMIN>
-__global__ void __launch_bounds__(kThreads, MINB)
+template <typename V, bool EXACT, int CH, int NB, int MINB, bool XNA, int KT, int LMIN, int NT,
+          bool HOT, int GD>
+__global__ void __launch_bounds__(NT, MINB)
     k_spmv_stream(const hbp_format_t f, const hbp_balanced_t b, const V *__restrict__ x,
                   V *__restrict__ y, double *__restrict__ partial) {
+    constexpr int kWarps = NT / 32;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
-    WarpSmem<V, CH, NB> &S = reinterpret_cast<WarpSmem<V, CH, NB> *>(smem_raw)[wib];
+    using Smem = WarpSmem<V, CH, NB, GD>;
+    Smem &S = reinterpret_cast<Smem *>(smem_raw)[wib];
+    V *const hot = reinterpret_cast<V *>(smem_raw + sizeof(Smem) * kWarps);
+    if constexpr (HOT) {  // stage x at the hot columns (b.x_hot, hbp_hot_gather)
+        const int32_t nv = (int32_t)(f.n_hot * (int64_t)sizeof(V) / 16);
+        const uint4 *src = (const uint4 *)b.x_hot;
+        for (int32_t i = threadIdx.x; i < nv; i += NT) reinterpret_cast<uint4 *>(hot)[i] = __ldcg(src + i);
+        __syncthreads();
+    }
     const int64_t w = (int64_t)blockIdx.x * kWarps + wib;
     const int64_t Nw = b.workers;
     if (w >= Nw) return;
@@ -429,13 +561,14 @@ __global__ void __launch_bounds__(kThreads, MINB)
         }
     }
     const int64_t base = c_lo & ~(int64_t)3;
-    Ring<V, EXACT, CH, NB, XNA> ring{S, x};
+    Ring<V, EXACT, CH, NB, XNA, HOT, GD> ring{S, x};
     ring.lane = lane;
+    if constexpr (HOT) ring.hot_base = smem_addr(hot);
     const int32_t len32 = (int32_t)(c_hi - base);
     const int32_t lo_s = (int32_t)(c_lo - base);  // slice start (0..3)
     if (lane == 0) {
         const int32_t nchunks = c_hi > c_lo ? (len32 + CH - 1) / CH : 0;
-        S.colg = f.col + base;
+        S.colg = (HOT ? f.scol : f.col) + base;
         S.valg = (const V *)f.data + base;
         S.len32 = len32;
         S.nchunks = nchunks;
@@ -448,6 +581,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         for (int c = 0; c <= NB - 3 && c < nchunks; ++c) ring.issue(c, nchunks, len32);
     }
     __syncwarp();
+    ring.prime(c_hi > c_lo ? (len32 + CH - 1) / CH : 0, len32);
 
     int64_t g = upper_group(gs, ngroups, c_lo);
     if (!(g < ngroups && gs[g] < c_lo)) g = lower_group(gs, ngroups, c_lo);
@@ -489,7 +623,9 @@ __global__ void __launch_bounds__(kThreads, MINB)
             perm_n = permp[(g + 1) * 32 + lane];
             pp0 = pp1;
             pp1 = pptr[g + 2];
-            ph_n = lane < pp1 - pp0 ? phs[pp0 + lane] : make_uint2(0u, 0u);
+            // address known now (no wait on pp1); lanes >= the phase count
+            // read the next group's phases (padded stream) and are ignored
+            ph_n = phs[pp0 + lane];
         }
         const int32_t lo = g0 > lo_s ? g0 : lo_s;
         const int32_t hi = g1 < len32 ? g1 : len32;
@@ -600,32 +736,43 @@ void set_attributes(K kernel, size_t smem, int minb) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
 }
 
-template <typename V, bool EXACT, int CH, int NB, int MINB, bool XNA, int KT, int LMIN>
+template <typename V, int CH, int NB, int NT, int GD>
+constexpr size_t ring_smem() {
+    return sizeof(WarpSmem<V, CH, NB, GD>) * (NT / 32);
+}
+
+template <typename V, bool EXACT, int CH, int NB, int MINB, bool XNA, int KT, int LMIN, int NT,
+          bool HOT, int GD>
 int launch(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y,
            double *partial, cudaStream_t st) {
-    const size_t smem = sizeof(WarpSmem<V, CH, NB>) * kWarps;
-    static bool attr = false;
-    if (!attr) {
-        set_attributes(k_spmv_stream<V, EXACT, CH, NB, MINB, XNA, KT, LMIN>, smem, MINB);
-        attr = true;
+    const size_t smem = ring_smem<V, CH, NB, NT, GD>() + (HOT ? (size_t)f->n_hot * sizeof(V) : 0);
+    static size_t attr = 0;
+    if (attr != smem) {
+        set_attributes(k_spmv_stream<V, EXACT, CH, NB, MINB, XNA, KT, LMIN, NT, HOT, GD>, smem, MINB);
+        attr = smem;
     }
-    unsigned grid = (unsigned)((b->workers + kWarps - 1) / kWarps);
-    k_spmv_stream<V, EXACT, CH, NB, MINB, XNA, KT, LMIN><<<grid, kThreads, smem, st>>>(
+    unsigned grid = (unsigned)((b->workers + NT / 32 - 1) / (NT / 32));
+    k_spmv_stream<V, EXACT, CH, NB, MINB, XNA, KT, LMIN, NT, HOT, GD><<<grid, NT, smem, st>>>(
         *f, *b, (const V *)x, (V *)y, partial);
     return (int)cudaGetLastError();
 }
 
-template <typename V, bool EXACT, int CH, int NB, int MINB, bool XNA, int KT, int LMIN>
-int occupancy_of(int *per_sm) {
-    const size_t smem = sizeof(WarpSmem<V, CH, NB>) * kWarps;
-    set_attributes(k_spmv_stream<V, EXACT, CH, NB, MINB, XNA, KT, LMIN>, smem, MINB);
+template <typename V, bool EXACT, int CH, int NB, int MINB, bool XNA, int KT, int LMIN, int NT,
+          bool HOT, int GD>
+int occupancy_of(const hbp_format_t *f, int *per_sm, int *warps_per_cta) {
+    const size_t smem = ring_smem<V, CH, NB, NT, GD>() + (HOT ? (size_t)f->n_hot * sizeof(V) : 0);
+    set_attributes(k_spmv_stream<V, EXACT, CH, NB, MINB, XNA, KT, LMIN, NT, HOT, GD>, smem, MINB);
+    *warps_per_cta = NT / 32;
     return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        per_sm, k_spmv_stream<V, EXACT, CH, NB, MINB, XNA, KT, LMIN>, kThreads, smem);
+        per_sm, k_spmv_stream<V, EXACT, CH, NB, MINB, XNA, KT, LMIN, NT, HOT, GD>, NT, smem);
 }
 
-// Tile / occupancy variants (chunk CH, ring slots NB, min CTAs per SM),
-// chosen with HBP_STREAM_VARIANT for sweeps; 0 is the default.
-constexpr int kVariants = 8;
+// Tile / occupancy variants (chunk CH, ring slots NB, min CTAs per SM,
+// threads per CTA), chosen with HBP_STREAM_VARIANT for sweeps; 0 is the
+// default.  Earlier sweeps (CH 64/128, L1 allocation of x, KT/LMIN of the
+// modular passes) are in the git history; 128/4/3x256 with L1::no_allocate x
+// gathers and KT=12, LMIN=4 won on cfg2 and H.
+constexpr int kVariants = 4;
 int variant() {
     static int v = -1;
     if (v < 0) {
@@ -636,27 +783,73 @@ int variant() {
     return v;
 }
 
-#define HBP_STREAM_VARIANTS(FN, V, EXACT, ...)                                \
-    switch (variant()) {                                                       \
-        case 1: return FN<V, EXACT, 64, 4, 3, true, 12, 4>(__VA_ARGS__);      \
-        case 2: return FN<V, EXACT, 128, 4, 3, false, 12, 4>(__VA_ARGS__);    \
-        case 3: return FN<V, EXACT, 128, 4, 2, true, 12, 4>(__VA_ARGS__);     \
-        case 4: return FN<V, EXACT, 128, 4, 3, true, 8, 8>(__VA_ARGS__);      \
-        case 5: return FN<V, EXACT, 128, 4, 3, true, 16, 2>(__VA_ARGS__);     \
-        case 6: return FN<V, EXACT, 128, 4, 3, true, 8, 2>(__VA_ARGS__);      \
-        case 7: return FN<V, EXACT, 128, 4, 3, true, 8, 16>(__VA_ARGS__);     \
-        default: return FN<V, EXACT, 128, 4, 3, true, 12, 4>(__VA_ARGS__);    \
+bool staged(const hbp_format_t *f) { return f->n_hot > 0 && f->scol && f->hot_cols; }
+
+// One variant = (chunk CH, ring slots NB, gather distance GD, threads NT,
+// CTAs per SM MINB).  f64 data always uses the register-gather ring
+// (CH 128, NB 4, GD 0).  Staged (hot-column) launches use one CTA per SM.
+#define HBP_VARIANT(FN, V, EXACT, HOT, CH, NB, GD, NT, MINB, ...)                          \
+    return FN<V, EXACT, (sizeof(V) == 4 ? CH : 128), (sizeof(V) == 4 ? NB : 4), MINB, true, \
+              12, 4, NT, HOT, (sizeof(V) == 4 ? GD : 0)>(__VA_ARGS__)
+
+#define HBP_VARIANTS(FN, V, EXACT, HOT, NTD, MINBD, ...)                                     \
+    switch (variant()) {                                                                    \
+        case 1: HBP_VARIANT(FN, V, EXACT, HOT, 128, 4, 1, NTD, MINBD, __VA_ARGS__);            \
+        case 2: HBP_VARIANT(FN, V, EXACT, HOT, 256, 4, 0, NTD, MINBD, __VA_ARGS__);            \
+        case 3: HBP_VARIANT(FN, V, EXACT, HOT, 256, 4, 0, 512, 1, __VA_ARGS__);                \
+        default: HBP_VARIANT(FN, V, EXACT, HOT, 128, 4, 0, NTD, MINBD, __VA_ARGS__);           \
     }
 
+#define HBP_STREAM_DISPATCH(FN, V, EXACT, ...)                            \
+    if (staged(f)) { HBP_VARIANTS(FN, V, EXACT, true, kHotThreads, 1, __VA_ARGS__) } \
+    HBP_VARIANTS(FN, V, EXACT, false, 256, 3, __VA_ARGS__)
+
+template <typename V, int CH, int NB, int MINB, int NT, int GD>
+int ring_bytes(size_t *out) {
+    *out = ring_smem<V, (sizeof(V) == 4 ? CH : 128), (sizeof(V) == 4 ? NB : 4), NT,
+                     (sizeof(V) == 4 ? GD : 0)>();
+    return 0;
+}
+#define HBP_RING_BYTES(V, CH, NB, GD, NT) ring_bytes<V, CH, NB, 1, NT, GD>(out)
+template <typename V>
+int hot_ring_bytes(size_t *out) {  // shared memory of the staged launch's rings
+    switch (variant()) {
+        case 1: return HBP_RING_BYTES(V, 128, 4, 1, kHotThreads);
+        case 2: return HBP_RING_BYTES(V, 256, 4, 0, kHotThreads);
+        case 3: return HBP_RING_BYTES(V, 256, 4, 0, 512);
+        default: return HBP_RING_BYTES(V, 128, 4, 0, kHotThreads);
+    }
+}
+
 template <typename V, bool EXACT>
-int occupancy(int *per_sm) {
-    HBP_STREAM_VARIANTS(occupancy_of, V, EXACT, per_sm)
+int occupancy(const hbp_format_t *f, int *per_sm, int *warps_per_cta) {
+    HBP_STREAM_DISPATCH(occupancy_of, V, EXACT, f, per_sm, warps_per_cta)
+}
+
+template <typename V>
+__global__ void k_hot_gather(const V *__restrict__ x, const uint32_t *__restrict__ hot_cols,
+                             int64_t n_hot, V *__restrict__ x_hot) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s < n_hot) x_hot[s] = __ldg(x + hot_cols[s]);
+}
+
+template <typename V>
+int hot_gather(const void *x, const uint32_t *hot_cols, int64_t n_hot, void *x_hot,
+               cudaStream_t st) {
+    if (n_hot == 0) return HBP_OK;
+    k_hot_gather<V><<<(unsigned)((n_hot + 255) / 256), 256, 0, st>>>(
+        (const V *)x, hot_cols, n_hot, (V *)x_hot);
+    return (int)cudaGetLastError();
 }
 
 template <typename V, bool EXACT>
 int run(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y, double *partial,
         cudaStream_t st) {
-    HBP_STREAM_VARIANTS(launch, V, EXACT, f, b, x, y, partial, st)
+    if (staged(f)) {
+        const int rc = hot_gather<V>(x, f->hot_cols, f->n_hot, b->x_hot, st);
+        if (rc) return rc;
+    }
+    HBP_STREAM_DISPATCH(launch, V, EXACT, f, b, x, y, partial, st)
 }
 
 }  // namespace
@@ -665,21 +858,50 @@ extern "C" {
 
 int hbp_stream_workers(const hbp_format_t *f, int64_t *workers) {
     if (!f) return HBP_E_ARG;
-    int dev = 0, sms = 0, per_sm = 0;
+    int dev = 0, sms = 0, per_sm = 0, wpc = 0;
     HBP_CUDA_TRY(cudaGetDevice(&dev));
     HBP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const bool exact = f->exact != 0 || f->dtype == HBP_F64;
     int rc;
     if (f->dtype == HBP_F64)
-        rc = exact ? occupancy<double, true>(&per_sm) : occupancy<double, false>(&per_sm);
+        rc = exact ? occupancy<double, true>(f, &per_sm, &wpc)
+                   : occupancy<double, false>(f, &per_sm, &wpc);
     else
-        rc = exact ? occupancy<float, true>(&per_sm) : occupancy<float, false>(&per_sm);
+        rc = exact ? occupancy<float, true>(f, &per_sm, &wpc)
+                   : occupancy<float, false>(f, &per_sm, &wpc);
     if (rc) return rc;
-    int64_t wmax = (int64_t)sms * per_sm * kWarps;
+    if (per_sm < 1) return HBP_E_UNSUPPORTED;  // e.g. n_hot beyond hbp_hot_capacity
+    int64_t wmax = (int64_t)sms * per_sm * wpc;
     int64_t wcap = f->nnz / 1024;
     if (wcap < 1) wcap = 1;
     *workers = wmax < wcap ? wmax : wcap;
     return HBP_OK;
+}
+
+int hbp_hot_capacity(int dtype, int64_t *n_hot_max) {
+    if (!n_hot_max || (dtype != HBP_F32 && dtype != HBP_F64)) return HBP_E_ARG;
+    // f32: 131 KB -> 132 KB carveout (sweep); f64 rings are
+    // twice as large, so its staged launch takes the 164 KB carveout
+    size_t budget = dtype == HBP_F64 ? 163 * 1024 : kHotBudgetDefault;
+    if (const char *e = getenv("HBP_HOT_BUDGET_KB")) budget = (size_t)atoi(e) * 1024;
+    int dev = 0, optin = 0;
+    HBP_CUDA_TRY(cudaGetDevice(&dev));
+    HBP_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    if (budget > (size_t)optin) budget = (size_t)optin;
+    size_t ring = 0;
+    if (dtype == HBP_F64) hot_ring_bytes<double>(&ring);
+    else hot_ring_bytes<float>(&ring);
+    const size_t sv = dtype == HBP_F64 ? 8 : 4;
+    *n_hot_max = budget > ring ? (int64_t)(((budget - ring) / sv) & ~(size_t)1023) : 0;
+    return HBP_OK;
+}
+
+int hbp_hot_gather(const void *x, int dtype, const uint32_t *hot_cols, int64_t n_hot,
+                   void *x_hot, hbp_stream_t stream) {
+    if (n_hot < 0 || (n_hot > 0 && (!x || !hot_cols || !x_hot))) return HBP_E_ARG;
+    if (dtype == HBP_F64) return hot_gather<double>(x, hot_cols, n_hot, x_hot, as_stream(stream));
+    if (dtype == HBP_F32) return hot_gather<float>(x, hot_cols, n_hot, x_hot, as_stream(stream));
+    return HBP_E_ARG;
 }
 
 int hbp_spmv_stream(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y,
@@ -693,6 +915,12 @@ int hbp_spmv_stream(const hbp_format_t *f, const hbp_balanced_t *b, const void *
     if ((f->nnz + b->workers - 1) / b->workers > (int64_t)1 << 30) return HBP_E_UNSUPPORTED;
     const bool exact = f->exact != 0 || f->dtype == HBP_F64;
     if (!exact && (!b->part_head || !b->part_tail || !b->counters)) return HBP_E_ARG;
+    if (staged(f)) {
+        int64_t cap = 0;
+        const int rc = hbp_hot_capacity(f->dtype, &cap);
+        if (rc) return rc;
+        if (f->n_hot > cap || (f->n_hot & 3) || !b->x_hot) return HBP_E_ARG;
+    }
     cudaStream_t st = as_stream(stream);
     if (f->dtype == HBP_F64)
         return exact ? run<double, true>(f, b, x, y, partial, st)

@@ -133,7 +133,7 @@ const char *hbp_status_string(int status) {
     }
 }
 
-int hbp_abi_version(void) { return 1; }
+int hbp_abi_version(void) { return 2; }
 
 int hbp_device_sm_count(int *sms) {
     int dev = 0;

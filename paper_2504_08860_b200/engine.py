@@ -148,8 +148,11 @@ class SpmvOperator:
     direct mode (one column block): the kernel writes y itself; otherwise the
     partial (f64, compact) is combined in ascending bc."""
 
+    HOT_MIN_SHARE = 0.10  # stage hot columns when they hold >= 10 % of the nonzeros
+
     def __init__(self, hbp: HbpMatrix, workers: int | None = None,
-                 fixed_fraction: float | None = None, schedule: str | None = None):
+                 fixed_fraction: float | None = None, schedule: str | None = None,
+                 hot: bool | int | None = None):
         self.hbp = hbp
         dev = hbp.data.device
         if schedule is None:
@@ -159,7 +162,14 @@ class SpmvOperator:
         self.schedule = schedule
         if schedule == "stream":
             hbp.ensure_phases()
-        f = hbp.format_struct()
+        # private descriptor: hot-column staging is a property of this operator
+        f = self._fmt = L.FormatT.from_buffer_copy(hbp.format_struct())
+        self.hot = None
+        if schedule == "stream" and hot is not False and hbp.nnz and hbp.cols:
+            hc = hbp.hot_columns(None if hot in (None, True) else int(hot))
+            if hc.n_hot and (hot is not None or hc.share >= self.HOT_MIN_SHARE):
+                self.hot = hc
+                hc.apply(f)
         if schedule in ("balanced", "stream"):
             if workers is None:
                 w = L.c_i64(0)
@@ -178,6 +188,10 @@ class SpmvOperator:
                 self._scratch = [ph, pt, ce, cn]
                 self.bal.part_head, self.bal.part_tail = ph.data_ptr(), pt.data_ptr()
                 self.bal.cut_end, self.bal.counters = ce.data_ptr(), cn.data_ptr()
+            if self.hot is not None:
+                xh = torch.empty(self.hot.n_hot, dtype=hbp.dtype, device=dev)
+                self._scratch.append(xh)
+                self.bal.x_hot = xh.data_ptr()
         else:
             self.workers = workers or default_workers(hbp.dtype, hbp.config.warp_size)
         fr = hbp.config.fixed_fraction if fixed_fraction is None else fixed_fraction
@@ -192,7 +206,8 @@ class SpmvOperator:
         self.sched.workers = self.workers
         self.sched.fixed_count = self.fixed_count
         self.sched.ticket = self.ticket.data_ptr()
-        self.launches_per_call = 1 + (0 if self.direct and not self.has_empty_row_blocks else 1)
+        self.launches_per_call = (1 + (0 if self.direct and not self.has_empty_row_blocks else 1)
+                                  + (1 if self.hot is not None else 0))
         self._graph = None
         self._gx = self._gy = None
 
@@ -208,7 +223,7 @@ class SpmvOperator:
         hbp = self.hbp
         if y is None:
             y = torch.empty(hbp.rows, dtype=hbp.dtype, device=hbp.data.device)
-        f = hbp.format_struct()
+        f = self._fmt
         s = L.stream()
         if self.direct:
             self._blocks(f, x, None, y, s)

@@ -18,6 +18,7 @@ derives addresses from slot lengths instead of chasing it.
 """
 from __future__ import annotations
 
+import ctypes
 import io
 import struct
 
@@ -43,6 +44,18 @@ def _padded(t: torch.Tensor, pad: int = 16) -> torch.Tensor:
     out = torch.zeros(t.numel() + pad, dtype=t.dtype, device=t.device)
     out[:t.numel()] = t
     return out[:t.numel()]
+
+
+class HotColumns:
+    """x staging of the heaviest columns (hbp_spmv_stream): hot_cols[s] is
+    the column of hot slot s, scol the element stream with hot columns as
+    HBP_HOT_FLAG | s, share the fraction of nonzeros in hot columns."""
+
+    def __init__(self, n_hot: int, hot_cols: torch.Tensor, scol: torch.Tensor, share: float):
+        self.n_hot, self.hot_cols, self.scol, self.share = n_hot, hot_cols, scol, share
+
+    def apply(self, f: "L.FormatT") -> None:
+        f.scol, f.hot_cols, f.n_hot = self.scol.data_ptr(), self.hot_cols.data_ptr(), self.n_hot
 
 
 class HbpFormatError(ValueError):
@@ -86,13 +99,45 @@ class HbpMatrix:
         L.call("hbp_phase_counts", L.P(self.slot_len), L.c_i64(ng), L.P(nph), L.stream())
         ptr = L.exclusive_sum(nph)
         total = int(ptr[-1].item())
-        phases = torch.zeros(max(1, total) * 2, dtype=torch.int32, device=dev)
+        # + 32 entries: the stream kernel reads a whole warp's worth of phases
+        # per group without waiting for the group's phase count
+        phases = torch.zeros((total + 32) * 2, dtype=torch.int32, device=dev)
         L.call("hbp_phase_emit", L.P(self.slot_len), L.c_i64(ng), L.P(ptr), L.P(phases),
                L.stream())
         self.phase_ptr, self.phases = ptr, phases
         if self._fmt is not None:
             self._fmt.phase_ptr = ptr.data_ptr()
             self._fmt.phases = phases.data_ptr()
+
+    def hot_columns(self, n_hot: int | None = None) -> "HotColumns":
+        """Hot-column staging metadata for hbp_spmv_stream (include/hbp.h
+        hbp_col_degree .. hbp_hot_remap): the n_hot columns with the most
+        nonzeros (ties: lower column first), capped by the kernel's
+        shared-memory capacity, and the staged column stream.  Cached."""
+        cap = L.c_i64(0)
+        L.call("hbp_hot_capacity", L.c_int(L.dtype_code(self.data.dtype)), ctypes.byref(cap))
+        n = int(cap.value) if n_hot is None else min(int(n_hot), int(cap.value))
+        n = max(0, min(n, self.cols)) & ~3
+        key = ("hot", n)
+        if key in self._ops:
+            return self._ops[key]
+        dev = self.data.device
+        col = self.col
+        deg = torch.zeros(self.cols, dtype=torch.int32, device=dev)
+        L.call("hbp_col_degree", L.P(col), L.c_i64(self.nnz), L.P(deg), L.stream())
+        # descending degree, stable (ascending column among equal degrees)
+        keys = (torch.iinfo(torch.int32).max - deg).contiguous()
+        vals = torch.arange(self.cols, dtype=torch.int32, device=dev)
+        _, order = L.sort_pairs_u32(keys, vals, 32)
+        hot_cols = order[:n].contiguous()
+        share = float(deg[hot_cols.long()].sum().item()) / max(1, self.nnz)
+        slot_of = torch.full((self.cols,), -1, dtype=torch.int32, device=dev)
+        L.call("hbp_hot_slots", L.P(hot_cols), L.c_i64(n), L.P(slot_of), L.stream())
+        scol = _padded(torch.empty(self.nnz, dtype=col.dtype, device=dev))
+        L.call("hbp_hot_remap", L.P(col), L.c_i64(self.nnz), L.P(slot_of), L.P(scol), L.stream())
+        hc = HotColumns(n, hot_cols, scol, share)
+        self._ops[key] = hc
+        return hc
 
     # ---- reference attributes
     @property

@@ -45,7 +45,7 @@ def test_ctypes_binding_covers_header(libpath):
     for name in _declared():
         assert hasattr(lib, name), name
     assert set(_declared()) <= set(L.EXPORTED)
-    assert lib.hbp_abi_version() == 1
+    assert lib.hbp_abi_version() == 2
     assert lib.hbp_status_string(1002).decode().startswith("permutation")
 
 

@@ -1,0 +1,150 @@
+"""Hot-column staging of x in shared memory (hbp_hot.cu, hbp_spmv_stream HOT).
+
+Staging changes where the x value of a hot column is read from (the SM's
+shared copy instead of global memory), never which value or in which order
+it is summed, so a staged SpMV must be BITWISE equal to the unstaged one
+(f32 fast mode and f64 exact mode) -- and hence to the oracle wherever the
+unstaged path is.  The metadata (degrees, hot order, staged stream) is
+checked against numpy.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import pytest
+
+from conftest import has_gpu
+
+pytestmark = pytest.mark.gpu
+
+if has_gpu():
+    import torch
+    import paper_2504_08860_b200 as H
+    from paper_2504_08860_b200 import _lib as L
+    from oracle import oracle as O
+
+FLAG = 0x80000000
+
+
+def _powerlaw(seed=0, rows=20000, cols=30000, per_row=12):
+    """Zipf-like column popularity (a few columns carry most nonzeros) and
+    skewed row lengths."""
+    rng = np.random.default_rng(seed)
+    lens = np.minimum(rng.zipf(1.7, rows) + per_row // 2, cols // 4)
+    r = np.repeat(np.arange(rows), lens)
+    w = 1.0 / np.arange(1, cols + 1) ** 1.1
+    relabel = rng.permutation(cols)
+    c = relabel[rng.choice(cols, r.size, p=w / w.sum())]
+    key = np.unique(r.astype(np.int64) * cols + c)
+    r, c = key // cols, key % cols
+    v = rng.uniform(-1, 1, r.size)
+    return rows, cols, r, c, v
+
+
+def _hbp(rows, cols, r, c, v, C=None, R=512):
+    cfg = H.PartitionConfig(col_width=C or cols, row_height=R, warp_size=32)
+    csr = H.coo_to_csr(H.TripletMatrix(rows, cols, r, c, v))
+    grid = H.make_grid(csr, cfg)
+    return H.build_hbp(csr, grid, H.hash_permutations(grid, H.sample_hash_params(grid, cfg)))
+
+
+@pytest.fixture(scope="module")
+def mat():
+    return _powerlaw()
+
+
+def test_hot_metadata(mat):
+    rows, cols, r, c, v = mat
+    hbp = _hbp(rows, cols, r, c, v)
+    hc = hbp.hot_columns(1000)
+    assert hc.n_hot == 1000
+    deg = np.bincount(c, minlength=cols)
+    order = np.argsort(-deg, kind="stable")  # descending degree, ties by column
+    np.testing.assert_array_equal(hc.hot_cols.cpu().numpy(), order[:1000])
+    assert hc.share == pytest.approx(deg[order[:1000]].sum() / c.size, rel=1e-12)
+    col = hbp.col.cpu().numpy().view(np.uint32).astype(np.int64)
+    slot = np.full(cols, -1, np.int64)
+    slot[order[:1000]] = np.arange(1000)
+    want = np.where(slot[col] >= 0, FLAG | slot[col], col).astype(np.uint32)
+    np.testing.assert_array_equal(hc.scol.cpu().numpy().view(np.uint32), want)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("n_hot", [4, 64, 1000, None])
+@pytest.mark.parametrize("workers", [1, 37, 500, None])
+def test_staged_bitwise_equals_unstaged(mat, dtype, n_hot, workers):
+    rows, cols, r, c, v = mat
+    vv = v.astype(np.float32) if dtype == "f32" else v
+    hbp = _hbp(rows, cols, r, c, vv)
+    x = np.random.default_rng(5).uniform(-1, 1, cols)
+    xd = torch.as_tensor(x.astype(vv.dtype), device="cuda")
+    plain = H.SpmvOperator(hbp, workers=workers, hot=False)
+    staged = H.SpmvOperator(hbp, workers=workers, hot=True if n_hot is None else n_hot)
+    assert plain.hot is None and staged.hot is not None
+    y0 = plain(xd).cpu().numpy()
+    y1 = staged(xd).cpu().numpy()
+    y2 = staged(xd).cpu().numpy()
+    np.testing.assert_array_equal(y1, y0)
+    np.testing.assert_array_equal(y2, y1)
+    if dtype == "f64":  # exact mode: the reference's bits
+        p = O.pipeline(rows, cols, r, c, v, cols, 512, 32)
+        np.testing.assert_array_equal(y1, O.hbp_spmv(p["hbp"], x, workers=2))
+    else:
+        err = O.componentwise_error(rows, r, c, vv.astype(np.float64),
+                                    x.astype(np.float32).astype(np.float64),
+                                    y1.astype(np.float64))
+        assert err <= 1e-5
+
+
+def test_auto_staging_policy(mat):
+    rows, cols, r, c, v = mat
+    hbp = _hbp(rows, cols, r, c, v.astype(np.float32))
+    op = H.SpmvOperator(hbp)
+    assert op.hot is not None and op.hot.share >= H.SpmvOperator.HOT_MIN_SHARE
+    assert op.launches_per_call == 2  # hot gather + stream kernel
+    # uniform columns over many more columns than the capacity: not staged
+    rng = np.random.default_rng(2)
+    n = 2_000_000
+    rr = np.repeat(np.arange(n), 2)
+    cc = rng.integers(0, n, rr.size)
+    key = np.unique(rr * n + cc)
+    hb2 = _hbp(n, n, key // n, key % n, rng.uniform(-1, 1, key.size).astype(np.float32))
+    assert H.SpmvOperator(hb2).hot is None
+
+
+def test_staged_multi_col_block(mat):
+    """Staging with a partial + combine (C < cols) stays bitwise."""
+    rows, cols, r, c, v = mat
+    hbp = _hbp(rows, cols, r, c, v, C=4096)
+    x = torch.as_tensor(np.random.default_rng(9).uniform(-1, 1, cols), device="cuda")
+    y0 = H.SpmvOperator(hbp, hot=False)(x).cpu().numpy()
+    y1 = H.SpmvOperator(hbp, hot=True)(x).cpu().numpy()
+    np.testing.assert_array_equal(y1, y0)
+
+
+def test_hot_gather_and_capacity():
+    cap = L.c_i64(0)
+    L.call("hbp_hot_capacity", L.c_int(L.HBP_F32), ctypes.byref(cap))
+    cap32 = int(cap.value)
+    L.call("hbp_hot_capacity", L.c_int(L.HBP_F64), ctypes.byref(cap))
+    assert cap32 >= 4096 and int(cap.value) >= 4096 and cap32 % 1024 == 0
+    x = torch.randn(100000, device="cuda", dtype=torch.float64)
+    hot = torch.randint(0, 100000, (4096,), device="cuda", dtype=torch.int32)
+    out = torch.empty(4096, device="cuda", dtype=torch.float64)
+    L.call("hbp_hot_gather", L.P(x), L.c_int(L.HBP_F64), L.P(hot), L.c_i64(4096), L.P(out),
+           L.stream())
+    assert torch.equal(out, x[hot.long()])
+
+
+def test_n_hot_beyond_capacity_rejected(mat):
+    rows, cols, r, c, v = mat
+    hbp = _hbp(rows, cols, r, c, v.astype(np.float32))
+    op = H.SpmvOperator(hbp, hot=True)
+    f = L.FormatT.from_buffer_copy(op._fmt)
+    f.n_hot = 1 << 20
+    x = torch.zeros(cols, device="cuda", dtype=torch.float32)
+    y = torch.empty(rows, device="cuda", dtype=torch.float32)
+    with pytest.raises(ValueError):
+        L.call("hbp_spmv_stream", ctypes.byref(f), ctypes.byref(op.bal), L.P(x), L.P(y),
+               L.P(None), L.stream())

@@ -20,6 +20,7 @@ ap.add_argument("--schedule", default=None)
 ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--workers", type=int, default=None)
 ap.add_argument("--persist", action="store_true")
+ap.add_argument("--hot", default="auto", help="auto | on | off | column count")
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 desc, rows, cols, rp, col, val, C, vdt = bench.make_matrix_gpu(a.config, 0, dev)
@@ -28,7 +29,9 @@ csr = H.CsrMatrix(rows, cols, rp, col, val)
 grid = H.make_grid(csr, cfg)
 hbp = H.build_hbp(csr, grid, H.hash_permutations(grid, H.sample_hash_params(grid, cfg)),
                   with_add_sign=False, with_zero_row=False)
-op = H.SpmvOperator(hbp, workers=a.workers, schedule=a.schedule)
+hot = {"auto": None, "on": True, "off": False}.get(a.hot, None if a.hot == "auto" else a.hot)
+op = H.SpmvOperator(hbp, workers=a.workers, schedule=a.schedule,
+                    hot=int(hot) if isinstance(hot, str) else hot)
 x = torch.as_tensor(np.random.default_rng(0).uniform(-1, 1, cols), device=dev).to(vdt)
 y = torch.empty(rows, dtype=vdt, device=dev)
 if a.persist:
@@ -45,4 +48,4 @@ e.record()
 torch.cuda.synchronize()
 ms = s.elapsed_time(e) / a.iters
 print(f"{a.config} schedule={op.schedule} workers={op.workers} nnz={csr.nnz} "
-      f"ms={ms:.4f} GFLOP/s={2 * csr.nnz / ms / 1e6:.1f}")
+      f"hot={op.hot.n_hot if op.hot else 0} ms={ms:.4f} GFLOP/s={2 * csr.nnz / ms / 1e6:.1f}")
