@@ -248,10 +248,14 @@ typedef struct {
     /* Hot-column staging (hbp_spmv_stream only; all nullable / 0 = off):
      * scol[e] = HBP_HOT_FLAG | s when col[e] == hot_cols[s], else col[e]. */
     const uint32_t *scol;        /* [nnz] (+16 pad) staged column stream */
-    const uint32_t *hot_cols;    /* [n_hot] global column of hot slot s */
+    const uint32_t *hot_cols;    /* [n_hot + n_warm] column of hot slot s, then of warm slot w */
     int64_t n_hot;               /* multiple of 4, see hbp_hot_capacity */
+    int64_t n_warm;              /* warm tier: scol = HBP_WARM_FLAG | w (cols < 2^30) */
+    int32_t cold_last;           /* 1: cold columns gathered L2 evict-last too (x fits L2) */
+    int32_t reserved;
 } hbp_format_t;
 #define HBP_HOT_FLAG 0x80000000u
+#define HBP_WARM_FLAG 0x40000000u
 
 /* Phase stream (runtime index used by hbp_spmv_stream, W = 32): a group's
  * phases are its maximal step ranges with a fixed live-lane set; phase j is
@@ -293,7 +297,7 @@ typedef struct {
     double *part_tail;
     int64_t *cut_end;
     uint32_t *counters;
-    void *x_hot; /* [n_hot] scratch for hot-column staging (x at hot_cols) */
+    void *x_hot; /* [n_hot + n_warm] scratch: x at hot_cols (hot, then warm tier) */
 } hbp_balanced_t;
 
 int hbp_balanced_workers(const hbp_format_t *f, int64_t *workers);
@@ -313,17 +317,24 @@ int hbp_spmv_stream(const hbp_format_t *f, const hbp_balanced_t *b, const void *
  * random-gather SpMV).  Results are unchanged: the same x
  * values are multiplied in the same order.  Not a reference interface; the
  * reference reads x[col] directly (_kernels.py:41-46).
- *   hbp_col_degree:  deg[c] += #{e : col[e] == c} (deg zero-filled).
+ *   hbp_col_degree:  deg[c] += #{e = i * stride : col[e] == c} (deg zero-filled;
+ *                    stride 1 = exact degrees, larger = a deterministic sample).
  *   hbp_hot_capacity: largest n_hot the stream kernel can stage for dtype.
  *   hbp_hot_slots:   slot_of[hot_cols[s]] = s (slot_of filled with -1).
- *   hbp_hot_remap:   scol[e] = slot_of[col[e]] >= 0 ? HBP_HOT_FLAG | slot : col[e].
- *   hbp_hot_gather:  x_hot[s] = x[hot_cols[s]] (run inside hbp_spmv_stream). */
-int hbp_col_degree(const uint32_t *col, int64_t nnz, uint32_t *deg, hbp_stream_t stream);
+ *   hbp_hot_remap:   scol[e] = slot s = slot_of[col[e]]: s < n_hot -> HBP_HOT_FLAG | s,
+ *                    n_hot <= s -> HBP_WARM_FLAG | (s - n_hot), none -> col[e].
+ *   hbp_hot_gather:  x_hot[s] = x[hot_cols[s]] (run inside hbp_spmv_stream).
+ * The warm tier (next-heaviest columns after the hot ones) is a compact copy
+ * of x that the kernel gathers with an L2 evict-last policy while the other
+ * ("cold") columns are gathered evict-first: on matrices whose x exceeds L2
+ * (cfg5: 256 MB) the heavy columns stay L2-resident in a dense array. */
+int hbp_col_degree(const uint32_t *col, int64_t nnz, int64_t stride, uint32_t *deg,
+                   hbp_stream_t stream);
 int hbp_hot_capacity(int dtype, int64_t *n_hot_max);
 int hbp_hot_slots(const uint32_t *hot_cols, int64_t n_hot, int32_t *slot_of,
                   hbp_stream_t stream);
-int hbp_hot_remap(const uint32_t *col, int64_t nnz, const int32_t *slot_of, uint32_t *scol,
-                  hbp_stream_t stream);
+int hbp_hot_remap(const uint32_t *col, int64_t nnz, const int32_t *slot_of, int64_t n_hot,
+                  uint32_t *scol, hbp_stream_t stream);
 int hbp_hot_gather(const void *x, int dtype, const uint32_t *hot_cols, int64_t n_hot,
                    void *x_hot, hbp_stream_t stream);
 int hbp_spmv_balanced(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y,

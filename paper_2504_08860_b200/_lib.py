@@ -39,7 +39,8 @@ class FormatT(ctypes.Structure):
         ("blk_br", c_vp), ("blk_bc", c_vp), ("slot_len", c_vp), ("perm", c_vp),
         ("group_start", c_vp), ("col", c_vp), ("data", c_vp), ("rb_ptr", c_vp), ("rb_blk", c_vp),
         ("phase_ptr", c_vp), ("phases", c_vp),
-        ("scol", c_vp), ("hot_cols", c_vp), ("n_hot", c_i64),
+        ("scol", c_vp), ("hot_cols", c_vp), ("n_hot", c_i64), ("n_warm", c_i64),
+        ("cold_last", ctypes.c_int32), ("reserved", ctypes.c_int32),
     ]
 
 
@@ -107,10 +108,10 @@ _SIGS = {
     "hbp_stream_workers": [ctypes.POINTER(FormatT), ctypes.POINTER(c_i64)],
     "hbp_spmv_stream": [ctypes.POINTER(FormatT), ctypes.POINTER(BalancedT), c_vp, c_vp, c_vp,
                         c_vp],
-    "hbp_col_degree": [c_vp, c_i64, c_vp, c_vp],
+    "hbp_col_degree": [c_vp, c_i64, c_i64, c_vp, c_vp],
     "hbp_hot_capacity": [c_int, ctypes.POINTER(c_i64)],
     "hbp_hot_slots": [c_vp, c_i64, c_vp, c_vp],
-    "hbp_hot_remap": [c_vp, c_i64, c_vp, c_vp, c_vp],
+    "hbp_hot_remap": [c_vp, c_i64, c_vp, c_i64, c_vp, c_vp],
     "hbp_hot_gather": [c_vp, c_int, c_vp, c_i64, c_vp, c_vp],
     "hbp_l2_persist": [c_vp, ctypes.c_size_t, ctypes.c_float, c_vp],
     "hbp_l2_persist_reset": [c_vp],
@@ -242,3 +243,10 @@ def default_workers(dtype: torch.dtype, warp_size: int) -> int:
     v = c_i64(0)
     call("hbp_spmv_default_workers", c_int(dtype_code(dtype)), c_i64(warp_size), ctypes.byref(v))
     return int(v.value)
+
+
+def l2_bytes() -> int:
+    """Device L2 capacity (hbp_l2_info)."""
+    l2, mp, mw = c_int(0), c_int(0), c_int(0)
+    call("hbp_l2_info", ctypes.byref(l2), ctypes.byref(mp), ctypes.byref(mw))
+    return int(l2.value)

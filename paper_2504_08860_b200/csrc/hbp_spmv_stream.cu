@@ -77,7 +77,8 @@ struct __align__(16) WarpSmem {
     int32_t ready;         // chunks <= ready hold products
     int32_t pending;       // chunk whose x gathers are in flight (-1: none; GD = 0)
     uint64_t pol_stream;   // L2 evict-first policy (element stream)
-    uint64_t pol_x;        // L2 evict-last policy (x gathers)
+    uint64_t pol_x;        // L2 evict-last policy (x gathers; warm tier when staged)
+    uint64_t pol_cold;     // L2 evict-normal policy (cold columns when staged)
 };
 
 // ---- PTX helpers: mbarrier + bulk async copy (sm_90+ / sm_100a) ------------
@@ -222,7 +223,72 @@ __device__ __forceinline__ double ld_x_staged(const double *x, uint32_t hot_base
     return v;
 }
 
-template <typename V, bool EXACT, int CH, int NB, bool XNA, bool HOT, int GD>
+// XM = 2: the same gathers without an L2 cache-policy operand (no policy
+// register to materialise per load)
+__device__ __forceinline__ float ld_x_nh(const float *p) {
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double ld_x_nh(const double *p) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float ld_x_staged_nh(const float *x, uint32_t hot_base, uint32_t c) {
+    float v;
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "setp.lt.s32 p, %2, 0;\n"
+        "@p ld.shared.f32 %0, [%3];\n"
+        "@!p ld.global.nc.L1::no_allocate.f32 %0, [%1];\n}"
+        : "=f"(v)
+        : "l"(x + c), "r"(c), "r"(hot_base + ((c & 0x7fffffffu) << 2)));
+    return v;
+}
+__device__ __forceinline__ double ld_x_staged_nh(const double *x, uint32_t hot_base, uint32_t c) {
+    double v;
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "setp.lt.s32 p, %2, 0;\n"
+        "@p ld.shared.f64 %0, [%3];\n"
+        "@!p ld.global.nc.L1::no_allocate.f64 %0, [%1];\n}"
+        : "=d"(v)
+        : "l"(x + c), "r"(c), "r"(hot_base + ((c & 0x7fffffffu) << 3)));
+    return v;
+}
+
+// Staged gather (hot + warm tiers, hbp_hot.cu): HBP_HOT_FLAG | s reads the
+// CTA's shared copy, HBP_WARM_FLAG | w the compact warm copy xw[w] (L2
+// evict-last), anything else x[c] (L2 evict-normal); global loads skip L1.
+template <typename V>
+__device__ __forceinline__ V ld_x_tiered(const V *x, const V *xw, uint32_t hot_base, uint32_t c,
+                                         uint64_t pol_warm, uint64_t pol_cold) {
+    const bool warm = (c & HBP_WARM_FLAG) != 0;
+    const V *g = warm ? xw + (c & 0x3fffffffu) : x + c;
+    const uint64_t pol = warm ? pol_warm : pol_cold;
+    const uint32_t hs = hot_base + ((c & 0x7fffffffu) * (uint32_t)sizeof(V));
+    V v;
+    if constexpr (sizeof(V) == 4)
+        asm volatile(
+            "{\n.reg .pred p;\n"
+            "setp.lt.s32 p, %3, 0;\n"
+            "@p ld.shared.f32 %0, [%4];\n"
+            "@!p ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;\n}"
+            : "=f"(v)
+            : "l"(g), "l"(pol), "r"(c), "r"(hs));
+    else
+        asm volatile(
+            "{\n.reg .pred p;\n"
+            "setp.lt.s32 p, %3, 0;\n"
+            "@p ld.shared.f64 %0, [%4];\n"
+            "@!p ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;\n}"
+            : "=d"(v)
+            : "l"(g), "l"(pol), "r"(c), "r"(hs));
+    return v;
+}
+
+template <typename V, bool EXACT, int CH, int NB, int XM, bool HOT, int GD>
 struct Ring {
     static_assert((NB & (NB - 1)) == 0 && (CH & (CH - 1)) == 0, "NB, CH: powers of two");
     static_assert(GD == 0 || (sizeof(V) == 4 && GD < NB - 2), "async gathers: f32, GD < NB-2");
@@ -232,6 +298,7 @@ struct Ring {
     WarpSmem<V, CH, NB, GD> &S;
     const V *__restrict__ x;
     uint32_t hot_base = 0;  // shared address of the staged x (HOT)
+    const V *xw = nullptr;  // warm tier (HOT)
     int32_t res32 = 0;  // products resident for offsets < res32
     int lane;
     V xr[GD > 0 ? 1 : EPL];  // gathered x of the pending chunk (GD = 0)
@@ -295,8 +362,19 @@ struct Ring {
         } else {
 #pragma unroll
             for (int e = 0; e < EPL; ++e) {
-                if constexpr (HOT) xr[e] = ld_x_staged(x, hot_base, cc[e], pl);
-                else xr[e] = XNA ? ld_x_na(x + cc[e], pl) : ld_x(x + cc[e], pl);
+                constexpr int XG = XM & 3;
+                if constexpr ((XM & 8) != 0) {  // diagnostic: no global gathers (wrong y)
+                    V hv;
+                    const uint32_t a = hot_base + ((cc[e] & 4095u) * (uint32_t)sizeof(V));
+                    if constexpr (sizeof(V) == 4) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(hv) : "r"(a));
+                    else asm volatile("ld.shared.f64 %0, [%1];" : "=d"(hv) : "r"(a));
+                    xr[e] = hv;
+                } else if constexpr (HOT && (XM & 32) != 0) {  // + warm tier
+                    xr[e] = ld_x_tiered(x, xw, hot_base, cc[e], pl, S.pol_cold);
+                } else if constexpr (HOT) xr[e] = XG == 2 ? ld_x_staged_nh(x, hot_base, cc[e])
+                                                   : ld_x_staged(x, hot_base, cc[e], pl);
+                else if constexpr (XG == 2) xr[e] = ld_x_nh(x + cc[e]);
+                else xr[e] = XG ? ld_x_na(x + cc[e], pl) : ld_x(x + cc[e], pl);
             }
         }
     }
@@ -436,11 +514,12 @@ struct Ring {
 //     a deterministic shuffle tree folds the S sums of a rank and the row's
 //     owner lane takes its rank's total;
 //   - otherwise step by step: each live lane adds its element of the step.
-template <bool PIECE, int KT, int LMIN, class RingT>
+template <bool PIECE, int KT, int LMIN, bool SHORT, class RingT>
 __device__ __forceinline__ double walk_fast(RingT &ring, const uint2 ph, const int np,
                                             const int32_t gb, const int32_t gend,
                                             const int32_t lo_r, const int32_t hi_r,
                                             const int lane) {
+    const unsigned lt = lanemask_lt();
     double acc = 0.0;
     int j = 0;
     if (PIECE)  // phase containing lo
@@ -452,7 +531,17 @@ __device__ __forceinline__ double walk_fast(RingT &ring, const uint2 ph, const i
         const int32_t pe = gb + (j + 1 < np ? pe_o : gend);
         const int k = __popc(pm);
         const int32_t stop = PIECE ? (pe < hi_r ? pe : hi_r) : pe;
-        if (k < KT && pe - ps > LMIN * k) {
+        if (SHORT && !PIECE && pe - ps <= 2 * k) {
+            // one- or two-step phase (most phases on skewed rows, few
+            // elements): each live lane adds its one or two elements; same
+            // arithmetic as the step loop below (pair added in f32)
+            if (pe > ring.res32) ring.advance(pe);
+            if ((pm >> lane) & 1u) {
+                const int32_t P = ps + __popc(pm & lt);
+                if (pe - ps > k) acc += ring.at2(P, P + k);
+                else acc += ring.at(P);
+            }
+        } else if (k < KT && pe - ps > LMIN * k) {
             const uint32_t mk = c_magic16[k];
             const int SS = (int)((32u * mk) >> 16);  // floor(32 / k)
             const int32_t stride = SS * k;
@@ -480,13 +569,13 @@ __device__ __forceinline__ double walk_fast(RingT &ring, const uint2 ph, const i
                     if ((s & (2 * d - 1)) == 0 && s + d < SS) v += o;
                 }
             }
-            const double tot = __shfl_sync(FULL, v, __popc(pm & lanemask_lt()));
+            const double tot = __shfl_sync(FULL, v, __popc(pm & lt));
             if ((pm >> lane) & 1u) acc += tot;
         } else if (!PIECE) {
             // whole phase, steps end exactly at pe: bound checks merged with
             // the residency limit, two steps per iteration
             const bool live = (pm >> lane) & 1u;
-            const int32_t P0 = ps + __popc(pm & lanemask_lt());
+            const int32_t P0 = ps + __popc(pm & lt);
             int32_t pb = 0;  // element offset of the step within the phase
             const int32_t plen = pe - ps;
             for (;;) {
@@ -504,7 +593,7 @@ __device__ __forceinline__ double walk_fast(RingT &ring, const uint2 ph, const i
             }
         } else {
             const bool live = (pm >> lane) & 1u;
-            const int32_t rank = __popc(pm & lanemask_lt());
+            const int32_t rank = __popc(pm & lt);
             int32_t pb = ps;
             if (lo_r > ps) pb = ps + div_small(lo_r - ps, k) * k;
             for (; pb < stop; pb += k) {
@@ -520,12 +609,21 @@ __device__ __forceinline__ double walk_fast(RingT &ring, const uint2 ph, const i
     return acc;
 }
 
-template <typename V, bool EXACT, int CH, int NB, int MINB, bool XNA, int KT, int LMIN, int NT,
+template <typename V, bool EXACT, int CH, int NB, int MINB, int XM, int KT, int LMIN, int NT,
           bool HOT, int GD>
 __global__ void __launch_bounds__(NT, MINB)
     k_spmv_stream(const hbp_format_t f, const hbp_balanced_t b, const V *__restrict__ x,
                   V *__restrict__ y, double *__restrict__ partial) {
     constexpr int kWarps = NT / 32;
+    // XM & 4: group metadata and y are touched once -> L2 evict-first, so
+    // they do not displace x (evict-last) from L2
+    constexpr bool MS = (XM & 4) != 0;
+    constexpr bool SHORT = (XM & 16) != 0;  // fast path for 1-2 step phases
+    auto ldm = [](const auto *p) { return MS ? __ldcs(p) : *p; };
+    auto stm = [](auto *p, auto v) {
+        if constexpr (MS) __stcs(p, v);
+        else *p = v;
+    };
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
@@ -561,9 +659,12 @@ __global__ void __launch_bounds__(NT, MINB)
         }
     }
     const int64_t base = c_lo & ~(int64_t)3;
-    Ring<V, EXACT, CH, NB, XNA, HOT, GD> ring{S, x};
+    Ring<V, EXACT, CH, NB, XM, HOT, GD> ring{S, x};
     ring.lane = lane;
-    if constexpr (HOT) ring.hot_base = smem_addr(hot);
+    if constexpr (HOT) {
+        ring.hot_base = smem_addr(hot);
+        ring.xw = (const V *)b.x_hot + f.n_hot;
+    }
     const int32_t len32 = (int32_t)(c_hi - base);
     const int32_t lo_s = (int32_t)(c_lo - base);  // slice start (0..3)
     if (lane == 0) {
@@ -576,6 +677,7 @@ __global__ void __launch_bounds__(NT, MINB)
         S.pending = -1;
         S.pol_stream = policy_evict_first();
         S.pol_x = policy_evict_last();
+        S.pol_cold = f.cold_last ? policy_evict_last() : policy_evict_normal();
         for (int i = 0; i < NB; ++i) mbar_init(&S.mbar[i], 1);
         fence_mbar_init();
         for (int c = 0; c <= NB - 3 && c < nchunks; ++c) ring.issue(c, nchunks, len32);
@@ -619,13 +721,13 @@ __global__ void __launch_bounds__(NT, MINB)
         const uint2 ph = ph_n;
         if (g + 1 < ngroups) {  // prefetch the next group's metadata
             gr0 = g1;
-            gr1 = (int32_t)(gs[g + 2] - base);
-            perm_n = permp[(g + 1) * 32 + lane];
+            gr1 = (int32_t)(ldm(gs + g + 2) - base);
+            perm_n = ldm(permp + (g + 1) * 32 + lane);
             pp0 = pp1;
-            pp1 = pptr[g + 2];
+            pp1 = ldm(pptr + g + 2);
             // address known now (no wait on pp1); lanes >= the phase count
             // read the next group's phases (padded stream) and are ignored
-            ph_n = phs[pp0 + lane];
+            ph_n = ldm(phs + pp0 + lane);
         }
         const int32_t lo = g0 > lo_s ? g0 : lo_s;
         const int32_t hi = g1 < len32 ? g1 : len32;
@@ -633,8 +735,8 @@ __global__ void __launch_bounds__(NT, MINB)
 
         double acc = 0.0;
         if (!EXACT && lo < hi) {
-            acc = piece ? walk_fast<true, KT, LMIN>(ring, ph, np, g0, g1 - g0, lo, hi, lane)
-                        : walk_fast<false, KT, LMIN>(ring, ph, np, g0, g1 - g0, lo, hi, lane);
+            acc = piece ? walk_fast<true, KT, LMIN, SHORT>(ring, ph, np, g0, g1 - g0, lo, hi, lane)
+                        : walk_fast<false, KT, LMIN, SHORT>(ring, ph, np, g0, g1 - g0, lo, hi, lane);
         } else if (lo < hi) {
             __syncwarp();  // previous group's table reads are done
             if (lane < np) {
@@ -681,7 +783,7 @@ __global__ void __launch_bounds__(NT, MINB)
         if (!piece) {
             if (valid) {
                 if (pb_now) pb_now[row_local] = acc;
-                else yb_now[row_local] = (V)acc;
+                else stm(yb_now + row_local, (V)acc);
             }
             continue;
         }
@@ -710,7 +812,7 @@ __global__ void __launch_bounds__(NT, MINB)
         }
         if (valid) {
             if (pb_now) pb_now[row_local] = s;
-            else yb_now[row_local] = (V)s;
+            else stm(yb_now + row_local, (V)s);
         }
         if (lane == 0) b.counters[g] = 0u;
     }
@@ -741,30 +843,30 @@ constexpr size_t ring_smem() {
     return sizeof(WarpSmem<V, CH, NB, GD>) * (NT / 32);
 }
 
-template <typename V, bool EXACT, int CH, int NB, int MINB, bool XNA, int KT, int LMIN, int NT,
+template <typename V, bool EXACT, int CH, int NB, int MINB, int XM, int KT, int LMIN, int NT,
           bool HOT, int GD>
 int launch(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y,
            double *partial, cudaStream_t st) {
     const size_t smem = ring_smem<V, CH, NB, NT, GD>() + (HOT ? (size_t)f->n_hot * sizeof(V) : 0);
     static size_t attr = 0;
     if (attr != smem) {
-        set_attributes(k_spmv_stream<V, EXACT, CH, NB, MINB, XNA, KT, LMIN, NT, HOT, GD>, smem, MINB);
+        set_attributes(k_spmv_stream<V, EXACT, CH, NB, MINB, XM, KT, LMIN, NT, HOT, GD>, smem, MINB);
         attr = smem;
     }
     unsigned grid = (unsigned)((b->workers + NT / 32 - 1) / (NT / 32));
-    k_spmv_stream<V, EXACT, CH, NB, MINB, XNA, KT, LMIN, NT, HOT, GD><<<grid, NT, smem, st>>>(
+    k_spmv_stream<V, EXACT, CH, NB, MINB, XM, KT, LMIN, NT, HOT, GD><<<grid, NT, smem, st>>>(
         *f, *b, (const V *)x, (V *)y, partial);
     return (int)cudaGetLastError();
 }
 
-template <typename V, bool EXACT, int CH, int NB, int MINB, bool XNA, int KT, int LMIN, int NT,
+template <typename V, bool EXACT, int CH, int NB, int MINB, int XM, int KT, int LMIN, int NT,
           bool HOT, int GD>
 int occupancy_of(const hbp_format_t *f, int *per_sm, int *warps_per_cta) {
     const size_t smem = ring_smem<V, CH, NB, NT, GD>() + (HOT ? (size_t)f->n_hot * sizeof(V) : 0);
-    set_attributes(k_spmv_stream<V, EXACT, CH, NB, MINB, XNA, KT, LMIN, NT, HOT, GD>, smem, MINB);
+    set_attributes(k_spmv_stream<V, EXACT, CH, NB, MINB, XM, KT, LMIN, NT, HOT, GD>, smem, MINB);
     *warps_per_cta = NT / 32;
     return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        per_sm, k_spmv_stream<V, EXACT, CH, NB, MINB, XNA, KT, LMIN, NT, HOT, GD>, NT, smem);
+        per_sm, k_spmv_stream<V, EXACT, CH, NB, MINB, XM, KT, LMIN, NT, HOT, GD>, NT, smem);
 }
 
 // Tile / occupancy variants (chunk CH, ring slots NB, min CTAs per SM,
@@ -789,19 +891,28 @@ bool staged(const hbp_format_t *f) { return f->n_hot > 0 && f->scol && f->hot_co
 // CTAs per SM MINB).  f64 data always uses the register-gather ring
 // (CH 128, NB 4, GD 0).  Staged (hot-column) launches use one CTA per SM.
 #define HBP_VARIANT(FN, V, EXACT, HOT, CH, NB, GD, NT, MINB, ...)                          \
-    return FN<V, EXACT, (sizeof(V) == 4 ? CH : 128), (sizeof(V) == 4 ? NB : 4), MINB, true, \
+    HBP_VARIANT_X(FN, V, EXACT, HOT, CH, NB, GD, NT, MINB, 21, __VA_ARGS__)
+#define HBP_VARIANT_X(FN, V, EXACT, HOT, CH, NB, GD, NT, MINB, XM, ...)                     \
+    return FN<V, EXACT, (sizeof(V) == 4 ? CH : 128), (sizeof(V) == 4 ? NB : 4), MINB, XM,   \
               12, 4, NT, HOT, (sizeof(V) == 4 ? GD : 0)>(__VA_ARGS__)
 
 #define HBP_VARIANTS(FN, V, EXACT, HOT, NTD, MINBD, ...)                                     \
     switch (variant()) {                                                                    \
-        case 1: HBP_VARIANT(FN, V, EXACT, HOT, 128, 4, 1, NTD, MINBD, __VA_ARGS__);            \
-        case 2: HBP_VARIANT(FN, V, EXACT, HOT, 256, 4, 0, NTD, MINBD, __VA_ARGS__);            \
-        case 3: HBP_VARIANT(FN, V, EXACT, HOT, 256, 4, 0, 512, 1, __VA_ARGS__);                \
+        case 1: HBP_VARIANT_X(FN, V, EXACT, HOT, 128, 4, 0, NTD, MINBD, 29, __VA_ARGS__);      \
+        case 2: HBP_VARIANT(FN, V, EXACT, HOT, 128, 4, 0, (HOT ? 1024 : 256), (HOT ? 1 : 4), __VA_ARGS__); \
+        case 3: HBP_VARIANT_X(FN, V, EXACT, HOT, 128, 4, 0, NTD, MINBD, 5, __VA_ARGS__);       \
         default: HBP_VARIANT(FN, V, EXACT, HOT, 128, 4, 0, NTD, MINBD, __VA_ARGS__);           \
     }
 
-#define HBP_STREAM_DISPATCH(FN, V, EXACT, ...)                            \
-    if (staged(f)) { HBP_VARIANTS(FN, V, EXACT, true, kHotThreads, 1, __VA_ARGS__) } \
+// a warm tier (XM | 32) costs an address/policy select per gather, so it has
+// its own instantiation
+#define HBP_STREAM_DISPATCH(FN, V, EXACT, ...)                                              \
+    if (staged(f)) {                                                                        \
+        if (f->n_warm > 0) {                                                                \
+            HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, 0, kHotThreads, 1, 53, __VA_ARGS__);    \
+        }                                                                                   \
+        HBP_VARIANTS(FN, V, EXACT, true, kHotThreads, 1, __VA_ARGS__)                       \
+    }                                                                                       \
     HBP_VARIANTS(FN, V, EXACT, false, 256, 3, __VA_ARGS__)
 
 template <typename V, int CH, int NB, int MINB, int NT, int GD>
@@ -814,9 +925,9 @@ int ring_bytes(size_t *out) {
 template <typename V>
 int hot_ring_bytes(size_t *out) {  // shared memory of the staged launch's rings
     switch (variant()) {
-        case 1: return HBP_RING_BYTES(V, 128, 4, 1, kHotThreads);
-        case 2: return HBP_RING_BYTES(V, 256, 4, 0, kHotThreads);
-        case 3: return HBP_RING_BYTES(V, 256, 4, 0, 512);
+        case 1: return HBP_RING_BYTES(V, 128, 4, 0, kHotThreads);
+        case 2: return HBP_RING_BYTES(V, 128, 4, 0, 1024);
+        case 3: return HBP_RING_BYTES(V, 128, 4, 0, kHotThreads);
         default: return HBP_RING_BYTES(V, 128, 4, 0, kHotThreads);
     }
 }
@@ -846,7 +957,7 @@ template <typename V, bool EXACT>
 int run(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y, double *partial,
         cudaStream_t st) {
     if (staged(f)) {
-        const int rc = hot_gather<V>(x, f->hot_cols, f->n_hot, b->x_hot, st);
+        const int rc = hot_gather<V>(x, f->hot_cols, f->n_hot + f->n_warm, b->x_hot, st);
         if (rc) return rc;
     }
     HBP_STREAM_DISPATCH(launch, V, EXACT, f, b, x, y, partial, st)
@@ -920,6 +1031,7 @@ int hbp_spmv_stream(const hbp_format_t *f, const hbp_balanced_t *b, const void *
         const int rc = hbp_hot_capacity(f->dtype, &cap);
         if (rc) return rc;
         if (f->n_hot > cap || (f->n_hot & 3) || !b->x_hot) return HBP_E_ARG;
+        if (f->n_warm < 0 || (f->n_warm > 0 && f->cols > (int64_t)1 << 30)) return HBP_E_ARG;
     }
     cudaStream_t st = as_stream(stream);
     if (f->dtype == HBP_F64)

@@ -14,6 +14,7 @@ graph.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -149,10 +150,11 @@ class SpmvOperator:
     partial (f64, compact) is combined in ascending bc."""
 
     HOT_MIN_SHARE = 0.10  # stage hot columns when they hold >= 10 % of the nonzeros
+    WARM_BYTES = 64 << 20  # warm tier: a 64 MB L2-resident copy of x at the next columns
 
     def __init__(self, hbp: HbpMatrix, workers: int | None = None,
                  fixed_fraction: float | None = None, schedule: str | None = None,
-                 hot: bool | int | None = None):
+                 hot: bool | int | None = None, warm_bytes: int | None = None):
         self.hbp = hbp
         dev = hbp.data.device
         if schedule is None:
@@ -166,10 +168,19 @@ class SpmvOperator:
         f = self._fmt = L.FormatT.from_buffer_copy(hbp.format_struct())
         self.hot = None
         if schedule == "stream" and hot is not False and hbp.nnz and hbp.cols:
-            hc = hbp.hot_columns(None if hot in (None, True) else int(hot))
-            if hc.n_hot and (hot is not None or hc.share >= self.HOT_MIN_SHARE):
-                self.hot = hc
-                hc.apply(f)
+            n_hot = None if hot in (None, True) else int(hot)
+            # x well inside L2 (cfg2: 64 MB of 126 MB) stays there with an
+            # evict-last policy on every gather; a larger x (cfg5: 256 MB) gets
+            # a warm tier, a compact evict-last copy of the next heaviest columns
+            fits = hbp.cols * hbp.data.element_size() <= L.l2_bytes() * 0.6
+            wb = (0 if fits else int(os.environ.get("HBP_WARM_BYTES", self.WARM_BYTES))) \
+                if warm_bytes is None else int(warm_bytes)
+            cap = hbp.hot_capacity()
+            n = (cap if n_hot is None else min(n_hot, cap)) & ~3
+            if n > 0 and (hot is not None or hbp.column_share(n) >= self.HOT_MIN_SHARE):
+                self.hot = hbp.hot_columns(n_hot, max(0, wb) // hbp.data.element_size())
+                self.hot.apply(f)
+                f.cold_last = int(fits)
         if schedule in ("balanced", "stream"):
             if workers is None:
                 w = L.c_i64(0)
@@ -189,7 +200,7 @@ class SpmvOperator:
                 self.bal.part_head, self.bal.part_tail = ph.data_ptr(), pt.data_ptr()
                 self.bal.cut_end, self.bal.counters = ce.data_ptr(), cn.data_ptr()
             if self.hot is not None:
-                xh = torch.empty(self.hot.n_hot, dtype=hbp.dtype, device=dev)
+                xh = torch.empty(self.hot.n_hot + self.hot.n_warm, dtype=hbp.dtype, device=dev)
                 self._scratch.append(xh)
                 self.bal.x_hot = xh.data_ptr()
         else:

@@ -48,14 +48,18 @@ def _padded(t: torch.Tensor, pad: int = 16) -> torch.Tensor:
 
 class HotColumns:
     """x staging of the heaviest columns (hbp_spmv_stream): hot_cols[s] is
-    the column of hot slot s, scol the element stream with hot columns as
-    HBP_HOT_FLAG | s, share the fraction of nonzeros in hot columns."""
+    the column of hot slot s (then of warm slot w at n_hot + w), scol the
+    element stream with hot columns as HBP_HOT_FLAG | s and warm ones as
+    HBP_WARM_FLAG | w, share / warm_share the fractions of nonzeros."""
 
-    def __init__(self, n_hot: int, hot_cols: torch.Tensor, scol: torch.Tensor, share: float):
+    def __init__(self, n_hot: int, hot_cols: torch.Tensor, scol: torch.Tensor, share: float,
+                 n_warm: int = 0, warm_share: float = 0.0):
         self.n_hot, self.hot_cols, self.scol, self.share = n_hot, hot_cols, scol, share
+        self.n_warm, self.warm_share = n_warm, warm_share
 
     def apply(self, f: "L.FormatT") -> None:
-        f.scol, f.hot_cols, f.n_hot = self.scol.data_ptr(), self.hot_cols.data_ptr(), self.n_hot
+        f.scol, f.hot_cols = self.scol.data_ptr(), self.hot_cols.data_ptr()
+        f.n_hot, f.n_warm = self.n_hot, self.n_warm
 
 
 class HbpFormatError(ValueError):
@@ -109,33 +113,67 @@ class HbpMatrix:
             self._fmt.phase_ptr = ptr.data_ptr()
             self._fmt.phases = phases.data_ptr()
 
-    def hot_columns(self, n_hot: int | None = None) -> "HotColumns":
-        """Hot-column staging metadata for hbp_spmv_stream (include/hbp.h
-        hbp_col_degree .. hbp_hot_remap): the n_hot columns with the most
-        nonzeros (ties: lower column first), capped by the kernel's
-        shared-memory capacity, and the staged column stream.  Cached."""
+    def hot_capacity(self) -> int:
+        """Largest hot set the stream kernel can stage for this dtype."""
         cap = L.c_i64(0)
         L.call("hbp_hot_capacity", L.c_int(L.dtype_code(self.data.dtype)), ctypes.byref(cap))
-        n = int(cap.value) if n_hot is None else min(int(n_hot), int(cap.value))
+        return int(cap.value)
+
+    RANK_SAMPLE = 1 << 28  # column degrees from at most ~256M sampled elements
+
+    def column_ranking(self):
+        """(degree, order): nonzeros per column and the columns by descending
+        degree, ties by ascending column (hbp_col_degree + stable radix sort).
+        Above RANK_SAMPLE elements the degrees count every stride-th element
+        (a power of two): the ranking only picks which columns are staged.
+        Cached."""
+        if "rank" not in self._ops:
+            dev = self.data.device
+            stride = 1
+            while self.nnz // stride > self.RANK_SAMPLE:
+                stride *= 2
+            deg = torch.zeros(self.cols, dtype=torch.int32, device=dev)
+            L.call("hbp_col_degree", L.P(self.col), L.c_i64(self.nnz), L.c_i64(stride), L.P(deg),
+                   L.stream())
+            keys = (torch.iinfo(torch.int32).max - deg).contiguous()
+            vals = torch.arange(self.cols, dtype=torch.int32, device=dev)
+            _, order = L.sort_pairs_u32(keys, vals, 32)
+            self._ops["rank"] = (deg, order)
+        return self._ops["rank"]
+
+    def column_share(self, n: int) -> float:
+        """Fraction of the (sampled) nonzeros in the n heaviest columns."""
+        if n <= 0 or not self.nnz:
+            return 0.0
+        deg, order = self.column_ranking()
+        return float(deg[order[:n].long()].to(torch.int64).sum().item()) / max(
+            1, int(deg.to(torch.int64).sum().item()))
+
+    def hot_columns(self, n_hot: int | None = None, n_warm: int = 0) -> "HotColumns":
+        """Hot-column staging metadata for hbp_spmv_stream (include/hbp.h
+        hbp_col_degree .. hbp_hot_remap): the n_hot heaviest columns (capped
+        by the kernel's shared-memory capacity), then the n_warm next ones
+        (warm tier), and the staged column stream.  Cached."""
+        cap = self.hot_capacity()
+        n = cap if n_hot is None else min(int(n_hot), cap)
         n = max(0, min(n, self.cols)) & ~3
-        key = ("hot", n)
+        nw = max(0, min(int(n_warm), self.cols - n)) if self.cols <= (1 << 30) else 0
+        key = ("hot", n, nw)
         if key in self._ops:
             return self._ops[key]
         dev = self.data.device
-        col = self.col
-        deg = torch.zeros(self.cols, dtype=torch.int32, device=dev)
-        L.call("hbp_col_degree", L.P(col), L.c_i64(self.nnz), L.P(deg), L.stream())
-        # descending degree, stable (ascending column among equal degrees)
-        keys = (torch.iinfo(torch.int32).max - deg).contiguous()
-        vals = torch.arange(self.cols, dtype=torch.int32, device=dev)
-        _, order = L.sort_pairs_u32(keys, vals, 32)
-        hot_cols = order[:n].contiguous()
-        share = float(deg[hot_cols.long()].sum().item()) / max(1, self.nnz)
+        deg, order = self.column_ranking()
+        hot_cols = order[:n + nw].contiguous()
+        dsum = torch.cumsum(deg[hot_cols.long()].to(torch.int64), 0)
+        total = max(1, int(deg.to(torch.int64).sum().item()))
+        share = float(dsum[n - 1].item()) / total if n else 0.0
+        warm_share = (float(dsum[-1].item()) / total - share) if nw else 0.0
         slot_of = torch.full((self.cols,), -1, dtype=torch.int32, device=dev)
-        L.call("hbp_hot_slots", L.P(hot_cols), L.c_i64(n), L.P(slot_of), L.stream())
-        scol = _padded(torch.empty(self.nnz, dtype=col.dtype, device=dev))
-        L.call("hbp_hot_remap", L.P(col), L.c_i64(self.nnz), L.P(slot_of), L.P(scol), L.stream())
-        hc = HotColumns(n, hot_cols, scol, share)
+        L.call("hbp_hot_slots", L.P(hot_cols), L.c_i64(n + nw), L.P(slot_of), L.stream())
+        scol = _padded(torch.empty(self.nnz, dtype=self.col.dtype, device=dev))
+        L.call("hbp_hot_remap", L.P(self.col), L.c_i64(self.nnz), L.P(slot_of), L.c_i64(n),
+               L.P(scol), L.stream())
+        hc = HotColumns(n, hot_cols, scol, share, nw, warm_share)
         self._ops[key] = hc
         return hc
 

@@ -70,17 +70,36 @@ def test_hot_metadata(mat):
     np.testing.assert_array_equal(hc.scol.cpu().numpy().view(np.uint32), want)
 
 
+def test_warm_metadata(mat):
+    rows, cols, r, c, v = mat
+    hbp = _hbp(rows, cols, r, c, v)
+    hc = hbp.hot_columns(64, 3000)
+    assert (hc.n_hot, hc.n_warm) == (64, 3000)
+    deg = np.bincount(c, minlength=cols)
+    order = np.argsort(-deg, kind="stable")
+    np.testing.assert_array_equal(hc.hot_cols.cpu().numpy(), order[:3064])
+    assert hc.warm_share == pytest.approx(deg[order[64:3064]].sum() / c.size, rel=1e-12)
+    col = hbp.col.cpu().numpy().view(np.uint32).astype(np.int64)
+    slot = np.full(cols, -1, np.int64)
+    slot[order[:3064]] = np.arange(3064)
+    s = slot[col]
+    want = np.where(s < 0, col, np.where(s < 64, FLAG | s, 0x40000000 | (s - 64)))
+    np.testing.assert_array_equal(hc.scol.cpu().numpy().view(np.uint32), want.astype(np.uint32))
+
+
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
-@pytest.mark.parametrize("n_hot", [4, 64, 1000, None])
+@pytest.mark.parametrize("n_hot,warm", [(4, 0), (64, 0), (1000, 0), (None, 0), (4, 20000),
+                                        (64, 2000), (None, 1 << 30)])
 @pytest.mark.parametrize("workers", [1, 37, 500, None])
-def test_staged_bitwise_equals_unstaged(mat, dtype, n_hot, workers):
+def test_staged_bitwise_equals_unstaged(mat, dtype, n_hot, warm, workers):
     rows, cols, r, c, v = mat
     vv = v.astype(np.float32) if dtype == "f32" else v
     hbp = _hbp(rows, cols, r, c, vv)
     x = np.random.default_rng(5).uniform(-1, 1, cols)
     xd = torch.as_tensor(x.astype(vv.dtype), device="cuda")
     plain = H.SpmvOperator(hbp, workers=workers, hot=False)
-    staged = H.SpmvOperator(hbp, workers=workers, hot=True if n_hot is None else n_hot)
+    staged = H.SpmvOperator(hbp, workers=workers, hot=True if n_hot is None else n_hot,
+                            warm_bytes=warm * vv.itemsize)
     assert plain.hot is None and staged.hot is not None
     y0 = plain(xd).cpu().numpy()
     y1 = staged(xd).cpu().numpy()
@@ -148,3 +167,14 @@ def test_n_hot_beyond_capacity_rejected(mat):
     with pytest.raises(ValueError):
         L.call("hbp_spmv_stream", ctypes.byref(f), ctypes.byref(op.bal), L.P(x), L.P(y),
                L.P(None), L.stream())
+
+
+@pytest.mark.parametrize("stride", [1, 3, 16])
+def test_col_degree_sampled(mat, stride):
+    rows, cols, r, c, v = mat
+    hbp = _hbp(rows, cols, r, c, v.astype(np.float32))
+    deg = torch.zeros(cols, dtype=torch.int32, device="cuda")
+    L.call("hbp_col_degree", L.P(hbp.col), L.c_i64(hbp.nnz), L.c_i64(stride), L.P(deg),
+           L.stream())
+    col = hbp.col.cpu().numpy().view(np.uint32)
+    np.testing.assert_array_equal(deg.cpu().numpy(), np.bincount(col[::stride], minlength=cols))
