@@ -310,7 +310,7 @@ def run_gpu(args):
         torch.cuda.synchronize()
         t4 = time.perf_counter()
         # runtime operator: phase stream + hot-column staging (hbp_hot.cu)
-        op = H.SpmvOperator(hbp, schedule=args.schedule, hot=hot_arg)
+        op = H.SpmvOperator(hbp, schedule=args.schedule, hot=hot_arg, workers=args.workers)
         torch.cuda.synchronize()
         t5 = time.perf_counter()
         pre = dict(grid=(t1 - t0) * 1e3, sample=(t2 - t1) * 1e3, hash=(t3 - t2) * 1e3,
@@ -411,7 +411,8 @@ def run_gpu(args):
     # x_i H2D, SpMV, y_i D2H on 2 rotating streams; every step moves its own
     # x in and y out).  With an L2 flush, steps run one at a time instead.
     depth = 1 if flush else 2
-    pipe = H.HostPipeline(hbp, depth=depth, schedule=args.schedule, hot=hot_arg)
+    pipe = H.HostPipeline(hbp, depth=depth, schedule=args.schedule, hot=hot_arg,
+                          workers=args.workers)
     xh = torch.as_tensor(x_host).to(vdt).pin_memory()
     yhs = [torch.empty(rows, dtype=vdt).pin_memory() for _ in range(depth)]
     nw = max(depth, args.warmup)
@@ -536,6 +537,8 @@ def run_gpu(args):
                    "schedule": op.schedule,
                    "hot_columns": op.hot.n_hot if op.hot is not None else 0,
                    "hot_share": round(op.hot.share, 4) if op.hot is not None else 0.0,
+                   "warm_columns": op.hot.n_warm if op.hot is not None else 0,
+                   "warm_share": round(op.hot.warm_share, 4) if op.hot is not None else 0.0,
                    "hash_params": [params.a, params.b, params.c, params.d],
                    "step": ("power iteration: SpMV + ||y|| all-reduce + y all-gather"
                             if iterated else "SpMV (+ combine when ncb > 1)"),
@@ -616,6 +619,8 @@ def main():
     ap.add_argument("--no-baselines", action="store_true",
                     help="skip the CSR / 2D / cuSPARSE comparison timings")
     ap.add_argument("--schedule", default=None, choices=[None, "stream", "balanced", "plan"])
+    ap.add_argument("--workers", type=int, default=None,
+                    help="persistent warps of the SpMV (default: one per resident warp slot)")
     ap.add_argument("--hot", default="auto",
                     help="hot-column x staging: auto (>= 10%% of nnz), on, off, or a column count")
     args = ap.parse_args()

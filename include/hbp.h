@@ -298,6 +298,8 @@ typedef struct {
     int64_t *cut_end;
     uint32_t *counters;
     void *x_hot; /* [n_hot + n_warm] scratch: x at hot_cols (hot, then warm tier) */
+    int64_t *slice_lo; /* nullable [workers + 1]: stream slice bounds (hbp_stream_slices) */
+    int64_t *slice_g;  /* nullable [workers]: first group of each stream slice */
 } hbp_balanced_t;
 
 int hbp_balanced_workers(const hbp_format_t *f, int64_t *workers);
@@ -308,6 +310,10 @@ int hbp_balanced_workers(const hbp_format_t *f, int64_t *workers);
  * at arbitrary element offsets in fast mode (no cut_end needed).  col and
  * data must be readable 16 bytes past nnz (the builder pads them). */
 int hbp_stream_workers(const hbp_format_t *f, int64_t *workers);
+/* Precomputes the stream kernel's per-worker slice bounds and first groups
+ * (otherwise every warp binary-searches group_start at launch -- ~20
+ * dependent loads, visible on small matrices). */
+int hbp_stream_slices(const hbp_format_t *f, const hbp_balanced_t *b, hbp_stream_t stream);
 int hbp_spmv_stream(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y,
                     double *partial, hbp_stream_t stream);
 /* Hot-column staging for power-law column degrees (R-MAT): the n_hot

@@ -55,7 +55,8 @@ class ScheduleT(ctypes.Structure):
 class BalancedT(ctypes.Structure):
     """Mirror of hbp_balanced_t."""
     _fields_ = [("workers", c_i64), ("part_head", c_vp), ("part_tail", c_vp),
-                ("cut_end", c_vp), ("counters", c_vp), ("x_hot", c_vp)]
+                ("cut_end", c_vp), ("counters", c_vp), ("x_hot", c_vp),
+                ("slice_lo", c_vp), ("slice_g", c_vp)]
 
 
 # name -> argtypes (all return int status)
@@ -106,6 +107,7 @@ _SIGS = {
     "hbp_spmv_balanced": [ctypes.POINTER(FormatT), ctypes.POINTER(BalancedT), c_vp, c_vp, c_vp,
                           c_vp],
     "hbp_stream_workers": [ctypes.POINTER(FormatT), ctypes.POINTER(c_i64)],
+    "hbp_stream_slices": [ctypes.POINTER(FormatT), ctypes.POINTER(BalancedT), c_vp],
     "hbp_spmv_stream": [ctypes.POINTER(FormatT), ctypes.POINTER(BalancedT), c_vp, c_vp, c_vp,
                         c_vp],
     "hbp_col_degree": [c_vp, c_i64, c_i64, c_vp, c_vp],

@@ -155,9 +155,19 @@ __global__ void k_combine(const hbp_format_t f, const double *__restrict__ parti
         const int64_t lo = f.rb_ptr[br], hi = f.rb_ptr[br + 1];
         double s = 0.0;
         if (lo < hi) {
+            // the same left-to-right sum, four independent loads in flight
             s = partial[(int64_t)f.rb_blk[lo] * R + local];
-            for (int64_t i = lo + 1; i < hi; ++i)
-                s = __dadd_rn(s, partial[(int64_t)f.rb_blk[i] * R + local]);
+            int64_t i = lo + 1;
+            for (; i + 4 <= hi; i += 4) {
+                const int32_t b0 = f.rb_blk[i], b1 = f.rb_blk[i + 1], b2 = f.rb_blk[i + 2],
+                              b3 = f.rb_blk[i + 3];
+                const double p0 = partial[(int64_t)b0 * R + local];
+                const double p1 = partial[(int64_t)b1 * R + local];
+                const double p2 = partial[(int64_t)b2 * R + local];
+                const double p3 = partial[(int64_t)b3 * R + local];
+                s = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(s, p0), p1), p2), p3);
+            }
+            for (; i < hi; ++i) s = __dadd_rn(s, partial[(int64_t)f.rb_blk[i] * R + local]);
         }
         y[r] = (V)s;
     }

@@ -186,6 +186,42 @@ __device__ __forceinline__ int64_t cut_at(int64_t w, int64_t E, int64_t Nw) {
     return (int64_t)((__int128)w * E / Nw);
 }
 
+// Slice of worker w: equal element ranges [cut(w), cut(w+1)); exact mode
+// rounds both ends up to group boundaries (every row summed by one lane in
+// step order).  g = the first group whose elements the slice touches.
+__device__ __forceinline__ void stream_slice(const int64_t *__restrict__ gs, int64_t ngroups,
+                                             int64_t E, int64_t w, int64_t Nw, bool exact,
+                                             int64_t *lo, int64_t *hi, int64_t *g0) {
+    int64_t c_lo = cut_at(w, E, Nw), c_hi = cut_at(w + 1, E, Nw);
+    if (exact) {
+        if (c_lo > 0 && c_lo < E) {
+            int64_t g = upper_group(gs, ngroups, c_lo);
+            if (gs[g] != c_lo) c_lo = gs[g + 1];
+        }
+        if (c_hi > 0 && c_hi < E) {
+            int64_t g = upper_group(gs, ngroups, c_hi);
+            if (gs[g] != c_hi) c_hi = gs[g + 1];
+        }
+    }
+    int64_t g = upper_group(gs, ngroups, c_lo);
+    if (!(g < ngroups && gs[g] < c_lo)) g = lower_group(gs, ngroups, c_lo);
+    *lo = c_lo;
+    *hi = c_hi;
+    *g0 = g;
+}
+
+__global__ void k_stream_slices(const int64_t *__restrict__ gs, int64_t ngroups, int64_t E,
+                                int64_t Nw, bool exact, int64_t *__restrict__ slice_lo,
+                                int64_t *__restrict__ slice_g) {
+    const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= Nw) return;
+    int64_t lo, hi, g;
+    stream_slice(gs, ngroups, E, w, Nw, exact, &lo, &hi, &g);
+    slice_lo[w] = lo;
+    slice_g[w] = g;
+    if (w == Nw - 1) slice_lo[Nw] = hi;
+}
+
 template <typename V, bool EXACT>
 __device__ __forceinline__ V product(V v, V xv) {
     if (EXACT) return (V)__dmul_rn((double)v, (double)xv);
@@ -647,16 +683,13 @@ __global__ void __launch_bounds__(NT, MINB)
     const uint2 *__restrict__ phs = (const uint2 *)f.phases;
     const uint32_t *__restrict__ permp = (const uint32_t *)f.perm;
 
-    int64_t c_lo = cut_at(w, E, Nw), c_hi = cut_at(w + 1, E, Nw);
-    if (EXACT) {  // round slice ends up to group boundaries
-        if (c_lo > 0 && c_lo < E) {
-            int64_t g = upper_group(gs, ngroups, c_lo);
-            if (gs[g] != c_lo) c_lo = gs[g + 1];
-        }
-        if (c_hi > 0 && c_hi < E) {
-            int64_t g = upper_group(gs, ngroups, c_hi);
-            if (gs[g] != c_hi) c_hi = gs[g + 1];
-        }
+    int64_t c_lo, c_hi, g;
+    if (b.slice_lo) {  // precomputed (hbp_stream_slices): no binary searches here
+        c_lo = b.slice_lo[w];
+        c_hi = b.slice_lo[w + 1];
+        g = b.slice_g[w];
+    } else {
+        stream_slice(gs, ngroups, E, w, Nw, EXACT, &c_lo, &c_hi, &g);
     }
     const int64_t base = c_lo & ~(int64_t)3;
     Ring<V, EXACT, CH, NB, XM, HOT, GD> ring{S, x};
@@ -685,8 +718,6 @@ __global__ void __launch_bounds__(NT, MINB)
     __syncwarp();
     ring.prime(c_hi > c_lo ? (len32 + CH - 1) / CH : 0, len32);
 
-    int64_t g = upper_group(gs, ngroups, c_lo);
-    if (!(g < ngroups && gs[g] < c_lo)) g = lower_group(gs, ngroups, c_lo);
     const bool last_warp = (w == Nw - 1);
     // output position of group g: nonzero block blk, group gi within it
     int32_t blk = (int32_t)(g / gpb), gi = (int32_t)(g - (int64_t)blk * gpb);
@@ -1013,6 +1044,16 @@ int hbp_hot_gather(const void *x, int dtype, const uint32_t *hot_cols, int64_t n
     if (dtype == HBP_F64) return hot_gather<double>(x, hot_cols, n_hot, x_hot, as_stream(stream));
     if (dtype == HBP_F32) return hot_gather<float>(x, hot_cols, n_hot, x_hot, as_stream(stream));
     return HBP_E_ARG;
+}
+
+int hbp_stream_slices(const hbp_format_t *f, const hbp_balanced_t *b, hbp_stream_t stream) {
+    if (!f || !b || b->workers < 1 || !b->slice_lo || !b->slice_g) return HBP_E_ARG;
+    if (f->warp_size != 32 || f->row_height % 32) return HBP_E_UNSUPPORTED;
+    const int64_t ngroups = f->nzb * (f->row_height / 32);
+    const bool exact = f->exact != 0 || f->dtype == HBP_F64;
+    k_stream_slices<<<(unsigned)((b->workers + 127) / 128), 128, 0, as_stream(stream)>>>(
+        f->group_start, ngroups, f->nnz, b->workers, exact, b->slice_lo, b->slice_g);
+    return (int)cudaGetLastError();
 }
 
 int hbp_spmv_stream(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y,

@@ -203,6 +203,12 @@ class SpmvOperator:
                 xh = torch.empty(self.hot.n_hot + self.hot.n_warm, dtype=hbp.dtype, device=dev)
                 self._scratch.append(xh)
                 self.bal.x_hot = xh.data_ptr()
+            if schedule == "stream" and hbp.nzb:
+                sl = torch.empty(self.workers + 1, dtype=torch.int64, device=dev)
+                sg = torch.empty(self.workers, dtype=torch.int64, device=dev)
+                self._scratch += [sl, sg]
+                self.bal.slice_lo, self.bal.slice_g = sl.data_ptr(), sg.data_ptr()
+                L.call("hbp_stream_slices", ctypes.byref(f), ctypes.byref(self.bal), L.stream())
         else:
             self.workers = workers or default_workers(hbp.dtype, hbp.config.warp_size)
         fr = hbp.config.fixed_fraction if fixed_fraction is None else fixed_fraction

@@ -117,3 +117,21 @@ def test_plan_schedule_still_available():
     c = H.SpmvOperator(hbp, schedule="stream")(xd).cpu().numpy()
     np.testing.assert_array_equal(a, b)
     np.testing.assert_array_equal(a, c)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("workers", [1, 7, 333, None])
+def test_stream_precomputed_slices(dtype, workers):
+    """hbp_stream_slices (one-time slice bounds) == the in-kernel search."""
+    rows, cols, r, c, v = _hot_matrix(seed=5)
+    hbp = _hbp(rows, cols, r, c, v.astype(dtype), C=cols)
+    x = torch.as_tensor(np.random.default_rng(2).uniform(-1, 1, cols).astype(dtype),
+                        device="cuda")
+    op = H.SpmvOperator(hbp, workers=workers, hot=False)
+    assert op.bal.slice_lo and op.bal.slice_g
+    y1 = op(x).cpu().numpy()
+    lo = op._scratch[-2].cpu().numpy()
+    assert lo[0] == 0 and lo[-1] == hbp.nnz and np.all(np.diff(lo) >= 0)
+    op.bal.slice_lo = op.bal.slice_g = 0
+    y2 = op(x).cpu().numpy()
+    np.testing.assert_array_equal(y1, y2)
