@@ -314,6 +314,10 @@ int hbp_stream_workers(const hbp_format_t *f, int64_t *workers);
  * (otherwise every warp binary-searches group_start at launch -- ~20
  * dependent loads, visible on small matrices). */
 int hbp_stream_slices(const hbp_format_t *f, const hbp_balanced_t *b, hbp_stream_t stream);
+/* Tuning: kernel variant of hbp_spmv_stream for later calls (0 = default;
+ * the others are measured alternatives and diagnostics).
+ * Not thread-safe; for benchmarks. */
+int hbp_stream_set_variant(int variant);
 int hbp_spmv_stream(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y,
                     double *partial, hbp_stream_t stream);
 /* Hot-column staging for power-law column degrees (R-MAT): the n_hot

@@ -108,6 +108,7 @@ _SIGS = {
                           c_vp],
     "hbp_stream_workers": [ctypes.POINTER(FormatT), ctypes.POINTER(c_i64)],
     "hbp_stream_slices": [ctypes.POINTER(FormatT), ctypes.POINTER(BalancedT), c_vp],
+    "hbp_stream_set_variant": [c_int],
     "hbp_spmv_stream": [ctypes.POINTER(FormatT), ctypes.POINTER(BalancedT), c_vp, c_vp, c_vp,
                         c_vp],
     "hbp_col_degree": [c_vp, c_i64, c_i64, c_vp, c_vp],

@@ -348,7 +348,7 @@ struct Ring {
             bc = (uint32_t)((n * 4 + 15) & ~15);
             bv = (uint32_t)((n * (int)sizeof(V) + 15) & ~15);
         }
-        const uint64_t pe = S.pol_stream;
+        const uint64_t pe = policy_evict_first();  // created in place: no smem load + R2UR
         mbar_expect_tx(&S.mbar[slot], bc + bv);
         bulk_g2s(&S.col[(c & (NCOL - 1)) * CH], S.colg + (int64_t)c * CH, bc, &S.mbar[slot], pe);
         bulk_g2s(&S.val[slot * CH], S.valg + (int64_t)c * CH, bv, &S.mbar[slot], pe);
@@ -379,7 +379,7 @@ struct Ring {
             for (int e = 0; e < EPL; ++e)
                 if (EPL * lane + e >= n) cc[e] = 0u;
         }
-        const uint64_t pl = S.pol_x;
+        const uint64_t pl = policy_evict_last();
         if constexpr (GD > 0) {  // x replaces the columns in the slot
             const uint32_t dst = smem_addr(cs);
 #pragma unroll
@@ -585,7 +585,26 @@ __device__ __forceinline__ double walk_fast(RingT &ring, const uint2 ph, const i
             if (PIECE && lo_r > ps) q = ps + ((lo_r - ps) / stride) * stride;
             const bool act = lane < stride;
             double v0 = 0.0, v1 = 0.0;
-            for (; q < stop; q += 2 * stride) {
+            if constexpr (!PIECE) {
+                // whole phase: tight double passes over the resident window, the
+                // ring advance outside the inner loop (same sums as below)
+                for (;;) {
+                    const int32_t lim = ring.res32 < stop ? ring.res32 : stop;
+                    for (; q + 2 * stride <= lim; q += 2 * stride)
+                        if (act) v0 += ring.at2(q + lane, q + stride + lane);
+                    if (q >= stop) break;
+                    const int32_t need = q + 2 * stride < stop ? q + 2 * stride : stop;
+                    if (need > ring.res32) {
+                        ring.advance(need);
+                        continue;
+                    }
+                    const int32_t P0 = q + lane, P1 = q + stride + lane;  // last, partial
+                    if (act && P1 < stop) v0 += ring.at2(P0, P1);
+                    else if (act && P0 < stop) v0 += ring.at(P0);
+                    break;
+                }
+            }
+            for (; PIECE && q < stop; q += 2 * stride) {
                 const int32_t q2 = q + stride;
                 const int32_t need = q2 + stride < stop ? q2 + stride : stop;
                 if (need > ring.res32) ring.advance(need);
@@ -906,14 +925,14 @@ int occupancy_of(const hbp_format_t *f, int *per_sm, int *warps_per_cta) {
 // modular passes) are in the git history; 128/4/3x256 with L1::no_allocate x
 // gathers and KT=12, LMIN=4 won on cfg2 and H.
 constexpr int kVariants = 4;
+int g_variant = -1;  // tuning knob (HBP_STREAM_VARIANT / hbp_stream_set_variant)
 int variant() {
-    static int v = -1;
-    if (v < 0) {
+    if (g_variant < 0) {
         const char *e = getenv("HBP_STREAM_VARIANT");
-        v = e ? atoi(e) : 0;
-        if (v < 0 || v >= kVariants) v = 0;
+        g_variant = e ? atoi(e) : 0;
+        if (g_variant < 0 || g_variant >= kVariants) g_variant = 0;
     }
-    return v;
+    return g_variant;
 }
 
 bool staged(const hbp_format_t *f) { return f->n_hot > 0 && f->scol && f->hot_cols; }
@@ -1044,6 +1063,12 @@ int hbp_hot_gather(const void *x, int dtype, const uint32_t *hot_cols, int64_t n
     if (dtype == HBP_F64) return hot_gather<double>(x, hot_cols, n_hot, x_hot, as_stream(stream));
     if (dtype == HBP_F32) return hot_gather<float>(x, hot_cols, n_hot, x_hot, as_stream(stream));
     return HBP_E_ARG;
+}
+
+int hbp_stream_set_variant(int v) {
+    if (v < 0 || v >= kVariants) return HBP_E_ARG;
+    g_variant = v;
+    return HBP_OK;
 }
 
 int hbp_stream_slices(const hbp_format_t *f, const hbp_balanced_t *b, hbp_stream_t stream) {

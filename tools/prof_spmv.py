@@ -21,6 +21,8 @@ ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--workers", type=int, default=None)
 ap.add_argument("--persist", action="store_true")
 ap.add_argument("--hot", default="auto", help="auto | on | off | column count")
+ap.add_argument("--persist-warm", action="store_true",
+                help="L2 persisting window over the staged x copy (hot + warm tiers)")
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 desc, rows, cols, rp, col, val, C, vdt = bench.make_matrix_gpu(a.config, 0, dev)
@@ -34,6 +36,11 @@ op = H.SpmvOperator(hbp, workers=a.workers, schedule=a.schedule,
                     hot=int(hot) if isinstance(hot, str) else hot)
 x = torch.as_tensor(np.random.default_rng(0).uniform(-1, 1, cols), device=dev).to(vdt)
 y = torch.empty(rows, dtype=vdt, device=dev)
+if a.persist_warm and op.hot is not None:
+    from paper_2504_08860_b200 import _lib as L
+    xh = op._scratch[[t.numel() for t in op._scratch].index(op.hot.n_hot + op.hot.n_warm)]
+    L.call("hbp_l2_persist", L.P(xh), xh.numel() * xh.element_size(), 1.0, L.stream())
+    print("persisting", xh.numel() * xh.element_size() >> 20, "MB")
 if a.persist:
     from paper_2504_08860_b200 import _lib as L
     L.call("hbp_l2_persist", L.P(x), x.numel() * x.element_size(), 1.0, L.stream())
