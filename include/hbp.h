@@ -300,6 +300,8 @@ typedef struct {
     void *x_hot; /* [n_hot + n_warm] scratch: x at hot_cols (hot, then warm tier) */
     int64_t *slice_lo; /* nullable [workers + 1]: stream slice bounds (hbp_stream_slices) */
     int64_t *slice_g;  /* nullable [workers]: first group of each stream slice */
+    uint32_t *rb_done; /* nullable [nrb], zero-filled once: fused combine (stream
+                          kernel with partial AND y; the kernel leaves it zeroed) */
 } hbp_balanced_t;
 
 int hbp_balanced_workers(const hbp_format_t *f, int64_t *workers);

@@ -741,6 +741,7 @@ __global__ void __launch_bounds__(NT, MINB)
     // output position of group g: nonzero block blk, group gi within it
     int32_t blk = (int32_t)(g / gpb), gi = (int32_t)(g - (int64_t)blk * gpb);
     int32_t rows_left = 0;  // rows of block blk (<= R)
+    int32_t br_cur = 0;     // its row block
     V *yb = nullptr;
     double *pb_out = nullptr;
     auto enter_block = [&]() {
@@ -748,9 +749,59 @@ __global__ void __launch_bounds__(NT, MINB)
             const int64_t br = f.blk_br[blk];
             const int64_t left = f.rows - br * R;
             rows_left = (int32_t)(left < R ? left : R);
+            br_cur = (int32_t)br;
             yb = y + br * R;
             pb_out = partial ? partial + (int64_t)blk * R : nullptr;
         }
+    };
+    // Fused combine (engine.py:196-201; b.rb_done set, partial and y given):
+    // every finished group counts toward its row block; the warp that
+    // completes a row block's nb * gpb groups sums its partials in ascending
+    // bc (the rb_blk order, as hbp_combine does -- bitwise the same) and
+    // writes y, then resets the counter.
+    // Groups are counted locally and published once per row block the warp
+    // leaves (one fence per block, not per group).
+    int32_t pend_br = -1, pend_rows = 0;
+    uint32_t pend_n = 0;
+    auto flush_done = [&](int32_t br, uint32_t n, int32_t nrows) {
+        __syncwarp();
+        __threadfence();  // this warp's partials before the count
+        const int64_t lo = f.rb_ptr[br], hi = f.rb_ptr[br + 1];
+        uint32_t last = 0;
+        if (lane == 0) {
+            const uint32_t total = (uint32_t)((hi - lo) * gpb);
+            last = (atomicAdd(b.rb_done + br, n) + n == total);
+        }
+        if (!__shfl_sync(FULL, last, 0)) return;
+        __threadfence();
+        V *yr = y + (int64_t)br * R;
+        // four rows per lane at a time (independent loads in flight), each
+        // summed left to right over the row block's blocks
+        for (int32_t r0 = 0; r0 < nrows; r0 += 128) {
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            for (int64_t i = lo; i < hi; ++i) {
+                const double *pp = partial + (int64_t)f.rb_blk[i] * R + r0 + lane;
+                const double p0 = __ldcg(pp), p1 = __ldcg(pp + 32), p2 = __ldcg(pp + 64),
+                             p3 = __ldcg(pp + 96);
+                if (i == lo) a0 = p0, a1 = p1, a2 = p2, a3 = p3;
+                else a0 = __dadd_rn(a0, p0), a1 = __dadd_rn(a1, p1), a2 = __dadd_rn(a2, p2),
+                     a3 = __dadd_rn(a3, p3);
+            }
+            const int32_t r = r0 + lane;
+            if (r < nrows) stm(yr + r, (V)a0);
+            if (r + 32 < nrows) stm(yr + r + 32, (V)a1);
+            if (r + 64 < nrows) stm(yr + r + 64, (V)a2);
+            if (r + 96 < nrows) stm(yr + r + 96, (V)a3);
+        }
+        if (lane == 0) b.rb_done[br] = 0u;
+    };
+    auto group_done = [&](int32_t br, int32_t nrows) {
+        if (!b.rb_done) return;
+        if (br != pend_br) {
+            if (pend_n) flush_done(pend_br, pend_n, pend_rows);
+            pend_br = br, pend_rows = nrows, pend_n = 0;
+        }
+        ++pend_n;
     };
     enter_block();
 
@@ -825,6 +876,7 @@ __global__ void __launch_bounds__(NT, MINB)
         const bool valid = gi_now * 32 + lane < rows_left;
         V *const yb_now = yb;
         double *const pb_now = pb_out;
+        const int32_t br_now = br_cur, rows_now = rows_left;
         if (++gi == gpb) {
             gi = 0;
             ++blk;
@@ -835,6 +887,7 @@ __global__ void __launch_bounds__(NT, MINB)
                 if (pb_now) pb_now[row_local] = acc;
                 else stm(yb_now + row_local, (V)acc);
             }
+            if (pb_now) group_done(br_now, rows_now);
             continue;
         }
         // fast mode only: a piece of a group cut by slice boundaries
@@ -865,7 +918,9 @@ __global__ void __launch_bounds__(NT, MINB)
             else stm(yb_now + row_local, (V)s);
         }
         if (lane == 0) b.counters[g] = 0u;
+        if (pb_now) group_done(br_now, rows_now);
     }
+    if (b.rb_done && pend_n) flush_done(pend_br, pend_n, pend_rows);
 }
 
 // Shared memory per SM is kept to what MINB CTAs need: the rest of the
@@ -1087,6 +1142,7 @@ int hbp_spmv_stream(const hbp_format_t *f, const hbp_balanced_t *b, const void *
     if (f->warp_size != 32 || f->row_height % 32) return HBP_E_UNSUPPORTED;
     if (!f->phases || !f->phase_ptr) return HBP_E_ARG;  // hbp_phase_emit first
     if (!partial && (!y || f->ncb != 1)) return HBP_E_ARG;
+    if (b->rb_done && (!partial || !y || !f->rb_ptr || !f->rb_blk)) return HBP_E_ARG;
     if (f->nzb == 0) return HBP_OK;
     // slices are addressed with 32-bit offsets
     if ((f->nnz + b->workers - 1) / b->workers > (int64_t)1 << 30) return HBP_E_UNSUPPORTED;

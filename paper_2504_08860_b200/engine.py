@@ -219,12 +219,20 @@ class SpmvOperator:
         self.partial = None if self.direct else torch.empty(hbp.nzb * R, dtype=torch.float64,
                                                             device=dev)
         self.has_empty_row_blocks = bool((hbp.rb_ptr[1:] == hbp.rb_ptr[:-1]).any())
+        # stream schedule with several column blocks: the combine is fused into
+        # the SpMV kernel (last warp of each row block sums its partials)
+        self.fused_combine = (not self.direct and schedule == "stream" and hbp.nzb > 0
+                              and os.environ.get("HBP_FUSED_COMBINE", "1") != "0")
+        if self.fused_combine:
+            rb = torch.zeros(max(1, hbp.num_row_blocks), dtype=torch.int32, device=dev)
+            self._scratch.append(rb)
+            self.bal.rb_done = rb.data_ptr()
         self.sched = L.ScheduleT()
         self.sched.workers = self.workers
         self.sched.fixed_count = self.fixed_count
         self.sched.ticket = self.ticket.data_ptr()
-        self.launches_per_call = (1 + (0 if self.direct and not self.has_empty_row_blocks else 1)
-                                  + (1 if self.hot is not None else 0))
+        self.launches_per_call = (1 + (1 if self.has_empty_row_blocks or not (
+            self.direct or self.fused_combine) else 0) + (1 if self.hot is not None else 0))
         self._graph = None
         self._gx = self._gy = None
 
@@ -244,6 +252,10 @@ class SpmvOperator:
         s = L.stream()
         if self.direct:
             self._blocks(f, x, None, y, s)
+            if self.has_empty_row_blocks:
+                L.call("hbp_zero_empty_rows", ctypes.byref(f), L.P(y), s)
+        elif self.fused_combine:
+            self._blocks(f, x, self.partial, y, s)
             if self.has_empty_row_blocks:
                 L.call("hbp_zero_empty_rows", ctypes.byref(f), L.P(y), s)
         else:

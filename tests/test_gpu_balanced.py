@@ -135,3 +135,29 @@ def test_stream_precomputed_slices(dtype, workers):
     op.bal.slice_lo = op.bal.slice_g = 0
     y2 = op(x).cpu().numpy()
     np.testing.assert_array_equal(y1, y2)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("C,workers", [(4096, None), (4096, 3), (1000, 77), (777, None)])
+def test_stream_fused_combine(dtype, C, workers, monkeypatch):
+    """Several column blocks: the kernel's last-arriver combine == hbp_combine
+    (bitwise), including row blocks without nonzero blocks."""
+    rows, cols, r, c, v = _hot_matrix(seed=7)
+    keep = (r < 1500) | (r >= 2100)  # a gap of empty row blocks (R = 512 -> block 3)
+    r, c, v = r[keep], c[keep], v[keep]
+    hbp = _hbp(rows, cols, r, c, v.astype(dtype), C=C)
+    x = torch.as_tensor(np.random.default_rng(3).uniform(-1, 1, cols).astype(dtype),
+                        device="cuda")
+    fused = H.SpmvOperator(hbp, workers=workers, hot=False)
+    assert fused.fused_combine
+    monkeypatch.setenv("HBP_FUSED_COMBINE", "0")
+    plain = H.SpmvOperator(hbp, workers=workers, hot=False)
+    assert not plain.fused_combine
+    y0 = plain(x).cpu().numpy()
+    y1 = fused(x).cpu().numpy()
+    y2 = fused(x).cpu().numpy()  # counters self-reset
+    np.testing.assert_array_equal(y1, y0)
+    np.testing.assert_array_equal(y2, y0)
+    if dtype == np.float64:
+        p = O.pipeline(rows, cols, r, c, v, C, 512, 32)
+        np.testing.assert_array_equal(y1, O.hbp_spmv(p["hbp"], x.cpu().numpy(), workers=2))
