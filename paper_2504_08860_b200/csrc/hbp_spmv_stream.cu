@@ -674,6 +674,7 @@ __global__ void __launch_bounds__(NT, MINB)
     // they do not displace x (evict-last) from L2
     constexpr bool MS = (XM & 4) != 0;
     constexpr bool SHORT = (XM & 16) != 0;  // fast path for 1-2 step phases
+    constexpr bool FC = (XM & 512) != 0;     // fused combine (b.rb_done; partial mode)
     auto ldm = [](const auto *p) { return MS ? __ldcs(p) : *p; };
     auto stm = [](auto *p, auto v) {
         if constexpr (MS) __stcs(p, v);
@@ -796,7 +797,7 @@ __global__ void __launch_bounds__(NT, MINB)
         if (lane == 0) b.rb_done[br] = 0u;
     };
     auto group_done = [&](int32_t br, int32_t nrows) {
-        if (!b.rb_done) return;
+        if constexpr (!FC) return;
         if (br != pend_br) {
             if (pend_n) flush_done(pend_br, pend_n, pend_rows);
             pend_br = br, pend_rows = nrows, pend_n = 0;
@@ -887,7 +888,7 @@ __global__ void __launch_bounds__(NT, MINB)
                 if (pb_now) pb_now[row_local] = acc;
                 else stm(yb_now + row_local, (V)acc);
             }
-            if (pb_now) group_done(br_now, rows_now);
+            if (FC && pb_now) group_done(br_now, rows_now);
             continue;
         }
         // fast mode only: a piece of a group cut by slice boundaries
@@ -918,9 +919,9 @@ __global__ void __launch_bounds__(NT, MINB)
             else stm(yb_now + row_local, (V)s);
         }
         if (lane == 0) b.counters[g] = 0u;
-        if (pb_now) group_done(br_now, rows_now);
+        if (FC && pb_now) group_done(br_now, rows_now);
     }
-    if (b.rb_done && pend_n) flush_done(pend_br, pend_n, pend_rows);
+    if (FC && pend_n) flush_done(pend_br, pend_n, pend_rows);
 }
 
 // Shared memory per SM is kept to what MINB CTAs need: the rest of the
@@ -1011,13 +1012,23 @@ bool staged(const hbp_format_t *f) { return f->n_hot > 0 && f->scol && f->hot_co
 
 // a warm tier (XM | 32) costs an address/policy select per gather, so it has
 // its own instantiation
-#define HBP_STREAM_DISPATCH(FN, V, EXACT, ...)                                              \
+// The fused combine (XM | 512) and the warm tier (XM | 32) each have their
+// own instantiation of the default variant: their bookkeeping would cost the
+// direct-mode kernel registers (spills) it does not need.
+#define HBP_STREAM_DISPATCH(FN, V, EXACT, FUSED, ...)                                       \
     if (staged(f)) {                                                                        \
+        if (FUSED && f->n_warm > 0) {                                                       \
+            HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, 0, kHotThreads, 1, 53 | 512, __VA_ARGS__); \
+        }                                                                                   \
+        if (FUSED) {                                                                        \
+            HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, 0, kHotThreads, 1, 21 | 512, __VA_ARGS__); \
+        }                                                                                   \
         if (f->n_warm > 0) {                                                                \
             HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, 0, kHotThreads, 1, 53, __VA_ARGS__);    \
         }                                                                                   \
         HBP_VARIANTS(FN, V, EXACT, true, kHotThreads, 1, __VA_ARGS__)                       \
     }                                                                                       \
+    if (FUSED) { HBP_VARIANT_X(FN, V, EXACT, false, 128, 4, 0, 256, 3, 21 | 512, __VA_ARGS__); } \
     HBP_VARIANTS(FN, V, EXACT, false, 256, 3, __VA_ARGS__)
 
 template <typename V, int CH, int NB, int MINB, int NT, int GD>
@@ -1039,7 +1050,7 @@ int hot_ring_bytes(size_t *out) {  // shared memory of the staged launch's rings
 
 template <typename V, bool EXACT>
 int occupancy(const hbp_format_t *f, int *per_sm, int *warps_per_cta) {
-    HBP_STREAM_DISPATCH(occupancy_of, V, EXACT, f, per_sm, warps_per_cta)
+    HBP_STREAM_DISPATCH(occupancy_of, V, EXACT, false, f, per_sm, warps_per_cta)
 }
 
 template <typename V>
@@ -1065,7 +1076,7 @@ int run(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y, 
         const int rc = hot_gather<V>(x, f->hot_cols, f->n_hot + f->n_warm, b->x_hot, st);
         if (rc) return rc;
     }
-    HBP_STREAM_DISPATCH(launch, V, EXACT, f, b, x, y, partial, st)
+    HBP_STREAM_DISPATCH(launch, V, EXACT, (b->rb_done != nullptr), f, b, x, y, partial, st)
 }
 
 }  // namespace
