@@ -148,6 +148,7 @@ def test_stream_fused_combine(dtype, C, workers, monkeypatch):
     hbp = _hbp(rows, cols, r, c, v.astype(dtype), C=C)
     x = torch.as_tensor(np.random.default_rng(3).uniform(-1, 1, cols).astype(dtype),
                         device="cuda")
+    monkeypatch.setenv("HBP_FUSED_COMBINE", "1")
     fused = H.SpmvOperator(hbp, workers=workers, hot=False)
     assert fused.fused_combine
     monkeypatch.setenv("HBP_FUSED_COMBINE", "0")
