@@ -333,18 +333,21 @@ def run_gpu(args):
         y = y_pad[:rows]
         cur = [0]
 
+        sq = torch.zeros(1, dtype=torch.float64, device=dev)
+        sq_scratch = torch.empty(1024, dtype=torch.float64, device=dev)
+
         def step():
             x = xs[cur[0]]
             op(x[:cols], y)
-            sq = torch.linalg.vector_norm(y, dtype=torch.float64).square().reshape(1)
+            H.sumsq(y, sq, sq_scratch)          # ||y_local||^2 (hbp_sumsq, f64)
             if dist:
                 dist.all_reduce(sq)
-            y.mul_(torch.rsqrt(sq).to(vdt))
             nxt = xs[1 - cur[0]]
             if dist:
+                H.scale(y, sq, y)                # y / ||y|| in place, then all-gather
                 dist.all_gather_into_tensor(nxt, y_pad)
             else:
-                nxt[:rows].copy_(y)
+                H.scale(y, sq, nxt[:rows])       # straight into the next x
             cur[0] = 1 - cur[0]
         x_res = lambda: xs[cur[0]][:cols]  # noqa: E731
     else:
@@ -521,7 +524,7 @@ def run_gpu(args):
     if os.path.exists(prof):
         with open(prof) as fh:
             traffic = json.load(fh).get(args.config, {}).get("dram_bytes_per_launch")
-    launches_step = op.launches_per_call
+    launches_step = op.launches_per_call + (3 if iterated else 0)  # + sumsq (2) + scale
     out = {
         "metric": METRIC, "value": round(gflops, 3), "unit": UNIT, "n_gpus": world,
         "steps": K, "warmup": args.warmup, "ms_per_step": round(per_step_ms, 5),
@@ -551,7 +554,7 @@ def run_gpu(args):
                      "algorithmic_bytes": b_alg, "peak_source": peak_src,
                      "kernel_ms": round(spmv_ms, 5),
                      "kernel": f"k_spmv_{op.schedule}" + (" (+ hot-column gather)" if op.hot is not None else "")
-                     + ("" if launches_step == 1 + (op.hot is not None) else " (+ combine/zero launch)")},
+                     + ("" if op.launches_per_call == 1 + (op.hot is not None) else " (+ combine/zero launch)")},
         "e2e": {"value": round(2.0 * total_nnz / (e2e_ms * 1e-3) / 1e9, 3), "unit": UNIT,
                 "h2d_bytes_per_step": cols * esz, "d2h_bytes_per_step": rows * esz,
                 "ms_per_step": round(e2e_ms, 4),

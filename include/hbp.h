@@ -367,6 +367,17 @@ int hbp_expand_partial(const hbp_format_t *f, const double *partial, double *par
 int hbp_to_triplets(const hbp_format_t *f, int64_t *row_out, int64_t *col_out, void *val_out,
                     hbp_stream_t stream);
 
+/* ------------------------------------------------ iterated SpMV (cfg5) */
+/* Power iteration x <- A x / ||A x||_2 (the reference has no iterated path;
+ * SURVEY.md §8(e) config 5).  hbp_sumsq: out[0] = sum y_i^2 in f64,
+ * deterministic; scratch holds hbp_sumsq_scratch() doubles.  hbp_scale:
+ * out_i = y_i * (V)(1 / sqrt(sumsq[0])), sumsq read on the device (after an
+ * optional all-reduce), out may alias y. */
+int hbp_sumsq(const void *y, int dtype, int64_t n, double *scratch, double *out,
+              hbp_stream_t stream);
+int hbp_sumsq_scratch(int64_t *doubles);
+int hbp_scale(const void *y, int dtype, int64_t n, const double *sumsq, void *out,
+              hbp_stream_t stream);
 #ifdef __cplusplus
 }
 #endif

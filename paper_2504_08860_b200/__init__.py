@@ -27,7 +27,7 @@ from .hbp import (HbpFormatError, HbpMatrix, build_hbp, deserialize_hbp, hbp_to_
                   load_hbp, save_hbp, serialize_hbp)
 from .engine import (ExecutionLog, ExecutionPlan, HostPipeline, PartialVector, SpmvOperator,
                      block2d_spmv_baseline, block_spmv, combine, hbp_spmv, plan_execution,
-                     run_spmv)
+                     run_spmv, scale, sumsq)
 from .metrics import (BenchReport, GroupStats, GroupStatsTable, Timing, gflops, group_stats,
                       group_stats_csv, mean_group_std, reduction_summary, time_kernel)
 
@@ -37,7 +37,7 @@ __all__ = [
     "BUCKET_MAX", "BlockGrid", "BlockPermutations", "CsrMatrix", "ExecutionLog",
     "ExecutionPlan", "HashParams", "HostPipeline", "HbpFormatError", "HbpMatrix", "OpCounter", "PartialVector",
     "PartitionConfig", "SpmvOperator", "TripletMatrix", "block2d_spmv_baseline", "block_rows_of",
-    "block_spmv", "csr_spmv",
+    "block_spmv", "csr_spmv", "scale", "sumsq",
     "build_block_permutation", "build_hbp", "combine", "coo_to_csr", "csr_to_triplets",
     "deserialize_hbp", "hash_permutations", "hash_slot", "hbp_spmv", "hbp_to_triplets",
     "identity_permutations", "load_hbp", "make_grid", "perm_for_block", "plan_execution",

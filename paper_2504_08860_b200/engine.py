@@ -25,6 +25,7 @@ from .hbp import HbpMatrix
 from .partition import BlockGrid, PartitionConfig
 
 __all__ = ["ExecutionPlan", "PartialVector", "ExecutionLog", "SpmvOperator", "plan_execution",
+           "sumsq", "scale",
            "block_spmv", "run_spmv", "combine", "hbp_spmv", "KIND_FIXED", "KIND_COMPETITIVE"]
 
 KIND_FIXED = 0
@@ -449,3 +450,22 @@ def hbp_spmv(hbp: HbpMatrix, x, workers: int | None = None) -> torch.Tensor:
         op = SpmvOperator(hbp, workers)
         hbp._ops[key] = op
     return op(xd)
+
+
+# ---- iterated SpMV helpers (config 5 power iteration; include/hbp.h hbp_sumsq / hbp_scale)
+def sumsq(y: torch.Tensor, out: torch.Tensor, scratch: torch.Tensor | None = None) -> torch.Tensor:
+    """out[0] = sum(y**2) in float64 on the device, deterministic."""
+    n = L.c_i64(0)
+    L.call("hbp_sumsq_scratch", ctypes.byref(n))
+    if scratch is None or scratch.numel() < n.value:
+        scratch = torch.empty(n.value, dtype=torch.float64, device=y.device)
+    L.call("hbp_sumsq", L.P(y), L.c_int(L.dtype_code(y.dtype)), L.c_i64(y.numel()), L.P(scratch),
+           L.P(out), L.stream())
+    return out
+
+
+def scale(y: torch.Tensor, sq: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+    """out = y / sqrt(sq[0]) (sq read on the device; out may be y)."""
+    L.call("hbp_scale", L.P(y), L.c_int(L.dtype_code(y.dtype)), L.c_i64(y.numel()), L.P(sq),
+           L.P(out), L.stream())
+    return out
