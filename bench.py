@@ -317,6 +317,21 @@ def run_gpu(args):
                    build=(t4 - t3) * 1e3, operator=(t5 - t4) * 1e3, total=(t5 - t0) * 1e3)
         if rep == 0:
             del op, hbp, perms, grid
+    # the paper's reordering comparison (Fig. 6/7 analogues): GPU time of
+    # the sort2D reorder beside the hash reorder, and the mean per-group std of lane
+    # counts (load imbalance) under no / hash / sort2D ordering
+    reorder = {"hash_ms": round(pre["hash"], 3)}
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    sperm = H.sort_permutations(grid)
+    torch.cuda.synchronize()
+    reorder["sort2d_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
+    gpc = -(-rows // R) * (R // 32)
+    if grid.num_col_blocks * gpc * 32 <= (1 << 27):
+        reorder["mean_group_std"] = {
+            name: round(H.mean_group_std(H.group_stats(grid, pm), 32), 4)
+            for name, pm in (("none", None), ("hash", perms), ("sort2d", sperm))}
+    del sperm
     esz = 4 if vdt == torch.float32 else 8
     x_host = np.random.default_rng(0).uniform(-1.0, 1.0, cols)  # cli.py:170-171
     stream = torch.cuda.current_stream()
@@ -564,6 +579,7 @@ def run_gpu(args):
         "gpu_launches": K * launches_step,
         "clocks": clk,
         "preprocess_ms": {k: round(v, 3) for k, v in pre.items()},
+        "reorder": reorder,
         "check": {"max_componentwise_err_vs_cusparse_f64": check, "zero_rows_exact": zero_ok,
                   "e2e_y_equals_device_y": e2e_ok},
     }
