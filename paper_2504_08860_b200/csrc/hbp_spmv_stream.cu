@@ -331,6 +331,13 @@ struct Ring {
     static constexpr int RMASK = NB * CH - 1;
     static constexpr int EPL = CH / 32;  // elements per lane per chunk
     static constexpr int NCOL = ColSlots<NB, GD>::value;
+    // f64 (XM & 2048): lane L owns elements 2L, 2L+1, 2L+64, 2L+65 of a chunk,
+    // so the product pass's 16-byte shared accesses are contiguous across lanes
+    // (4 instead of 8 wavefronts each); f32 keeps 4 consecutive per lane
+    static constexpr bool PAIR = sizeof(V) == 8 && EPL == 4 && GD == 0 && (XM & 2048) != 0;
+    __device__ __forceinline__ int elem_of(int e) const {
+        return PAIR ? 2 * lane + (e & 1) + 64 * (e >> 1) : EPL * lane + e;
+    }
     WarpSmem<V, CH, NB, GD> &S;
     const V *__restrict__ x;
     uint32_t hot_base = 0;  // shared address of the staged x (HOT)
@@ -360,7 +367,12 @@ struct Ring {
         mbar_wait(&S.mbar[slot], (uint32_t)((c / NB) & 1));
         uint32_t cc[EPL];
         const uint32_t *cs = &S.col[(c & (NCOL - 1)) * CH + EPL * lane];
-        if constexpr (EPL % 4 == 0) {
+        if constexpr (PAIR) {  // elements 2L, 2L+1, 2L+64, 2L+65
+            const uint32_t *cp = &S.col[(c & (NCOL - 1)) * CH + 2 * lane];
+            const uint2 t0 = *reinterpret_cast<const uint2 *>(cp);
+            const uint2 t1 = *reinterpret_cast<const uint2 *>(cp + 64);
+            cc[0] = t0.x, cc[1] = t0.y, cc[2] = t1.x, cc[3] = t1.y;
+        } else if constexpr (EPL % 4 == 0) {
 #pragma unroll
             for (int e = 0; e < EPL; e += 4) {
                 const uint4 t = *reinterpret_cast<const uint4 *>(cs + e);
@@ -377,7 +389,7 @@ struct Ring {
             const int32_t n = len32 - c * CH;
 #pragma unroll
             for (int e = 0; e < EPL; ++e)
-                if (EPL * lane + e >= n) cc[e] = 0u;
+                if (elem_of(e) >= n) cc[e] = 0u;
         }
         const uint64_t pl = policy_evict_last();
         if constexpr (GD > 0) {  // x replaces the columns in the slot
@@ -417,6 +429,18 @@ struct Ring {
 
     // chunk c (pending): values -> products (in place)
     __device__ __forceinline__ void finish(int32_t c) {
+        if constexpr (PAIR) {  // two conflict-free 16-byte accesses per lane
+            V *v = &S.val[(c & (NB - 1)) * CH + 2 * lane];
+            double2 t0 = *reinterpret_cast<double2 *>(v);
+            double2 t1 = *reinterpret_cast<double2 *>(v + 64);
+            t0.x = (double)product<V, EXACT>((V)t0.x, xr[0]);
+            t0.y = (double)product<V, EXACT>((V)t0.y, xr[1]);
+            t1.x = (double)product<V, EXACT>((V)t1.x, xr[2]);
+            t1.y = (double)product<V, EXACT>((V)t1.y, xr[3]);
+            *reinterpret_cast<double2 *>(v) = t0;
+            *reinterpret_cast<double2 *>(v + 64) = t1;
+            return;
+        }
         if constexpr (GD > 0) {  // this lane's gathers of chunk c are the oldest group
             cp_async_wait<GD - 1>();
             float *v = reinterpret_cast<float *>(&S.val[(c & (NB - 1)) * CH + EPL * lane]);
@@ -997,7 +1021,7 @@ bool staged(const hbp_format_t *f) { return f->n_hot > 0 && f->scol && f->hot_co
 // CTAs per SM MINB).  f64 data always uses the register-gather ring
 // (CH 128, NB 4, GD 0).  Staged (hot-column) launches use one CTA per SM.
 #define HBP_VARIANT(FN, V, EXACT, HOT, CH, NB, GD, NT, MINB, ...)                          \
-    HBP_VARIANT_X(FN, V, EXACT, HOT, CH, NB, GD, NT, MINB, 21, __VA_ARGS__)
+    HBP_VARIANT_X(FN, V, EXACT, HOT, CH, NB, GD, NT, MINB, 21 | 2048, __VA_ARGS__)
 #define HBP_VARIANT_X(FN, V, EXACT, HOT, CH, NB, GD, NT, MINB, XM, ...)                     \
     return FN<V, EXACT, (sizeof(V) == 4 ? CH : 128), (sizeof(V) == 4 ? NB : 4), MINB, XM,   \
               12, 4, NT, HOT, (sizeof(V) == 4 ? GD : 0)>(__VA_ARGS__)
@@ -1005,7 +1029,7 @@ bool staged(const hbp_format_t *f) { return f->n_hot > 0 && f->scol && f->hot_co
 #define HBP_VARIANTS(FN, V, EXACT, HOT, NTD, MINBD, ...)                                     \
     switch (variant()) {                                                                    \
         case 1: HBP_VARIANT_X(FN, V, EXACT, HOT, 128, 4, 0, NTD, MINBD, 29, __VA_ARGS__);      \
-        case 2: HBP_VARIANT(FN, V, EXACT, HOT, 128, 4, 0, (HOT ? 1024 : 256), (HOT ? 1 : 4), __VA_ARGS__); \
+        case 2: HBP_VARIANT_X(FN, V, EXACT, HOT, 128, 4, 0, NTD, MINBD, 21, __VA_ARGS__);      \
         case 3: HBP_VARIANT_X(FN, V, EXACT, HOT, 128, 4, 0, NTD, MINBD, 5, __VA_ARGS__);       \
         default: HBP_VARIANT(FN, V, EXACT, HOT, 128, 4, 0, NTD, MINBD, __VA_ARGS__);           \
     }
@@ -1018,17 +1042,17 @@ bool staged(const hbp_format_t *f) { return f->n_hot > 0 && f->scol && f->hot_co
 #define HBP_STREAM_DISPATCH(FN, V, EXACT, FUSED, ...)                                       \
     if (staged(f)) {                                                                        \
         if (FUSED && f->n_warm > 0) {                                                       \
-            HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, 0, kHotThreads, 1, 53 | 512, __VA_ARGS__); \
+            HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, 0, kHotThreads, 1, 53 | 512 | 2048, __VA_ARGS__); \
         }                                                                                   \
         if (FUSED) {                                                                        \
-            HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, 0, kHotThreads, 1, 21 | 512, __VA_ARGS__); \
+            HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, 0, kHotThreads, 1, 21 | 512 | 2048, __VA_ARGS__); \
         }                                                                                   \
         if (f->n_warm > 0) {                                                                \
-            HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, 0, kHotThreads, 1, 53, __VA_ARGS__);    \
+            HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, 0, kHotThreads, 1, 53 | 2048, __VA_ARGS__); \
         }                                                                                   \
         HBP_VARIANTS(FN, V, EXACT, true, kHotThreads, 1, __VA_ARGS__)                       \
     }                                                                                       \
-    if (FUSED) { HBP_VARIANT_X(FN, V, EXACT, false, 128, 4, 0, 256, 3, 21 | 512, __VA_ARGS__); } \
+    if (FUSED) { HBP_VARIANT_X(FN, V, EXACT, false, 128, 4, 0, 256, 3, 21 | 512 | 2048, __VA_ARGS__); } \
     HBP_VARIANTS(FN, V, EXACT, false, 256, 3, __VA_ARGS__)
 
 template <typename V, int CH, int NB, int MINB, int NT, int GD>
@@ -1042,7 +1066,7 @@ template <typename V>
 int hot_ring_bytes(size_t *out) {  // shared memory of the staged launch's rings
     switch (variant()) {
         case 1: return HBP_RING_BYTES(V, 128, 4, 0, kHotThreads);
-        case 2: return HBP_RING_BYTES(V, 128, 4, 0, 1024);
+        case 2: return HBP_RING_BYTES(V, 128, 4, 0, kHotThreads);
         case 3: return HBP_RING_BYTES(V, 128, 4, 0, kHotThreads);
         default: return HBP_RING_BYTES(V, 128, 4, 0, kHotThreads);
     }
