@@ -105,3 +105,35 @@ def test_rmat_csr_and_2d_baselines(rmat18):
     np.testing.assert_array_equal(y, want.astype(np.float32).astype(np.float64))
     y2 = H.block2d_spmv_baseline(m["csr"], m["grid"], x).cpu().numpy().astype(np.float64)
     np.testing.assert_array_equal(y2, want.astype(np.float32).astype(np.float64))
+
+
+@pytest.mark.parametrize("config", ["cfg2", "cfg5"])
+def test_full_scale_rmat_staging(config):
+    """BASELINE sizes (cfg2: 263M nnz, cfg5: 1.06B nnz, fp32): the staged
+    operator (hot tier, + warm tier on cfg5) is bitwise equal to the unstaged
+    one, and within 1e-5 componentwise of the f64 CSR reference (Alg. 1 on the
+    same fp32-rounded values and x), zero rows exact."""
+    import bench
+    dev = torch.device("cuda", 0)
+    desc, rows, cols, rp, col, val, C, vdt = bench.make_matrix_gpu(config, 0, dev)
+    cfg = H.PartitionConfig(col_width=C)
+    csr = H.CsrMatrix(rows, cols, rp, col, val)
+    grid = H.make_grid(csr, cfg)
+    hbp = H.build_hbp(csr, grid, H.hash_permutations(grid, H.sample_hash_params(grid, cfg)),
+                      with_add_sign=False, with_zero_row=False)
+    x = torch.as_tensor(np.random.default_rng(1).uniform(-1, 1, cols), device=dev).to(vdt)
+    staged = H.SpmvOperator(hbp)
+    assert staged.hot is not None and staged.hot.share > 0.1
+    if config == "cfg5":
+        assert staged.hot.n_warm > 0
+    y1 = staged(x)
+    y0 = H.SpmvOperator(hbp, hot=False)(x)
+    assert torch.equal(y0, y1)
+    c64 = H.CsrMatrix(rows, cols, rp, col, val.to(torch.float64))
+    ref = H.csr_spmv(c64, x.to(torch.float64))
+    scale = H.csr_spmv(H.CsrMatrix(rows, cols, rp, col, val.to(torch.float64).abs()),
+                       x.to(torch.float64).abs())
+    err = (y1.to(torch.float64) - ref).abs()
+    live = scale > 0
+    assert bool((err[~live] == 0).all())
+    assert float((err[live] / scale[live]).max()) <= 1e-5
