@@ -55,16 +55,17 @@ constexpr size_t kHotBudgetDefault = 131 * 1024;  // -> 132 KB carveout (sweep: 
 // Column slots: a chunk's columns are needed only until its gathers are
 // issued; while chunk ready+1 is started, chunks up to ready+NB-2 are in
 // flight, so NB-2 slots (rounded up to a power of two, >= 2) suffice.
-// With asynchronous gathers (GD > 0, f32) the slot keeps the chunk's columns
-// until they are replaced by the gathered x, so every chunk has its own slot.
-template <int NB, int GD>
+// Column slots: a chunk's columns are needed only until its gathers are
+// issued; while chunk ready+1 is started, chunks up to ready+NB-2 are in
+// flight, so NB-2 slots (rounded up to a power of two, >= 2) suffice.
+template <int NB>
 struct ColSlots {
-    static constexpr int value = GD > 0 ? NB : (NB <= 4 ? 2 : (NB <= 6 ? 4 : NB));
+    static constexpr int value = NB <= 4 ? 2 : (NB <= 6 ? 4 : NB);
 };
 
-template <typename V, int CH, int NB, int GD = 0>
+template <typename V, int CH, int NB>
 struct __align__(16) WarpSmem {
-    uint32_t col[ColSlots<NB, GD>::value * CH];  // columns, then x (GD > 0)
+    uint32_t col[ColSlots<NB>::value * CH];
     V val[NB * CH];  // values, then products in place
     uint32_t ph_mask[33];
     int32_t ph_off[33];
@@ -75,7 +76,7 @@ struct __align__(16) WarpSmem {
     int32_t len32;         // c_hi - base
     int32_t nchunks;
     int32_t ready;         // chunks <= ready hold products
-    int32_t pending;       // chunk whose x gathers are in flight (-1: none; GD = 0)
+    int32_t pending;       // chunk whose x gathers are in flight (-1: none)
     uint64_t pol_stream;   // L2 evict-first policy (element stream)
     uint64_t pol_x;        // L2 evict-last policy (x gathers; warm tier when staged)
     uint64_t pol_cold;     // L2 evict-normal policy (cold columns when staged)
@@ -117,21 +118,6 @@ __device__ __forceinline__ void fence_proxy_async() {
 }
 __device__ __forceinline__ void fence_mbar_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-// 4-byte asynchronous global -> shared copy (LDGSTS): the x gather lands in
-// shared memory without a destination register or scoreboard, so the walk
-// never waits on it implicitly; completion per thread via commit/wait_group.
-__device__ __forceinline__ void cp_async4(uint32_t dst, const void *src, uint64_t pol) {
-    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;" ::"r"(dst),
-                 "l"(src), "l"(pol)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-    asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -259,41 +245,6 @@ __device__ __forceinline__ double ld_x_staged(const double *x, uint32_t hot_base
     return v;
 }
 
-// XM = 2: the same gathers without an L2 cache-policy operand (no policy
-// register to materialise per load)
-__device__ __forceinline__ float ld_x_nh(const float *p) {
-    float v;
-    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
-    return v;
-}
-__device__ __forceinline__ double ld_x_nh(const double *p) {
-    double v;
-    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
-    return v;
-}
-__device__ __forceinline__ float ld_x_staged_nh(const float *x, uint32_t hot_base, uint32_t c) {
-    float v;
-    asm volatile(
-        "{\n.reg .pred p;\n"
-        "setp.lt.s32 p, %2, 0;\n"
-        "@p ld.shared.f32 %0, [%3];\n"
-        "@!p ld.global.nc.L1::no_allocate.f32 %0, [%1];\n}"
-        : "=f"(v)
-        : "l"(x + c), "r"(c), "r"(hot_base + ((c & 0x7fffffffu) << 2)));
-    return v;
-}
-__device__ __forceinline__ double ld_x_staged_nh(const double *x, uint32_t hot_base, uint32_t c) {
-    double v;
-    asm volatile(
-        "{\n.reg .pred p;\n"
-        "setp.lt.s32 p, %2, 0;\n"
-        "@p ld.shared.f64 %0, [%3];\n"
-        "@!p ld.global.nc.L1::no_allocate.f64 %0, [%1];\n}"
-        : "=d"(v)
-        : "l"(x + c), "r"(c), "r"(hot_base + ((c & 0x7fffffffu) << 3)));
-    return v;
-}
-
 // Staged gather (hot + warm tiers, hbp_hot.cu): HBP_HOT_FLAG | s reads the
 // CTA's shared copy, HBP_WARM_FLAG | w the compact warm copy xw[w] (L2
 // evict-last), anything else x[c] (L2 evict-normal); global loads skip L1.
@@ -324,27 +275,26 @@ __device__ __forceinline__ V ld_x_tiered(const V *x, const V *xw, uint32_t hot_b
     return v;
 }
 
-template <typename V, bool EXACT, int CH, int NB, int XM, bool HOT, int GD>
+template <typename V, bool EXACT, int CH, int NB, int XM, bool HOT>
 struct Ring {
     static_assert((NB & (NB - 1)) == 0 && (CH & (CH - 1)) == 0, "NB, CH: powers of two");
-    static_assert(GD == 0 || (sizeof(V) == 4 && GD < NB - 2), "async gathers: f32, GD < NB-2");
     static constexpr int RMASK = NB * CH - 1;
     static constexpr int EPL = CH / 32;  // elements per lane per chunk
-    static constexpr int NCOL = ColSlots<NB, GD>::value;
+    static constexpr int NCOL = ColSlots<NB>::value;
     // f64 (XM & 2048): lane L owns elements 2L, 2L+1, 2L+64, 2L+65 of a chunk,
     // so the product pass's 16-byte shared accesses are contiguous across lanes
     // (4 instead of 8 wavefronts each); f32 keeps 4 consecutive per lane
-    static constexpr bool PAIR = sizeof(V) == 8 && EPL == 4 && GD == 0 && (XM & 2048) != 0;
+    static constexpr bool PAIR = sizeof(V) == 8 && EPL == 4 && (XM & 2048) != 0;
     __device__ __forceinline__ int elem_of(int e) const {
         return PAIR ? 2 * lane + (e & 1) + 64 * (e >> 1) : EPL * lane + e;
     }
-    WarpSmem<V, CH, NB, GD> &S;
+    WarpSmem<V, CH, NB> &S;
     const V *__restrict__ x;
     uint32_t hot_base = 0;  // shared address of the staged x (HOT)
     const V *xw = nullptr;  // warm tier (HOT)
     int32_t res32 = 0;  // products resident for offsets < res32
     int lane;
-    V xr[GD > 0 ? 1 : EPL];  // gathered x of the pending chunk (GD = 0)
+    V xr[EPL];          // gathered x of the pending chunk
 
     // lane 0: bulk-copy chunk c (< nchunks) into its slot
     __device__ __forceinline__ void issue(int32_t c, int32_t nchunks, int32_t len32) {
@@ -392,22 +342,7 @@ struct Ring {
                 if (elem_of(e) >= n) cc[e] = 0u;
         }
         const uint64_t pl = policy_evict_last();
-        if constexpr (GD > 0) {  // x replaces the columns in the slot
-            const uint32_t dst = smem_addr(cs);
-#pragma unroll
-            for (int e = 0; e < EPL; ++e) {
-                if (HOT && (int32_t)cc[e] < 0) {
-                    float hv;
-                    asm volatile("ld.shared.f32 %0, [%1];"
-                                 : "=f"(hv)
-                                 : "r"(hot_base + ((cc[e] & 0x7fffffffu) << 2)));
-                    reinterpret_cast<float *>(const_cast<uint32_t *>(cs))[e] = hv;
-                } else {
-                    cp_async4(dst + 4 * e, x + cc[e], pl);
-                }
-            }
-            cp_async_commit();
-        } else {
+        {
 #pragma unroll
             for (int e = 0; e < EPL; ++e) {
                 constexpr int XG = XM & 3;
@@ -419,9 +354,7 @@ struct Ring {
                     xr[e] = hv;
                 } else if constexpr (HOT && (XM & 32) != 0) {  // + warm tier
                     xr[e] = ld_x_tiered(x, xw, hot_base, cc[e], pl, S.pol_cold);
-                } else if constexpr (HOT) xr[e] = XG == 2 ? ld_x_staged_nh(x, hot_base, cc[e])
-                                                   : ld_x_staged(x, hot_base, cc[e], pl);
-                else if constexpr (XG == 2) xr[e] = ld_x_nh(x + cc[e]);
+                } else if constexpr (HOT) xr[e] = ld_x_staged(x, hot_base, cc[e], pl);
                 else xr[e] = XG ? ld_x_na(x + cc[e], pl) : ld_x(x + cc[e], pl);
             }
         }
@@ -439,29 +372,6 @@ struct Ring {
             t1.y = (double)product<V, EXACT>((V)t1.y, xr[3]);
             *reinterpret_cast<double2 *>(v) = t0;
             *reinterpret_cast<double2 *>(v + 64) = t1;
-            return;
-        }
-        if constexpr (GD > 0) {  // this lane's gathers of chunk c are the oldest group
-            cp_async_wait<GD - 1>();
-            float *v = reinterpret_cast<float *>(&S.val[(c & (NB - 1)) * CH + EPL * lane]);
-            const float *xs = reinterpret_cast<const float *>(&S.col[(c & (NB - 1)) * CH + EPL * lane]);
-            if constexpr (EPL % 4 == 0) {
-#pragma unroll
-                for (int e = 0; e < EPL; e += 4) {
-                    float4 t = *reinterpret_cast<float4 *>(v + e);
-                    const float4 u = *reinterpret_cast<const float4 *>(xs + e);
-                    t.x *= u.x, t.y *= u.y, t.z *= u.z, t.w *= u.w;
-                    *reinterpret_cast<float4 *>(v + e) = t;
-                }
-            } else if constexpr (EPL == 2) {
-                float2 t = *reinterpret_cast<float2 *>(v);
-                const float2 u = *reinterpret_cast<const float2 *>(xs);
-                t.x *= u.x, t.y *= u.y;
-                *reinterpret_cast<float2 *>(v) = t;
-            } else {
-#pragma unroll
-                for (int e = 0; e < EPL; ++e) v[e] *= xs[e];
-            }
             return;
         }
         V *v = &S.val[(c & (NB - 1)) * CH + EPL * lane];
@@ -495,39 +405,9 @@ struct Ring {
     }
 
     // make offsets < need resident (warp-uniform); refills the ring
-    // GD > 0: chunks ready+1 .. ready+GD have gathers in flight (one commit
-    // group each; empty groups past the end keep the count uniform)
-    __device__ __forceinline__ void prime(int32_t nchunks, int32_t len32) {
-        if constexpr (GD > 0) {
-#pragma unroll
-            for (int c = 0; c < GD; ++c) {
-                if (c < nchunks) start(c, nchunks, len32);
-                else cp_async_commit();
-            }
-        }
-    }
-
     __device__ __forceinline__ void advance(int32_t need) {
         if (need <= res32) return;
         const int32_t nchunks = S.nchunks, len32 = S.len32;
-        if constexpr (GD > 0) {
-            int32_t ready = S.ready;
-            while (need > res32 && ready + 1 < nchunks) {
-                finish(ready + 1);  // own elements only: no cross-lane dependency
-                ++ready;
-                res32 = (ready * CH + CH < len32 ? ready * CH + CH : len32);
-                fence_proxy_async();  // ring accesses precede later bulk writes
-                __syncwarp();         // products visible; walk reads of old slots done
-                // the slot of chunk ready - 2 is free (the walk may still read
-                // ready - 1 for a step straddling the boundary)
-                if (lane == 0 && ready + NB - 2 < nchunks) issue(ready + NB - 2, nchunks, len32);
-                if (ready + GD < nchunks) start(ready + GD, nchunks, len32);
-                else cp_async_commit();
-            }
-            if (lane == 0) S.ready = ready;
-            __syncwarp();
-            return;
-        }
         int32_t ready = S.ready, pending = S.pending;
         while (need > res32) {
             if (pending < 0) {
@@ -689,7 +569,7 @@ __device__ __forceinline__ double walk_fast(RingT &ring, const uint2 ph, const i
 }
 
 template <typename V, bool EXACT, int CH, int NB, int MINB, int XM, int KT, int LMIN, int NT,
-          bool HOT, int GD>
+          bool HOT>
 __global__ void __launch_bounds__(NT, MINB)
     k_spmv_stream(const hbp_format_t f, const hbp_balanced_t b, const V *__restrict__ x,
                   V *__restrict__ y, double *__restrict__ partial) {
@@ -707,7 +587,7 @@ __global__ void __launch_bounds__(NT, MINB)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
-    using Smem = WarpSmem<V, CH, NB, GD>;
+    using Smem = WarpSmem<V, CH, NB>;
     Smem &S = reinterpret_cast<Smem *>(smem_raw)[wib];
     V *const hot = reinterpret_cast<V *>(smem_raw + sizeof(Smem) * kWarps);
     if constexpr (HOT) {  // stage x at the hot columns (b.x_hot, hbp_hot_gather)
@@ -736,7 +616,7 @@ __global__ void __launch_bounds__(NT, MINB)
         stream_slice(gs, ngroups, E, w, Nw, EXACT, &c_lo, &c_hi, &g);
     }
     const int64_t base = c_lo & ~(int64_t)3;
-    Ring<V, EXACT, CH, NB, XM, HOT, GD> ring{S, x};
+    Ring<V, EXACT, CH, NB, XM, HOT> ring{S, x};
     ring.lane = lane;
     if constexpr (HOT) {
         ring.hot_base = smem_addr(hot);
@@ -760,7 +640,6 @@ __global__ void __launch_bounds__(NT, MINB)
         for (int c = 0; c <= NB - 3 && c < nchunks; ++c) ring.issue(c, nchunks, len32);
     }
     __syncwarp();
-    ring.prime(c_hi > c_lo ? (len32 + CH - 1) / CH : 0, len32);
 
     const bool last_warp = (w == Nw - 1);
     // output position of group g: nonzero block blk, group gi within it
@@ -968,35 +847,35 @@ void set_attributes(K kernel, size_t smem, int minb) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
 }
 
-template <typename V, int CH, int NB, int NT, int GD>
+template <typename V, int CH, int NB, int NT>
 constexpr size_t ring_smem() {
-    return sizeof(WarpSmem<V, CH, NB, GD>) * (NT / 32);
+    return sizeof(WarpSmem<V, CH, NB>) * (NT / 32);
 }
 
 template <typename V, bool EXACT, int CH, int NB, int MINB, int XM, int KT, int LMIN, int NT,
-          bool HOT, int GD>
+          bool HOT>
 int launch(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y,
            double *partial, cudaStream_t st) {
-    const size_t smem = ring_smem<V, CH, NB, NT, GD>() + (HOT ? (size_t)f->n_hot * sizeof(V) : 0);
+    const size_t smem = ring_smem<V, CH, NB, NT>() + (HOT ? (size_t)f->n_hot * sizeof(V) : 0);
     static size_t attr = 0;
     if (attr != smem) {
-        set_attributes(k_spmv_stream<V, EXACT, CH, NB, MINB, XM, KT, LMIN, NT, HOT, GD>, smem, MINB);
+        set_attributes(k_spmv_stream<V, EXACT, CH, NB, MINB, XM, KT, LMIN, NT, HOT>, smem, MINB);
         attr = smem;
     }
     unsigned grid = (unsigned)((b->workers + NT / 32 - 1) / (NT / 32));
-    k_spmv_stream<V, EXACT, CH, NB, MINB, XM, KT, LMIN, NT, HOT, GD><<<grid, NT, smem, st>>>(
+    k_spmv_stream<V, EXACT, CH, NB, MINB, XM, KT, LMIN, NT, HOT><<<grid, NT, smem, st>>>(
         *f, *b, (const V *)x, (V *)y, partial);
     return (int)cudaGetLastError();
 }
 
 template <typename V, bool EXACT, int CH, int NB, int MINB, int XM, int KT, int LMIN, int NT,
-          bool HOT, int GD>
+          bool HOT>
 int occupancy_of(const hbp_format_t *f, int *per_sm, int *warps_per_cta) {
-    const size_t smem = ring_smem<V, CH, NB, NT, GD>() + (HOT ? (size_t)f->n_hot * sizeof(V) : 0);
-    set_attributes(k_spmv_stream<V, EXACT, CH, NB, MINB, XM, KT, LMIN, NT, HOT, GD>, smem, MINB);
+    const size_t smem = ring_smem<V, CH, NB, NT>() + (HOT ? (size_t)f->n_hot * sizeof(V) : 0);
+    set_attributes(k_spmv_stream<V, EXACT, CH, NB, MINB, XM, KT, LMIN, NT, HOT>, smem, MINB);
     *warps_per_cta = NT / 32;
     return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        per_sm, k_spmv_stream<V, EXACT, CH, NB, MINB, XM, KT, LMIN, NT, HOT, GD>, NT, smem);
+        per_sm, k_spmv_stream<V, EXACT, CH, NB, MINB, XM, KT, LMIN, NT, HOT>, NT, smem);
 }
 
 // Tile / occupancy variants (chunk CH, ring slots NB, min CTAs per SM,
@@ -1017,21 +896,21 @@ int variant() {
 
 bool staged(const hbp_format_t *f) { return f->n_hot > 0 && f->scol && f->hot_cols; }
 
-// One variant = (chunk CH, ring slots NB, gather distance GD, threads NT,
+// One variant = (chunk CH, ring slots NB, threads NT,
 // CTAs per SM MINB).  f64 data always uses the register-gather ring
-// (CH 128, NB 4, GD 0).  Staged (hot-column) launches use one CTA per SM.
-#define HBP_VARIANT(FN, V, EXACT, HOT, CH, NB, GD, NT, MINB, ...)                          \
-    HBP_VARIANT_X(FN, V, EXACT, HOT, CH, NB, GD, NT, MINB, 21 | 2048, __VA_ARGS__)
-#define HBP_VARIANT_X(FN, V, EXACT, HOT, CH, NB, GD, NT, MINB, XM, ...)                     \
+// (CH 128, NB 4).  Staged (hot-column) launches use one CTA per SM.
+#define HBP_VARIANT(FN, V, EXACT, HOT, CH, NB, NT, MINB, ...)                              \
+    HBP_VARIANT_X(FN, V, EXACT, HOT, CH, NB, NT, MINB, 21 | 2048, __VA_ARGS__)
+#define HBP_VARIANT_X(FN, V, EXACT, HOT, CH, NB, NT, MINB, XM, ...)                         \
     return FN<V, EXACT, (sizeof(V) == 4 ? CH : 128), (sizeof(V) == 4 ? NB : 4), MINB, XM,   \
-              12, 4, NT, HOT, (sizeof(V) == 4 ? GD : 0)>(__VA_ARGS__)
+              12, 4, NT, HOT>(__VA_ARGS__)
 
 #define HBP_VARIANTS(FN, V, EXACT, HOT, NTD, MINBD, ...)                                     \
     switch (variant()) {                                                                    \
-        case 1: HBP_VARIANT_X(FN, V, EXACT, HOT, 128, 4, 0, NTD, MINBD, 29, __VA_ARGS__);      \
-        case 2: HBP_VARIANT_X(FN, V, EXACT, HOT, 128, 4, 0, NTD, MINBD, 21, __VA_ARGS__);      \
-        case 3: HBP_VARIANT_X(FN, V, EXACT, HOT, 128, 4, 0, NTD, MINBD, 5, __VA_ARGS__);       \
-        default: HBP_VARIANT(FN, V, EXACT, HOT, 128, 4, 0, NTD, MINBD, __VA_ARGS__);           \
+        case 1: HBP_VARIANT_X(FN, V, EXACT, HOT, 128, 4, NTD, MINBD, 29, __VA_ARGS__);      \
+        case 2: HBP_VARIANT_X(FN, V, EXACT, HOT, 128, 4, NTD, MINBD, 21, __VA_ARGS__);      \
+        case 3: HBP_VARIANT_X(FN, V, EXACT, HOT, 128, 4, NTD, MINBD, 5, __VA_ARGS__);       \
+        default: HBP_VARIANT(FN, V, EXACT, HOT, 128, 4, NTD, MINBD, __VA_ARGS__);           \
     }
 
 // a warm tier (XM | 32) costs an address/policy select per gather, so it has
@@ -1042,34 +921,28 @@ bool staged(const hbp_format_t *f) { return f->n_hot > 0 && f->scol && f->hot_co
 #define HBP_STREAM_DISPATCH(FN, V, EXACT, FUSED, ...)                                       \
     if (staged(f)) {                                                                        \
         if (FUSED && f->n_warm > 0) {                                                       \
-            HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, 0, kHotThreads, 1, 53 | 512 | 2048, __VA_ARGS__); \
+            HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, kHotThreads, 1, 53 | 512 | 2048, __VA_ARGS__); \
         }                                                                                   \
         if (FUSED) {                                                                        \
-            HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, 0, kHotThreads, 1, 21 | 512 | 2048, __VA_ARGS__); \
+            HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, kHotThreads, 1, 21 | 512 | 2048, __VA_ARGS__); \
         }                                                                                   \
         if (f->n_warm > 0) {                                                                \
-            HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, 0, kHotThreads, 1, 53 | 2048, __VA_ARGS__); \
+            HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, kHotThreads, 1, 53 | 2048, __VA_ARGS__); \
         }                                                                                   \
         HBP_VARIANTS(FN, V, EXACT, true, kHotThreads, 1, __VA_ARGS__)                       \
     }                                                                                       \
-    if (FUSED) { HBP_VARIANT_X(FN, V, EXACT, false, 128, 4, 0, 256, 3, 21 | 512 | 2048, __VA_ARGS__); } \
+    if (FUSED) { HBP_VARIANT_X(FN, V, EXACT, false, 128, 4, 256, 3, 21 | 512 | 2048, __VA_ARGS__); } \
     HBP_VARIANTS(FN, V, EXACT, false, 256, 3, __VA_ARGS__)
 
-template <typename V, int CH, int NB, int MINB, int NT, int GD>
+template <typename V, int CH, int NB, int MINB, int NT>
 int ring_bytes(size_t *out) {
-    *out = ring_smem<V, (sizeof(V) == 4 ? CH : 128), (sizeof(V) == 4 ? NB : 4), NT,
-                     (sizeof(V) == 4 ? GD : 0)>();
+    *out = ring_smem<V, (sizeof(V) == 4 ? CH : 128), (sizeof(V) == 4 ? NB : 4), NT>();
     return 0;
 }
-#define HBP_RING_BYTES(V, CH, NB, GD, NT) ring_bytes<V, CH, NB, 1, NT, GD>(out)
+#define HBP_RING_BYTES(V, CH, NB, NT) ring_bytes<V, CH, NB, 1, NT>(out)
 template <typename V>
 int hot_ring_bytes(size_t *out) {  // shared memory of the staged launch's rings
-    switch (variant()) {
-        case 1: return HBP_RING_BYTES(V, 128, 4, 0, kHotThreads);
-        case 2: return HBP_RING_BYTES(V, 128, 4, 0, kHotThreads);
-        case 3: return HBP_RING_BYTES(V, 128, 4, 0, kHotThreads);
-        default: return HBP_RING_BYTES(V, 128, 4, 0, kHotThreads);
-    }
+    return HBP_RING_BYTES(V, 128, 4, kHotThreads);  // the same ring for every variant
 }
 
 template <typename V, bool EXACT>
