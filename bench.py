@@ -211,7 +211,22 @@ def cpu_reference(cfg_name: str, steps: int, warmup: int, seed: int = 0):
             break
     t = statistics.median(times)
     nnz = int(rp[-1])
+    # the reference also at 1 and 4 workers (it regresses past 4
+    # with Python threads; the C port's threads do not) -- informational
+    by_workers = {}
+    for wk in (1, 4):
+        pl = O.plan_execution(grid.block_nnz, 0.7, wk)
+        O.run_spmv(h, x, pl, wk)
+        ts = []
+        for _ in range(3):
+            a = time.perf_counter()
+            part, _ = O.run_spmv(h, x, pl, wk)
+            O.combine(part, rows, h.ncb)
+            ts.append(time.perf_counter() - a)
+        by_workers[str(wk)] = round(2.0 * nnz / statistics.median(ts) / 1e9, 3)
+    by_workers[str(workers)] = round(2.0 * nnz / t / 1e9, 3)
     return dict(value=2.0 * nnz / t / 1e9, unit=UNIT, cores=workers, kind="port",
+                gflops_by_workers=by_workers,
                 sample=f"{sample}: {rows} rows, {nnz} nnz, median of {len(times)} SpMV+combine",
                 ms_per_step=t * 1e3, nnz=nnz, rows=rows,
                 preprocess_ms=dict(grid=(t1 - t0) * 1e3, sample=(t2 - t1) * 1e3,
@@ -587,7 +602,8 @@ def run_gpu(args):
         out["baselines_same_gpu"] = baselines
     if world == 1 and not args.no_cpu_baseline:
         cb = cpu_reference(args.config, steps=5, warmup=1)
-        out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample",
+                                                   "gflops_by_workers")}
         out["cpu_baseline"]["preprocess_ms"] = {k: round(v, 1)
                                                 for k, v in cb["preprocess_ms"].items()}
         # SURVEY.md §8(d) gate: GPU preprocess vs one CPU reference SpMV of the
