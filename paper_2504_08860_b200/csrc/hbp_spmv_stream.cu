@@ -1062,6 +1062,7 @@ int hbp_spmv_stream(const hbp_format_t *f, const hbp_balanced_t *b, const void *
         if (rc) return rc;
         if (f->n_hot > cap || (f->n_hot & 3) || !b->x_hot) return HBP_E_ARG;
         if (f->n_warm < 0 || (f->n_warm > 0 && f->cols > (int64_t)1 << 30)) return HBP_E_ARG;
+        if (f->cols >= (int64_t)1 << 31) return HBP_E_ARG;  // bit 31 flags hot columns
     }
     cudaStream_t st = as_stream(stream);
     if (f->dtype == HBP_F64)

@@ -178,6 +178,8 @@ class SpmvOperator:
                 if warm_bytes is None else int(warm_bytes)
             cap = hbp.hot_capacity()
             n = (cap if n_hot is None else min(n_hot, cap)) & ~3
+            if hbp.cols >= (1 << 31):
+                n = 0
             if n > 0 and (hot is not None or hbp.column_share(n) >= self.HOT_MIN_SHARE):
                 self.hot = hbp.hot_columns(n_hot, max(0, wb) // hbp.data.element_size())
                 self.hot.apply(f)

@@ -157,6 +157,8 @@ class HbpMatrix:
         cap = self.hot_capacity()
         n = cap if n_hot is None else min(int(n_hot), cap)
         n = max(0, min(n, self.cols)) & ~3
+        if self.cols >= (1 << 31):  # the staged stream flags hot columns with bit 31
+            n = 0
         nw = max(0, min(int(n_warm), self.cols - n)) if self.cols <= (1 << 30) else 0
         key = ("hot", n, nw)
         if key in self._ops:
