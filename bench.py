@@ -443,7 +443,7 @@ def run_gpu(args):
     # ---- end to end through the public API with host buffers (HostPipeline:
     # x_i H2D, SpMV, y_i D2H on 2 rotating streams; every step moves its own
     # x in and y out).  With an L2 flush, steps run one at a time instead.
-    depth = 1 if flush else 2
+    depth = 1 if flush else int(os.environ.get("HBP_PIPE_DEPTH", "3"))
     pipe = H.HostPipeline(hbp, depth=depth, schedule=args.schedule, hot=hot_arg,
                           workers=args.workers)
     xh = torch.as_tensor(x_host).to(vdt).pin_memory()
@@ -590,7 +590,7 @@ def run_gpu(args):
                 "ms_per_step": round(e2e_ms, 4),
                 "how": ("HostPipeline (copy-in / compute / copy-out streams): pinned x H2D, SpMV, y D2H per step"
                         + (" (one step at a time, L2 flushed)" if flush
-                           else ", double-buffered"))},
+                           else f", {depth} buffers in flight"))},
         "gpu_launches": K * launches_step,
         "clocks": clk,
         "preprocess_ms": {k: round(v, 3) for k, v in pre.items()},
