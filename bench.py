@@ -614,6 +614,13 @@ def run_gpu(args):
             "cpu_reference_spmv_ms_scaled_to_workload": round(
                 cb["ms_per_step"] * (nnz_global if strong else nnz) / cb["nnz"], 1),
             "cpu_reference_preprocess_ms_on_sample": round(cb["preprocess_ms"]["total"], 1),
+            # linear in nnz (the reference's grid / hash / build passes are)
+            "cpu_reference_preprocess_ms_scaled_to_workload": round(
+                cb["preprocess_ms"]["total"] * (nnz_global if strong else nnz) / cb["nnz"], 1),
+            "speedup_vs_cpu_reference_preprocess": round(
+                cb["preprocess_ms"]["total"] * (nnz_global if strong else nnz) / cb["nnz"]
+                / pre["total"], 1),
+            "gpu_preprocess_in_gpu_spmvs": round(pre["total"] / per_step_ms, 2),
             "gpu_preprocess_faster_than_one_cpu_spmv":
                 pre["total"] < cb["ms_per_step"] * (nnz_global if strong else nnz) / cb["nnz"]}
     if dist:
