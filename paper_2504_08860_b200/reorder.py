@@ -13,7 +13,6 @@ indexing behave as in the reference.
 """
 from __future__ import annotations
 
-import ctypes
 import math
 from dataclasses import dataclass
 
