@@ -177,12 +177,14 @@ class SpmvOperator:
             wb = (0 if fits else int(os.environ.get("HBP_WARM_BYTES", self.WARM_BYTES))) \
                 if warm_bytes is None else int(warm_bytes)
             cap = hbp.hot_capacity()
-            n = (cap if n_hot is None else min(n_hot, cap)) & ~3
+            n = min(cap if n_hot is None else min(n_hot, cap), hbp.cols) & ~3
             if hbp.cols >= (1 << 31):
                 n = 0
             if n > 0 and (hot is not None or hbp.column_share(n) >= self.HOT_MIN_SHARE):
-                self.hot = hbp.hot_columns(n_hot, max(0, wb) // hbp.data.element_size())
-                self.hot.apply(f)
+                hc = hbp.hot_columns(n_hot, max(0, wb) // hbp.data.element_size())
+                if hc.n_hot > 0:
+                    self.hot = hc
+                    hc.apply(f)
                 f.cold_last = int(fits)
         if schedule in ("balanced", "stream"):
             if workers is None:

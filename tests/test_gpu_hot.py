@@ -178,3 +178,37 @@ def test_col_degree_sampled(mat, stride):
            L.stream())
     col = hbp.col.cpu().numpy().view(np.uint32)
     np.testing.assert_array_equal(deg.cpu().numpy(), np.bincount(col[::stride], minlength=cols))
+
+
+@pytest.mark.parametrize("rows,cols,per_row", [(1, 1, 1), (5, 3, 2), (31, 7, 3), (33, 4, 4),
+                                               (1000, 5, 3), (700, 64, 40)])
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_staging_tiny_shapes(rows, cols, per_row, dtype):
+    """Few columns (all of them hot, or fewer than 4 -> no staging), short row
+    blocks, dense rows: staged == unstaged bitwise, and the oracle."""
+    rng = np.random.default_rng(rows * 31 + cols)
+    lens = np.minimum(rng.integers(0, per_row + 1, rows), cols)
+    r = np.repeat(np.arange(rows), lens)
+    c = np.concatenate([rng.choice(cols, k, replace=False) for k in lens]) if r.size else \
+        np.zeros(0, np.int64)
+    v = rng.uniform(-1, 1, r.size)
+    vv = v.astype(np.float32) if dtype == "f32" else v
+    for R in (32, 512):
+        hbp = _hbp(rows, cols, r, c, vv, R=R)
+        x = rng.uniform(-1, 1, cols)
+        xd = torch.as_tensor(x.astype(vv.dtype), device="cuda")
+        y0 = H.SpmvOperator(hbp, hot=False)(xd).cpu().numpy()
+        st = H.SpmvOperator(hbp, hot=True)
+        assert (st.hot is None) == (cols < 4)
+        y1 = st(xd).cpu().numpy()
+        np.testing.assert_array_equal(y1, y0)
+        if dtype == "f64":
+            p = O.pipeline(rows, cols, r, c, v, cols, R, 32)
+            np.testing.assert_array_equal(y1, O.hbp_spmv(p["hbp"], x, workers=2))
+
+
+def test_staging_empty_matrix():
+    hbp = _hbp(100, 50, np.zeros(0, np.int64), np.zeros(0, np.int64), np.zeros(0))
+    op = H.SpmvOperator(hbp, hot=True)
+    y = op(torch.ones(50, dtype=torch.float64, device="cuda"))
+    assert torch.equal(y, torch.zeros(100, dtype=torch.float64, device="cuda"))
