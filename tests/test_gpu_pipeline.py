@@ -40,3 +40,40 @@ def test_pipeline_matches_device_spmv(depth, dtype):
     for xh, yh in zip(xs, ys):
         want = op(xh.cuda()).cpu()
         assert torch.equal(yh, want)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("C,hot", [(None, True), (None, False), (700, True), (700, False)])
+def test_operator_cuda_graph(dtype, C, hot):
+    """SpmvOperator.capture: a CUDA graph of one SpMV (hot gather + stream
+    kernel, or + combine) replays to the same y as a direct call."""
+    import torch
+    rng = np.random.default_rng(11)
+    rows, cols = 3000, 2000
+    lens = np.minimum(rng.zipf(1.8, rows) + 2, cols // 2)
+    r = np.repeat(np.arange(rows), lens)
+    w = 1.0 / np.arange(1, cols + 1)
+    c = rng.choice(cols, r.size, p=w / w.sum())
+    key = np.unique(r.astype(np.int64) * cols + c)
+    r, c = key // cols, key % cols
+    v = rng.uniform(-1, 1, r.size).astype(dtype)
+    cfg = H.PartitionConfig(col_width=C or cols, row_height=512, warp_size=32)
+    csr = H.coo_to_csr(H.TripletMatrix(rows, cols, r, c, v))
+    grid = H.make_grid(csr, cfg)
+    hbp = H.build_hbp(csr, grid, H.hash_permutations(grid, H.sample_hash_params(grid, cfg)))
+    op = H.SpmvOperator(hbp, hot=hot)
+    assert (op.hot is not None) == hot
+    x = torch.as_tensor(rng.uniform(-1, 1, cols).astype(dtype), device="cuda")
+    y = torch.empty(rows, dtype=x.dtype, device="cuda")
+    want = op(x).clone()
+    g = op.capture(x, y)
+    y.zero_()
+    x2 = torch.as_tensor(rng.uniform(-1, 1, cols).astype(dtype), device="cuda")
+    want2 = op(x2).clone()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(y, want)
+    x.copy_(x2)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(y, want2)
