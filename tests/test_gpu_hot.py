@@ -193,7 +193,7 @@ def test_staging_tiny_shapes(rows, cols, per_row, dtype):
         np.zeros(0, np.int64)
     v = rng.uniform(-1, 1, r.size)
     vv = v.astype(np.float32) if dtype == "f32" else v
-    for R in (32, 512):
+    for R in (32, 96, 512, 1024):
         hbp = _hbp(rows, cols, r, c, vv, R=R)
         x = rng.uniform(-1, 1, cols)
         xd = torch.as_tensor(x.astype(vv.dtype), device="cuda")
