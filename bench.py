@@ -466,13 +466,18 @@ def run_gpu(args):
             e2e_samples.append(a.elapsed_time(b))
         e2e_ms = statistics.mean(e2e_samples)
     else:
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        pipe.run([xh] * K, [yhs[i % depth] for i in range(K)])
-        e1.record(stream)
-        torch.cuda.synchronize()
-        e2e_ms = e0.elapsed_time(e1) / K
+        # three back-to-back runs of K steps, median (host-side jitter in the
+        # pinned copies otherwise moves a single run by ~10 %)
+        runs = []
+        for _ in range(3):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            pipe.run([xh] * K, [yhs[i % depth] for i in range(K)])
+            e1.record(stream)
+            torch.cuda.synchronize()
+            runs.append(e0.elapsed_time(e1) / K)
+        e2e_ms = statistics.median(runs)
     xd = torch.as_tensor(x_host, device=dev).to(vdt)
     ychk = torch.empty(rows, dtype=vdt, device=dev)
     op(xd, ychk)
