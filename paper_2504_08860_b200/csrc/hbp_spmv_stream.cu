@@ -10,12 +10,16 @@
 //      array (exact mode: slice ends rounded up to group boundaries);
 //   2. lane 0 streams the slice's col/data into a shared-memory ring of NB
 //      chunks of CH elements with cp.async.bulk (TMA bulk copies completing
-//      on per-slot mbarriers), NB-3 chunks ahead of the walk;
+//      on per-slot mbarriers), NB-2 chunks ahead of the walk;
 //   3. the x gathers of chunk c+1 are issued (registers) before the walk of
 //      chunk c needs them; when the walk reaches chunk c+1 the products are
 //      written over its values (f32 data: f32 products; exact f64 data:
 //      __dmul_rn products), so products of the chunks the walk can touch are
-//      always resident;
+//      always resident.  f32 lanes own 4 consecutive elements of a chunk,
+//      f64 lanes 2L, 2L+1, 2L+64, 2L+65 (conflict-free 16-byte accesses).
+//      With hot-column staging (hbp_hot.cu) the gathers of the heaviest
+//      columns read the SM's shared copy of x, and past L2 a warm tier reads
+//      a compact evict-last copy;
 //   4. each group's phases come precomputed from the phase stream (live mask
 //      and element offset per phase, hbp_phase_emit), one phase per lane
 //      register; the walk is
