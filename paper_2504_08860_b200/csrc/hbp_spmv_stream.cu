@@ -900,9 +900,8 @@ int variant() {
 
 bool staged(const hbp_format_t *f) { return f->n_hot > 0 && f->scol && f->hot_cols; }
 
-// One variant = (chunk CH, ring slots NB, threads NT,
-// CTAs per SM MINB).  f64 data always uses the register-gather ring
-// (CH 128, NB 4).  Every launch is one 768-thread CTA per SM (staged ones need one
+// One variant = (chunk CH, ring slots NB, threads NT, CTAs per SM MINB, the
+// XM feature bits).  f64 data always uses CH 128, NB 4.  Every launch is one 768-thread CTA per SM (staged ones need one
 // shared copy of x per SM; unstaged ones measured 1-1.5 % faster than 3 x 256).
 #define HBP_VARIANT(FN, V, EXACT, HOT, CH, NB, NT, MINB, ...)                              \
     HBP_VARIANT_X(FN, V, EXACT, HOT, CH, NB, NT, MINB, 21 | 2048, __VA_ARGS__)
