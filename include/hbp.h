@@ -252,8 +252,12 @@ typedef struct {
     int64_t n_hot;               /* multiple of 4, see hbp_hot_capacity */
     int64_t n_warm;              /* warm tier: scol = HBP_WARM_FLAG | w (cols < 2^30) */
     int32_t cold_last;           /* 1: cold columns gathered L2 evict-last too (x fits L2) */
-    int32_t reserved;
+    int32_t reserved;            /* flags: HBP_FLAG_DIRECT_SINGLE */
 } hbp_format_t;
+/* hbp_spmv_stream with a partial AND y: rows of row blocks that have exactly
+ * one nonzero block are written to y directly (there is nothing to combine;
+ * bitwise the same), and hbp_combine skips those row blocks. */
+#define HBP_FLAG_DIRECT_SINGLE 4
 #define HBP_HOT_FLAG 0x80000000u
 #define HBP_WARM_FLAG 0x40000000u
 

@@ -153,6 +153,8 @@ __global__ void k_combine(const hbp_format_t f, const double *__restrict__ parti
          r += (int64_t)gridDim.x * blockDim.x) {
         const int64_t br = r / R, local = r - br * R;
         const int64_t lo = f.rb_ptr[br], hi = f.rb_ptr[br + 1];
+        // single-block row blocks were written by the SpMV kernel itself
+        if ((f.reserved & HBP_FLAG_DIRECT_SINGLE) && hi - lo == 1) continue;
         double s = 0.0;
         if (lo < hi) {
             // the same left-to-right sum, four independent loads in flight

@@ -660,6 +660,11 @@ __global__ void __launch_bounds__(NT, MINB)
             br_cur = (int32_t)br;
             yb = y + br * R;
             pb_out = partial ? partial + (int64_t)blk * R : nullptr;
+            // a row block with a single nonzero block needs no combine: its
+            // rows go straight to y (hbp_combine then skips the row block)
+            if (pb_out && !FC && (f.reserved & HBP_FLAG_DIRECT_SINGLE) &&
+                f.rb_ptr[br + 1] - f.rb_ptr[br] == 1)
+                pb_out = nullptr;
         }
     };
     // Fused combine (engine.py:196-201; b.rb_done set, partial and y given):
@@ -1057,6 +1062,7 @@ int hbp_spmv_stream(const hbp_format_t *f, const hbp_balanced_t *b, const void *
     if (!f->phases || !f->phase_ptr) return HBP_E_ARG;  // hbp_phase_emit first
     if (!partial && (!y || f->ncb != 1)) return HBP_E_ARG;
     if (b->rb_done && (!partial || !y || !f->rb_ptr || !f->rb_blk)) return HBP_E_ARG;
+    if ((f->reserved & HBP_FLAG_DIRECT_SINGLE) && partial && (!y || !f->rb_ptr)) return HBP_E_ARG;
     if (f->nzb == 0) return HBP_OK;
     // slices are addressed with 32-bit offsets
     if ((f->nnz + b->workers - 1) / b->workers > (int64_t)1 << 30) return HBP_E_UNSUPPORTED;

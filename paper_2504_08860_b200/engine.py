@@ -230,6 +230,9 @@ class SpmvOperator:
         # (cfg3 3.56 vs 3.28 ms, cfg1 69 vs 61 us, same box)
         self.fused_combine = (not self.direct and schedule == "stream" and hbp.nzb > 0
                               and os.environ.get("HBP_FUSED_COMBINE", "0") == "1")
+        if (not self.direct and schedule == "stream" and not self.fused_combine
+                and os.environ.get("HBP_DIRECT_SINGLE", "1") != "0"):
+            f.reserved |= 4  # HBP_FLAG_DIRECT_SINGLE
         if self.fused_combine:
             rb = torch.zeros(max(1, hbp.num_row_blocks), dtype=torch.int32, device=dev)
             self._scratch.append(rb)
@@ -266,7 +269,8 @@ class SpmvOperator:
             if self.has_empty_row_blocks:
                 L.call("hbp_zero_empty_rows", ctypes.byref(f), L.P(y), s)
         else:
-            self._blocks(f, x, self.partial, None, s)
+            # stream schedule: single-block row blocks go straight to y
+            self._blocks(f, x, self.partial, y if f.reserved & 4 else None, s)
             L.call("hbp_combine", ctypes.byref(f), L.P(self.partial), L.P(y), s)
         return y
 

@@ -162,3 +162,23 @@ def test_stream_fused_combine(dtype, C, workers, monkeypatch):
     if dtype == np.float64:
         p = O.pipeline(rows, cols, r, c, v, C, 512, 32)
         np.testing.assert_array_equal(y1, O.hbp_spmv(p["hbp"], x.cpu().numpy(), workers=2))
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("C", [700, 4096])
+def test_stream_direct_single_row_blocks(dtype, C, monkeypatch):
+    """Row blocks with one nonzero block are written to y by the SpMV kernel
+    (HBP_FLAG_DIRECT_SINGLE) and skipped by the combine: bitwise the same as
+    routing everything through the partial."""
+    rows, cols, r, c, v = _hot_matrix(seed=9)
+    keep = (c < 600) | (r % 5 == 0)  # mostly one column block per row block, some more
+    r, c, v = r[keep], c[keep], v[keep]
+    hbp = _hbp(rows, cols, r, c, v.astype(dtype), C=C)
+    x = torch.as_tensor(np.random.default_rng(4).uniform(-1, 1, cols).astype(dtype),
+                        device="cuda")
+    direct = H.SpmvOperator(hbp, hot=False)
+    assert direct._fmt.reserved & 4
+    monkeypatch.setenv("HBP_DIRECT_SINGLE", "0")
+    routed = H.SpmvOperator(hbp, hot=False)
+    assert not routed._fmt.reserved & 4
+    np.testing.assert_array_equal(direct(x).cpu().numpy(), routed(x).cpu().numpy())
