@@ -650,21 +650,21 @@ __global__ void __launch_bounds__(NT, MINB)
     int32_t blk = (int32_t)(g / gpb), gi = (int32_t)(g - (int64_t)blk * gpb);
     int32_t rows_left = 0;  // rows of block blk (<= R)
     int32_t br_cur = 0;     // its row block
-    V *yb = nullptr;
-    double *pb_out = nullptr;
+    bool to_partial = false;  // outputs of block blk go to the partial (else y)
+    // (output addresses are formed at the store from blk / br_cur: two 64-bit
+    // pointers fewer live across the walk)
     auto enter_block = [&]() {
         if (blk < f.nzb) {
             const int64_t br = f.blk_br[blk];
             const int64_t left = f.rows - br * R;
             rows_left = (int32_t)(left < R ? left : R);
             br_cur = (int32_t)br;
-            yb = y + br * R;
-            pb_out = partial ? partial + (int64_t)blk * R : nullptr;
+            to_partial = partial != nullptr;
             // a row block with a single nonzero block needs no combine: its
             // rows go straight to y (hbp_combine then skips the row block)
-            if (pb_out && !FC && (f.reserved & HBP_FLAG_DIRECT_SINGLE) &&
+            if (to_partial && !FC && (f.reserved & HBP_FLAG_DIRECT_SINGLE) &&
                 f.rb_ptr[br + 1] - f.rb_ptr[br] == 1)
-                pb_out = nullptr;
+                to_partial = false;
         }
     };
     // Fused combine (engine.py:196-201; b.rb_done set, partial and y given):
@@ -787,9 +787,9 @@ __global__ void __launch_bounds__(NT, MINB)
         // ---- outputs
         const int32_t gi_now = gi;
         const bool valid = gi_now * 32 + lane < rows_left;
-        V *const yb_now = yb;
-        double *const pb_now = pb_out;
-        const int32_t br_now = br_cur, rows_now = rows_left;
+        const int32_t br_now = br_cur, rows_now = rows_left, blk_now = blk;
+        double *const pb_now = to_partial ? partial + (int64_t)blk_now * R : nullptr;
+        V *const yb_now = y + (int64_t)br_now * R;
         if (++gi == gpb) {
             gi = 0;
             ++blk;
