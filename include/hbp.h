@@ -335,7 +335,8 @@ int hbp_spmv_stream(const hbp_format_t *f, const hbp_balanced_t *b, const void *
  * reference reads x[col] directly (_kernels.py:41-46).
  *   hbp_col_degree:  deg[c] += #{e = i * stride : col[e] == c} (deg zero-filled;
  *                    stride 1 = exact degrees, larger = a deterministic sample).
- *   hbp_hot_capacity: largest n_hot the stream kernel can stage for dtype.
+ *   hbp_hot_capacity: largest n_hot the stream kernel can stage for dtype
+ *                    (warm != 0: for a launch that also has a warm tier).
  *   hbp_hot_slots:   slot_of[hot_cols[s]] = s (slot_of filled with -1).
  *   hbp_hot_remap:   scol[e] = slot s = slot_of[col[e]]: s < n_hot -> HBP_HOT_FLAG | s,
  *                    n_hot <= s -> HBP_WARM_FLAG | (s - n_hot), none -> col[e].
@@ -346,7 +347,7 @@ int hbp_spmv_stream(const hbp_format_t *f, const hbp_balanced_t *b, const void *
  * (cfg5: 256 MB) the heavy columns stay L2-resident in a dense array. */
 int hbp_col_degree(const uint32_t *col, int64_t nnz, int64_t stride, uint32_t *deg,
                    hbp_stream_t stream);
-int hbp_hot_capacity(int dtype, int64_t *n_hot_max);
+int hbp_hot_capacity(int dtype, int warm, int64_t *n_hot_max);
 int hbp_hot_slots(const uint32_t *hot_cols, int64_t n_hot, int32_t *slot_of,
                   hbp_stream_t stream);
 int hbp_hot_remap(const uint32_t *col, int64_t nnz, const int32_t *slot_of, int64_t n_hot,

@@ -112,7 +112,7 @@ _SIGS = {
     "hbp_spmv_stream": [ctypes.POINTER(FormatT), ctypes.POINTER(BalancedT), c_vp, c_vp, c_vp,
                         c_vp],
     "hbp_col_degree": [c_vp, c_i64, c_i64, c_vp, c_vp],
-    "hbp_hot_capacity": [c_int, ctypes.POINTER(c_i64)],
+    "hbp_hot_capacity": [c_int, c_int, ctypes.POINTER(c_i64)],
     "hbp_hot_slots": [c_vp, c_i64, c_vp, c_vp],
     "hbp_hot_remap": [c_vp, c_i64, c_vp, c_i64, c_vp, c_vp],
     "hbp_hot_gather": [c_vp, c_int, c_vp, c_i64, c_vp, c_vp],

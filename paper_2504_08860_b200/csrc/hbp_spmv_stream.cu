@@ -50,11 +50,13 @@ using namespace hbp;
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-// Hot-column staging (hbp_hot.cu): one 768-thread CTA per SM holds one copy
+// Hot-column staging (hbp_hot.cu): one CTA per SM holds one copy
 // of x at the hot columns after the warps' rings; shared memory per SM is
 // capped at kHotBudget so L1 keeps room to stage the remaining x gathers.
-constexpr int kHotThreads = 768;
-constexpr size_t kHotBudgetDefault = 131 * 1024;  // -> 132 KB carveout (sweep: r01_hot_sweep)
+constexpr int kHotThreads = 896;   // 28 warps at 72 registers (measured best)
+constexpr int kWarmThreads = 768;  // warm-tier launches (x beyond L2): 24 warps measured best
+constexpr size_t kHotBudgetDefault = 155 * 1024;   // hot tier only -> 164 KB carveout
+constexpr size_t kWarmBudgetDefault = 131 * 1024;  // with a warm tier -> 132 KB carveout
 
 // Column slots: a chunk's columns are needed only until its gathers are
 // issued; while chunk ready+1 is started, chunks up to ready+NB-2 are in
@@ -906,8 +908,8 @@ int variant() {
 bool staged(const hbp_format_t *f) { return f->n_hot > 0 && f->scol && f->hot_cols; }
 
 // One variant = (chunk CH, ring slots NB, threads NT, CTAs per SM MINB, the
-// XM feature bits).  f64 data always uses CH 128, NB 4.  Every launch is one 768-thread CTA per SM (staged ones need one
-// shared copy of x per SM; unstaged ones measured 1-1.5 % faster than 3 x 256).
+// XM feature bits).  f64 data always uses CH 128, NB 4.  Every launch is one CTA per SM (staged ones need one shared
+// copy of x per SM): 28 warps, or 24 with a warm tier.
 #define HBP_VARIANT(FN, V, EXACT, HOT, CH, NB, NT, MINB, ...)                              \
     HBP_VARIANT_X(FN, V, EXACT, HOT, CH, NB, NT, MINB, 21 | 2048, __VA_ARGS__)
 #define HBP_VARIANT_X(FN, V, EXACT, HOT, CH, NB, NT, MINB, XM, ...)                         \
@@ -930,13 +932,13 @@ bool staged(const hbp_format_t *f) { return f->n_hot > 0 && f->scol && f->hot_co
 #define HBP_STREAM_DISPATCH(FN, V, EXACT, FUSED, ...)                                       \
     if (staged(f)) {                                                                        \
         if (FUSED && f->n_warm > 0) {                                                       \
-            HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, kHotThreads, 1, 53 | 512 | 2048, __VA_ARGS__); \
+            HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, kWarmThreads, 1, 53 | 512 | 2048, __VA_ARGS__); \
         }                                                                                   \
         if (FUSED) {                                                                        \
             HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, kHotThreads, 1, 21 | 512 | 2048, __VA_ARGS__); \
         }                                                                                   \
         if (f->n_warm > 0) {                                                                \
-            HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, kHotThreads, 1, 53 | 2048, __VA_ARGS__); \
+            HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, kWarmThreads, 1, 53 | 2048, __VA_ARGS__); \
         }                                                                                   \
         HBP_VARIANTS(FN, V, EXACT, true, kHotThreads, 1, __VA_ARGS__)                       \
     }                                                                                       \
@@ -952,7 +954,8 @@ int ring_bytes(size_t *out) {
 }
 #define HBP_RING_BYTES(V, CH, NB, NT) ring_bytes<V, CH, NB, 1, NT>(out)
 template <typename V>
-int hot_ring_bytes(size_t *out) {  // shared memory of the staged launch's rings
+int hot_ring_bytes(size_t *out, bool warm) {  // shared memory of the staged launch's rings
+    if (warm) return HBP_RING_BYTES(V, 128, 4, kWarmThreads);
     return HBP_RING_BYTES(V, 128, 4, kHotThreads);  // the same ring for every variant
 }
 
@@ -1013,19 +1016,20 @@ int hbp_stream_workers(const hbp_format_t *f, int64_t *workers) {
     return HBP_OK;
 }
 
-int hbp_hot_capacity(int dtype, int64_t *n_hot_max) {
+int hbp_hot_capacity(int dtype, int warm, int64_t *n_hot_max) {
     if (!n_hot_max || (dtype != HBP_F32 && dtype != HBP_F64)) return HBP_E_ARG;
-    // f32: 131 KB -> 132 KB carveout (sweep); f64 rings are
-    // twice as large, so its staged launch takes the 164 KB carveout
-    size_t budget = dtype == HBP_F64 ? 163 * 1024 : kHotBudgetDefault;
+    // f32: 155 KB (hot tier only) / 131 KB (with a warm tier) of shared memory
+    // per SM (sweeps); f64 rings are twice as large, so its
+    // staged launch takes a larger carveout
+    size_t budget = dtype == HBP_F64 ? 187 * 1024 : (warm ? kWarmBudgetDefault : kHotBudgetDefault);
     if (const char *e = getenv("HBP_HOT_BUDGET_KB")) budget = (size_t)atoi(e) * 1024;
     int dev = 0, optin = 0;
     HBP_CUDA_TRY(cudaGetDevice(&dev));
     HBP_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     if (budget > (size_t)optin) budget = (size_t)optin;
     size_t ring = 0;
-    if (dtype == HBP_F64) hot_ring_bytes<double>(&ring);
-    else hot_ring_bytes<float>(&ring);
+    if (dtype == HBP_F64) hot_ring_bytes<double>(&ring, warm != 0);
+    else hot_ring_bytes<float>(&ring, warm != 0);
     const size_t sv = dtype == HBP_F64 ? 8 : 4;
     *n_hot_max = budget > ring ? (int64_t)(((budget - ring) / sv) & ~(size_t)1023) : 0;
     return HBP_OK;
@@ -1070,7 +1074,7 @@ int hbp_spmv_stream(const hbp_format_t *f, const hbp_balanced_t *b, const void *
     if (!exact && (!b->part_head || !b->part_tail || !b->counters)) return HBP_E_ARG;
     if (staged(f)) {
         int64_t cap = 0;
-        const int rc = hbp_hot_capacity(f->dtype, &cap);
+        const int rc = hbp_hot_capacity(f->dtype, f->n_warm > 0, &cap);
         if (rc) return rc;
         if (f->n_hot > cap || (f->n_hot & 3) || !b->x_hot) return HBP_E_ARG;
         if (f->n_warm < 0 || (f->n_warm > 0 && f->cols > (int64_t)1 << 30)) return HBP_E_ARG;

@@ -176,7 +176,7 @@ class SpmvOperator:
             fits = hbp.cols * hbp.data.element_size() <= L.l2_bytes() * 0.6
             wb = (0 if fits else int(os.environ.get("HBP_WARM_BYTES", self.WARM_BYTES))) \
                 if warm_bytes is None else int(warm_bytes)
-            cap = hbp.hot_capacity()
+            cap = hbp.hot_capacity(warm=wb > 0 and hbp.cols <= (1 << 30))
             n = min(cap if n_hot is None else min(n_hot, cap), hbp.cols) & ~3
             if hbp.cols >= (1 << 31):
                 n = 0

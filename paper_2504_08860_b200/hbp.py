@@ -113,10 +113,12 @@ class HbpMatrix:
             self._fmt.phase_ptr = ptr.data_ptr()
             self._fmt.phases = phases.data_ptr()
 
-    def hot_capacity(self) -> int:
-        """Largest hot set the stream kernel can stage for this dtype."""
+    def hot_capacity(self, warm: bool = False) -> int:
+        """Largest hot set the stream kernel can stage for this dtype (with or
+        without a warm tier in the same launch)."""
         cap = L.c_i64(0)
-        L.call("hbp_hot_capacity", L.c_int(L.dtype_code(self.data.dtype)), ctypes.byref(cap))
+        L.call("hbp_hot_capacity", L.c_int(L.dtype_code(self.data.dtype)), L.c_int(int(warm)),
+               ctypes.byref(cap))
         return int(cap.value)
 
     RANK_SAMPLE = 1 << 28  # column degrees from at most ~256M sampled elements
@@ -154,7 +156,7 @@ class HbpMatrix:
         hbp_col_degree .. hbp_hot_remap): the n_hot heaviest columns (capped
         by the kernel's shared-memory capacity), then the n_warm next ones
         (warm tier), and the staged column stream.  Cached."""
-        cap = self.hot_capacity()
+        cap = self.hot_capacity(warm=n_warm > 0)
         n = cap if n_hot is None else min(int(n_hot), cap)
         n = max(0, min(n, self.cols)) & ~3
         if self.cols >= (1 << 31):  # the staged stream flags hot columns with bit 31

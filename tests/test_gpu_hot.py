@@ -144,10 +144,11 @@ def test_staged_multi_col_block(mat):
 
 def test_hot_gather_and_capacity():
     cap = L.c_i64(0)
-    L.call("hbp_hot_capacity", L.c_int(L.HBP_F32), ctypes.byref(cap))
-    cap32 = int(cap.value)
-    L.call("hbp_hot_capacity", L.c_int(L.HBP_F64), ctypes.byref(cap))
-    assert cap32 >= 4096 and int(cap.value) >= 4096 and cap32 % 1024 == 0
+    for warm in (0, 1):
+        L.call("hbp_hot_capacity", L.c_int(L.HBP_F32), L.c_int(warm), ctypes.byref(cap))
+        cap32 = int(cap.value)
+        L.call("hbp_hot_capacity", L.c_int(L.HBP_F64), L.c_int(warm), ctypes.byref(cap))
+        assert cap32 >= 4096 and int(cap.value) >= 1024 and cap32 % 1024 == 0
     x = torch.randn(100000, device="cuda", dtype=torch.float64)
     hot = torch.randint(0, 100000, (4096,), device="cuda", dtype=torch.int32)
     out = torch.empty(4096, device="cuda", dtype=torch.float64)

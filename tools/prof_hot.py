@@ -27,7 +27,7 @@ grid = H.make_grid(csr, cfg)
 hbp = H.build_hbp(csr, grid, H.hash_permutations(grid, H.sample_hash_params(grid, cfg)),
                   with_add_sign=False, with_zero_row=False)
 cap = L.c_i64(0)
-L.call("hbp_hot_capacity", L.c_int(L.dtype_code(hbp.data.dtype)), ctypes.byref(cap))
+L.call("hbp_hot_capacity", L.c_int(L.dtype_code(hbp.data.dtype)), L.c_int(0), ctypes.byref(cap))
 n = int(cap.value)
 
 
