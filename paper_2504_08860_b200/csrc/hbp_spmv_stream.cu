@@ -725,8 +725,9 @@ __global__ void __launch_bounds__(NT, MINB)
     int32_t gr0 = g < ngroups ? (int32_t)(gs[g] - base) : len32;
     int32_t gr1 = g < ngroups ? (int32_t)(gs[g + 1] - base) : len32;
     uint32_t perm_n = g < ngroups ? permp[g * 32 + lane] : 0u;
-    int64_t pp0 = g < ngroups ? pptr[g] : 0;
-    int64_t pp1 = g < ngroups ? pptr[g + 1] : 0;
+    // phase-stream offsets fit 32 bits (hbp_spmv_stream checks the total)
+    int32_t pp0 = g < ngroups ? (int32_t)pptr[g] : 0;
+    int32_t pp1 = g < ngroups ? (int32_t)pptr[g + 1] : 0;
     uint2 ph_n = make_uint2(0u, 0u);
     if (g < ngroups && lane < pp1 - pp0) ph_n = phs[pp0 + lane];
 
@@ -740,7 +741,7 @@ __global__ void __launch_bounds__(NT, MINB)
             gr1 = (int32_t)(ldm(gs + g + 2) - base);
             perm_n = ldm(permp + (g + 1) * 32 + lane);
             pp0 = pp1;
-            pp1 = ldm(pptr + g + 2);
+            pp1 = (int32_t)ldm(pptr + g + 2);
             // address known now (no wait on pp1); lanes >= the phase count
             // read the next group's phases (padded stream) and are ignored
             ph_n = ldm(phs + pp0 + lane);
@@ -919,7 +920,7 @@ bool staged(const hbp_format_t *f) { return f->n_hot > 0 && f->scol && f->hot_co
 #define HBP_VARIANTS(FN, V, EXACT, HOT, NTD, MINBD, ...)                                     \
     switch (variant()) {                                                                    \
         case 1: HBP_VARIANT_X(FN, V, EXACT, HOT, 128, 4, NTD, MINBD, 29, __VA_ARGS__);      \
-        case 2: HBP_VARIANT_X(FN, V, EXACT, HOT, 128, 4, 256, 3, 21 | 2048, __VA_ARGS__);   \
+        case 2: HBP_VARIANT_X(FN, V, EXACT, HOT, 128, 4, 768, 1, 21 | 2048, __VA_ARGS__);   \
         case 3: HBP_VARIANT_X(FN, V, EXACT, HOT, 128, 4, NTD, MINBD, 5, __VA_ARGS__);       \
         default: HBP_VARIANT(FN, V, EXACT, HOT, 128, 4, NTD, MINBD, __VA_ARGS__);           \
     }
@@ -956,7 +957,8 @@ int ring_bytes(size_t *out) {
 template <typename V>
 int hot_ring_bytes(size_t *out, bool warm) {  // shared memory of the staged launch's rings
     if (warm) return HBP_RING_BYTES(V, 128, 4, kWarmThreads);
-    return HBP_RING_BYTES(V, 128, 4, kHotThreads);  // the same ring for every variant
+    if (variant() == 2) return HBP_RING_BYTES(V, 128, 4, 768);
+    return HBP_RING_BYTES(V, 128, 4, kHotThreads);
 }
 
 template <typename V, bool EXACT>

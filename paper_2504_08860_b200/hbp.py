@@ -103,6 +103,8 @@ class HbpMatrix:
         L.call("hbp_phase_counts", L.P(self.slot_len), L.c_i64(ng), L.P(nph), L.stream())
         ptr = L.exclusive_sum(nph)
         total = int(ptr[-1].item())
+        if total + 32 >= (1 << 31):  # the stream kernel keeps phase offsets in 32 bits
+            raise ValueError(f"phase stream of {total} entries exceeds the 32-bit kernel index")
         # + 32 entries: the stream kernel reads a whole warp's worth of phases
         # per group without waiting for the group's phase count
         phases = torch.zeros((total + 32) * 2, dtype=torch.int32, device=dev)
