@@ -650,6 +650,9 @@ __global__ void __launch_bounds__(NT, MINB)
     const bool last_warp = (w == Nw - 1);
     // output position of group g: nonzero block blk, group gi within it
     int32_t blk = (int32_t)(g / gpb), gi = (int32_t)(g - (int64_t)blk * gpb);
+    // the group loop in 32 bits (hbp_spmv_stream rejects >= 2^31 groups)
+    const int32_t ng32 = (int32_t)ngroups;
+    int32_t gq = (int32_t)g;
     int32_t rows_left = 0;  // rows of block blk (<= R)
     int32_t br_cur = 0;     // its row block
     bool to_partial = false;  // outputs of block blk go to the partial (else y)
@@ -722,26 +725,26 @@ __global__ void __launch_bounds__(NT, MINB)
 
     // prefetched metadata of group g: element range (base-relative), output
     // rows, phases
-    int32_t gr0 = g < ngroups ? (int32_t)(gs[g] - base) : len32;
-    int32_t gr1 = g < ngroups ? (int32_t)(gs[g + 1] - base) : len32;
-    uint32_t perm_n = g < ngroups ? permp[g * 32 + lane] : 0u;
+    int32_t gr0 = gq < ng32 ? (int32_t)(gs[gq] - base) : len32;
+    int32_t gr1 = gq < ng32 ? (int32_t)(gs[gq + 1] - base) : len32;
+    uint32_t perm_n = gq < ng32 ? permp[(int64_t)gq * 32 + lane] : 0u;
     // phase-stream offsets fit 32 bits (hbp_spmv_stream checks the total)
-    int32_t pp0 = g < ngroups ? (int32_t)pptr[g] : 0;
-    int32_t pp1 = g < ngroups ? (int32_t)pptr[g + 1] : 0;
+    int32_t pp0 = gq < ng32 ? (int32_t)pptr[gq] : 0;
+    int32_t pp1 = gq < ng32 ? (int32_t)pptr[gq + 1] : 0;
     uint2 ph_n = make_uint2(0u, 0u);
-    if (g < ngroups && lane < pp1 - pp0) ph_n = phs[pp0 + lane];
+    if (gq < ng32 && lane < pp1 - pp0) ph_n = phs[pp0 + lane];
 
-    for (; g < ngroups && (gr0 < len32 || last_warp); ++g) {
+    for (; gq < ng32 && (gr0 < len32 || last_warp); ++gq) {
         const uint32_t row_local = perm_n;
         const int32_t g0 = gr0, g1 = gr1;
         const int np = (int)(pp1 - pp0);
         const uint2 ph = ph_n;
-        if (g + 1 < ngroups) {  // prefetch the next group's metadata
+        if (gq + 1 < ng32) {  // prefetch the next group's metadata
             gr0 = g1;
-            gr1 = (int32_t)(ldm(gs + g + 2) - base);
-            perm_n = ldm(permp + (g + 1) * 32 + lane);
+            gr1 = (int32_t)(ldm(gs + gq + 2) - base);
+            perm_n = ldm(permp + (int64_t)(gq + 1) * 32 + lane);
             pp0 = pp1;
-            pp1 = (int32_t)ldm(pptr + g + 2);
+            pp1 = (int32_t)ldm(pptr + gq + 2);
             // address known now (no wait on pp1); lanes >= the phase count
             // read the next group's phases (padded stream) and are ignored
             ph_n = ldm(phs + pp0 + lane);
@@ -815,7 +818,7 @@ __global__ void __launch_bounds__(NT, MINB)
         uint32_t done = 0;
         if (lane == 0) {
             const uint32_t n = (uint32_t)(hi - lo);
-            const uint32_t old = atomicAdd(b.counters + g, n);
+            const uint32_t old = atomicAdd(b.counters + gq, n);
             done = (old + n == (uint32_t)(g1 - g0));
         }
         done = __shfl_sync(FULL, done, 0);
@@ -833,7 +836,7 @@ __global__ void __launch_bounds__(NT, MINB)
             if (pb_now) pb_now[row_local] = s;
             else stm(yb_now + row_local, (V)s);
         }
-        if (lane == 0) b.counters[g] = 0u;
+        if (lane == 0) b.counters[gq] = 0u;
         if (FC && pb_now) group_done(br_now, rows_now);
     }
     if (FC && pend_n) flush_done(pend_br, pend_n, pend_rows);
@@ -1070,6 +1073,7 @@ int hbp_spmv_stream(const hbp_format_t *f, const hbp_balanced_t *b, const void *
     if (b->rb_done && (!partial || !y || !f->rb_ptr || !f->rb_blk)) return HBP_E_ARG;
     if ((f->reserved & HBP_FLAG_DIRECT_SINGLE) && partial && (!y || !f->rb_ptr)) return HBP_E_ARG;
     if (f->nzb == 0) return HBP_OK;
+    if (f->nzb * (f->row_height / 32) >= ((int64_t)1 << 31) - 2) return HBP_E_UNSUPPORTED;
     // slices are addressed with 32-bit offsets
     if ((f->nnz + b->workers - 1) / b->workers > (int64_t)1 << 30) return HBP_E_UNSUPPORTED;
     const bool exact = f->exact != 0 || f->dtype == HBP_F64;
