@@ -363,21 +363,21 @@ def run_gpu(args):
         y = y_pad[:rows]
         cur = [0]
 
-        sq = torch.zeros(1, dtype=torch.float64, device=dev)
+        # the normalisation x / ||x|| is folded into the next SpMV (its y stores
+        # are multiplied by 1 / sqrt(sq), SpmvOperator x_sumsq): a step is the
+        # SpMV, hbp_sumsq (+ the all-reduce and the all-gather), no scaling pass
+        sq = torch.ones(1, dtype=torch.float64, device=dev)
         sq_scratch = torch.empty(1024, dtype=torch.float64, device=dev)
 
         def step():
             x = xs[cur[0]]
-            op(x[:cols], y)
-            H.sumsq(y, sq, sq_scratch)          # ||y_local||^2 (hbp_sumsq, f64)
+            nxt = xs[1 - cur[0]]
+            out = y if dist else nxt[:rows]
+            op(x[:cols], out, x_sumsq=sq)       # y = A (x / ||x||)
+            H.sumsq(out, sq, sq_scratch)        # ||y_local||^2 (hbp_sumsq, f64)
             if dist:
                 dist.all_reduce(sq)
-            nxt = xs[1 - cur[0]]
-            if dist:
-                H.scale(y, sq, y)                # y / ||y|| in place, then all-gather
                 dist.all_gather_into_tensor(nxt, y_pad)
-            else:
-                H.scale(y, sq, nxt[:rows])       # straight into the next x
             cur[0] = 1 - cur[0]
         x_res = lambda: xs[cur[0]][:cols]  # noqa: E731
     else:
@@ -559,7 +559,7 @@ def run_gpu(args):
     if os.path.exists(prof):
         with open(prof) as fh:
             traffic = json.load(fh).get(args.config, {}).get("dram_bytes_per_launch")
-    launches_step = op.launches_per_call + (3 if iterated else 0)  # + sumsq (2) + scale
+    launches_step = op.launches_per_call + (2 if iterated else 0)  # + sumsq (2 launches)
     out = {
         "metric": METRIC, "value": round(gflops, 3), "unit": UNIT, "n_gpus": world,
         "steps": K, "warmup": args.warmup, "ms_per_step": round(per_step_ms, 5),

@@ -306,6 +306,8 @@ typedef struct {
     int64_t *slice_g;  /* nullable [workers]: first group of each stream slice */
     uint32_t *rb_done; /* nullable [nrb], zero-filled once: fused combine (stream
                           kernel with partial AND y; the kernel leaves it zeroed) */
+    const double *y_sumsq; /* nullable: rows written straight to y are multiplied by
+                              1 / sqrt(*y_sumsq) (iterated SpMV: y = A (x / ||x||)) */
 } hbp_balanced_t;
 
 int hbp_balanced_workers(const hbp_format_t *f, int64_t *workers);

@@ -56,7 +56,7 @@ class BalancedT(ctypes.Structure):
     """Mirror of hbp_balanced_t."""
     _fields_ = [("workers", c_i64), ("part_head", c_vp), ("part_tail", c_vp),
                 ("cut_end", c_vp), ("counters", c_vp), ("x_hot", c_vp),
-                ("slice_lo", c_vp), ("slice_g", c_vp), ("rb_done", c_vp)]
+                ("slice_lo", c_vp), ("slice_g", c_vp), ("rb_done", c_vp), ("y_sumsq", c_vp)]
 
 
 # name -> argtypes (all return int status)

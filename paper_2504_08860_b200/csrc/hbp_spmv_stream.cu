@@ -648,6 +648,9 @@ __global__ void __launch_bounds__(NT, MINB)
     __syncwarp();
 
     const bool last_warp = (w == Nw - 1);
+    // y written directly is scaled by 1 / sqrt(*b.y_sumsq) when given (the
+    // power iteration folds x / ||x|| into the next SpMV); 1.0 is exact
+    const double ys = b.y_sumsq ? 1.0 / sqrt(*b.y_sumsq) : 1.0;
     // output position of group g: nonzero block blk, group gi within it
     int32_t blk = (int32_t)(g / gpb), gi = (int32_t)(g - (int64_t)blk * gpb);
     // the group loop in 32 bits (hbp_spmv_stream rejects >= 2^31 groups)
@@ -804,7 +807,7 @@ __global__ void __launch_bounds__(NT, MINB)
         if (!piece) {
             if (valid) {
                 if (pb_now) pb_now[row_local] = acc;
-                else stm(yb_now + row_local, (V)acc);
+                else stm(yb_now + row_local, (V)(acc * ys));
             }
             if (FC && pb_now) group_done(br_now, rows_now);
             continue;
@@ -834,7 +837,7 @@ __global__ void __launch_bounds__(NT, MINB)
         }
         if (valid) {
             if (pb_now) pb_now[row_local] = s;
-            else stm(yb_now + row_local, (V)s);
+            else stm(yb_now + row_local, (V)(s * ys));
         }
         if (lane == 0) b.counters[gq] = 0u;
         if (FC && pb_now) group_done(br_now, rows_now);

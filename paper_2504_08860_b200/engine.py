@@ -254,12 +254,22 @@ class SpmvOperator:
             L.call("hbp_spmv_blocks", ctypes.byref(f), ctypes.byref(self.sched), L.P(x),
                    L.P(partial), L.P(y), s)
 
-    def __call__(self, x: torch.Tensor, y: torch.Tensor | None = None) -> torch.Tensor:
+    def __call__(self, x: torch.Tensor, y: torch.Tensor | None = None,
+                 x_sumsq: torch.Tensor | None = None) -> torch.Tensor:
+        """y = A x, or y = A (x / sqrt(x_sumsq[0])) when x_sumsq (a float64
+        device scalar) is given -- the power-iteration step without a separate
+        scaling pass (stream schedule, one column block)."""
         hbp = self.hbp
         if y is None:
             y = torch.empty(hbp.rows, dtype=hbp.dtype, device=hbp.data.device)
         f = self._fmt
         s = L.stream()
+        if x_sumsq is not None:
+            if self.schedule != "stream" or not self.direct:
+                raise ValueError("x_sumsq needs the stream schedule and one column block")
+            self.bal.y_sumsq = x_sumsq.data_ptr()
+        elif self.schedule == "stream":
+            self.bal.y_sumsq = None
         if self.direct:
             self._blocks(f, x, None, y, s)
             if self.has_empty_row_blocks:

@@ -32,3 +32,34 @@ def test_sumsq_scale(dtype, n):
         assert torch.equal(out, want)
         H.scale(y, sq, y)  # in place
         assert torch.equal(y, want)
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_spmv_x_sumsq_scaling(dtype):
+    """SpmvOperator(x, y, x_sumsq): y = A x / sqrt(x_sumsq[0]) (the power
+    iteration's normalisation folded into the SpMV's y stores)."""
+    import numpy as np
+    dt = getattr(torch, dtype)
+    rng = np.random.default_rng(3)
+    rows = cols = 4000
+    lens = rng.poisson(8, rows)
+    r = np.repeat(np.arange(rows), lens)
+    c = rng.integers(0, cols, r.size)
+    key = np.unique(r * cols + c)
+    r, c = key // cols, key % cols
+    v = rng.uniform(-1, 1, r.size).astype(np.float32 if dtype == "float32" else np.float64)
+    cfg = H.PartitionConfig(col_width=cols)
+    csr = H.coo_to_csr(H.TripletMatrix(rows, cols, r, c, v))
+    grid = H.make_grid(csr, cfg)
+    hbp = H.build_hbp(csr, grid, H.hash_permutations(grid, H.sample_hash_params(grid, cfg)))
+    op = H.SpmvOperator(hbp)
+    x = torch.as_tensor(rng.uniform(-1, 1, cols), device="cuda").to(dt)
+    plain = op(x).clone()
+    one = torch.ones(1, dtype=torch.float64, device="cuda")
+    assert torch.equal(op(x, x_sumsq=one), plain)  # scale 1 is exact
+    s = torch.tensor([6.25], dtype=torch.float64, device="cuda")
+    got = op(x, x_sumsq=s).to(torch.float64)
+    want = plain.to(torch.float64) / 2.5
+    tol = 1e-6 if dtype == "float32" else 1e-14
+    assert torch.allclose(got, want, rtol=tol, atol=tol)
+    assert torch.equal(op(x), plain)  # the scale does not stick
