@@ -665,7 +665,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-baselines", action="store_true",
                     help="skip the CSR / 2D / cuSPARSE comparison timings")
-    ap.add_argument("--schedule", default=None, choices=[None, "stream", "balanced", "plan"])
+    ap.add_argument("--schedule", default=None, choices=[None, "stream", "balanced", "plan", "rowblock"])
     ap.add_argument("--workers", type=int, default=None,
                     help="persistent warps of the SpMV (default: one per resident warp slot)")
     ap.add_argument("--hot", default="auto",

@@ -363,6 +363,12 @@ int hbp_spmv_balanced(const hbp_format_t *f, const hbp_balanced_t *b, const void
  * (bitwise equal to the dense combine); rows of row blocks with
  * no nonzero block get +0.0. */
 int hbp_combine(const hbp_format_t *f, const double *partial, void *y, hbp_stream_t stream);
+/* Row-block-owner SpMV + combine in one launch (small matrices with several
+ * column blocks): one CTA per row block runs block_spmv (engine.py:123-134)
+ * over its nonzero blocks in ascending bc and folds them as combine does
+ * (engine.py:196-201), then writes y (+0.0 for empty row blocks).  Bitwise
+ * equal to hbp_spmv_blocks + hbp_combine.  row_height <= 3072. */
+int hbp_spmv_rowblock(const hbp_format_t *f, const void *x, void *y, hbp_stream_t stream);
 /* Zero y for row blocks with no nonzero block (direct mode companion). */
 int hbp_zero_empty_rows(const hbp_format_t *f, void *y, hbp_stream_t stream);
 /* Dense PartialVector view (engine.py:59-68): partial_dense[bc*rows + row]. */

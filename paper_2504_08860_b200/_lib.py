@@ -123,6 +123,7 @@ _SIGS = {
     "hbp_l2_persist_reset": [c_vp],
     "hbp_l2_info": [ctypes.POINTER(c_int), ctypes.POINTER(c_int), ctypes.POINTER(c_int)],
     "hbp_combine": [ctypes.POINTER(FormatT), c_vp, c_vp, c_vp],
+    "hbp_spmv_rowblock": [ctypes.POINTER(FormatT), c_vp, c_vp, c_vp],
     "hbp_zero_empty_rows": [ctypes.POINTER(FormatT), c_vp, c_vp],
     "hbp_expand_partial": [ctypes.POINTER(FormatT), c_vp, c_vp, c_vp],
     "hbp_to_triplets": [ctypes.POINTER(FormatT), c_vp, c_vp, c_vp, c_vp],

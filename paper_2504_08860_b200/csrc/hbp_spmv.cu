@@ -20,6 +20,7 @@
 //   f32: products are exact in f64, sums in f64, one rounding at the end.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "hbp.h"
 #include "hbp_common.cuh"
@@ -38,7 +39,7 @@ __device__ __forceinline__ double fmadd(double acc, V v, V xv) {
 }
 
 // Sum of one slot's elements in step order.  All segment lanes must call it.
-template <typename V, bool EXACT>
+template <typename V, bool EXACT, int U = 4>
 __device__ __forceinline__ double group_dot(const Seg &sg, const uint32_t *__restrict__ col,
                                             const V *__restrict__ data,
                                             const V *__restrict__ x, uint32_t len,
@@ -57,7 +58,7 @@ __device__ __forceinline__ double group_dot(const Seg &sg, const uint32_t *__res
             const V *dp = data + base + rank;
             const uint32_t M = t1 - t0;
             uint32_t t = 0;
-            for (; t + 4 <= M; t += 4) {
+            for (; U == 4 && t + 4 <= M; t += 4) {
                 uint32_t c0 = ld_stream_u32(cp, pe), c1 = ld_stream_u32(cp + k, pe),
                          c2 = ld_stream_u32(cp + 2 * k, pe), c3 = ld_stream_u32(cp + 3 * k, pe);
                 V v0 = ld_stream(dp, pe), v1 = ld_stream(dp + k, pe), v2 = ld_stream(dp + 2 * k, pe),
@@ -69,6 +70,15 @@ __device__ __forceinline__ double group_dot(const Seg &sg, const uint32_t *__res
                 acc = fmadd<V, EXACT>(acc, v3, x3);
                 cp += 4 * k;
                 dp += 4 * k;
+            }
+            for (; U == 2 && t + 2 <= M; t += 2) {
+                uint32_t c0 = ld_stream_u32(cp, pe), c1 = ld_stream_u32(cp + k, pe);
+                V v0 = ld_stream(dp, pe), v1 = ld_stream(dp + k, pe);
+                V x0 = ld_x(x + c0, pl), x1 = ld_x(x + c1, pl);
+                acc = fmadd<V, EXACT>(acc, v0, x0);
+                acc = fmadd<V, EXACT>(acc, v1, x1);
+                cp += 2 * k;
+                dp += 2 * k;
             }
             for (; t < M; ++t) {
                 uint32_t c0 = ld_stream_u32(cp, pe);
@@ -141,6 +151,69 @@ __global__ void __launch_bounds__(kSpmvThreads)
         const int64_t idx = sch.fixed_count + (int64_t)t;
         if (idx >= f.nzb) break;
         run_block(idx, 1);
+    }
+}
+
+// Row-block-owner schedule (small matrices with several column blocks): one
+// CTA per row block computes the block partials of its nonzero blocks into
+// shared memory -- up to `kmax` blocks at once, one (block, group) task per
+// warp segment, so the blocks' load chains overlap -- and folds them in
+// ascending bc exactly as combine does (engine.py:196-201: s = p_first;
+// s += p_next ...), carrying the running sum across chunks of kmax blocks.
+// The per-slot sums are k_spmv's (group_dot), so results are bitwise those
+// of hbp_spmv_blocks + hbp_combine, without the partial array, the combine
+// launch or the empty-row pass.
+constexpr int kRowThreadsMax = 512;
+constexpr int64_t kRowSmem = 48 * 1024;                  // no opt-in needed
+constexpr int64_t kRowBlockMaxR = kRowSmem / 16;         // kmax >= 1 plus the running sum
+
+template <typename V, bool EXACT, int MINB, int U>
+__global__ void __launch_bounds__(kRowThreadsMax, MINB)
+    k_spmv_rowblock(const hbp_format_t f, const V *__restrict__ x, V *__restrict__ y, int kmax) {
+    extern __shared__ double sm[];  // pl[kmax][R], then the running sum ys[R]
+    const Seg sg = make_seg((int)f.warp_size);
+    const int64_t R = f.row_height, W = f.warp_size, gpb = R / W;
+    const int64_t nrb = (f.rows + R - 1) / R;
+    double *ys = sm + (int64_t)kmax * R;
+    const V *__restrict__ data = (const V *)f.data;
+    const uint64_t pe = policy_evict_first(), pl = policy_evict_last();
+    const int seg0 = (threadIdx.x >> 5) * sg.spw + sg.seg;
+    const int nseg = (blockDim.x >> 5) * sg.spw;
+    for (int64_t br = blockIdx.x; br < nrb; br += gridDim.x) {
+        const int64_t lo = f.rb_ptr[br], hi = f.rb_ptr[br + 1];
+        int64_t n64 = f.rows - br * R;
+        const int n = (int)(n64 > R ? R : n64);
+        const int ng = (int)((n + W - 1) / W);
+        V *yb = y + br * R;
+        if (lo == hi) {
+            for (int r = threadIdx.x; r < n; r += blockDim.x) yb[r] = (V)0;
+            continue;
+        }
+        for (int64_t c0 = lo; c0 < hi; c0 += kmax) {
+            const int cnt = (int)(hi - c0 < kmax ? hi - c0 : kmax);
+            if (!sg.idle()) {
+                for (int t = seg0; t < cnt * ng; t += nseg) {
+                    const int j = t / ng, g = t - j * ng;
+                    const int64_t idx = f.rb_blk[c0 + j];
+                    const int slot = g * (int)W + sg.q;
+                    const bool valid = slot < n;
+                    const uint32_t len = valid ? f.slot_len[idx * R + slot] : 0u;
+                    const uint32_t row = valid ? f.perm[idx * R + slot] : 0u;
+                    const int64_t gs = f.group_start[idx * gpb + g];
+                    const double acc = group_dot<V, EXACT, U>(sg, f.col, data, x, len, gs, pe, pl);
+                    if (valid) sm[(int64_t)j * R + row] = acc;
+                }
+            }
+            __syncthreads();
+            const bool last = c0 + kmax >= hi;
+            for (int r = threadIdx.x; r < n; r += blockDim.x) {
+                double v = c0 == lo ? sm[r] : __dadd_rn(ys[r], sm[r]);
+                for (int j = 1; j < cnt; ++j) v = __dadd_rn(v, sm[(int64_t)j * R + r]);
+                if (last) yb[r] = (V)v;
+                else ys[r] = v;
+            }
+            __syncthreads();
+        }
     }
 }
 
@@ -291,6 +364,45 @@ int hbp_spmv_blocks(const hbp_format_t *f, const hbp_schedule_t *s, const void *
     if (f->dtype == HBP_F64) dispatch_spmv<double, true>(f, s, x, partial, y_direct, st);
     else if (f->dtype == HBP_F32) dispatch_spmv<float, false>(f, s, x, partial, y_direct, st);
     else return HBP_E_ARG;
+    HBP_LAUNCH_CHECK();
+    return HBP_OK;
+}
+
+int hbp_spmv_rowblock(const hbp_format_t *f, const void *x, void *y, hbp_stream_t stream) {
+    if (!f || f->rows < 0 || (f->rows > 0 && !y)) return HBP_E_ARG;
+    if (f->warp_size < 1 || f->warp_size > 32 || f->row_height % f->warp_size ||
+        f->row_height > kRowBlockMaxR)
+        return HBP_E_UNSUPPORTED;
+    if (f->rows == 0) return HBP_OK;
+    if (f->nzb > 0 && !x) return HBP_E_ARG;
+    const int64_t R = f->row_height, spw = 32 / f->warp_size;
+    const int64_t warps = (R / f->warp_size + spw - 1) / spw;
+    const int threads = (int)(warps * 32 < kRowThreadsMax ? warps * 32 : kRowThreadsMax);
+    const int64_t nrb = (f->rows + R - 1) / R;
+    const unsigned grid = (unsigned)(nrb < (1 << 30) ? nrb : (1 << 30));
+    int kmax = (int)(kRowSmem / (8 * R)) - 1;
+    if (kmax > 8) kmax = 8;
+    const size_t smem = sizeof(double) * (size_t)R * (size_t)(kmax + 1);
+    cudaStream_t st = as_stream(stream);
+    if (f->dtype != HBP_F64 && f->dtype != HBP_F32) return HBP_E_ARG;
+    static const int variant =  // tuning A/B only
+        getenv("HBP_ROWBLOCK_VARIANT") ? atoi(getenv("HBP_ROWBLOCK_VARIANT")) : 0;
+#define HBP_RB_LAUNCH(MINB, U)                                                                      \
+    do {                                                                                         \
+        if (f->dtype == HBP_F64)                                                                 \
+            k_spmv_rowblock<double, true, MINB, U><<<grid, threads, smem, st>>>(                 \
+                *f, (const double *)x, (double *)y, kmax);                                       \
+        else                                                                                     \
+            k_spmv_rowblock<float, false, MINB, U><<<grid, threads, smem, st>>>(                 \
+                *f, (const float *)x, (float *)y, kmax);                                         \
+    } while (0)
+    // cfg1 (same box, L2 flushed): 4 CTAs x 32 regs, two-step unroll 41.3 us;
+    // 3 CTAs x 40 regs 48.6 (unroll 4) / 49.8 (unroll 2) / 48.4 us (no unroll);
+    // 2 CTAs x 64 regs 53.6 us.  A step-batched walk (positions of 4 or 8
+    // steps from per-step ballots, then all loads) was slower: 51.6 / 66 us.
+    if (variant == 1) HBP_RB_LAUNCH(3, 4);
+    else HBP_RB_LAUNCH(4, 2);
+#undef HBP_RB_LAUNCH
     HBP_LAUNCH_CHECK();
     return HBP_OK;
 }

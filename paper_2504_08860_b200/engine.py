@@ -147,9 +147,14 @@ class SpmvOperator:
     schedule="balanced": the same slices walked from global memory
     (hbp_spmv_balanced, step-aligned cuts).  schedule="plan": the reference's fixed + competitive
     block schedule (hbp_spmv_blocks) with this fixed_fraction.
+    schedule="rowblock": one CTA per row block runs its nonzero blocks in
+    ascending bc and folds them as the combine does (hbp_spmv_rowblock; one
+    launch, no partial array -- for small matrices with several column blocks).
     direct mode (one column block): the kernel writes y itself; otherwise the
     partial (f64, compact) is combined in ascending bc."""
 
+    ROWBLOCK_MAX_NNZ = 1 << 24  # auto: row-block owner below this size ...
+    ROWBLOCK_MAX_SKEW = 8.0     # ... when no row block holds > 8x the mean
     HOT_MIN_SHARE = 0.10  # stage hot columns when they hold >= 10 % of the nonzeros
     WARM_BYTES = 64 << 20  # warm tier: a 64 MB L2-resident copy of x at the next columns
 
@@ -159,7 +164,7 @@ class SpmvOperator:
         self.hbp = hbp
         dev = hbp.data.device
         if schedule is None:
-            schedule = "stream" if hbp.config.warp_size == 32 else "plan"
+            schedule = os.environ.get("HBP_SCHEDULE") or self._auto_schedule(hbp, hot)
         if schedule in ("balanced", "stream") and hbp.config.warp_size != 32:
             raise ValueError(f"the {schedule} schedule needs warp_size == 32")
         self.schedule = schedule
@@ -221,7 +226,7 @@ class SpmvOperator:
         self.ticket = torch.zeros(1, dtype=torch.int32, device=dev)
         self.direct = hbp.num_col_blocks == 1
         R = hbp.config.row_height
-        self.partial = None if self.direct else torch.empty(hbp.nzb * R, dtype=torch.float64,
+        self.partial = None if self.direct or schedule == "rowblock" else torch.empty(hbp.nzb * R, dtype=torch.float64,
                                                             device=dev)
         self.has_empty_row_blocks = bool((hbp.rb_ptr[1:] == hbp.rb_ptr[:-1]).any())
         # stream schedule with several column blocks: optionally fuse the combine
@@ -241,10 +246,27 @@ class SpmvOperator:
         self.sched.workers = self.workers
         self.sched.fixed_count = self.fixed_count
         self.sched.ticket = self.ticket.data_ptr()
-        self.launches_per_call = (1 + (1 if self.has_empty_row_blocks or not (
+        self.launches_per_call = 1 if schedule == "rowblock" else (1 + (1 if self.has_empty_row_blocks or not (
             self.direct or self.fused_combine) else 0) + (1 if self.hot is not None else 0))
         self._graph = None
         self._gx = self._gy = None
+
+    @classmethod
+    def _auto_schedule(cls, hbp: HbpMatrix, hot=None) -> str:
+        """stream for W = 32, plan otherwise; rowblock for small, evenly
+        spread matrices with several column blocks (one launch instead of
+        SpMV + combine; cfg1: 41 vs 61 us) unless hot staging was asked
+        about (a stream-schedule feature)."""
+        R = hbp.config.row_height
+        if (hot is None and hbp.num_col_blocks > 1 and 0 < hbp.nnz <= cls.ROWBLOCK_MAX_NNZ and R <= 3072):
+            gpb = R // hbp.config.warp_size
+            gs = hbp.group_start_c.view(-1)
+            blk_nnz = gs[gpb::gpb] - gs[:-1:gpb]
+            rb = torch.zeros(hbp.num_row_blocks, dtype=torch.int64, device=gs.device)
+            rb.index_add_(0, hbp.blk_br.long(), blk_nnz)
+            if float(rb.max()) <= cls.ROWBLOCK_MAX_SKEW * hbp.nnz / hbp.num_row_blocks:
+                return "rowblock"
+        return "stream" if hbp.config.warp_size == 32 else "plan"
 
     def _blocks(self, f, x, partial, y, s):
         if self.schedule in ("balanced", "stream"):
@@ -270,6 +292,9 @@ class SpmvOperator:
             self.bal.y_sumsq = x_sumsq.data_ptr()
         elif self.schedule == "stream":
             self.bal.y_sumsq = None
+        if self.schedule == "rowblock":
+            L.call("hbp_spmv_rowblock", ctypes.byref(f), L.P(x), L.P(y), s)
+            return y
         if self.direct:
             self._blocks(f, x, None, y, s)
             if self.has_empty_row_blocks:

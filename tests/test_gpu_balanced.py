@@ -127,7 +127,7 @@ def test_stream_precomputed_slices(dtype, workers):
     hbp = _hbp(rows, cols, r, c, v.astype(dtype), C=cols)
     x = torch.as_tensor(np.random.default_rng(2).uniform(-1, 1, cols).astype(dtype),
                         device="cuda")
-    op = H.SpmvOperator(hbp, workers=workers, hot=False)
+    op = H.SpmvOperator(hbp, workers=workers, hot=False, schedule="stream")
     assert op.bal.slice_lo and op.bal.slice_g
     y1 = op(x).cpu().numpy()
     lo = op._scratch[-2].cpu().numpy()
@@ -149,10 +149,10 @@ def test_stream_fused_combine(dtype, C, workers, monkeypatch):
     x = torch.as_tensor(np.random.default_rng(3).uniform(-1, 1, cols).astype(dtype),
                         device="cuda")
     monkeypatch.setenv("HBP_FUSED_COMBINE", "1")
-    fused = H.SpmvOperator(hbp, workers=workers, hot=False)
+    fused = H.SpmvOperator(hbp, workers=workers, hot=False, schedule="stream")
     assert fused.fused_combine
     monkeypatch.setenv("HBP_FUSED_COMBINE", "0")
-    plain = H.SpmvOperator(hbp, workers=workers, hot=False)
+    plain = H.SpmvOperator(hbp, workers=workers, hot=False, schedule="stream")
     assert not plain.fused_combine
     y0 = plain(x).cpu().numpy()
     y1 = fused(x).cpu().numpy()
@@ -176,9 +176,9 @@ def test_stream_direct_single_row_blocks(dtype, C, monkeypatch):
     hbp = _hbp(rows, cols, r, c, v.astype(dtype), C=C)
     x = torch.as_tensor(np.random.default_rng(4).uniform(-1, 1, cols).astype(dtype),
                         device="cuda")
-    direct = H.SpmvOperator(hbp, hot=False)
+    direct = H.SpmvOperator(hbp, hot=False, schedule="stream")
     assert direct._fmt.reserved & 4
     monkeypatch.setenv("HBP_DIRECT_SINGLE", "0")
-    routed = H.SpmvOperator(hbp, hot=False)
+    routed = H.SpmvOperator(hbp, hot=False, schedule="stream")
     assert not routed._fmt.reserved & 4
     np.testing.assert_array_equal(direct(x).cpu().numpy(), routed(x).cpu().numpy())
