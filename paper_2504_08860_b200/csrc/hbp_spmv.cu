@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kSpmvThreads)
 }
 
 // Row-block-owner schedule (small matrices with several column blocks): one
-// CTA per row block computes the block partials of its nonzero blocks into
+// CTA (8 warps) per row block computes the block partials of its nonzero blocks into
 // shared memory -- up to `kmax` blocks at once, one (block, group) task per
 // warp segment, so the blocks' load chains overlap -- and folds them in
 // ascending bc exactly as combine does (engine.py:196-201: s = p_first;
@@ -167,8 +167,8 @@ constexpr int kRowThreadsMax = 512;
 constexpr int64_t kRowSmem = 48 * 1024;                  // no opt-in needed
 constexpr int64_t kRowBlockMaxR = kRowSmem / 16;         // kmax >= 1 plus the running sum
 
-template <typename V, bool EXACT, int MINB, int U>
-__global__ void __launch_bounds__(kRowThreadsMax, MINB)
+template <typename V, bool EXACT, int NT, int MINB, int U>
+__global__ void __launch_bounds__(NT, MINB)
     k_spmv_rowblock(const hbp_format_t f, const V *__restrict__ x, V *__restrict__ y, int kmax) {
     extern __shared__ double sm[];  // pl[kmax][R], then the running sum ys[R]
     const Seg sg = make_seg((int)f.warp_size);
@@ -377,31 +377,38 @@ int hbp_spmv_rowblock(const hbp_format_t *f, const void *x, void *y, hbp_stream_
     if (f->nzb > 0 && !x) return HBP_E_ARG;
     const int64_t R = f->row_height, spw = 32 / f->warp_size;
     const int64_t warps = (R / f->warp_size + spw - 1) / spw;
-    const int threads = (int)(warps * 32 < kRowThreadsMax ? warps * 32 : kRowThreadsMax);
     const int64_t nrb = (f->rows + R - 1) / R;
     const unsigned grid = (unsigned)(nrb < (1 << 30) ? nrb : (1 << 30));
-    int kmax = (int)(kRowSmem / (8 * R)) - 1;
-    if (kmax > 8) kmax = 8;
-    const size_t smem = sizeof(double) * (size_t)R * (size_t)(kmax + 1);
     cudaStream_t st = as_stream(stream);
     if (f->dtype != HBP_F64 && f->dtype != HBP_F32) return HBP_E_ARG;
     static const int variant =  // tuning A/B only
         getenv("HBP_ROWBLOCK_VARIANT") ? atoi(getenv("HBP_ROWBLOCK_VARIANT")) : 0;
-#define HBP_RB_LAUNCH(MINB, U)                                                                      \
+    const int nt = variant == 1 || variant == 2 ? kRowThreadsMax : variant == 3 ? 128 : 256;
+    const int kcap = variant == 1 || variant == 2 ? 8 : variant == 3 ? 2 : 4;
+    const int threads = (int)(warps * 32 < nt ? warps * 32 : nt);
+    int kmax = (int)(kRowSmem / (8 * R)) - 1;
+    if (kmax > kcap) kmax = kcap;
+    const size_t smem = sizeof(double) * (size_t)R * (size_t)(kmax + 1);
+#define HBP_RB_LAUNCH(NT, MINB, U)                                                                    \
     do {                                                                                         \
         if (f->dtype == HBP_F64)                                                                 \
-            k_spmv_rowblock<double, true, MINB, U><<<grid, threads, smem, st>>>(                 \
+            k_spmv_rowblock<double, true, NT, MINB, U><<<grid, threads, smem, st>>>(                 \
                 *f, (const double *)x, (double *)y, kmax);                                       \
         else                                                                                     \
-            k_spmv_rowblock<float, false, MINB, U><<<grid, threads, smem, st>>>(                 \
+            k_spmv_rowblock<float, false, NT, MINB, U><<<grid, threads, smem, st>>>(                 \
                 *f, (const float *)x, (float *)y, kmax);                                         \
     } while (0)
-    // cfg1 (same box, L2 flushed): 4 CTAs x 32 regs, two-step unroll 41.3 us;
-    // 3 CTAs x 40 regs 48.6 (unroll 4) / 49.8 (unroll 2) / 48.4 us (no unroll);
-    // 2 CTAs x 64 regs 53.6 us.  A step-batched walk (positions of 4 or 8
-    // steps from per-step ballots, then all loads) was slower: 51.6 / 66 us.
-    if (variant == 1) HBP_RB_LAUNCH(3, 4);
-    else HBP_RB_LAUNCH(4, 2);
+    // cfg1 (same box, L2 flushed, tools/prof_spmv.py --flush): 8 CTAs x 8 warps
+    // x 32 regs, two-step unroll, 4 blocks per chunk 37.6 us; 16 x 4 warps 38.1;
+    // 4 x 16 warps 41.6 (warps idle at the barrier when a row block has 1.5
+    // blocks x 16 groups); 3 x 16 warps x 40 regs 48.6 (unroll 4) / 49.8
+    // (unroll 2) / 48.4 us (no unroll); 2 x 16 x 64 regs 53.6 us.  A
+    // step-batched walk (positions of 4 or 8 steps from per-step ballots, then
+    // all loads) was slower: 51.6 / 66 us.
+    if (variant == 1) HBP_RB_LAUNCH(512, 3, 4);
+    else if (variant == 2) HBP_RB_LAUNCH(512, 4, 2);
+    else if (variant == 3) HBP_RB_LAUNCH(128, 16, 2);
+    else HBP_RB_LAUNCH(256, 8, 2);
 #undef HBP_RB_LAUNCH
     HBP_LAUNCH_CHECK();
     return HBP_OK;

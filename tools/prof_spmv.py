@@ -20,6 +20,7 @@ ap.add_argument("--schedule", default=None)
 ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--workers", type=int, default=None)
 ap.add_argument("--persist", action="store_true")
+ap.add_argument("--flush", action="store_true", help="flush L2 before each timed SpMV (as bench.py does for cfg1)")
 ap.add_argument("--hot", default="auto", help="auto | on | off | column count")
 ap.add_argument("--persist-warm", action="store_true",
                 help="L2 persisting window over the staged x copy (hot + warm tiers)")
@@ -48,11 +49,22 @@ for _ in range(a.iters):
     op(x, y)
 torch.cuda.synchronize()
 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-s.record()
-for _ in range(a.iters):
-    op(x, y)
-e.record()
-torch.cuda.synchronize()
-ms = s.elapsed_time(e) / a.iters
+if a.flush:
+    scratch = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ms = 0.0
+    for _ in range(a.iters):
+        scratch.fill_(1)
+        s.record()
+        op(x, y)
+        e.record()
+        torch.cuda.synchronize()
+        ms += s.elapsed_time(e) / a.iters
+else:
+    s.record()
+    for _ in range(a.iters):
+        op(x, y)
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / a.iters
 print(f"{a.config} schedule={op.schedule} workers={op.workers} nnz={csr.nnz} "
       f"hot={op.hot.n_hot if op.hot else 0} ms={ms:.4f} GFLOP/s={2 * csr.nnz / ms / 1e6:.1f}")
