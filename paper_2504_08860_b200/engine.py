@@ -155,6 +155,7 @@ class SpmvOperator:
 
     ROWBLOCK_MAX_NNZ = 1 << 24  # auto: row-block owner below this size ...
     ROWBLOCK_MAX_SKEW = 8.0     # ... when no row block holds > 8x the mean
+    ROWBLOCK_MAX_BLOCKS = 4     # ... and row blocks average <= 4 nonzero blocks
     HOT_MIN_SHARE = 0.10  # stage hot columns when they hold >= 10 % of the nonzeros
     WARM_BYTES = 64 << 20  # warm tier: a 64 MB L2-resident copy of x at the next columns
 
@@ -254,11 +255,15 @@ class SpmvOperator:
     @classmethod
     def _auto_schedule(cls, hbp: HbpMatrix, hot=None) -> str:
         """stream for W = 32, plan otherwise; rowblock for small, evenly
-        spread matrices with several column blocks (one launch instead of
-        SpMV + combine; cfg1: 41 vs 61 us) unless hot staging was asked
-        about (a stream-schedule feature)."""
+        spread matrices with several column blocks and few nonzero blocks
+        per row block (one launch instead of SpMV + combine; cfg1: 38.7 vs
+        61 us) unless hot staging was asked about (a stream-schedule
+        feature).  With many small blocks per row block (uniform columns,
+        C << cols) the stream schedule wins: 0.19 vs 0.30 ms at 4M nnz,
+        64 blocks per row block (tools/prof_sched.py)."""
         R = hbp.config.row_height
-        if (hot is None and hbp.num_col_blocks > 1 and 0 < hbp.nnz <= cls.ROWBLOCK_MAX_NNZ and R <= 3072):
+        if (hot is None and hbp.num_col_blocks > 1 and 0 < hbp.nnz <= cls.ROWBLOCK_MAX_NNZ
+                and R <= 3072 and hbp.nzb <= cls.ROWBLOCK_MAX_BLOCKS * hbp.num_row_blocks):
             gpb = R // hbp.config.warp_size
             gs = hbp.group_start_c.view(-1)
             blk_nnz = gs[gpb::gpb] - gs[:-1:gpb]

@@ -114,6 +114,13 @@ def test_auto_schedule():
     skew = _hbp(n, n, key // n, key % n, np.ones(key.size), C=512, R=64)
     assert H.SpmvOperator(skew).schedule == "stream"
     assert H.SpmvOperator(_hbp(n, n, r, c, v, C=512, R=64)).schedule == "rowblock"
+    # uniform columns over many column blocks: many small blocks per row block
+    rng = np.random.default_rng(4)
+    ru = np.repeat(np.arange(n), 16)
+    key = np.unique(ru * n + rng.integers(0, n, ru.size))
+    many = _hbp(n, n, key // n, key % n, np.ones(key.size), C=256)
+    assert many.nzb > 4 * many.num_row_blocks
+    assert H.SpmvOperator(many).schedule == "stream"
     x = torch.as_tensor(np.random.default_rng(0).uniform(-1, 1, n), device="cuda")
     np.testing.assert_array_equal(op(x).cpu().numpy(),
                                   H.SpmvOperator(hbp, schedule="plan")(x).cpu().numpy())
