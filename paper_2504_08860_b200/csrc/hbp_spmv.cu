@@ -405,6 +405,9 @@ int hbp_spmv_rowblock(const hbp_format_t *f, const void *x, void *y, hbp_stream_
     // (unroll 2) / 48.4 us (no unroll); 2 x 16 x 64 regs 53.6 us.  A
     // step-batched walk (positions of 4 or 8 steps from per-step ballots, then
     // all loads) was slower: 51.6 / 66 us.
+    // f32 spills 68 B at 32 registers; 4 CTAs x 64 registers (no spill) is
+    // slower where the auto schedule picks this kernel (banded 35M / 138M nnz:
+    // 0.106 / 0.349 vs 0.102 / 0.320 ms), so both dtypes use 8 x 32.
     if (variant == 1) HBP_RB_LAUNCH(512, 3, 4);
     else if (variant == 2) HBP_RB_LAUNCH(512, 4, 2);
     else if (variant == 3) HBP_RB_LAUNCH(128, 16, 2);
