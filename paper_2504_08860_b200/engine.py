@@ -153,7 +153,8 @@ class SpmvOperator:
     direct mode (one column block): the kernel writes y itself; otherwise the
     partial (f64, compact) is combined in ascending bc."""
 
-    ROWBLOCK_MAX_NNZ = 1 << 24  # auto: row-block owner below this size ...
+    ROWBLOCK_MAX_NNZ = 1 << 24  # auto: row-block owner below this size (f64) ...
+    ROWBLOCK_MAX_NNZ_F32 = 1 << 28  # (f32: banded 138M nnz 0.32 vs 0.35 ms stream)
     ROWBLOCK_MAX_SKEW = 8.0     # ... when no row block holds > 8x the mean
     ROWBLOCK_MAX_BLOCKS = 4     # ... and row blocks average <= 4 nonzero blocks
     HOT_MIN_SHARE = 0.10  # stage hot columns when they hold >= 10 % of the nonzeros
@@ -262,7 +263,8 @@ class SpmvOperator:
         C << cols) the stream schedule wins: 0.19 vs 0.30 ms at 4M nnz,
         64 blocks per row block (tools/prof_sched.py)."""
         R = hbp.config.row_height
-        if (hot is None and hbp.num_col_blocks > 1 and 0 < hbp.nnz <= cls.ROWBLOCK_MAX_NNZ
+        cap = cls.ROWBLOCK_MAX_NNZ_F32 if hbp.dtype == torch.float32 else cls.ROWBLOCK_MAX_NNZ
+        if (hot is None and hbp.num_col_blocks > 1 and 0 < hbp.nnz <= cap
                 and R <= 3072 and hbp.nzb <= cls.ROWBLOCK_MAX_BLOCKS * hbp.num_row_blocks):
             gpb = R // hbp.config.warp_size
             gs = hbp.group_start_c.view(-1)
