@@ -295,12 +295,24 @@ __global__ void k_combine(const hbp_format_t f, const double *__restrict__ parti
 }
 
 template <typename V>
-__global__ void k_zero_empty(const hbp_format_t f, V *__restrict__ y) {
+__global__ void k_zero_empty(const hbp_format_t f, V *__restrict__ y, int64_t nrb) {
+    // same warp scan as k_combine: one rb_ptr load + ballot per 32 row blocks
     const int64_t R = f.row_height;
-    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < f.rows;
-         r += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t br = r / R;
-        if (f.rb_ptr[br] == f.rb_ptr[br + 1]) y[r] = (V)0;
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c * 32 < nrb;
+         c += nwarps) {
+        const int64_t br = c * 32 + lane;
+        const bool empty = br < nrb && f.rb_ptr[br] == f.rb_ptr[br + 1];
+        unsigned mask = __ballot_sync(0xffffffffu, empty);
+        while (mask) {
+            const int b = __ffs(mask) - 1;
+            mask &= mask - 1;
+            const int64_t rb = c * 32 + b;
+            int64_t n = f.rows - rb * R;
+            if (n > R) n = R;
+            for (int64_t local = lane; local < n; local += 32) y[rb * R + local] = (V)0;
+        }
     }
 }
 
@@ -488,9 +500,11 @@ int hbp_combine(const hbp_format_t *f, const double *partial, void *y, hbp_strea
 int hbp_zero_empty_rows(const hbp_format_t *f, void *y, hbp_stream_t stream) {
     if (!f || f->rows < 1) return HBP_E_ARG;
     cudaStream_t st = as_stream(stream);
-    unsigned grid = grid_for(f->rows, 256);
-    if (f->dtype == HBP_F64) k_zero_empty<double><<<grid, 256, 0, st>>>(*f, (double *)y);
-    else if (f->dtype == HBP_F32) k_zero_empty<float><<<grid, 256, 0, st>>>(*f, (float *)y);
+    if (f->row_height < 1) return HBP_E_ARG;
+    const int64_t nrb = (f->rows + f->row_height - 1) / f->row_height;
+    const unsigned grid = grid_for((nrb + 31) / 32 * 32, 256);
+    if (f->dtype == HBP_F64) k_zero_empty<double><<<grid, 256, 0, st>>>(*f, (double *)y, nrb);
+    else if (f->dtype == HBP_F32) k_zero_empty<float><<<grid, 256, 0, st>>>(*f, (float *)y, nrb);
     else return HBP_E_ARG;
     HBP_LAUNCH_CHECK();
     return HBP_OK;
