@@ -42,10 +42,12 @@ CONFIGS = {
     "cfg2": ("R-MAT scale 24 (16,777,216 rows), edge factor 16, Graph500 (0.57,0.19,0.19,0.05), "
              "random vertex relabel, duplicates removed, fp32, C=cols R=512 W=32",
              dict(kind="rmat", scale=24, edge_factor=16), "f32", None),
-    "cfg4": ("uniform 8,388,608^2, Poisson(16) per row, fp32, C=cols R=512 W=32",
-             dict(kind="uniform", rows=8388608, cols=8388608, mean=16.0), "f32", None),
-    "H": ("uniform 6,250,000^2, Poisson(16) per row (~100M nnz), fp32, C=cols R=512 W=32",
-          dict(kind="uniform", rows=6250000, cols=6250000, mean=16.0), "f32", None),
+    "cfg4": ("the reference generator's SyntheticSpec(8388608, 8388608, 'uniform', 16.0, seed=0) "
+             "(134,197,939 nnz), fp32, C=cols R=512 W=32",
+             dict(kind="synth", rows=8388608, cols=8388608, mean=16.0), "f32", None),
+    "H": ("the reference generator's SyntheticSpec(6250000, 6250000, 'uniform', 16.0, seed=0) "
+          "(~100M nnz), fp32, C=cols R=512 W=32",
+          dict(kind="synth", rows=6250000, cols=6250000, mean=16.0), "f32", None),
     "cfg1": ("5-point Laplacian 1024x1024 grid, fp64, C=4096 R=512 W=32",
              dict(kind="laplacian", n=1024), "f64", 4096),
     "cfg3": ("banded FEM-like 33,554,432 rows, 33 diagonals at even offsets -32..32 "
@@ -135,6 +137,9 @@ def make_matrix_gpu(cfg_name: str, seed: int, device):
     elif gen["kind"] == "uniform":
         rows, cols, rp, col, val = BI.uniform_csr_torch(gen["rows"], gen["cols"], gen["mean"],
                                                         seed, device, vdt)
+    elif gen["kind"] == "synth":
+        rows, cols, rp, col, val = BI.synth_csr_torch(gen["rows"], gen["cols"], "uniform",
+                                                      gen["mean"], seed, device, vdt)
     elif gen["kind"] == "banded":
         rows, cols, rp, col, val = BI.banded_csr_torch(gen["n"], device, vdt)
     else:
@@ -153,6 +158,15 @@ def make_matrix_cpu_sample(cfg_name: str, seed: int):
         scale = int(os.environ.get("HBP_CPU_SCALE", "20"))
         rows, cols, rp, col, val = BI.rmat_csr_numpy(scale, gen["edge_factor"], seed)
         sample = f"R-MAT scale {scale} (same generator, edge factor, geometry C=cols)"
+    elif gen["kind"] == "synth":
+        from paper_2504_08860_b200.synth import SyntheticSpec, generate_arrays
+        n = int(os.environ.get("HBP_CPU_ROWS", str(1 << 20)))
+        r, c, val = generate_arrays(SyntheticSpec(n, n, "uniform", gen["mean"], seed=seed))
+        rp = np.concatenate(([0], np.cumsum(np.bincount(r, minlength=n)))).astype(np.int64)
+        rows = cols = n
+        col = c
+        sample = (f"the reference generator's SyntheticSpec({n}, {n}, 'uniform', {gen['mean']}, "
+                  f"seed={seed}) (same generator at 1/{gen['rows'] // n} size, C=cols)")
     elif gen["kind"] == "uniform":
         n = int(os.environ.get("HBP_CPU_ROWS", str(1 << 20)))
         rng = np.random.default_rng(seed)

@@ -148,3 +148,19 @@ def uniform_csr_torch(rows: int, cols: int, mean: float, seed: int, device, valu
     row_ptr[1:] = torch.cumsum(torch.bincount(row, minlength=rows), 0)
     val = torch.rand(col.numel(), generator=g, device=device, dtype=torch.float64) * 2 - 1
     return rows, cols, row_ptr, col, val.to(value_dtype)
+
+
+def synth_csr_torch(rows: int, cols: int, pattern: str, mean: float, seed: int, device,
+                    value_dtype):
+    """The reference's own generator (synth.py generate(SyntheticSpec(...)),
+    reproduced bit for bit by paper_2504_08860_b200.synth; its stable sorts
+    run on `device`) as device CSR.  cfg4 = SyntheticSpec(8388608, 8388608,
+    "uniform", 16.0, seed=0): 134,197,939 nnz."""
+    import torch
+    from paper_2504_08860_b200.synth import SyntheticSpec, generate_arrays
+    r, c, v = generate_arrays(SyntheticSpec(rows, cols, pattern, mean, seed=seed), device=device)
+    row_ptr = torch.zeros(rows + 1, dtype=torch.int64, device=device)
+    row_ptr[1:] = torch.cumsum(torch.bincount(torch.as_tensor(r, device=device), minlength=rows), 0)
+    col = torch.as_tensor(c.astype(np.int32), device=device)
+    val = torch.as_tensor(v, device=device).to(value_dtype)
+    return rows, cols, row_ptr, col, val

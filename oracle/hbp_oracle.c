@@ -41,6 +41,35 @@ void orc_csr_kernel(const int64_t *row_ptr, const int64_t *col_idx,
     }
 }
 
+/* The reference's y for selected rows without its dense layout: per row,
+ * each column block's run is summed left to right from 0.0 exactly as
+ * hbp_block_kernel (_kernels.py:22-47) chases the row's add_sign chain (a
+ * row's elements in a block are its CSR run, step order), and the blocks'
+ * partials are folded in ascending bc as combine (engine.py:196-201) does.
+ * Empty blocks contribute the dense partial's +0.0, which never changes a
+ * sum that started from 0.0 (partials are never -0.0), so they are skipped.
+ * rows_sel[k] names the k-th row; out[k] gets its y.  Used for parity at
+ * sizes where the dense rows x ncb arrays do not fit host memory. */
+void orc_rows_blocked(const int64_t *row_ptr, const int64_t *col_idx,
+                      const double *values, const double *x, int64_t C,
+                      const int64_t *rows_sel, int64_t nsel, double *out) {
+    for (int64_t k = 0; k < nsel; ++k) {
+        const int64_t i = rows_sel[k];
+        double y = 0.0;
+        int first = 1;
+        int64_t j = row_ptr[i];
+        while (j < row_ptr[i + 1]) {
+            const int64_t bc = col_idx[j] / C;
+            double s = 0.0;
+            for (; j < row_ptr[i + 1] && col_idx[j] / C == bc; ++j)
+                s += values[j] * x[col_idx[j]];
+            if (first) y = s, first = 0;
+            else y += s;
+        }
+        out[k] = y;
+    }
+}
+
 /* reorder.py:112-136 build_block_permutation: rows claim slots in ascending
  * local-row order; preliminary slot = hash_slot (reorder.py:106-109) mod n;
  * +1 linear probing with wraparound.  Returns the probe count (inspections of

@@ -101,6 +101,23 @@ def csr_spmv(row_ptr, col_idx, values, x):
     return out
 
 
+def rows_blocked(row_ptr, col_idx, values, x, C, rows_sel):
+    """y[rows_sel] as the reference computes it (hbp_block_kernel per column
+    block, _kernels.py:22-47, then combine in ascending bc, engine.py:196-201)
+    without the dense layout: CSR rows with C-wide column blocks (C
+    restatement, orc_rows_blocked).  row_ptr / col_idx / values may be the
+    CSR of just the selected rows' neighbourhood as long as rows_sel indexes
+    into row_ptr."""
+    sel = np.ascontiguousarray(rows_sel, np.int64)
+    out = np.zeros(sel.size)
+    lib().orc_rows_blocked(_p(np.ascontiguousarray(row_ptr, np.int64)),
+                           _p(np.ascontiguousarray(col_idx, np.int64)),
+                           _p(np.ascontiguousarray(values, np.float64)),
+                           _p(np.ascontiguousarray(x, np.float64)), I64(C), _p(sel),
+                           I64(sel.size), _p(out))
+    return out
+
+
 def dense_oracle_spmv(rows, row, col, val, x):
     """formats.py:276-283: np.add.at brute force."""
     y = np.zeros(rows)

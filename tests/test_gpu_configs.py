@@ -1,0 +1,211 @@
+"""Parity at the BASELINE.json configurations, at the size each is benchmarked.
+
+- cfg1 (5-point Laplacian 1024^2, fp64, C=4096, R=512, W=32): the full oracle
+  pipeline in the reference's dense layout; every reference array (grid,
+  hash parameters, probe count, the six HBP arrays) and y bitwise, for every
+  schedule.
+- cfg3 structure (banded, 33 diagonals, fp64, C=4096): a 2^20-row instance
+  through the full oracle pipeline, bitwise; and the benchmarked 33.5M-row,
+  1.1B-nnz matrix through per-block spot checks (hash permutation and probe
+  count of sampled blocks vs the reference's per-block FCFS probing,
+  slot lengths, zero_row, group sizes, the hash parameters from the
+  reference's own 4096-entry sample) and sampled row blocks' y bitwise
+  against the reference's per-block order (O.rows_blocked).
+- H and cfg4 (uniform, fp32, C=cols; the reference generator): y within
+  1e-5 componentwise of a host f64 evaluation on sampled rows, zero rows
+  exactly zero; cfg4 is the SURVEY matrix (134,197,939 nnz).
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import has_gpu
+
+pytestmark = pytest.mark.gpu
+
+if has_gpu():
+    import torch
+    import paper_2504_08860_b200 as H
+    from oracle import oracle as O
+    import bench
+    import bench_inputs as BI
+
+FP32_TOL = 1e-5  # north_star: 1e-5 relative for fp32 (componentwise, |A||x| scale)
+
+
+def _free():
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()
+
+
+def _full_pipeline_bitwise(rows, cols, rp, ci, v, C, schedules):
+    """Every reference array and y bitwise against the oracle pipeline."""
+    R, W = 512, 32
+    r = np.repeat(np.arange(rows), np.diff(rp))
+    p = O.pipeline(rows, cols, r, ci, v, C, R, W)
+    cfg = H.PartitionConfig(col_width=C, row_height=R, warp_size=W)
+    csr = H.CsrMatrix(rows, cols, rp, ci, v)
+    grid = H.make_grid(csr, cfg)
+    g = p["grid"]
+    np.testing.assert_array_equal(grid.block_nnz, g.block_nnz)
+    np.testing.assert_array_equal(grid.block_elem_start, g.block_elem_start)
+    params = H.sample_hash_params(grid, cfg)
+    assert (params.a, params.b, params.c, params.d) == tuple(p["params"])
+    ctr = H.OpCounter()
+    perms = H.hash_permutations(grid, params, counter=ctr)
+    assert ctr.probes == p["probes"]
+    hbp = H.build_hbp(csr, grid, perms)
+    ref = hbp.to_reference()
+    for k in ("col", "data", "add_sign", "zero_row", "group_start", "output_hash"):
+        np.testing.assert_array_equal(ref[k], getattr(p["hbp"], k), err_msg=k)
+    del ref
+    x = np.random.default_rng(0).uniform(-1, 1, cols)
+    want = O.hbp_spmv(p["hbp"], x, workers=8)
+    xd = torch.as_tensor(x, device="cuda")
+    got = {}
+    for schedule in schedules:
+        op = H.SpmvOperator(hbp, schedule=schedule)
+        y = op(xd).cpu().numpy()
+        np.testing.assert_array_equal(y, want, err_msg=f"schedule {schedule} ({op.schedule})")
+        got[schedule] = op.schedule
+    np.testing.assert_array_equal(H.hbp_spmv(hbp, x).cpu().numpy(), want)
+    return got
+
+
+def test_cfg1_full_size_bitwise():
+    rows, cols, rp, ci, v = BI.laplacian_csr(1024)
+    assert rp[-1] == 5_238_784
+    got = _full_pipeline_bitwise(rows, cols, rp, ci, v, 4096, (None, "stream", "plan"))
+    assert got[None] == "rowblock"  # the auto schedule cfg1 is benchmarked with
+    _free()
+
+
+def test_cfg3_structure_2p20_rows_bitwise():
+    rows, cols, rp, ci, v = BI.banded_csr(1 << 20)
+    assert rp[-1] == 33 * (1 << 20) - 544
+    _full_pipeline_bitwise(rows, cols, rp, ci, v, 4096, (None, "stream", "rowblock", "plan"))
+    _free()
+
+
+def _host_rows(rp_d, col_d, val_d, r0, r1):
+    """CSR of rows [r0, r1) on the host (row_ptr rebased to 0)."""
+    rp = rp_d[r0:r1 + 1].cpu().numpy().astype(np.int64)
+    e0, e1 = int(rp[0]), int(rp[-1])
+    return (rp - e0, col_d[e0:e1].cpu().numpy().astype(np.int64),
+            val_d[e0:e1].cpu().numpy().astype(np.float64))
+
+
+def test_cfg3_full_size_spot_checks_bitwise():
+    """The benchmarked cfg3 matrix (33,554,432 rows, 1,107,295,712 nnz, fp64,
+    C=4096): the dense reference layout would need 275G slots, so the
+    per-block functions of the reference are checked on sampled blocks and y
+    bitwise on sampled row blocks."""
+    dev = torch.device("cuda", 0)
+    desc, rows, cols, rp_d, col_d, val_d, C, vdt = bench.make_matrix_gpu("cfg3", 0, dev)
+    assert int(rp_d[-1]) == 33 * rows - 544
+    R, W = 512, 32
+    cfg = H.PartitionConfig(col_width=C, row_height=R, warp_size=W)
+    csr = H.CsrMatrix(rows, cols, rp_d, col_d, val_d)
+    grid = H.make_grid(csr, cfg)
+    params = H.sample_hash_params(grid, cfg)
+    ncb = -(-cols // C)
+
+    # hash parameters from the reference's own sample (reorder.py:69-103):
+    # the 4096 flat (bc, row) indices of the dense row_counts, counted here
+    flat = O.sample_indices(ncb * rows, 4096, 0)
+    sample = np.empty(flat.size, np.int64)
+    for k, f in enumerate(flat):
+        bc, row = divmod(int(f), rows)
+        rp, ci, _ = _host_rows(rp_d, col_d, val_d, row, row + 1)
+        sample[k] = int(((ci >= bc * C) & (ci < (bc + 1) * C)).sum())
+    assert (params.a, params.b, params.c, params.d) == tuple(O.params_from_sample(sample, R))
+
+    perms = H.hash_permutations(grid, params)
+    hbp = H.build_hbp(csr, grid, perms, with_add_sign=False)
+    nzb, gpb = hbp.nzb, R // W
+    blk_br, blk_bc = hbp.blk_br.cpu().numpy(), hbp.blk_bc.cpu().numpy()
+    gs = hbp.group_start_c
+    rng = np.random.default_rng(3)
+    # first / last blocks (ragged edges) plus a random sample
+    pick = np.unique(np.concatenate(([0, 1, nzb - 2, nzb - 1], rng.choice(nzb, 60, replace=False))))
+    for i in pick:
+        br, bc = int(blk_br[i]), int(blk_bc[i])
+        r0, n = br * R, min(R, rows - br * R)
+        rp, ci, _ = _host_rows(rp_d, col_d, val_d, r0, r0 + n)
+        inb = (ci >= bc * C) & (ci < (bc + 1) * C)
+        lens = np.bincount(np.repeat(np.arange(n), np.diff(rp))[inb], minlength=n)
+        want_perm, _ = O.hash_perm_block(lens, params.a, params.b, params.c, params.d)
+        got_perm = hbp.perm[i * R:i * R + n].cpu().numpy().view(np.uint32)
+        np.testing.assert_array_equal(got_perm, want_perm, err_msg=f"block {i}")
+        slot_len = hbp.slot_len[i * R:i * R + n].cpu().numpy().astype(np.int64)
+        np.testing.assert_array_equal(slot_len, lens[want_perm], err_msg=f"block {i}")
+        zr = O.zero_row_for(slot_len == 0, W)
+        np.testing.assert_array_equal(hbp.zero_row_c[i * R:i * R + n].cpu().numpy(), zr)
+        ng = -(-n // W)
+        gsz = np.diff(gs[i * gpb:i * gpb + ng + 1].cpu().numpy())
+        pad = np.zeros(ng * W, np.int64)
+        pad[:n] = slot_len
+        np.testing.assert_array_equal(gsz, pad.reshape(ng, W).sum(1), err_msg=f"block {i}")
+
+    # y bitwise on sampled row blocks (every schedule the auto rule can pick)
+    x = np.random.default_rng(0).uniform(-1, 1, cols)
+    xd = torch.as_tensor(x, device=dev)
+    nrb = -(-rows // R)
+    rbs = np.unique(np.concatenate(([0, nrb - 1], rng.choice(nrb, 30, replace=False))))
+    for schedule in (None, "stream"):
+        op = H.SpmvOperator(hbp, schedule=schedule)
+        y = op(xd)
+        for br in rbs:
+            r0, r1 = int(br) * R, min(rows, (int(br) + 1) * R)
+            rp, ci, v = _host_rows(rp_d, col_d, val_d, r0, r1)
+            want = O.rows_blocked(rp, ci, v, x, C, np.arange(r1 - r0))
+            np.testing.assert_array_equal(y[r0:r1].cpu().numpy(), want,
+                                          err_msg=f"{op.schedule} row block {br}")
+        del op, y
+    del hbp, grid, csr, rp_d, col_d, val_d
+    _free()
+
+
+def _sampled_rows_f32(config, expect_nnz=None):
+    dev = torch.device("cuda", 0)
+    desc, rows, cols, rp_d, col_d, val_d, C, vdt = bench.make_matrix_gpu(config, 0, dev)
+    assert vdt == torch.float32
+    if expect_nnz is not None:
+        assert int(rp_d[-1]) == expect_nnz
+    cfg = H.PartitionConfig(col_width=C)
+    csr = H.CsrMatrix(rows, cols, rp_d, col_d, val_d)
+    grid = H.make_grid(csr, cfg)
+    hbp = H.build_hbp(csr, grid, H.hash_permutations(grid, H.sample_hash_params(grid, cfg)),
+                      with_add_sign=False, with_zero_row=False)
+    x32 = np.random.default_rng(0).uniform(-1, 1, cols).astype(np.float32)
+    x64 = x32.astype(np.float64)
+    op = H.SpmvOperator(hbp)
+    y = op(torch.as_tensor(x32, device=dev)).cpu().numpy().astype(np.float64)
+    rp = rp_d.cpu().numpy()
+    ci = col_d.cpu().numpy()
+    v = val_d.cpu().numpy().astype(np.float64)
+    rng = np.random.default_rng(5)
+    sel = np.unique(np.concatenate(([0, rows - 1], rng.choice(rows, 20000, replace=False))))
+    worst = 0.0
+    for r in sel:
+        a, b = int(rp[r]), int(rp[r + 1])
+        ref = float(np.dot(v[a:b], x64[ci[a:b]]))
+        scale = float(np.dot(np.abs(v[a:b]), np.abs(x64[ci[a:b]])))
+        if scale == 0.0:
+            assert y[r] == 0.0, r  # empty (or all-zero) rows exactly zero
+            continue
+        worst = max(worst, abs(y[r] - ref) / scale)
+    assert worst <= FP32_TOL, worst
+    del op, hbp, grid, csr, rp_d, col_d, val_d
+    _free()
+    return worst
+
+
+def test_headline_H_full_size_fp32_within_tolerance():
+    _sampled_rows_f32("H")
+
+
+def test_cfg4_reference_generator_full_size_fp32_within_tolerance():
+    _sampled_rows_f32("cfg4", expect_nnz=134_197_939)
