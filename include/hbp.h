@@ -12,8 +12,12 @@
  *   - nothing allocates: outputs and scratch are caller-provided; functions
  *     that need CUB scratch take (temp, temp_bytes) and report the size when
  *     called with temp == NULL (CUB convention);
- *   - no global mutable state: the work ticket lives in caller memory, so
- *     calls are re-entrant per stream;
+ *   - no mutable state on the data path: the work ticket, partials and
+ *     per-SpMV scratch live in caller memory, so calls are re-entrant per
+ *     stream and per device.  Process-wide state is limited to (a) a
+ *     per-device cache of kernel launch attributes (idempotent) and (b) the
+ *     A/B tuning selectors hbp_stream_set_variant / HBP_STREAM_VARIANT /
+ *     HBP_ROWBLOCK_VARIANT, read once; every variant computes the same y;
  *   - return value: HBP_OK, an HBP_E_* code, or a cudaError_t (< 1000).
  *     hbp_status_string() maps it to the reference's error vocabulary.
  *
@@ -228,6 +232,15 @@ int hbp_walk_chains(int64_t rows, int64_t cols, int64_t col_width, int64_t row_h
                     int64_t nnz, int64_t *row_out, int32_t *seen, int32_t *err,
                     hbp_stream_t stream);
 
+/* deserialize_hbp (hbp.py:349-381) support: per dense slot [ncb*rows] the
+ * length of its add_sign chain (0 for empty slots, zero_row < 0), walked as
+ * hbp_block_kernel walks it (_kernels.py:35-46) but bounded to the slot's
+ * group range.  Validation is the caller's (hbp.py:102-135 first). */
+int hbp_chain_lengths(int64_t rows, int64_t cols, int64_t col_width, int64_t row_height,
+                      int64_t warp_size, const int32_t *zero_row, const int64_t *group_start,
+                      const int32_t *add_sign, int64_t nnz, int32_t *len_out,
+                      hbp_stream_t stream);
+
 /* ------------------------------------------------------------------ SpMV */
 typedef struct {
     int64_t rows, cols, col_width, row_height, warp_size;
@@ -369,6 +382,11 @@ int hbp_combine(const hbp_format_t *f, const double *partial, void *y, hbp_strea
  * (engine.py:196-201), then writes y (+0.0 for empty row blocks).  Bitwise
  * equal to hbp_spmv_blocks + hbp_combine.  row_height <= 3072. */
 int hbp_spmv_rowblock(const hbp_format_t *f, const void *x, void *y, hbp_stream_t stream);
+/* engine.py:196-201 combine of a caller-made dense PartialVector
+ * partial[bc*rows + row] (PartialVector(values, rows, ncb)): y = seg 0, then
+ * y += seg bc for bc = 1..ncb-1 (__dadd_rn), f64 out. */
+int hbp_combine_dense(const double *partial, int64_t rows, int64_t ncb, double *y,
+                      hbp_stream_t stream);
 /* Zero y for row blocks with no nonzero block (direct mode companion). */
 int hbp_zero_empty_rows(const hbp_format_t *f, void *y, hbp_stream_t stream);
 /* Dense PartialVector view (engine.py:59-68): partial_dense[bc*rows + row]. */

@@ -101,6 +101,8 @@ _SIGS = {
                              c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
     "hbp_walk_chains": [c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64,
                         c_vp, c_vp, c_vp, c_vp],
+    "hbp_chain_lengths": [c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp],
+    "hbp_combine_dense": [c_vp, c_i64, c_i64, c_vp, c_vp],
     "hbp_spmv_blocks": [ctypes.POINTER(FormatT), ctypes.POINTER(ScheduleT), c_vp, c_vp, c_vp,
                         c_vp],
     "hbp_balanced_workers": [ctypes.POINTER(FormatT), ctypes.POINTER(c_i64)],

@@ -694,6 +694,37 @@ __global__ void k_walk_chains(int64_t rows, int64_t cols, int64_t C, int64_t R, 
     }
 }
 
+// Slot lengths of a reference-layout matrix (deserialize_hbp): per dense slot
+// the number of elements on its add_sign chain, walked as hbp_block_kernel
+// walks it (_kernels.py:35-46) but bounded to the group's element range, so a
+// corrupt chain ends instead of running away (validation is separate).
+__global__ void k_chain_lengths(int64_t rows, int64_t R, int64_t W, int64_t ncb, int64_t gpc,
+                                const int32_t *__restrict__ zero_row,
+                                const int64_t *__restrict__ group_start,
+                                const int32_t *__restrict__ add, int64_t nnz,
+                                int32_t *__restrict__ len_out) {
+    int64_t total = ncb * rows;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t zr = zero_row[i];
+        int32_t k = 0;
+        if (zr >= 0) {
+            int64_t bc = i / rows, row = i - bc * rows;
+            int64_t br = row / R, s = row - br * R, g = s / W, q = s - g * W;
+            int64_t gb = bc * gpc + br * (R / W) + g;
+            int64_t gs = group_start[gb], ge = group_start[gb + 1];
+            int64_t j = gs + q - zr;
+            for (;;) {
+                ++k;
+                int32_t st = (j >= 0 && j < nnz) ? add[j] : -1;
+                if (st < 0 || j + st >= ge) break;
+                j += st;
+            }
+        }
+        len_out[i] = k;
+    }
+}
+
 }  // namespace
 
 // ====================================================================== ABI
@@ -978,6 +1009,23 @@ int hbp_walk_chains(int64_t rows, int64_t cols, int64_t col_width, int64_t row_h
     k_walk_chains<<<grid_for(ncb * rows, kThreads), kThreads, 0, as_stream(stream)>>>(
         rows, cols, col_width, R, W, ncb, gpc, zero_row, output_hash, group_start, col, add_sign,
         nnz, row_out, seen, err);
+    HBP_LAUNCH_CHECK();
+    return HBP_OK;
+}
+
+int hbp_chain_lengths(int64_t rows, int64_t cols, int64_t col_width, int64_t row_height,
+                      int64_t warp_size, const int32_t *zero_row, const int64_t *group_start,
+                      const int32_t *add_sign, int64_t nnz, int32_t *len_out,
+                      hbp_stream_t stream) {
+    if (warp_size < 1 || row_height < 1 || row_height % warp_size || col_width < 1)
+        return HBP_E_ARG;
+    if (rows < 1 || cols < 1) return HBP_OK;
+    int64_t R = row_height, W = warp_size;
+    int64_t nrb = (rows + R - 1) / R, ncb = (cols + col_width - 1) / col_width;
+    int64_t last = rows - (nrb - 1) * R;
+    int64_t gpc = (nrb - 1) * (R / W) + (last + W - 1) / W;
+    k_chain_lengths<<<grid_for(ncb * rows, kThreads), kThreads, 0, as_stream(stream)>>>(
+        rows, R, W, ncb, gpc, zero_row, group_start, add_sign, nnz, len_out);
     HBP_LAUNCH_CHECK();
     return HBP_OK;
 }

@@ -390,6 +390,18 @@ void dispatch_spmv(const hbp_format_t *f, const hbp_schedule_t *s, const void *x
     }
 }
 
+// engine.py:196-201 combine over a caller-made dense PartialVector
+// [ncb][rows] (reference layout): y = seg0; y += seg_bc, ascending bc.
+__global__ void k_combine_dense(const double *__restrict__ p, int64_t rows, int64_t ncb,
+                                double *__restrict__ y) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        double s = p[r];
+        for (int64_t bc = 1; bc < ncb; ++bc) s = __dadd_rn(s, p[bc * rows + r]);
+        y[r] = s;
+    }
+}
+
 }  // namespace
 
 extern "C" {
@@ -493,6 +505,15 @@ int hbp_combine(const hbp_format_t *f, const double *partial, void *y, hbp_strea
     else if (f->dtype == HBP_F32)
         k_combine<float><<<grid, threads, 0, st>>>(*f, partial, (float *)y, nrb);
     else return HBP_E_ARG;
+    HBP_LAUNCH_CHECK();
+    return HBP_OK;
+}
+
+int hbp_combine_dense(const double *partial, int64_t rows, int64_t ncb, double *y,
+                      hbp_stream_t stream) {
+    if (rows < 0 || ncb < 1) return HBP_E_ARG;
+    if (rows == 0) return HBP_OK;
+    k_combine_dense<<<grid_for(rows, 256), 256, 0, as_stream(stream)>>>(partial, rows, ncb, y);
     HBP_LAUNCH_CHECK();
     return HBP_OK;
 }

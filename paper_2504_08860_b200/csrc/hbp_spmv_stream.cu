@@ -39,11 +39,15 @@
 // at most u of the pair's magnitude), everything else summed in f64, one
 // final rounding to f32: componentwise error <= ~3u |A||x| (1.8e-7).
 #include <cuda_runtime.h>
+
+#include <atomic>
 #include <stdint.h>
 #include <stdlib.h>
 
 #include "hbp.h"
 #include "hbp_common.cuh"
+
+constexpr int kMaxDevices = 64;
 
 using namespace hbp;
 
@@ -702,8 +706,13 @@ __global__ void __launch_bounds__(NT, MINB)
             double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
             for (int64_t i = lo; i < hi; ++i) {
                 const double *pp = partial + (int64_t)f.rb_blk[i] * R + r0 + lane;
-                const double p0 = __ldcg(pp), p1 = __ldcg(pp + 32), p2 = __ldcg(pp + 64),
-                             p3 = __ldcg(pp + 96);
+                // rows past the row block's end belong to the next block's
+                // partial (or lie past the allocation for the last one)
+                const int32_t r = r0 + lane;
+                const double p0 = r < nrows ? __ldcg(pp) : 0.0,
+                             p1 = r + 32 < nrows ? __ldcg(pp + 32) : 0.0,
+                             p2 = r + 64 < nrows ? __ldcg(pp + 64) : 0.0,
+                             p3 = r + 96 < nrows ? __ldcg(pp + 96) : 0.0;
                 if (i == lo) a0 = p0, a1 = p1, a2 = p2, a3 = p3;
                 else a0 = __dadd_rn(a0, p0), a1 = __dadd_rn(a1, p1), a2 = __dadd_rn(a2, p2),
                      a3 = __dadd_rn(a3, p3);
@@ -875,10 +884,14 @@ template <typename V, bool EXACT, int CH, int NB, int MINB, int XM, int KT, int 
 int launch(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y,
            double *partial, cudaStream_t st) {
     const size_t smem = ring_smem<V, CH, NB, NT>() + (HOT ? (size_t)f->n_hot * sizeof(V) : 0);
-    static size_t attr = 0;
-    if (attr != smem) {
+    // kernel attributes are per device: cache the shared-memory size they were
+    // last set for on each device (idempotent, so a lost race only repeats it)
+    static std::atomic<size_t> attr[kMaxDevices];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return HBP_E_ARG;
+    if (attr[dev].load(std::memory_order_relaxed) != smem) {
         set_attributes(k_spmv_stream<V, EXACT, CH, NB, MINB, XM, KT, LMIN, NT, HOT>, smem, MINB);
-        attr = smem;
+        attr[dev].store(smem, std::memory_order_relaxed);
     }
     unsigned grid = (unsigned)((b->workers + NT / 32 - 1) / (NT / 32));
     k_spmv_stream<V, EXACT, CH, NB, MINB, XM, KT, LMIN, NT, HOT><<<grid, NT, smem, st>>>(
@@ -902,14 +915,18 @@ int occupancy_of(const hbp_format_t *f, int *per_sm, int *warps_per_cta) {
 // modular passes) are in the git history; 128/4/3x256 with L1::no_allocate x
 // gathers and KT=12, LMIN=4 won on cfg2 and H.
 constexpr int kVariants = 4;
-int g_variant = -1;  // tuning knob (HBP_STREAM_VARIANT / hbp_stream_set_variant)
+// tuning knob for A/B sweeps only (HBP_STREAM_VARIANT / hbp_stream_set_variant):
+// process-wide by design, read once; every variant computes the same y
+std::atomic<int> g_variant{-1};
 int variant() {
-    if (g_variant < 0) {
+    int v = g_variant.load(std::memory_order_relaxed);
+    if (v < 0) {
         const char *e = getenv("HBP_STREAM_VARIANT");
-        g_variant = e ? atoi(e) : 0;
-        if (g_variant < 0 || g_variant >= kVariants) g_variant = 0;
+        v = e ? atoi(e) : 0;
+        if (v < 0 || v >= kVariants) v = 0;
+        g_variant.store(v, std::memory_order_relaxed);
     }
-    return g_variant;
+    return v;
 }
 
 bool staged(const hbp_format_t *f) { return f->n_hot > 0 && f->scol && f->hot_cols; }

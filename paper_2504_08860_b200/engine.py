@@ -54,19 +54,29 @@ class ExecutionPlan:
 
 
 class PartialVector:
-    """engine.py:59-68.  ``compact`` is f64 [nzb * R] (block-major, original
-    local row); ``values`` / ``segment`` give the reference's dense
-    [bc][global row] layout on demand."""
+    """engine.py:59-68: per-(column block, row) partial sums.
 
-    def __init__(self, hbp: HbpMatrix, compact: torch.Tensor):
-        self.hbp = hbp
-        self.compact = compact
-        self.rows = hbp.rows
-        self.num_col_blocks = hbp.num_col_blocks
-        self._dense = None
+    ``PartialVector(values, rows, num_col_blocks)`` is the reference's
+    constructor: a caller-made dense [bc][global row] vector (numpy or a
+    device tensor, float64), which block_spmv writes into and combine sums.
+    The runtime path (run_spmv) makes ``PartialVector.from_compact(hbp, c)``:
+    f64 [nzb * R] (block-major, original local row), with ``values`` /
+    ``segment`` expanding to the dense layout on demand."""
+
+    def __init__(self, values, rows: int, num_col_blocks: int):
+        self.rows, self.num_col_blocks = int(rows), int(num_col_blocks)
+        self.hbp = None
+        self.compact = None
+        self._dense = values
+
+    @classmethod
+    def from_compact(cls, hbp: HbpMatrix, compact: torch.Tensor) -> "PartialVector":
+        pv = cls(None, hbp.rows, hbp.num_col_blocks)
+        pv.hbp, pv.compact = hbp, compact
+        return pv
 
     @property
-    def values(self) -> torch.Tensor:
+    def values(self):
         if self._dense is None:
             d = torch.empty(self.num_col_blocks * self.rows, dtype=torch.float64,
                             device=self.compact.device)
@@ -75,7 +85,7 @@ class PartialVector:
             self._dense = d
         return self._dense
 
-    def segment(self, bc: int) -> torch.Tensor:
+    def segment(self, bc: int):
         return self.values[bc * self.rows:(bc + 1) * self.rows]
 
 
@@ -289,8 +299,11 @@ class SpmvOperator:
         device scalar) is given -- the power-iteration step without a separate
         scaling pass (stream schedule, one column block)."""
         hbp = self.hbp
+        self._check_vec(x, hbp.cols, "x")
         if y is None:
             y = torch.empty(hbp.rows, dtype=hbp.dtype, device=hbp.data.device)
+        else:
+            self._check_vec(y, hbp.rows, "y")
         f = self._fmt
         s = L.stream()
         if x_sumsq is not None:
@@ -315,6 +328,17 @@ class SpmvOperator:
             self._blocks(f, x, self.partial, y if f.reserved & 4 else None, s)
             L.call("hbp_combine", ctypes.byref(f), L.P(self.partial), L.P(y), s)
         return y
+
+    def _check_vec(self, v, n: int, name: str) -> None:
+        """Device, dtype, contiguity and length of a caller vector (the
+        kernels take raw pointers)."""
+        d = self.hbp.data
+        if not isinstance(v, torch.Tensor) or not v.is_cuda or v.device != d.device:
+            raise ValueError(f"{name} must be a CUDA tensor on {d.device}")
+        if v.dtype != d.dtype:
+            raise ValueError(f"{name} dtype {v.dtype} != matrix dtype {d.dtype}")
+        if not v.is_contiguous() or v.numel() != n:
+            raise ValueError(f"{name} length {v.numel()} != {n} (or not contiguous)")
 
     def capture(self, x: torch.Tensor, y: torch.Tensor) -> "torch.cuda.CUDAGraph":
         """Capture one SpMV (+combine) on fixed x / y buffers in a CUDA graph."""
@@ -390,7 +414,12 @@ class HostPipeline:
 
 
 def block_spmv(hbp: HbpMatrix, block, x, partial: PartialVector) -> None:
-    """engine.py:123-134: run one block into the partial vector."""
+    """engine.py:123-134: run one block (the reference's lane-per-row chain
+    walk, hbp_spmv_blocks with one worker) into the partial vector: entry
+    bc*rows + br*R + output_hash[slot] of a dense PartialVector (numpy
+    arrays are updated in place, like the reference), or the block's compact
+    slice of a runtime one.  Every row of the block is written (+0.0 for
+    empty rows, which a pre-zeroed partial holds already)."""
     br, bc = int(block[0]), int(block[1])
     keys = (hbp.blk_bc.to(torch.int64) * hbp.num_row_blocks + hbp.blk_br).cpu().numpy()
     k = bc * hbp.num_row_blocks + br
@@ -411,9 +440,27 @@ def block_spmv(hbp: HbpMatrix, block, x, partial: PartialVector) -> None:
     sched.workers, sched.fixed_count = 1, 0
     ticket = torch.zeros(1, dtype=torch.int32, device=xd.device)
     sched.ticket = ticket.data_ptr()
-    L.call("hbp_spmv_blocks", ctypes.byref(f), ctypes.byref(sched), L.P(xd),
-           L.c_vp(partial.compact.data_ptr() + i * R * esz8), L.P(None), L.stream())
-    partial._dense = None
+    n = min(R, hbp.rows - br * R)
+    if partial.compact is not None:
+        if partial.hbp is not hbp:
+            raise ValueError("partial belongs to another HbpMatrix")
+        out = torch.empty(R, dtype=torch.float64, device=xd.device)
+    else:
+        if (partial.rows, partial.num_col_blocks) != (hbp.rows, hbp.num_col_blocks):
+            raise ValueError("partial length disagrees with the matrix")
+        out = torch.empty(R, dtype=torch.float64, device=xd.device)
+    L.call("hbp_spmv_blocks", ctypes.byref(f), ctypes.byref(sched), L.P(xd), L.P(out),
+           L.P(None), L.stream())
+    if partial.compact is not None:
+        partial.compact[i * R:i * R + n] = out[:n]
+        partial._dense = None
+        return
+    base = bc * hbp.rows + br * R
+    vals = partial.values
+    if isinstance(vals, torch.Tensor):
+        vals[base:base + n] = out[:n].to(device=vals.device, dtype=vals.dtype)
+    else:
+        vals[base:base + n] = out[:n].cpu().numpy()
 
 
 def run_spmv(hbp: HbpMatrix, x, plan: ExecutionPlan, workers: int):
@@ -441,11 +488,24 @@ def run_spmv(hbp: HbpMatrix, x, plan: ExecutionPlan, workers: int):
            L.P(None), L.stream())
     log = ExecutionLog(lw[:n].cpu().numpy(), lk[:n].cpu().numpy(), ls[:n].cpu().numpy(),
                        le[:n].cpu().numpy())
-    return PartialVector(hbp, compact), log
+    return PartialVector.from_compact(hbp, compact), log
 
 
 def combine(partial: PartialVector) -> torch.Tensor:
-    """engine.py:196-201: sum partials over column blocks, ascending bc."""
+    """engine.py:196-201: sum partials over column blocks, ascending bc
+    (f64 device tensor for a caller-made dense PartialVector, the matrix's
+    dtype for a runtime one)."""
+    if partial.compact is None:
+        v = partial.values
+        dev = L.require_cuda()
+        vd = (v if isinstance(v, torch.Tensor) else torch.as_tensor(np.asarray(v, np.float64)))
+        vd = vd.to(device=dev, dtype=torch.float64).contiguous()
+        if vd.numel() != partial.rows * partial.num_col_blocks:
+            raise ValueError("partial length disagrees with rows * num_col_blocks")
+        y = torch.empty(partial.rows, dtype=torch.float64, device=dev)
+        L.call("hbp_combine_dense", L.P(vd), L.c_i64(partial.rows),
+               L.c_i64(partial.num_col_blocks), L.P(y), L.stream())
+        return y
     hbp = partial.hbp
     y = torch.empty(hbp.rows, dtype=hbp.dtype, device=partial.compact.device)
     f = hbp.format_struct()
@@ -490,14 +550,24 @@ def block2d_spmv_baseline(csr, grid: BlockGrid, x, workers: int = 1) -> torch.Te
     return y
 
 
-def hbp_spmv(hbp: HbpMatrix, x, workers: int | None = None) -> torch.Tensor:
+def hbp_spmv(hbp: HbpMatrix, x, workers: int = 1, *, gpu_workers: int | None = None
+             ) -> torch.Tensor:
     """engine.py:228-232: plan, run and combine in one call (device tensor y).
-    workers=None fills the device with persistent warps."""
+
+    ``workers`` keeps the reference's signature, default and validation
+    (plan_execution: ValueError for < 1).  The result does not depend on it
+    (engine.py:1-8: bitwise identical for any worker count), so the GPU
+    operator always fills the device; ``gpu_workers`` pins the number of
+    persistent warps instead.  The operator (and its partial / ticket
+    scratch) is cached per (gpu_workers, CUDA stream): calls on different
+    streams never share scratch."""
+    if int(workers) < 1:
+        raise ValueError("workers must be >= 1")
     xd = _as_x(hbp, x)
-    key = ("op", workers)
+    key = ("op", gpu_workers, torch.cuda.current_stream(xd.device).cuda_stream)
     op = hbp._ops.get(key)
     if op is None:
-        op = SpmvOperator(hbp, workers)
+        op = SpmvOperator(hbp, gpu_workers)
         hbp._ops[key] = op
     return op(xd)
 

@@ -32,7 +32,7 @@ from .partition import (BlockGrid, PartitionConfig, _check_gpu_geometry, groups_
 from .reorder import BlockPermutations
 
 __all__ = ["HbpMatrix", "HbpFormatError", "build_hbp", "hbp_to_triplets", "serialize_hbp",
-           "deserialize_hbp", "save_hbp", "load_hbp"]
+           "deserialize_hbp", "save_hbp", "load_hbp", "validate_reference_arrays"]
 
 MAGIC = b"HBP1"
 VERSION = 1
@@ -325,49 +325,67 @@ class HbpMatrix:
 
     # ---- validation (hbp.py:102-135) on the reference-layout views
     def validate_structure(self) -> None:
-        nrb, ncb = self.grid_shape
-        R, W = self.config.row_height, self.config.warp_size
-        if nrb != -(-self.rows // R) or ncb != -(-self.cols // self.config.col_width):
-            raise HbpFormatError("grid shape inconsistent with dimensions")
-        nnz = self.nnz
-        if not (self.col.numel() == self.data.numel()
-                and (self._add_sign is None or self._add_sign.numel() == nnz)):
-            raise HbpFormatError("element array lengths differ")
-        n_slots = ncb * self.rows
-        zr, oh, gs = self.zero_row, self.output_hash, self.group_start
-        if zr.numel() != n_slots or oh.numel() != n_slots:
-            raise HbpFormatError("slot array length mismatch")
-        n_groups = ncb * groups_per_col_block(self.rows, R, W)
-        if gs.numel() != n_groups + 1:
-            raise HbpFormatError("group_start length mismatch")
-        ends = gs[[0, -1]].cpu().tolist()
-        if ends[0] != 0 or ends[1] != nnz:
-            raise HbpFormatError("group_start must span [0, nnz]")
-        if bool((gs[1:] < gs[:-1]).any()):
-            raise HbpFormatError("group_start must be non-decreasing")
-        if self._add_sign is not None and nnz and bool(
-                ((self._add_sign < 1) & (self._add_sign != -1)).any()):
-            raise HbpFormatError("add_sign entries must be >= 1 or -1")
-        bad = torch.full((1,), L.LLONG_MAX, dtype=torch.int64, device=zr.device)
-        L.call("hbp_gather_dense_perm", L.P(oh), L.c_i64(self.rows), L.c_i64(ncb), L.c_i64(R),
-               L.P(None), L.P(None), L.c_i64(0), L.P(None), L.P(bad), L.stream())
-        b = int(bad.item())
-        if b != L.LLONG_MAX:
-            bc, br = divmod(b, nrb)
-            raise HbpFormatError(f"output_hash of block ({br}, {bc}) is not a permutation")
-        # zero_row implied by the empty-slot mask, per W-lane group
-        i = torch.arange(n_slots, device=zr.device)
-        q = (i % self.rows) % R % W
-        is_zero = (zr == -1).to(torch.int64)
-        cs = torch.cumsum(is_zero, 0)
-        g0 = i - q
-        before = cs - is_zero - (cs[g0] - is_zero[g0])
-        expected = torch.where(is_zero.bool(), torch.full_like(before, -1), before)
-        wrong = torch.nonzero(expected != zr.to(torch.int64))
-        if wrong.numel():
-            s = int(wrong[0, 0])
-            bc, r = divmod(s, self.rows)
-            raise HbpFormatError(f"zero_row of block ({r // R}, {bc}) has wrong lane counts")
+        validate_reference_arrays(self.rows, self.cols, self.config, self.grid_shape,
+                                  col=self.col, data=self.data, add_sign=self._add_sign,
+                                  zero_row=self.zero_row, group_start=self.group_start,
+                                  output_hash=self.output_hash)
+
+
+def validate_reference_arrays(rows: int, cols: int, config: PartitionConfig, grid_shape, *,
+                              col, data, add_sign, zero_row, group_start, output_hash) -> None:
+    """hbp.py:102-135 validate_structure on the six reference-layout arrays
+    (device tensors; add_sign may be None), in the reference's order: grid
+    shape, element lengths, slot lengths, group_start length / span /
+    monotonicity, add_sign domain, then block by block in bc-major order
+    output_hash bijection before zero_row lane counts."""
+    nrb, ncb = grid_shape
+    R, W = config.row_height, config.warp_size
+    if nrb != -(-rows // R) or ncb != -(-cols // config.col_width):
+        raise HbpFormatError("grid shape inconsistent with dimensions")
+    nnz = data.numel()
+    if not (col.numel() == nnz and (add_sign is None or add_sign.numel() == nnz)):
+        raise HbpFormatError("element array lengths differ")
+    n_slots = ncb * rows
+    if zero_row.numel() != n_slots or output_hash.numel() != n_slots:
+        raise HbpFormatError("slot array length mismatch")
+    n_groups = ncb * groups_per_col_block(rows, R, W)
+    gs = group_start
+    if gs.numel() != n_groups + 1:
+        raise HbpFormatError("group_start length mismatch")
+    ends = gs[[0, -1]].cpu().tolist()
+    if ends[0] != 0 or ends[1] != nnz:
+        raise HbpFormatError("group_start must span [0, nnz]")
+    if bool((gs[1:] < gs[:-1]).any()):
+        raise HbpFormatError("group_start must be non-decreasing")
+    if add_sign is not None and nnz and bool(((add_sign < 1) & (add_sign != -1)).any()):
+        raise HbpFormatError("add_sign entries must be >= 1 or -1")
+    if not n_slots:
+        return
+    dev = zero_row.device
+    # first block (bc-major key bc*nrb + br) whose output_hash is not a bijection
+    bad = torch.full((1,), L.LLONG_MAX, dtype=torch.int64, device=dev)
+    L.call("hbp_gather_dense_perm", L.P(output_hash), L.c_i64(rows), L.c_i64(ncb), L.c_i64(R),
+           L.P(None), L.P(None), L.c_i64(0), L.P(None), L.P(bad), L.stream())
+    b_perm = int(bad.item())
+    # first block whose zero_row disagrees with its empty-slot mask, per W-lane group
+    i = torch.arange(n_slots, device=dev)
+    q = (i % rows) % R % W
+    is_zero = (zero_row == -1).to(torch.int64)
+    cs = torch.cumsum(is_zero, 0)
+    g0 = i - q
+    before = cs - is_zero - (cs[g0] - is_zero[g0])
+    expected = torch.where(is_zero.bool(), torch.full_like(before, -1), before)
+    wrong = torch.nonzero(expected != zero_row.to(torch.int64))
+    b_zr = L.LLONG_MAX
+    if wrong.numel():
+        bc, r = divmod(int(wrong[0, 0]), rows)
+        b_zr = bc * nrb + r // R
+    if b_perm != L.LLONG_MAX and b_perm <= b_zr:
+        bc, br = divmod(b_perm, nrb)
+        raise HbpFormatError(f"output_hash of block ({br}, {bc}) is not a permutation")
+    if b_zr != L.LLONG_MAX:
+        bc, br = divmod(b_zr, nrb)
+        raise HbpFormatError(f"zero_row of block ({br}, {bc}) has wrong lane counts")
 
 
 def _bad_block_message(grid_or_hbp, idx: int, dense: bool, nrb: int) -> str:
@@ -524,9 +542,29 @@ def _read_exact(stream, n: int) -> bytes:
     return buf
 
 
+_TORCH_OF = {"<u8": torch.int64, "<u4": torch.int32, "<f8": torch.float64, "<i4": torch.int32}
+
+
+def _dev_array(a, dt: str) -> torch.Tensor:
+    """A reference array (numpy of codec type `dt`, or a tensor) as a
+    contiguous device tensor of the same bits (u32 -> int32, u64 -> int64)."""
+    tt = _TORCH_OF[dt]
+    if isinstance(a, torch.Tensor):
+        a = a.to(device=L.require_cuda())
+        if a.dtype != tt:
+            a = a.view(tt) if a.element_size() == torch.empty(0, dtype=tt).element_size() \
+                and not a.is_floating_point() else a.to(tt)
+        return a.contiguous()
+    h = np.array(np.asarray(a, dt), copy=True)  # writable (frombuffer arrays are read-only)
+    return torch.as_tensor(h.view({"<u8": np.int64, "<u4": np.int32}.get(dt, h.dtype)),
+                           device=L.require_cuda()).contiguous()
+
+
 def deserialize_hbp(stream) -> HbpMatrix:
-    """hbp.py:349-381: read a .hbp stream into a device HbpMatrix (compact
-    arrays rebuilt from the dense ones), validating structure."""
+    """hbp.py:349-381: read a .hbp stream into a device HbpMatrix.  The raw
+    reference-layout arrays are validated first (hbp.py:102-135, same order
+    and messages), then the compact runtime arrays are derived from them on
+    the device."""
     if _read_exact(stream, 4) != MAGIC:
         raise HbpFormatError("bad magic; not an .hbp stream")
     (version,) = struct.unpack("<I", _read_exact(stream, 4))
@@ -543,79 +581,71 @@ def deserialize_hbp(stream) -> HbpMatrix:
         raise HbpFormatError(f"invalid partition config in header: {exc}") from exc
     if arrays["data"].size != nnz:
         raise HbpFormatError("element array length disagrees with header nnz")
-    hbp = from_reference(int(rows), int(cols), config, (int(nrb), int(ncb)), **arrays)
-    hbp.validate_structure()
-    return hbp
+    _check_gpu_geometry(config)
+    t = {name: _dev_array(arrays[name], dt) for name, dt in _ARRAY_SPECS}
+    rows, cols, grid_shape = int(rows), int(cols), (int(nrb), int(ncb))
+    validate_reference_arrays(rows, cols, config, grid_shape, **t)
+    return from_reference(rows, cols, config, grid_shape, **t)
 
 
 def from_reference(rows, cols, config: PartitionConfig, grid_shape, *, col, data, add_sign,
                    zero_row, group_start, output_hash, dtype=torch.float64) -> HbpMatrix:
-    """Build the device HbpMatrix from the reference's six dense arrays."""
+    """Build the device HbpMatrix from the reference's six dense arrays
+    (numpy or device tensors; structure assumed valid -- see
+    validate_reference_arrays).  Everything is derived on the device:
+    nonzero blocks from group_start, the compact slot tables by gathers,
+    slot lengths by walking the add_sign chains (hbp_chain_lengths)."""
     _check_gpu_geometry(config)
     dev = L.require_cuda()
-    R, W = config.row_height, config.warp_size
+    col, add_sign = _dev_array(col, "<u4"), _dev_array(add_sign, "<i4")
+    zr, gs = _dev_array(zero_row, "<i4"), _dev_array(group_start, "<u8")
+    oh = _dev_array(output_hash, "<u4")
+    data = (data if isinstance(data, torch.Tensor) else torch.as_tensor(
+        np.asarray(data, np.float64))).to(device=dev, dtype=dtype).contiguous()
+    R, W, C = config.row_height, config.warp_size, config.col_width
     nrb, ncb = grid_shape
     gpb = R // W
     gpc = groups_per_col_block(rows, R, W)
-    gs = np.asarray(group_start, np.int64)
-    # nonzero blocks: their group range spans at least one element
-    bc_i, br_i = np.meshgrid(np.arange(ncb), np.arange(nrb), indexing="ij")
-    bc_i, br_i = bc_i.ravel(), br_i.ravel()
+    nnz = data.numel()
+    # nonzero blocks (bc-major): their group range spans at least one element
+    bc_i = torch.arange(ncb, device=dev).repeat_interleave(nrb)
+    br_i = torch.arange(nrb, device=dev).repeat(ncb)
     first = bc_i * gpc + br_i * gpb
-    ng = np.minimum(R, rows - br_i * R)
-    ng = -(-ng // W)
-    nnz_b = gs[np.minimum(first + ng, gs.size - 1)] - gs[np.minimum(first, gs.size - 1)]
+    n_b = torch.clamp(rows - br_i * R, max=R)
+    ng_b = (n_b + W - 1) // W
+    last = gs.numel() - 1
+    nnz_b = gs[torch.clamp(first + ng_b, max=last)] - gs[torch.clamp(first, max=last)]
     nzmask = nnz_b > 0
-    blk_bc = bc_i[nzmask].astype(np.int32)
-    blk_br = br_i[nzmask].astype(np.int32)
-    nzb = blk_br.size
-    oh = np.asarray(output_hash, np.uint32)
-    zr = np.asarray(zero_row, np.int32)
-    perm = np.zeros((nzb, R), np.uint32)
-    zrc = np.full((nzb, R), -1, np.int32)
-    slot_len = np.zeros((nzb, R), np.int64)
-    gsc = np.zeros(nzb * gpb + 1, np.int64)
-    gsc[-1] = gs[-1] if gs.size else 0
-    for i in range(nzb):
-        br, bc = int(blk_br[i]), int(blk_bc[i])
-        n = min(R, rows - br * R)
-        base = bc * rows + br * R
-        perm[i, :n] = oh[base:base + n]
-        zrc[i, :n] = zr[base:base + n]
-        g0 = bc * gpc + br * gpb
-        ngi = -(-n // W)
-        gsc[i * gpb:i * gpb + ngi] = gs[g0:g0 + ngi]
-        gsc[i * gpb + ngi:(i + 1) * gpb] = gs[g0 + ngi]
-        # slot lengths from the add_sign chains
-        add = np.asarray(add_sign)
-        for g in range(ngi):
-            a0, a1 = gs[g0 + g], gs[g0 + g + 1]
-            for q in range(min(W, n - g * W)):
-                z = int(zrc[i, g * W + q])
-                if z < 0:
-                    continue
-                j, k = a0 + q - z, 0
-                while True:
-                    k += 1
-                    st = int(add[j]) if 0 <= j < add.size else -1
-                    if st < 0 or j + st >= a1:
-                        break
-                    j += st
-                slot_len[i, g * W + q] = k
-    t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a), device=dev).to(dt)  # noqa: E731
-    rb_count = np.bincount(blk_br, minlength=nrb + 1).astype(np.int64)
-    rb_ptr = np.concatenate(([0], np.cumsum(rb_count)[:-1]))
-    rb_blk = np.argsort(blk_br, kind="stable").astype(np.int32)
+    blk_bc = bc_i[nzmask].to(torch.int32)
+    blk_br = br_i[nzmask].to(torch.int32)
+    nzb = blk_br.numel()
+    # compact slot tables: slot s of nonzero block i is dense slot bc*rows + br*R + s
+    s_loc = torch.arange(R, device=dev)
+    base = (blk_bc.to(torch.int64) * rows + blk_br.to(torch.int64) * R)[:, None] + s_loc
+    valid = (blk_br.to(torch.int64)[:, None] * R + s_loc) < rows
+    base_c = torch.where(valid, base, torch.zeros_like(base))
+    dense_len = torch.empty(ncb * rows, dtype=torch.int32, device=dev)
+    L.call("hbp_chain_lengths", L.c_i64(rows), L.c_i64(cols), L.c_i64(C), L.c_i64(R),
+           L.c_i64(W), L.P(zr), L.P(gs), L.P(add_sign), L.c_i64(nnz), L.P(dense_len), L.stream())
+    zero_i = torch.zeros((), dtype=torch.int32, device=dev)
+    perm = torch.where(valid, oh[base_c], zero_i).reshape(-1).contiguous()
+    zrc = torch.where(valid, zr[base_c], torch.full((), -1, dtype=torch.int32,
+                                                     device=dev)).reshape(-1).contiguous()
+    slot_len = torch.where(valid, dense_len[base_c], zero_i).reshape(-1).contiguous()
+    # compact group starts: group g of block i is dense group bc*gpc + br*gpb + g;
+    # groups past the block's last one repeat its end
+    g_loc = torch.arange(gpb, device=dev)
+    g0 = (blk_bc.to(torch.int64) * gpc + blk_br.to(torch.int64) * gpb)[:, None]
+    ngi = ((torch.clamp(rows - blk_br.to(torch.int64) * R, max=R) + W - 1) // W)[:, None]
+    gsc = torch.empty(nzb * gpb + 1, dtype=torch.int64, device=dev)
+    gsc[:-1] = gs[g0 + torch.minimum(g_loc, ngi)].reshape(-1)
+    gsc[-1] = nnz
+    rb_ptr, rb_blk = row_block_lists(blk_br, nrb)
     return HbpMatrix(rows, cols, config, grid_shape,
-                     col=_padded(t(np.asarray(col, np.uint32).view(np.int32), torch.int32)),
-                     data=_padded(t(np.asarray(data, np.float64), dtype)),
-                     add_sign=t(np.asarray(add_sign, np.int32), torch.int32),
-                     blk_br=t(blk_br, torch.int32), blk_bc=t(blk_bc, torch.int32),
-                     slot_len=t(slot_len.astype(np.int32).ravel(), torch.int32),
-                     perm=t(perm.view(np.int32).ravel(), torch.int32),
-                     group_start_c=t(gsc, torch.int64), zero_row_c=t(zrc.ravel(), torch.int32),
-                     rb_ptr=t(rb_ptr, torch.int64), rb_blk=t(rb_blk, torch.int32),
-                     permutations=t(oh.view(np.int32), torch.int32))
+                     col=_padded(col), data=_padded(data), add_sign=add_sign,
+                     blk_br=blk_br, blk_bc=blk_bc, slot_len=slot_len, perm=perm,
+                     group_start_c=gsc, zero_row_c=zrc, rb_ptr=rb_ptr, rb_blk=rb_blk,
+                     permutations=oh)
 
 
 def save_hbp(hbp: HbpMatrix, path) -> None:

@@ -164,6 +164,21 @@ def test_stream_fused_combine(dtype, C, workers, monkeypatch):
         np.testing.assert_array_equal(y1, O.hbp_spmv(p["hbp"], x.cpu().numpy(), workers=2))
 
 
+@pytest.mark.parametrize("R", [32, 96, 160])
+def test_stream_fused_combine_short_row_blocks(R, monkeypatch):
+    """Fused combine with row_height not a multiple of 128: the
+    last-arriver combine reads only its own row block's partial rows."""
+    rows, cols, r, c, v = _hot_matrix(seed=8, rows=1000, cols=6000)
+    hbp = _hbp(rows, cols, r, c, v, C=1500, R=R)
+    x = torch.as_tensor(np.random.default_rng(5).uniform(-1, 1, cols), device="cuda")
+    monkeypatch.setenv("HBP_FUSED_COMBINE", "1")
+    fused = H.SpmvOperator(hbp, hot=False, schedule="stream")
+    assert fused.fused_combine
+    y1 = fused(x).cpu().numpy()
+    p = O.pipeline(rows, cols, r, c, v, 1500, R, 32)
+    np.testing.assert_array_equal(y1, O.hbp_spmv(p["hbp"], x.cpu().numpy(), workers=2))
+
+
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
 @pytest.mark.parametrize("C", [700, 4096])
 def test_stream_direct_single_row_blocks(dtype, C, monkeypatch):
