@@ -70,6 +70,33 @@ def _peaks():
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
+def gather_roofline(nnz: int, hot_share: float, warm_share: float, x_fits_l2: bool,
+                    kernel_ms: float, sm_mhz, sms: int):
+    """Random-column SpMV bound by the measured gather rates
+    (profiles/gather_peaks.json, tools/gather_peaks.cu): every element's x
+    gather costs one L1 line request -- ~0.93 per SM-cycle while x is
+    L2-resident, ~0.24 beyond L2 -- and a hot-tier gather one shared-memory
+    load (~2 per SM-cycle).  t_min = sum(n_tier / (rate_tier * SMs * clock));
+    frac = t_min / kernel time."""
+    p = os.path.join(ROOT, "profiles", "gather_peaks.json")
+    if not os.path.exists(p) or not sm_mhz:
+        return None
+    with open(p) as fh:
+        g = json.load(fh)
+    hz = float(sm_mhz) * 1e6 * sms
+    r_l2 = g["ldg_l2_resident"]["per_sm_cycle"]
+    r_far = g["ldg_beyond_l2"]["per_sm_cycle"]
+    r_lds = g["lds_random_128KB"]["per_sm_cycle"]
+    cold = 1.0 - hot_share - warm_share
+    t = nnz * (hot_share / r_lds + warm_share / r_l2 + cold / (r_l2 if x_fits_l2 else r_far)) / hz
+    return {"bound": "l1_gather", "unit": "Ggathers/s", "achieved": round(nnz / (kernel_ms * 1e-3) / 1e9, 2),
+            "peak": round(nnz / t / 1e9, 2), "frac": round(t * 1e3 / kernel_ms, 4),
+            "min_ms": round(t * 1e3, 5), "sm_mhz": sm_mhz,
+            "tiers": {"hot_lds": round(hot_share, 4), "warm_l2": round(warm_share, 4),
+                      "cold": round(cold, 4), "cold_rate": "l2_resident" if x_fits_l2 else "beyond_l2"},
+            "source": "profiles/gather_peaks.json (measured on B200: random 4-byte gathers per SM-cycle)"}
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -574,6 +601,13 @@ def run_gpu(args):
         with open(prof) as fh:
             traffic = json.load(fh).get(args.config, {}).get("dram_bytes_per_launch")
     launches_step = op.launches_per_call + (2 if iterated else 0)  # + sumsq (2 launches)
+    groof = None
+    if hbp.num_col_blocks == 1:  # random columns over all of x: gather-bound, not HBM-bound
+        groof = gather_roofline(
+            nnz, op.hot.share if op.hot is not None else 0.0,
+            op.hot.warm_share if op.hot is not None else 0.0,
+            cols * esz <= 0.6 * _l2_bytes(), spmv_ms, clk.get("sm_mhz"),
+            torch.cuda.get_device_properties(dev).multi_processor_count)
     out = {
         "metric": METRIC, "value": round(gflops, 3), "unit": UNIT, "n_gpus": world,
         "steps": K, "warmup": args.warmup, "ms_per_step": round(per_step_ms, 5),
@@ -598,12 +632,14 @@ def run_gpu(args):
                                    else f"independent instances x{world} (weak)"),
                    "l2": ("working set < 2x L2: L2 flushed between timed steps" if flush
                           else "inputs larger than L2 (no flush); x reused from L2 by design")},
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+        "roofline": {"bound": "hbm", "binding": "l1_gather" if groof else "hbm",
+                     "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                      "algorithmic_bytes": b_alg, "peak_source": peak_src,
                      "kernel_ms": round(spmv_ms, 5),
                      "kernel": f"k_spmv_{op.schedule}" + (" (+ hot-column gather)" if op.hot is not None else "")
                      + ("" if op.launches_per_call == 1 + (op.hot is not None) else " (+ combine/zero launch)")},
+        "gather_roofline": groof,
         "e2e": {"value": round(2.0 * total_nnz / (e2e_ms * 1e-3) / 1e9, 3), "unit": UNIT,
                 "h2d_bytes_per_step": cols * esz, "d2h_bytes_per_step": rows * esz,
                 "ms_per_step": round(e2e_ms, 4),
@@ -679,7 +715,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-baselines", action="store_true",
                     help="skip the CSR / 2D / cuSPARSE comparison timings")
-    ap.add_argument("--schedule", default=None, choices=[None, "stream", "balanced", "plan", "rowblock"])
+    ap.add_argument("--schedule", default=None, choices=[None, "stream", "balanced", "plan", "rowblock", "seg"])
     ap.add_argument("--workers", type=int, default=None,
                     help="persistent warps of the SpMV (default: one per resident warp slot)")
     ap.add_argument("--hot", default="auto",

@@ -372,6 +372,35 @@ int hbp_hot_gather(const void *x, int dtype, const uint32_t *hot_cols, int64_t n
 int hbp_spmv_balanced(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y,
                       double *partial, hbp_stream_t stream);
 
+/* Column-segment schedule (warp_size == 32, several column blocks):
+ * engine.py:123-134 block_spmv per nonzero block, with the block's
+ * x-segment x[bc*C, (bc+1)*C) (engine.py:127-134) staged in shared memory --
+ * only the window [win_lo, win_hi) its columns touch (hbp_seg_windows), one
+ * TMA bulk copy per block, double-buffered.  One persistent CTA per worker
+ * runs engine.py:96-176's plan: its fixed contiguous chunk of the bc-major
+ * nonzero blocks, then blocks [fixed_count, nzb) drawn from an atomic
+ * ticket.  The CTA's warps walk the block's groups lane-per-row in step
+ * order (exact mode: bitwise _kernels.py:41-46).  Outputs as
+ * hbp_spmv_stream: y when ncb == 1, else the compact partial (and y for
+ * single-block row blocks with HBP_FLAG_DIRECT_SINGLE). */
+typedef struct {
+    int64_t ctas;           /* persistent CTAs (hbp_seg_workers) */
+    int64_t fixed_count;    /* engine.py:107 int(f * nzb + 0.5) */
+    uint32_t *ticket;       /* [2] device words, zeroed once by the caller; left zeroed */
+    const int32_t *win_lo;  /* [nzb] first column the block touches */
+    const int32_t *win_hi;  /* [nzb] one past the last */
+    int64_t win_cap;        /* max(win_hi - win_lo): shared buffer size */
+} hbp_seg_t;
+/* Per nonzero block column window; *win_cap (device int64) = max width. */
+int hbp_seg_windows(const hbp_format_t *f, int32_t *win_lo, int32_t *win_hi, int64_t *win_cap,
+                    hbp_stream_t stream);
+/* Resident CTAs for a window capacity (SMs x occupancy, at most nzb). */
+int hbp_seg_workers(const hbp_format_t *f, int64_t win_cap, int64_t *ctas);
+int hbp_spmv_seg(const hbp_format_t *f, const hbp_seg_t *s, const void *x, void *y,
+                 double *partial, hbp_stream_t stream);
+/* A/B tuning selector of the launch shape (HBP_SEG_VARIANT); 0 = default. */
+int hbp_seg_set_variant(int v);
+
 /* engine.py:196-201 combine over nonzero blocks only, ascending bc
  * (bitwise equal to the dense combine); rows of row blocks with
  * no nonzero block get +0.0. */

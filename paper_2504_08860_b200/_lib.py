@@ -52,6 +52,12 @@ class ScheduleT(ctypes.Structure):
     ]
 
 
+class SegT(ctypes.Structure):
+    """Mirror of hbp_seg_t."""
+    _fields_ = [("ctas", c_i64), ("fixed_count", c_i64), ("ticket", c_vp), ("win_lo", c_vp),
+                ("win_hi", c_vp), ("win_cap", c_i64)]
+
+
 class BalancedT(ctypes.Structure):
     """Mirror of hbp_balanced_t."""
     _fields_ = [("workers", c_i64), ("part_head", c_vp), ("part_tail", c_vp),
@@ -124,6 +130,10 @@ _SIGS = {
     "hbp_l2_persist": [c_vp, ctypes.c_size_t, ctypes.c_float, c_vp],
     "hbp_l2_persist_reset": [c_vp],
     "hbp_l2_info": [ctypes.POINTER(c_int), ctypes.POINTER(c_int), ctypes.POINTER(c_int)],
+    "hbp_seg_windows": [ctypes.POINTER(FormatT), c_vp, c_vp, c_vp, c_vp],
+    "hbp_seg_workers": [ctypes.POINTER(FormatT), c_i64, ctypes.POINTER(c_i64)],
+    "hbp_seg_set_variant": [c_int],
+    "hbp_spmv_seg": [ctypes.POINTER(FormatT), ctypes.POINTER(SegT), c_vp, c_vp, c_vp, c_vp],
     "hbp_combine": [ctypes.POINTER(FormatT), c_vp, c_vp, c_vp],
     "hbp_spmv_rowblock": [ctypes.POINTER(FormatT), c_vp, c_vp, c_vp],
     "hbp_zero_empty_rows": [ctypes.POINTER(FormatT), c_vp, c_vp],

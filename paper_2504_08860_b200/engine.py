@@ -157,6 +157,9 @@ class SpmvOperator:
     schedule="balanced": the same slices walked from global memory
     (hbp_spmv_balanced, step-aligned cuts).  schedule="plan": the reference's fixed + competitive
     block schedule (hbp_spmv_blocks) with this fixed_fraction.
+    schedule="seg": one persistent CTA per worker runs whole nonzero blocks
+    (its fixed chunk, then the atomic ticket), with the block's x-segment
+    window staged in shared memory by TMA (hbp_spmv_seg).
     schedule="rowblock": one CTA per row block runs its nonzero blocks in
     ascending bc and folds them as the combine does (hbp_spmv_rowblock; one
     launch, no partial array -- for small matrices with several column blocks).
@@ -167,6 +170,10 @@ class SpmvOperator:
     ROWBLOCK_MAX_NNZ_F32 = 1 << 28  # (f32: banded 138M nnz 0.32 vs 0.35 ms stream)
     ROWBLOCK_MAX_SKEW = 8.0     # ... when no row block holds > 8x the mean
     ROWBLOCK_MAX_BLOCKS = 4     # ... and row blocks average <= 4 nonzero blocks
+    # auto: column-segment schedule for column-blocked matrices whose nonzero
+    # blocks are large (cfg3: 16.9K elements per block, 2.18 vs 2.65 ms stream)
+    SEG_MIN_BLOCK_NNZ = 4096
+    SEG_MAX_WINDOW_BYTES = 64 << 10
     HOT_MIN_SHARE = 0.10  # stage hot columns when they hold >= 10 % of the nonzeros
     WARM_BYTES = 64 << 20  # warm tier: a 64 MB L2-resident copy of x at the next columns
 
@@ -177,7 +184,7 @@ class SpmvOperator:
         dev = hbp.data.device
         if schedule is None:
             schedule = os.environ.get("HBP_SCHEDULE") or self._auto_schedule(hbp, hot)
-        if schedule in ("balanced", "stream") and hbp.config.warp_size != 32:
+        if schedule in ("balanced", "stream", "seg") and hbp.config.warp_size != 32:
             raise ValueError(f"the {schedule} schedule needs warp_size == 32")
         self.schedule = schedule
         if schedule == "stream":
@@ -231,11 +238,17 @@ class SpmvOperator:
                 self._scratch += [sl, sg]
                 self.bal.slice_lo, self.bal.slice_g = sl.data_ptr(), sg.data_ptr()
                 L.call("hbp_stream_slices", ctypes.byref(f), ctypes.byref(self.bal), L.stream())
+        elif schedule == "seg":
+            self.seg = self._seg_setup(hbp, f, workers)
+            self.workers = int(self.seg.ctas)
         else:
             self.workers = workers or default_workers(hbp.dtype, hbp.config.warp_size)
         fr = hbp.config.fixed_fraction if fixed_fraction is None else fixed_fraction
         self.fixed_count = int(fr * hbp.nzb + 0.5)
-        self.ticket = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.ticket = torch.zeros(2, dtype=torch.int32, device=dev)
+        if schedule == "seg":
+            self.seg.fixed_count = self.fixed_count
+            self.seg.ticket = self.ticket.data_ptr()
         self.direct = hbp.num_col_blocks == 1
         R = hbp.config.row_height
         self.partial = None if self.direct or schedule == "rowblock" else torch.empty(hbp.nzb * R, dtype=torch.float64,
@@ -247,7 +260,7 @@ class SpmvOperator:
         # (cfg3 3.56 vs 3.28 ms, cfg1 69 vs 61 us, same box)
         self.fused_combine = (not self.direct and schedule == "stream" and hbp.nzb > 0
                               and os.environ.get("HBP_FUSED_COMBINE", "0") == "1")
-        if (not self.direct and schedule == "stream" and not self.fused_combine
+        if (not self.direct and schedule in ("stream", "seg") and not self.fused_combine
                 and os.environ.get("HBP_DIRECT_SINGLE", "1") != "0"):
             f.reserved |= 4  # HBP_FLAG_DIRECT_SINGLE
         if self.fused_combine:
@@ -263,9 +276,33 @@ class SpmvOperator:
         self._graph = None
         self._gx = self._gy = None
 
+    def _seg_setup(self, hbp: HbpMatrix, f, workers) -> "L.SegT":
+        """Column windows of the nonzero blocks (hbp_seg_windows, cached on
+        the matrix) and the CTA count of the column-segment schedule."""
+        dev = hbp.data.device
+        if "seg_win" not in hbp._ops:
+            lo = torch.empty(max(1, hbp.nzb), dtype=torch.int32, device=dev)
+            hi = torch.empty(max(1, hbp.nzb), dtype=torch.int32, device=dev)
+            cap = torch.zeros(1, dtype=torch.int64, device=dev)
+            L.call("hbp_seg_windows", ctypes.byref(f), L.P(lo), L.P(hi), L.P(cap), L.stream())
+            hbp._ops["seg_win"] = (lo, hi, int(cap.item()))
+        lo, hi, cap = hbp._ops["seg_win"]
+        sg = L.SegT()
+        sg.win_lo, sg.win_hi, sg.win_cap = lo.data_ptr(), hi.data_ptr(), cap
+        if workers is None:
+            n = L.c_i64(0)
+            L.call("hbp_seg_workers", ctypes.byref(f), L.c_i64(cap), ctypes.byref(n))
+            workers = int(n.value)
+        sg.ctas = max(1, int(workers))
+        self._seg_keep = (lo, hi)
+        return sg
+
     @classmethod
     def _auto_schedule(cls, hbp: HbpMatrix, hot=None) -> str:
-        """stream for W = 32, plan otherwise; rowblock for small, evenly
+        """stream for W = 32, plan otherwise; seg (x-segment staged per
+        block, CTA per block) for column-blocked matrices with large nonzero
+        blocks (>= 4096 elements on average) and x-segments of <= 64 KB;
+        rowblock for small, evenly
         spread matrices with several column blocks and few nonzero blocks
         per row block (one launch instead of SpMV + combine; cfg1: 38.7 vs
         61 us) unless hot staging was asked about (a stream-schedule
@@ -283,10 +320,17 @@ class SpmvOperator:
             rb.index_add_(0, hbp.blk_br.long(), blk_nnz)
             if float(rb.max()) <= cls.ROWBLOCK_MAX_SKEW * hbp.nnz / hbp.num_row_blocks:
                 return "rowblock"
+        if (hbp.config.warp_size == 32 and hbp.num_col_blocks > 1 and hbp.nzb
+                and hbp.nnz >= cls.SEG_MIN_BLOCK_NNZ * hbp.nzb
+                and hbp.config.col_width * hbp.data.element_size() <= cls.SEG_MAX_WINDOW_BYTES):
+            return "seg"
         return "stream" if hbp.config.warp_size == 32 else "plan"
 
     def _blocks(self, f, x, partial, y, s):
-        if self.schedule in ("balanced", "stream"):
+        if self.schedule == "seg":
+            L.call("hbp_spmv_seg", ctypes.byref(f), ctypes.byref(self.seg), L.P(x), L.P(y),
+                   L.P(partial), s)
+        elif self.schedule in ("balanced", "stream"):
             L.call(f"hbp_spmv_{self.schedule}", ctypes.byref(f), ctypes.byref(self.bal), L.P(x), L.P(y),
                    L.P(partial), s)
         else:
@@ -324,7 +368,7 @@ class SpmvOperator:
             if self.has_empty_row_blocks:
                 L.call("hbp_zero_empty_rows", ctypes.byref(f), L.P(y), s)
         else:
-            # stream schedule: single-block row blocks go straight to y
+            # stream / seg schedule: single-block row blocks go straight to y
             self._blocks(f, x, self.partial, y if f.reserved & 4 else None, s)
             L.call("hbp_combine", ctypes.byref(f), L.P(self.partial), L.P(y), s)
         return y

@@ -177,7 +177,7 @@ __device__ __forceinline__ void cluster_sync_all() {
 
 // CL == 0: plain ld.shared on the CTA's own segment; CL >= 1: the segment of
 // cluster rank (idx / SEG) % CL through ld.shared::cluster
-template <int CL, int U>
+template <int CL, int U, int ILP = 1>
 __global__ void __launch_bounds__(512) k_smem(const uint32_t *__restrict__ idx, const float *x,
                                               int64_t n4, float *out) {
     extern __shared__ __align__(16) float seg[];
@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(512) k_smem(const uint32_t *__restrict__ idx, 
     const uint32_t base = smem_u32(seg);
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-    float acc = 0.f;
+    float accs[ILP * 4] = {};
     for (int64_t i = tid; i < n4; i += nth * U) {
         uint4 c[U];
 #pragma unroll
@@ -200,6 +200,7 @@ __global__ void __launch_bounds__(512) k_smem(const uint32_t *__restrict__ idx, 
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
+            float &acc = accs[(u % ILP) * 4 + (ILP > 1 ? 0 : 0)];
             const uint32_t cs[4] = {c[u].x, c[u].y, c[u].z, c[u].w};
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -213,10 +214,14 @@ __global__ void __launch_bounds__(512) k_smem(const uint32_t *__restrict__ idx, 
                     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(r));
                     asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(ra));
                 }
-                acc += v;
+                if constexpr (ILP > 1) accs[(u % ILP) * 4 + k] += v;
+                else acc += v;
             }
         }
     }
+    float acc = 0.f;
+#pragma unroll
+    for (int k = 0; k < ILP * 4; ++k) acc += accs[k];
     out[tid] = acc;
     stamp(1);
     if (CL >= 1) cluster_sync_all();
@@ -390,7 +395,9 @@ int main(int argc, char **argv) {
                (long long)hb, ms2, hb / ms2 / 1e6);
     }
     const int64_t xsizes[] = {(int64_t)1 << 20, 6250000, (int64_t)16 << 20, (int64_t)64 << 20};
-    for (int64_t nc : xsizes) {
+    const int64_t xsizes_g[] = {(int64_t)16 << 10, (int64_t)1 << 20, 6250000, (int64_t)16 << 20,
+                                (int64_t)64 << 20};
+    for (int64_t nc : xsizes_g) {
         if (only_tma) break;
         const double xmb = nc * 4.0 / 1e6;
         k_fill_idx<<<2048, 256>>>(idx, n, (uint32_t)nc, 12345);
@@ -447,6 +454,11 @@ int main(int argc, char **argv) {
         const size_t sm = SEG * 4;
         CK(cudaFuncSetAttribute(k_smem<0, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         report("lds_128KB", 0.131, n, time_ms([&] { k_smem<0, 4><<<g_sms, 512, sm>>>(idx, x, n4, out); }));
+        // independent accumulators: the shared-memory crossbar's own rate, not
+        // the add chain's latency
+        CK(cudaFuncSetAttribute(k_smem<0, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        report("lds_128KB_ilp", 0.131, n,
+               time_ms([&] { k_smem<0, 4, 4><<<g_sms, 512, sm>>>(idx, x, n4, out); }));
         auto dsm = [&](auto kern, int cl, const char *name) {
             CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             if (cl > 8) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
