@@ -42,6 +42,9 @@ CONFIGS = {
     "cfg2": ("R-MAT scale 24 (16,777,216 rows), edge factor 16, Graph500 (0.57,0.19,0.19,0.05), "
              "random vertex relabel, duplicates removed, fp32, C=cols R=512 W=32",
              dict(kind="rmat", scale=24, edge_factor=16), "f32", None),
+    "cfg2d": ("R-MAT scale 24 as cfg2 in fp64 (exact mode; hub rows split over warps with "
+              "--hub auto), C=cols R=512 W=32",
+              dict(kind="rmat", scale=24, edge_factor=16), "f64", None),
     "cfg4": ("the reference generator's SyntheticSpec(8388608, 8388608, 'uniform', 16.0, seed=0) "
              "(134,197,939 nnz), fp32, C=cols R=512 W=32",
              dict(kind="synth", rows=8388608, cols=8388608, mean=16.0), "f32", None),
@@ -332,6 +335,8 @@ def run_gpu(args):
     rows = stripe.rows if strong else rows_g
     nnz = int(rp[-1].item())
     cfg = H.PartitionConfig(col_width=C, row_height=R, warp_size=32, fixed_fraction=0.7)
+    hub_arg = None if args.hub in (None, "off", "0") else (
+        "auto" if args.hub == "auto" else int(args.hub))
     hot_arg = {"auto": None, "off": False, "on": True}.get(args.hot)
     if hot_arg is None and args.hot != "auto":
         hot_arg = int(args.hot)
@@ -366,7 +371,8 @@ def run_gpu(args):
         torch.cuda.synchronize()
         t4 = time.perf_counter()
         # runtime operator: phase stream + hot-column staging (hbp_hot.cu)
-        op = H.SpmvOperator(hbp, schedule=args.schedule, hot=hot_arg, workers=args.workers)
+        op = H.SpmvOperator(hbp, schedule=args.schedule, hot=hot_arg, workers=args.workers,
+                            hub_min=hub_arg)
         torch.cuda.synchronize()
         t5 = time.perf_counter()
         pre = dict(grid=(t1 - t0) * 1e3, sample=(t2 - t1) * 1e3, hash=(t3 - t2) * 1e3,
@@ -486,7 +492,7 @@ def run_gpu(args):
     # x in and y out).  With an L2 flush, steps run one at a time instead.
     depth = 1 if flush else int(os.environ.get("HBP_PIPE_DEPTH", "3"))
     pipe = H.HostPipeline(hbp, depth=depth, schedule=args.schedule, hot=hot_arg,
-                          workers=args.workers)
+                          workers=args.workers, hub_min=hub_arg)
     xh = torch.as_tensor(x_host).to(vdt).pin_memory()
     yhs = [torch.empty(rows, dtype=vdt).pin_memory() for _ in range(depth)]
     nw = max(depth, args.warmup)
@@ -621,6 +627,7 @@ def run_gpu(args):
                    "nonzero_blocks": hbp.nzb, "col_width": C, "row_height": R,
                    "warp_size": 32, "fixed_fraction": 0.7, "workers": op.workers,
                    "schedule": op.schedule,
+                   "hub_min": getattr(op, "hub_min", 0),
                    "hot_columns": op.hot.n_hot if op.hot is not None else 0,
                    "hot_share": round(op.hot.share, 4) if op.hot is not None else 0.0,
                    "warm_columns": op.hot.n_warm if op.hot is not None else 0,
@@ -718,6 +725,8 @@ def main():
     ap.add_argument("--schedule", default=None, choices=[None, "stream", "balanced", "plan", "rowblock", "seg"])
     ap.add_argument("--workers", type=int, default=None,
                     help="persistent warps of the SpMV (default: one per resident warp slot)")
+    ap.add_argument("--hub", default=None,
+                    help="f64 hub-row path: off (exact everywhere), auto, or a group-length threshold")
     ap.add_argument("--hot", default="auto",
                     help="hot-column x staging: auto (>= 10%% of nnz), on, off, or a column count")
     args = ap.parse_args()

@@ -56,6 +56,9 @@ enum {
 enum { HBP_F32 = 0, HBP_F64 = 1 };
 
 const char *hbp_status_string(int status);
+/* The CUDA runtime's pending (non-sticky) error of this library, cleared on
+ * read (cudaGetLastError) -- for tests that check no call left one behind. */
+int hbp_last_error(void);
 int hbp_abi_version(void);
 
 /* Device facts for sizing persistent grids (replaces the worker-count
@@ -321,6 +324,11 @@ typedef struct {
                           kernel with partial AND y; the kernel leaves it zeroed) */
     const double *y_sumsq; /* nullable: rows written straight to y are multiplied by
                               1 / sqrt(*y_sumsq) (iterated SpMV: y = A (x / ||x||)) */
+    int64_t hub_min;       /* exact mode only; 0 = off.  Groups longer than hub_min
+                              elements (hub rows) are cut across warps and summed as
+                              in fast mode (deterministic, not the reference's order:
+                              within ~1e-14 relative for f64); every other row stays
+                              bitwise the reference.  Needs the fast-mode scratch. */
 } hbp_balanced_t;
 
 int hbp_balanced_workers(const hbp_format_t *f, int64_t *workers);

@@ -62,12 +62,14 @@ class BalancedT(ctypes.Structure):
     """Mirror of hbp_balanced_t."""
     _fields_ = [("workers", c_i64), ("part_head", c_vp), ("part_tail", c_vp),
                 ("cut_end", c_vp), ("counters", c_vp), ("x_hot", c_vp),
-                ("slice_lo", c_vp), ("slice_g", c_vp), ("rb_done", c_vp), ("y_sumsq", c_vp)]
+                ("slice_lo", c_vp), ("slice_g", c_vp), ("rb_done", c_vp), ("y_sumsq", c_vp),
+                ("hub_min", c_i64)]
 
 
 # name -> argtypes (all return int status)
 _SIGS = {
     "hbp_abi_version": [],
+    "hbp_last_error": [],
     "hbp_device_sm_count": [ctypes.POINTER(c_int)],
     "hbp_spmv_default_workers": [c_int, c_i64, ctypes.POINTER(c_i64)],
     "hbp_exclusive_sum_i64": [c_vp, c_vp, c_i64, c_vp, c_size_p, c_vp],

@@ -42,6 +42,7 @@
 
 #include <atomic>
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "hbp.h"
@@ -147,18 +148,22 @@ __device__ __forceinline__ int64_t cut_at(int64_t w, int64_t E, int64_t Nw) {
 // Slice of worker w: equal element ranges [cut(w), cut(w+1)); exact mode
 // rounds both ends up to group boundaries (every row summed by one lane in
 // step order).  g = the first group whose elements the slice touches.
+// With hub_min > 0 (exact mode), a cut inside a group longer than hub_min
+// elements stays where it is: that group is split over warps like a
+// fast-mode group (the thresholded hub-row path).
 __device__ __forceinline__ void stream_slice(const int64_t *__restrict__ gs, int64_t ngroups,
                                              int64_t E, int64_t w, int64_t Nw, bool exact,
-                                             int64_t *lo, int64_t *hi, int64_t *g0) {
+                                             int64_t hub_min, int64_t *lo, int64_t *hi,
+                                             int64_t *g0) {
     int64_t c_lo = cut_at(w, E, Nw), c_hi = cut_at(w + 1, E, Nw);
     if (exact) {
         if (c_lo > 0 && c_lo < E) {
             int64_t g = upper_group(gs, ngroups, c_lo);
-            if (gs[g] != c_lo) c_lo = gs[g + 1];
+            if (gs[g] != c_lo && !(hub_min > 0 && gs[g + 1] - gs[g] > hub_min)) c_lo = gs[g + 1];
         }
         if (c_hi > 0 && c_hi < E) {
             int64_t g = upper_group(gs, ngroups, c_hi);
-            if (gs[g] != c_hi) c_hi = gs[g + 1];
+            if (gs[g] != c_hi && !(hub_min > 0 && gs[g + 1] - gs[g] > hub_min)) c_hi = gs[g + 1];
         }
     }
     int64_t g = upper_group(gs, ngroups, c_lo);
@@ -169,12 +174,12 @@ __device__ __forceinline__ void stream_slice(const int64_t *__restrict__ gs, int
 }
 
 __global__ void k_stream_slices(const int64_t *__restrict__ gs, int64_t ngroups, int64_t E,
-                                int64_t Nw, bool exact, int64_t *__restrict__ slice_lo,
-                                int64_t *__restrict__ slice_g) {
+                                int64_t Nw, bool exact, int64_t hub_min,
+                                int64_t *__restrict__ slice_lo, int64_t *__restrict__ slice_g) {
     const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (w >= Nw) return;
     int64_t lo, hi, g;
-    stream_slice(gs, ngroups, E, w, Nw, exact, &lo, &hi, &g);
+    stream_slice(gs, ngroups, E, w, Nw, exact, hub_min, &lo, &hi, &g);
     slice_lo[w] = lo;
     slice_g[w] = g;
     if (w == Nw - 1) slice_lo[Nw] = hi;
@@ -551,6 +556,7 @@ __global__ void __launch_bounds__(NT, MINB)
     constexpr bool MS = (XM & 4) != 0;
     constexpr bool SHORT = (XM & 16) != 0;  // fast path for 1-2 step phases
     constexpr bool FC = (XM & 512) != 0;     // fused combine (b.rb_done; partial mode)
+    constexpr bool HUBT = EXACT && (XM & 4096) != 0;  // exact mode with the hub-row path
     auto ldm = [](const auto *p) { return MS ? __ldcs(p) : *p; };
     auto stm = [](auto *p, auto v) {
         if constexpr (MS) __stcs(p, v);
@@ -585,7 +591,7 @@ __global__ void __launch_bounds__(NT, MINB)
         c_hi = b.slice_lo[w + 1];
         g = b.slice_g[w];
     } else {
-        stream_slice(gs, ngroups, E, w, Nw, EXACT, &c_lo, &c_hi, &g);
+        stream_slice(gs, ngroups, E, w, Nw, EXACT, EXACT ? b.hub_min : 0, &c_lo, &c_hi, &g);
     }
     const int64_t base = c_lo & ~(int64_t)3;
     Ring<V, EXACT, CH, NB, XM, HOT> ring{S, x};
@@ -728,7 +734,10 @@ __global__ void __launch_bounds__(NT, MINB)
         const bool piece = (lo > g0) || (hi < g1);
 
         double acc = 0.0;
-        if (!EXACT && lo < hi) {
+        // exact mode with the hub-row path: groups longer than b.hub_min are
+        // walked (and split over warps) as in fast mode
+        const bool hub = HUBT && (int64_t)(g1 - g0) > b.hub_min;
+        if ((!EXACT || hub) && lo < hi) {
             acc = piece ? walk_fast<true, KT, LMIN, SHORT>(ring, ph, np, g0, g1 - g0, lo, hi, lane)
                         : walk_fast<false, KT, LMIN, SHORT>(ring, ph, np, g0, g1 - g0, lo, hi, lane);
         } else if (lo < hi) {
@@ -841,13 +850,14 @@ constexpr size_t ring_smem() {
     return sizeof(WarpSmem<V, CH, NB>) * (NT / 32);
 }
 
+// Kernel attributes are per device and per instantiation: the shared-memory
+// size each instantiation was last configured for on each device.  Both the
+// occupancy query and the launch go through here (a staged launch's size
+// depends on n_hot, so a query for another matrix re-sets it).  Idempotent,
+// so a lost race only repeats the call.
 template <typename V, bool EXACT, int CH, int NB, int MINB, int XM, int KT, int LMIN, int NT,
           bool HOT>
-int launch(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y,
-           double *partial, cudaStream_t st) {
-    const size_t smem = ring_smem<V, CH, NB, NT>() + (HOT ? (size_t)f->n_hot * sizeof(V) : 0);
-    // kernel attributes are per device: cache the shared-memory size they were
-    // last set for on each device (idempotent, so a lost race only repeats it)
+int ensure_attributes(size_t smem) {
     static std::atomic<size_t> attr[kMaxDevices];
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return HBP_E_ARG;
@@ -855,6 +865,16 @@ int launch(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *
         set_attributes(k_spmv_stream<V, EXACT, CH, NB, MINB, XM, KT, LMIN, NT, HOT>, smem, MINB);
         attr[dev].store(smem, std::memory_order_relaxed);
     }
+    return HBP_OK;
+}
+
+template <typename V, bool EXACT, int CH, int NB, int MINB, int XM, int KT, int LMIN, int NT,
+          bool HOT>
+int launch(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y,
+           double *partial, cudaStream_t st) {
+    const size_t smem = ring_smem<V, CH, NB, NT>() + (HOT ? (size_t)f->n_hot * sizeof(V) : 0);
+    const int ra = ensure_attributes<V, EXACT, CH, NB, MINB, XM, KT, LMIN, NT, HOT>(smem);
+    if (ra) return ra;
     unsigned grid = (unsigned)((b->workers + NT / 32 - 1) / (NT / 32));
     k_spmv_stream<V, EXACT, CH, NB, MINB, XM, KT, LMIN, NT, HOT><<<grid, NT, smem, st>>>(
         *f, *b, (const V *)x, (V *)y, partial);
@@ -865,7 +885,8 @@ template <typename V, bool EXACT, int CH, int NB, int MINB, int XM, int KT, int 
           bool HOT>
 int occupancy_of(const hbp_format_t *f, int *per_sm, int *warps_per_cta) {
     const size_t smem = ring_smem<V, CH, NB, NT>() + (HOT ? (size_t)f->n_hot * sizeof(V) : 0);
-    set_attributes(k_spmv_stream<V, EXACT, CH, NB, MINB, XM, KT, LMIN, NT, HOT>, smem, MINB);
+    const int ra = ensure_attributes<V, EXACT, CH, NB, MINB, XM, KT, LMIN, NT, HOT>(smem);
+    if (ra) return ra;
     *warps_per_cta = NT / 32;
     return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(
         per_sm, k_spmv_stream<V, EXACT, CH, NB, MINB, XM, KT, LMIN, NT, HOT>, NT, smem);
@@ -915,7 +936,19 @@ bool staged(const hbp_format_t *f) { return f->n_hot > 0 && f->scol && f->hot_co
 // The fused combine (XM | 512) and the warm tier (XM | 32) each have their
 // own instantiation of the default variant: their bookkeeping would cost the
 // direct-mode kernel registers (spills) it does not need.
-#define HBP_STREAM_DISPATCH(FN, V, EXACT, FUSED, ...)                                       \
+// exact mode with the hub-row path (b->hub_min > 0) is its own instantiation
+// (XM | 4096): the fast-mode walk it adds would cost the plain exact kernel
+// registers
+#define HBP_STREAM_DISPATCH(FN, V, EXACT, FUSED, HUB, ...)                                  \
+    if (EXACT && HUB) {                                                                     \
+        if (staged(f) && f->n_warm > 0) {                                                   \
+            HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, kWarmThreads, 1, 53 | 2048 | 4096, __VA_ARGS__); \
+        }                                                                                   \
+        if (staged(f)) {                                                                    \
+            HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, kHotThreads, 1, 21 | 2048 | 4096, __VA_ARGS__); \
+        }                                                                                   \
+        HBP_VARIANT_X(FN, V, EXACT, false, 128, 4, kHotThreads, 1, 21 | 2048 | 4096, __VA_ARGS__); \
+    }                                                                                       \
     if (staged(f)) {                                                                        \
         if (FUSED && f->n_warm > 0) {                                                       \
             HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, kWarmThreads, 1, 53 | 512 | 2048, __VA_ARGS__); \
@@ -948,7 +981,7 @@ int hot_ring_bytes(size_t *out, bool warm) {  // shared memory of the staged lau
 
 template <typename V, bool EXACT>
 int occupancy(const hbp_format_t *f, int *per_sm, int *warps_per_cta) {
-    HBP_STREAM_DISPATCH(occupancy_of, V, EXACT, false, f, per_sm, warps_per_cta)
+    HBP_STREAM_DISPATCH(occupancy_of, V, EXACT, false, false, f, per_sm, warps_per_cta)
 }
 
 template <typename V>
@@ -974,7 +1007,8 @@ int run(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y, 
         const int rc = hot_gather<V>(x, f->hot_cols, f->n_hot + f->n_warm, b->x_hot, st);
         if (rc) return rc;
     }
-    HBP_STREAM_DISPATCH(launch, V, EXACT, (b->rb_done != nullptr), f, b, x, y, partial, st)
+    HBP_STREAM_DISPATCH(launch, V, EXACT, (b->rb_done != nullptr), (b->hub_min > 0), f, b, x, y,
+                        partial, st)
 }
 
 }  // namespace
@@ -1042,7 +1076,8 @@ int hbp_stream_slices(const hbp_format_t *f, const hbp_balanced_t *b, hbp_stream
     const int64_t ngroups = f->nzb * (f->row_height / 32);
     const bool exact = f->exact != 0 || f->dtype == HBP_F64;
     k_stream_slices<<<(unsigned)((b->workers + 127) / 128), 128, 0, as_stream(stream)>>>(
-        f->group_start, ngroups, f->nnz, b->workers, exact, b->slice_lo, b->slice_g);
+        f->group_start, ngroups, f->nnz, b->workers, exact, exact ? b->hub_min : 0, b->slice_lo,
+        b->slice_g);
     return (int)cudaGetLastError();
 }
 
@@ -1059,7 +1094,9 @@ int hbp_spmv_stream(const hbp_format_t *f, const hbp_balanced_t *b, const void *
     // slices are addressed with 32-bit offsets
     if ((f->nnz + b->workers - 1) / b->workers > (int64_t)1 << 30) return HBP_E_UNSUPPORTED;
     const bool exact = f->exact != 0 || f->dtype == HBP_F64;
-    if (!exact && (!b->part_head || !b->part_tail || !b->counters)) return HBP_E_ARG;
+    if ((!exact || b->hub_min > 0) && (!b->part_head || !b->part_tail || !b->counters))
+        return HBP_E_ARG;
+    if (b->hub_min < 0) return HBP_E_ARG;
     if (staged(f)) {
         int64_t cap = 0;
         const int rc = hbp_hot_capacity(f->dtype, f->n_warm > 0, &cap);

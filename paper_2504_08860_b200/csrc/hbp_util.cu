@@ -135,6 +135,8 @@ const char *hbp_status_string(int status) {
 
 int hbp_abi_version(void) { return 2; }
 
+int hbp_last_error(void) { return (int)cudaGetLastError(); }
+
 int hbp_device_sm_count(int *sms) {
     int dev = 0;
     HBP_CUDA_TRY(cudaGetDevice(&dev));

@@ -157,6 +157,11 @@ class SpmvOperator:
     schedule="balanced": the same slices walked from global memory
     (hbp_spmv_balanced, step-aligned cuts).  schedule="plan": the reference's fixed + competitive
     block schedule (hbp_spmv_blocks) with this fixed_fraction.
+    hub_min (f64, stream schedule): groups of more than hub_min elements --
+    hub rows -- are cut across warps and summed in fast-mode order
+    (deterministic, within ~1e-14 relative, not bitwise); every other row
+    stays bitwise the reference.  0 / None: exact everywhere; "auto": a
+    quarter of a warp's slice.
     schedule="seg": one persistent CTA per worker runs whole nonzero blocks
     (its fixed chunk, then the atomic ticket), with the block's x-segment
     window staged in shared memory by TMA (hbp_spmv_seg).
@@ -179,7 +184,8 @@ class SpmvOperator:
 
     def __init__(self, hbp: HbpMatrix, workers: int | None = None,
                  fixed_fraction: float | None = None, schedule: str | None = None,
-                 hot: bool | int | None = None, warm_bytes: int | None = None):
+                 hot: bool | int | None = None, warm_bytes: int | None = None,
+                 hub_min: int | str | None = None):
         self.hbp = hbp
         dev = hbp.data.device
         if schedule is None:
@@ -219,7 +225,15 @@ class SpmvOperator:
             self.bal = L.BalancedT()
             self.bal.workers = self.workers
             self._scratch = []
-            if not f.exact:
+            # f64 hub-row path (stream schedule): groups longer than hub_min
+            # elements are split over warps and summed in fast-mode order
+            if hub_min == "auto":  # a group longer than a quarter slice is a hub
+                hub_min = max(1024, hbp.nnz // (4 * self.workers))
+            self.hub_min = int(hub_min or 0) if (schedule == "stream" and f.exact) else 0
+            if self.hub_min < 0:
+                raise ValueError("hub_min must be >= 0")
+            self.bal.hub_min = self.hub_min
+            if not f.exact or self.hub_min:
                 ph = torch.empty(self.workers * 32, dtype=torch.float64, device=dev)
                 pt = torch.empty(self.workers * 32, dtype=torch.float64, device=dev)
                 ce = torch.empty(self.workers, dtype=torch.int64, device=dev)

@@ -54,3 +54,17 @@ def has_gpu():
         return torch.cuda.is_available()
     except Exception:  # pragma: no cover
         return False
+
+
+@pytest.fixture(autouse=True)
+def _no_pending_cuda_error(request):
+    """GPU tests: no libhbp.so call may leave a CUDA error pending (it would
+    surface in an unrelated later launch check)."""
+    yield
+    if request.node.get_closest_marker("gpu") is None or not has_gpu():
+        return
+    from paper_2504_08860_b200 import _lib as L
+    if L._lib is None:
+        return
+    st = L.lib().hbp_last_error()
+    assert st == 0, f"pending CUDA error {st} after {request.node.nodeid}"
