@@ -13,9 +13,11 @@ on the launching stream, barrier + synchronize on both sides, max over
 ranks; when a rank's working set is below 2x L2 (cfg1) L2 is flushed between
 timed steps (untimed), otherwise the inputs exceed L2 and x stays
 cache-resident by design.
-Multi-GPU (torchrun): weak configs (cfg2, cfg4, H, cfg1) run one full-size
-instance per rank with no collective; strong configs (cfg3, cfg5) split one
-global matrix into equal row-block stripes (x replicated).
+Multi-GPU (torchrun): every config but cfg1 is strong -- one global matrix
+split into nnz-balanced row stripes (stripes.plan_stripes / StripedOperator),
+x replicated; a single SpMV has no collective, cfg5's power iteration
+all-gathers the y stripes (overlapped with the next step's own-column part).
+cfg1 (5M nnz) runs an independent full instance per rank (weak).
 """
 from __future__ import annotations
 
@@ -60,7 +62,9 @@ CONFIGS = {
              "power iteration x <- Ax/||Ax|| with y all-gather, row stripes over the ranks",
              dict(kind="rmat", scale=26, edge_factor=16), "f32", None),
 }
-STRONG = {"cfg3", "cfg5"}    # one global matrix, row stripes over the ranks
+# one global matrix, nnz-balanced row stripes over the ranks (stripes.py); cfg1
+# (5M nnz, 38 us) runs an independent instance per rank instead
+STRONG = {"cfg2", "cfg2d", "cfg3", "cfg4", "cfg5", "H"}
 ITERATED = {"cfg5"}          # a step is one power-iteration step
 
 
@@ -300,89 +304,61 @@ def _l2_bytes() -> int:
         return 126 * 1024 * 1024
 
 
-def _stripe_of(rank: int, world: int, rows: int, R: int):
-    """Equal row-block stripes of the global matrix (strong-scaling configs):
-    stripe r = row blocks [r*q, (r+1)*q), q = ceil(nrb / world)."""
-    from paper_2504_08860_b200.stripes import Stripe
-    nrb = -(-rows // R)
-    q = -(-nrb // world)
-    lo, hi = min(rank * q, nrb), min((rank + 1) * q, nrb)
-    return Stripe(rank, lo, hi, min(lo * R, rows), min(hi * R, rows)), q * R
-
-
 def run_gpu(args):
     import torch
     import paper_2504_08860_b200 as H
 
+    from paper_2504_08860_b200.stripes import (PowerIteration, Stripe, StripedOperator,
+                                               plan_stripes, row_block_nnz)
     dist, rank, world, local = _dist()
     dev = torch.device("cuda", local)
-    kind = CONFIGS[args.config][1]["kind"]
     strong = args.config in STRONG
     iterated = args.config in ITERATED
     R = 512
-    # weak configs: an independent full-size instance per rank (seed = rank);
     # strong configs: every rank generates the same global matrix (seed 0) and
-    # keeps its row stripe
+    # keeps its nnz-balanced row stripe (stripes.plan_stripes); weak configs
+    # (cfg1): an independent full instance per rank
     desc, rows_g, cols, rp, col, val, C, vdt = make_matrix_gpu(args.config, 0 if strong else rank,
                                                               device=dev)
     torch.cuda.synchronize()
     nnz_global = int(rp[-1].item())
-    stripe, stripe_pad = _stripe_of(rank if strong else 0, world if strong else 1, rows_g, R)
     if strong:
-        e0, e1 = int(rp[stripe.row_lo].item()), int(rp[stripe.row_hi].item())
-        rp = (rp[stripe.row_lo:stripe.row_hi + 1] - e0).contiguous()
-        col, val = col[e0:e1].contiguous(), val[e0:e1].contiguous()
-    rows = stripe.rows if strong else rows_g
-    nnz = int(rp[-1].item())
+        stripes = plan_stripes(row_block_nnz(rp, rows_g, R), rows_g, R, world)
+        me = rank
+    else:
+        stripes, me = [Stripe(0, 0, -(-rows_g // R), 0, rows_g)], 0
     cfg = H.PartitionConfig(col_width=C, row_height=R, warp_size=32, fixed_fraction=0.7)
-    hub_arg = None if args.hub in (None, "off", "0") else (
-        "auto" if args.hub == "auto" else int(args.hub))
     hot_arg = {"auto": None, "off": False, "on": True}.get(args.hot)
     if hot_arg is None and args.hot != "auto":
         hot_arg = int(args.hot)
+    hub_arg = None if args.hub in (None, "off", "0") else (
+        "auto" if args.hub == "auto" else int(args.hub))
+    op_kwargs = dict(schedule=args.schedule, hot=hot_arg, workers=args.workers, hub_min=hub_arg)
+    split = iterated and world > 1 and not args.no_overlap
 
-    # ---- preprocessing (timed like cli.py:150-158, GPU stages)
-    csr = H.CsrMatrix(rows, cols, rp, col, val)
-    del col, val
+    # ---- preprocessing (timed like cli.py:150-158, GPU stages; the global
+    # hash-parameter draw is part of "sample" at N > 1)
     pre = {}
     for rep in range(2):  # first pass warms allocator / module load; report the second
-        torch.cuda.synchronize()
+        tm = {}
         t0 = time.perf_counter()
-        grid = H.make_grid(csr, cfg)
+        sop = StripedOperator(rows_g, cols, rp, col, val, stripes, me, cfg,
+                              x_layout="padded" if iterated else "global", split_own=split,
+                              op_kwargs=op_kwargs, distributed=strong and world > 1, timings=tm)
         torch.cuda.synchronize()
-        t1 = time.perf_counter()
-        if dist:
-            # (a, c) from the global sample (stripes.sample_hash_params_global);
-            # weak configs see the ranks' instances as one stacked matrix
-            from paper_2504_08860_b200.reorder import _grid_counts_at
-            from paper_2504_08860_b200.stripes import Stripe, sample_hash_params_global
-            st = stripe if strong else Stripe(rank, 0, 0, rank * rows, (rank + 1) * rows)
-            params = sample_hash_params_global(lambda flat: _grid_counts_at(grid, flat), st,
-                                               rows_g if strong else world * rows,
-                                               grid.num_col_blocks, R, device=dev)
-        else:
-            params = H.sample_hash_params(grid, cfg)
-        torch.cuda.synchronize()
-        t2 = time.perf_counter()
-        perms = H.hash_permutations(grid, params)
-        torch.cuda.synchronize()
-        t3 = time.perf_counter()
-        hbp = H.build_hbp(csr, grid, perms, with_add_sign=False, with_zero_row=False)
-        torch.cuda.synchronize()
-        t4 = time.perf_counter()
-        # runtime operator: phase stream + hot-column staging (hbp_hot.cu)
-        op = H.SpmvOperator(hbp, schedule=args.schedule, hot=hot_arg, workers=args.workers,
-                            hub_min=hub_arg)
-        torch.cuda.synchronize()
-        t5 = time.perf_counter()
-        pre = dict(grid=(t1 - t0) * 1e3, sample=(t2 - t1) * 1e3, hash=(t3 - t2) * 1e3,
-                   build=(t4 - t3) * 1e3, operator=(t5 - t4) * 1e3, total=(t5 - t0) * 1e3)
+        tm["total"] = (time.perf_counter() - t0) * 1e3
+        pre = tm
         if rep == 0:
-            del op, hbp, perms, grid
+            del sop
+    del col, val
+    stripe = sop.stripe
+    rows = stripe.rows
+    nnz = sop.nnz
+    hbp, op, grid, csr, params = sop.hbp, sop.op, sop.grid, sop.csr, sop.params
     # the paper's reordering comparison (Fig. 6/7 analogues, SURVEY §8(f)): GPU time of
     # the sort2D reorder beside the hash reorder, and the mean per-group std of lane
     # counts (load imbalance) under no / hash / sort2D ordering
-    reorder = {"hash_ms": round(pre["hash"], 3)}
+    reorder = {"hash_ms": round(pre.get("hash", 0.0), 3)}
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     sperm = H.sort_permutations(grid)
@@ -390,9 +366,11 @@ def run_gpu(args):
     reorder["sort2d_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
     gpc = -(-rows // R) * (R // 32)
     if grid.num_col_blocks * gpc * 32 <= (1 << 27):
+        perms = H.hash_permutations(grid, params)
         reorder["mean_group_std"] = {
             name: round(H.mean_group_std(H.group_stats(grid, pm), 32), 4)
             for name, pm in (("none", None), ("hash", perms), ("sort2d", sperm))}
+        del perms
     del sperm
     esz = 4 if vdt == torch.float32 else 8
     x_host = np.random.default_rng(0).uniform(-1.0, 1.0, cols)  # cli.py:170-171
@@ -400,39 +378,20 @@ def run_gpu(args):
 
     # ---- the step
     if iterated:
-        # power iteration x <- A x / ||A x||_2 (config 5): x replicated in a
-        # buffer padded to world * stripe_pad rows so the y stripes all-gather
-        # straight into it (NCCL all_gather_into_tensor, no copy); ||y||^2 is
-        # one 8-byte all-reduce
-        xs = [torch.zeros(world * stripe_pad, dtype=vdt, device=dev) for _ in range(2)]
-        xs[0][:cols] = torch.as_tensor(x_host, device=dev).to(vdt)
-        y_pad = torch.zeros(stripe_pad, dtype=vdt, device=dev)
-        y = y_pad[:rows]
-        cur = [0]
-
-        # the normalisation x / ||x|| is folded into the next SpMV (its y stores
-        # are multiplied by 1 / sqrt(sq), SpmvOperator x_sumsq): a step is the
-        # SpMV, hbp_sumsq (+ the all-reduce and the all-gather), no scaling pass
-        sq = torch.ones(1, dtype=torch.float64, device=dev)
-        sq_scratch = torch.empty(1024, dtype=torch.float64, device=dev)
-
-        def step():
-            x = xs[cur[0]]
-            nxt = xs[1 - cur[0]]
-            out = y if dist else nxt[:rows]
-            op(x[:cols], out, x_sumsq=sq)       # y = A (x / ||x||)
-            H.sumsq(out, sq, sq_scratch)        # ||y_local||^2 (hbp_sumsq, f64)
-            if dist:
-                dist.all_reduce(sq)
-                dist.all_gather_into_tensor(nxt, y_pad)
-            cur[0] = 1 - cur[0]
-        x_res = lambda: xs[cur[0]][:cols]  # noqa: E731
+        # power iteration x <- A x / ||A x||_2 (config 5, stripes.PowerIteration):
+        # the stripe SpMV with the normalisation folded into its y stores, hbp_sumsq,
+        # an 8-byte all-reduce and an in-place all-gather of the y stripes into the
+        # next x (padded layout); at N > 1 the gather overlaps the next step's
+        # own-column part
+        pit = PowerIteration(sop, torch.as_tensor(x_host, device=dev))
+        step = pit.step
+        x_res = pit.x_global
     else:
         x = torch.as_tensor(x_host, device=dev).to(vdt)
         y = torch.empty(rows, dtype=vdt, device=dev)
 
         def step():
-            op(x, y)
+            sop(x, y)
 
     # algorithmic bytes of one step on this rank
     b_alg = nnz * (esz + 4) + cols * esz + rows * esz
@@ -471,16 +430,18 @@ def run_gpu(args):
     kernel_ms = statistics.mean(step_ms)
     per_step_ms = kernel_ms if flush else start.elapsed_time(end) / K
 
-    # the SpMV kernel alone (roofline): time op() by itself on this rank
+    # the SpMV kernel alone (roofline): time the stripe SpMV by itself on this rank
     if iterated:
-        xk = xs[cur[0]][:cols]
+        pit.finish()
+        xk = pit.xs[pit.cur]
+        yk = torch.empty(rows, dtype=vdt, device=dev)
         kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(K)]
         for a, b in kev:
             if flush:
                 scratch.fill_(0.0)
             a.record(stream)
-            op(xk, y)
+            sop(xk, yk)
             b.record(stream)
         torch.cuda.synchronize()
         spmv_ms = statistics.mean(a.elapsed_time(b) for a, b in kev)
@@ -491,9 +452,16 @@ def run_gpu(args):
     # x_i H2D, SpMV, y_i D2H on 2 rotating streams; every step moves its own
     # x in and y out).  With an L2 flush, steps run one at a time instead.
     depth = 1 if flush else int(os.environ.get("HBP_PIPE_DEPTH", "3"))
-    pipe = H.HostPipeline(hbp, depth=depth, schedule=args.schedule, hot=hot_arg,
-                          workers=args.workers, hub_min=hub_arg)
-    xh = torch.as_tensor(x_host).to(vdt).pin_memory()
+    x_len = sop.width
+    pipe = H.HostPipeline(None, depth=depth, operator=sop, x_len=x_len)
+    if iterated:  # x in the stripes' padded layout
+        xpad = torch.zeros(x_len, dtype=torch.float64)
+        for st in stripes:
+            xpad[st.rank * sop.pad:st.rank * sop.pad + st.rows] = torch.as_tensor(
+                x_host[st.row_lo:st.row_hi])
+        xh = xpad.to(vdt).pin_memory()
+    else:
+        xh = torch.as_tensor(x_host).to(vdt).pin_memory()
     yhs = [torch.empty(rows, dtype=vdt).pin_memory() for _ in range(depth)]
     nw = max(depth, args.warmup)
     pipe.run([xh] * nw, [yhs[i % depth] for i in range(nw)])
@@ -525,16 +493,16 @@ def run_gpu(args):
             torch.cuda.synchronize()
             runs.append(e0.elapsed_time(e1) / K)
         e2e_ms = statistics.median(runs)
-    xd = torch.as_tensor(x_host, device=dev).to(vdt)
+    xd = xh.to(dev)  # x in the operator's layout (global, or the stripes' padded one)
     ychk = torch.empty(rows, dtype=vdt, device=dev)
-    op(xd, ychk)
+    sop(xd, ychk)
     e2e_ok = bool(torch.equal(yhs[(K - 1) % depth], ychk.cpu()))
 
     # ---- correctness check (not timed): componentwise vs cuSPARSE fp64
     A = torch.sparse_csr_tensor(csr.row_ptr, csr.col_idx.to(torch.int64),
-                                csr.values.to(torch.float64), (rows, cols))
+                                csr.values.to(torch.float64), (rows, sop.width))
     Aabs = torch.sparse_csr_tensor(csr.row_ptr, csr.col_idx.to(torch.int64),
-                                   csr.values.to(torch.float64).abs(), (rows, cols))
+                                   csr.values.to(torch.float64).abs(), (rows, sop.width))
     x64 = xd.to(torch.float64)
     yref = A @ x64
     scale = Aabs @ x64.abs()
@@ -565,7 +533,7 @@ def run_gpu(args):
                 ts.append(a.elapsed_time(b))
             return statistics.mean(ts)
         Acs = torch.sparse_csr_tensor(csr.row_ptr, csr.col_idx.to(torch.int64), csr.values,
-                                      (rows, cols))
+                                      (rows, sop.width))
         bl = {"csr_alg1_ms": _time(lambda: H.csr_spmv(csr, xd)),
               "block2d_ms": _time(lambda: H.block2d_spmv_baseline(csr, grid, xd)),
               "cusparse_ms": _time(lambda: Acs @ xd)}
@@ -593,6 +561,28 @@ def run_gpu(args):
         if not bool(torch.isfinite(res).all().item()):
             raise RuntimeError("power iteration produced non-finite values")
 
+    # collectives alone (N > 1, cfg5): the step's 8-byte all-reduce + y all-gather,
+    # device-timed on this rank, max over ranks
+    comm_ms = None
+    if dist and iterated:
+        nxt = pit.xs[1 - pit.cur]
+        c0 = torch.cuda.Event(enable_timing=True)
+        c1 = torch.cuda.Event(enable_timing=True)
+        dist.barrier()
+        c0.record(stream)
+        for _ in range(K):
+            dist.all_reduce(pit.sq)
+            dist.all_gather_into_tensor(nxt, nxt[rank * sop.pad:(rank + 1) * sop.pad])
+        c1.record(stream)
+        torch.cuda.synchronize()
+        cm = torch.tensor([c0.elapsed_time(c1) / K], dtype=torch.float64, device=dev)
+        dist.all_reduce(cm, op=dist.ReduceOp.MAX)
+        comm_ms = round(float(cm.item()), 5)
+    stripe_nnz = row_block_nnz(rp, rows_g, R) if strong else None
+    stripe_info = ([{"rank": st.rank, "rows": [st.row_lo, st.row_hi],
+                     "nnz": int(stripe_nnz[st.rb_lo:st.rb_hi].sum())} for st in stripes]
+                   if strong else None)
+
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -606,7 +596,7 @@ def run_gpu(args):
     if os.path.exists(prof):
         with open(prof) as fh:
             traffic = json.load(fh).get(args.config, {}).get("dram_bytes_per_launch")
-    launches_step = op.launches_per_call + (2 if iterated else 0)  # + sumsq (2 launches)
+    launches_step = sop.launches_per_call + (2 if iterated else 0)  # + sumsq (2 launches)
     groof = None
     if hbp.num_col_blocks == 1:  # random columns over all of x: gather-bound, not HBM-bound
         groof = gather_roofline(
@@ -628,6 +618,8 @@ def run_gpu(args):
                    "warp_size": 32, "fixed_fraction": 0.7, "workers": op.workers,
                    "schedule": op.schedule,
                    "hub_min": getattr(op, "hub_min", 0),
+                   "hub_groups": getattr(op, "hub_groups", 0),
+                   "hub_element_share": round(getattr(op, "hub_share", 0.0), 4),
                    "hot_columns": op.hot.n_hot if op.hot is not None else 0,
                    "hot_share": round(op.hot.share, 4) if op.hot is not None else 0.0,
                    "warm_columns": op.hot.n_warm if op.hot is not None else 0,
@@ -637,6 +629,10 @@ def run_gpu(args):
                             if iterated else "SpMV (+ combine when ncb > 1)"),
                    "parallelism": (f"row stripes x{world} of one matrix (strong)" if strong
                                    else f"independent instances x{world} (weak)"),
+                   "stripes": stripe_info,
+                   "own_column_split": sop.split,
+                   "own_column_share_rank0": round(sop.own_share, 4),
+                   "comm_ms_per_step": comm_ms,
                    "l2": ("working set < 2x L2: L2 flushed between timed steps" if flush
                           else "inputs larger than L2 (no flush); x reused from L2 by design")},
         "roofline": {"bound": "hbm", "binding": "l1_gather" if groof else "hbm",
@@ -648,7 +644,7 @@ def run_gpu(args):
                      + ("" if op.launches_per_call == 1 + (op.hot is not None) else " (+ combine/zero launch)")},
         "gather_roofline": groof,
         "e2e": {"value": round(2.0 * total_nnz / (e2e_ms * 1e-3) / 1e9, 3), "unit": UNIT,
-                "h2d_bytes_per_step": cols * esz, "d2h_bytes_per_step": rows * esz,
+                "h2d_bytes_per_step": x_len * esz, "d2h_bytes_per_step": rows * esz,
                 "ms_per_step": round(e2e_ms, 4),
                 "how": ("HostPipeline (copy-in / compute / copy-out streams): pinned x H2D, SpMV, y D2H per step"
                         + (" (one step at a time, L2 flushed)" if flush
@@ -725,6 +721,8 @@ def main():
     ap.add_argument("--schedule", default=None, choices=[None, "stream", "balanced", "plan", "rowblock", "seg"])
     ap.add_argument("--workers", type=int, default=None,
                     help="persistent warps of the SpMV (default: one per resident warp slot)")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="cfg5 at N > 1: no own-column split, all-gather then SpMV")
     ap.add_argument("--hub", default=None,
                     help="f64 hub-row path: off (exact everywhere), auto, or a group-length threshold")
     ap.add_argument("--hot", default="auto",

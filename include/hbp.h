@@ -443,6 +443,9 @@ int hbp_to_triplets(const hbp_format_t *f, int64_t *row_out, int64_t *col_out, v
  * optional all-reduce), out may alias y. */
 int hbp_sumsq(const void *y, int dtype, int64_t n, double *scratch, double *out,
               hbp_stream_t stream);
+/* y_i += a_i (the two column parts of a row stripe in the overlapped power
+ * iteration: own columns while the all-gather runs, the rest after it). */
+int hbp_add(void *y, const void *a, int dtype, int64_t n, hbp_stream_t stream);
 int hbp_sumsq_scratch(int64_t *doubles);
 int hbp_scale(const void *y, int dtype, int64_t n, const double *sumsq, void *out,
               hbp_stream_t stream);

@@ -128,6 +128,7 @@ _SIGS = {
     "hbp_hot_gather": [c_vp, c_int, c_vp, c_i64, c_vp, c_vp],
     "hbp_sumsq": [c_vp, c_int, c_i64, c_vp, c_vp, c_vp],
     "hbp_sumsq_scratch": [ctypes.POINTER(c_i64)],
+    "hbp_add": [c_vp, c_vp, c_int, c_i64, c_vp],
     "hbp_scale": [c_vp, c_int, c_i64, c_vp, c_vp, c_vp],
     "hbp_l2_persist": [c_vp, ctypes.c_size_t, ctypes.c_float, c_vp],
     "hbp_l2_persist_reset": [c_vp],

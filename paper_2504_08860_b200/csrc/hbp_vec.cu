@@ -62,6 +62,13 @@ __global__ void k_scale(const V *__restrict__ y, int64_t n, const double *__rest
         out[i] = __ldcs(y + i) * f;
 }
 
+template <typename V>
+__global__ void k_add(V *__restrict__ y, const V *__restrict__ a, int64_t n) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        y[i] = y[i] + __ldcs(a + i);
+}
+
 }  // namespace
 
 extern "C" {
@@ -98,6 +105,17 @@ int hbp_scale(const void *y, int dtype, int64_t n, const double *sumsq, void *ou
         k_scale<double><<<grid, 256, 0, st>>>((const double *)y, n, sumsq, (double *)out);
     else
         return HBP_E_ARG;
+    return (int)cudaGetLastError();
+}
+
+int hbp_add(void *y, const void *a, int dtype, int64_t n, hbp_stream_t stream) {
+    if (n < 0 || (n > 0 && (!y || !a))) return HBP_E_ARG;
+    if (n == 0) return HBP_OK;
+    cudaStream_t st = as_stream(stream);
+    const unsigned grid = grid_for(n, 256, 148LL * 16);
+    if (dtype == HBP_F32) k_add<float><<<grid, 256, 0, st>>>((float *)y, (const float *)a, n);
+    else if (dtype == HBP_F64) k_add<double><<<grid, 256, 0, st>>>((double *)y, (const double *)a, n);
+    else return HBP_E_ARG;
     return (int)cudaGetLastError();
 }
 

@@ -23,7 +23,8 @@ import torch
 from .reorder import BUCKET_MAX, HashParams
 
 __all__ = ["Stripe", "plan_stripes", "sample_hash_params_global", "gather_rows",
-           "power_iteration"]
+           "power_iteration", "row_block_nnz", "padded_columns", "StripedOperator",
+           "PowerIteration"]
 
 
 @dataclass(frozen=True)
@@ -142,3 +143,238 @@ def power_iteration(spmv_local: Callable[[torch.Tensor], torch.Tensor], x0: torc
         y = y / torch.sqrt(sq).to(y.dtype)
         x = gather_rows(y, stripes, group)
     return x
+
+
+# ------------------------------------------------------------- GPU striping
+def row_block_nnz(row_ptr: torch.Tensor, rows: int, row_height: int) -> np.ndarray:
+    """nnz per row block from a CSR row_ptr (the weights of plan_stripes)."""
+    nrb = -(-rows // row_height)
+    idx = torch.clamp(torch.arange(nrb + 1, device=row_ptr.device) * row_height, max=rows)
+    return torch.diff(row_ptr[idx]).cpu().numpy()
+
+
+def padded_columns(col_idx: torch.Tensor, stripes: Sequence[Stripe], pad: int) -> torch.Tensor:
+    """Global column c of a square matrix whose x is distributed like y ->
+    its slot in the all-gather buffer [world * pad]: owner * pad + (c -
+    row_lo(owner)).  Monotone in c, so every row keeps its column order (and
+    the HBP layout its element order)."""
+    lo = torch.tensor([st.row_lo for st in stripes], dtype=torch.int64, device=col_idx.device)
+    c = col_idx.to(torch.int64)
+    owner = torch.searchsorted(lo, c, right=True) - 1
+    return (owner * pad + (c - lo[owner])).to(torch.int32)
+
+
+class StripedOperator:
+    """This rank's row stripe of a global CSR matrix as HBP SpMV operators
+    (SURVEY.md §8e): rows [row_lo, row_hi) of whole row blocks, hash
+    parameters from the global sample (sample_hash_params_global), so every
+    block's permutation and layout equal the single-GPU build's.
+
+    x_layout="global": x is the full global vector (a single SpMV, x
+    replicated).  x_layout="padded": x lives in the all-gather buffer
+    [world * pad] (padded_columns), the iterated SpMV's layout; with
+    split_own the stripe is built as two operators, the columns this rank
+    owns (usable before the all-gather lands) and the rest.
+
+    Compute is the CUDA path (build_hbp, SpmvOperator); the collectives are
+    torch.distributed (NCCL on B200; gloo works for tests)."""
+
+    def __init__(self, rows: int, cols: int, row_ptr: torch.Tensor, col_idx: torch.Tensor,
+                 values: torch.Tensor, stripes: Sequence[Stripe], rank: int, config,
+                 x_layout: str = "global", split_own: bool = False, group=None,
+                 op_kwargs: dict | None = None, seed: int = 0,
+                 distributed: bool | None = None, timings: dict | None = None):
+        from .formats import CsrMatrix
+        from .hbp import build_hbp
+        from .partition import PartitionConfig, make_grid
+        from .reorder import _grid_counts_at, hash_permutations
+        from .engine import SpmvOperator
+        import torch.distributed as dist
+
+        if x_layout not in ("global", "padded"):
+            raise ValueError("x_layout must be 'global' or 'padded'")
+        if x_layout == "padded" and rows != cols:
+            raise ValueError("the padded (iterated) layout needs a square matrix")
+        self.stripes, self.rank, self.world = list(stripes), rank, len(stripes)
+        self.stripe = st = self.stripes[rank]
+        self.pad = max(x.rows for x in self.stripes)
+        self.rows_global, self.cols_global = rows, cols
+        self.x_layout = x_layout
+        self.dtype = values.dtype
+        dev = values.device
+        e0, e1 = int(row_ptr[st.row_lo].item()), int(row_ptr[st.row_hi].item())
+        rp = (row_ptr[st.row_lo:st.row_hi + 1] - e0).contiguous()
+        ci = col_idx[e0:e1]
+        vals = values[e0:e1].contiguous()
+        if x_layout == "padded":
+            ci = padded_columns(ci, self.stripes, self.pad)
+            width = self.world * self.pad
+        else:
+            ci = ci.contiguous()
+            width = cols
+        # C = cols configs keep one column block over the (padded) width
+        C = width if config.col_width >= cols else config.col_width
+        cfg = PartitionConfig(col_width=C, row_height=config.row_height,
+                              warp_size=config.warp_size, fixed_fraction=config.fixed_fraction)
+        self.config = cfg
+        self.width = width
+        self.nnz = e1 - e0
+        import time
+
+        def mark(name):
+            # stage times (cli.py:150-158 analogue) when asked for: synchronised
+            if timings is not None:
+                torch.cuda.synchronize(dev)
+                now = time.perf_counter()
+                timings[name] = (now - mark.t) * 1e3
+                mark.t = now
+        if timings is not None:
+            torch.cuda.synchronize(dev)
+        mark.t = time.perf_counter()
+        csr = CsrMatrix(st.rows, width, rp, ci, vals)
+        grid = make_grid(csr, cfg)
+        mark("grid")
+        ncb = -(-width // C)
+        if distributed is None:
+            distributed = self.world > 1
+        if distributed:
+            self.params = sample_hash_params_global(lambda flat: _grid_counts_at(grid, flat), st,
+                                                    rows, ncb, cfg.row_height, group=group,
+                                                    seed=seed, device=dev if dev.type == "cuda"
+                                                    and dist.get_backend(group) == "nccl" else None)
+        else:
+            from .reorder import sample_hash_params
+            self.params = sample_hash_params(grid, cfg, seed=seed)
+        mark("sample")
+        kw = dict(op_kwargs or {})
+        own_lo, own_hi = rank * self.pad, rank * self.pad + st.rows
+        self.split = bool(split_own and x_layout == "padded" and self.world > 1)
+        self.csr, self.grid = csr, grid
+
+        def build(csr_part, g=None):
+            g = make_grid(csr_part, cfg) if g is None else g
+            perms = hash_permutations(g, self.params)
+            mark("hash")
+            h = build_hbp(csr_part, g, perms, with_add_sign=False, with_zero_row=False)
+            mark("build")
+            o = SpmvOperator(h, **kw)
+            mark("operator")
+            return h, o
+
+        if self.split:
+            # entries of own columns vs the rest, each as its own CSR stripe
+            own = (ci >= own_lo) & (ci < own_hi)
+            row_of = torch.repeat_interleave(torch.arange(st.rows, device=dev), torch.diff(rp))
+            parts = []
+            for m in (own, ~own):
+                cnt = torch.zeros(st.rows, dtype=torch.int64, device=dev)
+                cnt.index_add_(0, row_of[m], torch.ones_like(row_of[m]))
+                rpm = torch.zeros(st.rows + 1, dtype=torch.int64, device=dev)
+                rpm[1:] = torch.cumsum(cnt, 0)
+                parts.append(CsrMatrix(st.rows, width, rpm, ci[m].contiguous(),
+                                       vals[m].contiguous()))
+            del row_of, own
+            (self.hbp_own, self.op_own), (self.hbp, self.op) = build(parts[0]), build(parts[1])
+            self.y_own = torch.empty(st.rows, dtype=self.dtype, device=dev)
+        else:
+            self.hbp, self.op = build(csr, grid)
+            self.hbp_own = self.op_own = None
+        self.own_share = (self.hbp_own.nnz / max(1, self.nnz)) if self.split else 0.0
+
+    @property
+    def ops(self):
+        return [o for o in (self.op_own, self.op) if o is not None]
+
+    @property
+    def launches_per_call(self) -> int:
+        return sum(o.launches_per_call for o in self.ops) + (1 if self.split else 0)
+
+    def __call__(self, x: torch.Tensor, y: torch.Tensor, x_sumsq: torch.Tensor | None = None,
+                 before_remote=None) -> torch.Tensor:
+        """y (this stripe's rows) = A_stripe x.  With the own-column split,
+        before_remote() (e.g. waiting for the all-gather) runs between the
+        own-column part and the rest."""
+        if self.split:
+            self.op_own(x, self.y_own, x_sumsq=x_sumsq)
+            if before_remote is not None:
+                before_remote()
+            self.op(x, y, x_sumsq=x_sumsq)
+            from . import _lib as L
+            L.call("hbp_add", L.P(y), L.P(self.y_own), L.c_int(L.dtype_code(self.dtype)),
+                   L.c_i64(y.numel()), L.stream())
+            return y
+        if before_remote is not None:
+            before_remote()
+        return self.op(x, y, x_sumsq=x_sumsq)
+
+
+class PowerIteration:
+    """Config 5 over row stripes: x <- A x / ||A x||_2.  A step is the
+    stripe SpMV (normalisation folded into its y stores), hbp_sumsq, an
+    8-byte all-reduce of ||y||^2 and an in-place all-gather of the y
+    stripes straight into the next x buffer (padded layout, no copy).  With
+    overlap, the gather runs asynchronously and the next step's own-column
+    part (StripedOperator split_own) computes while it is in flight."""
+
+    def __init__(self, op: StripedOperator, x0: torch.Tensor, group=None, overlap: bool = True):
+        import torch.distributed as dist
+        from . import engine as E
+        if op.x_layout != "padded":
+            raise ValueError("PowerIteration needs a padded-layout StripedOperator")
+        self.op, self.group = op, group
+        self.dist = dist if op.world > 1 else None
+        self.overlap = overlap and op.world > 1
+        dev = x0.device
+        n = op.world * op.pad
+        self.xs = [torch.zeros(n, dtype=op.dtype, device=dev) for _ in range(2)]
+        for st in op.stripes:
+            self.xs[0][st.rank * op.pad:st.rank * op.pad + st.rows] = x0[st.row_lo:st.row_hi].to(
+                op.dtype)
+        self.sq = torch.ones(1, dtype=torch.float64, device=dev)
+        n_scr = E.L.c_i64(0)
+        E.L.call("hbp_sumsq_scratch", E.ctypes.byref(n_scr))
+        self.scratch = torch.empty(n_scr.value, dtype=torch.float64, device=dev)
+        self.cur = 0
+        self.pending = None
+        self._sumsq = E.sumsq
+
+    def _own(self, buf: torch.Tensor) -> torch.Tensor:
+        o = self.op
+        return buf[o.rank * o.pad:(o.rank + 1) * o.pad]
+
+    def step(self) -> None:
+        o = self.op
+        x, nxt = self.xs[self.cur], self.xs[1 - self.cur]
+        y = self._own(nxt)[:o.stripe.rows]
+
+        def wait_gather():
+            if self.pending is not None:
+                self.pending.wait()
+                self.pending = None
+
+        o(x, y, x_sumsq=self.sq, before_remote=wait_gather)
+        wait_gather()
+        self._sumsq(y, self.sq, self.scratch)
+        if self.dist is not None:
+            self.dist.all_reduce(self.sq, group=self.group)
+            work = self.dist.all_gather_into_tensor(nxt, self._own(nxt), group=self.group,
+                                                    async_op=True)
+            if self.overlap:
+                self.pending = work
+            else:
+                work.wait()
+        self.cur = 1 - self.cur
+
+    def finish(self) -> None:
+        if self.pending is not None:
+            self.pending.wait()
+            self.pending = None
+
+    def x_global(self) -> torch.Tensor:
+        """The current iterate x_k / ||x_k|| in the global row order."""
+        self.finish()
+        o = self.op
+        x = self.xs[self.cur]
+        parts = [x[st.rank * o.pad:st.rank * o.pad + st.rows] for st in o.stripes]
+        v = torch.cat(parts).to(torch.float64)
+        return v / torch.sqrt((v * v).sum())

@@ -100,3 +100,22 @@ def test_world2_matches_single_process():
         x = y / np.sqrt((y ** 2).sum())
     for k in range(world):
         np.testing.assert_allclose(out[k]["x"], x, rtol=1e-12, atol=1e-15)
+
+
+def test_padded_columns_and_row_block_nnz():
+    from paper_2504_08860_b200.stripes import padded_columns, row_block_nnz
+    rp = torch.tensor([0, 2, 2, 5, 6, 9, 9, 10], dtype=torch.int64)  # 7 rows
+    np.testing.assert_array_equal(row_block_nnz(rp, 7, 3), [5, 4, 1])
+    st = plan_stripes([5, 4, 1], rows=7, row_height=3, world=2)
+    assert [(s.row_lo, s.row_hi) for s in st] == [(0, 3), (3, 7)]
+    pad = max(s.rows for s in st)  # 4
+    cols = torch.arange(7, dtype=torch.int32)
+    np.testing.assert_array_equal(padded_columns(cols, st, pad), [0, 1, 2, 4, 5, 6, 7])
+    # an empty stripe (fewer row blocks than ranks) owns no column
+    st3 = plan_stripes([5, 4, 1], rows=7, row_height=3, world=4)
+    pad3 = max(s.rows for s in st3)
+    got = padded_columns(cols, st3, pad3).numpy()
+    owner = got // pad3
+    for c, o in zip(range(7), owner):
+        assert st3[o].row_lo <= c < st3[o].row_hi
+    assert np.all(np.diff(got) > 0)
