@@ -157,6 +157,11 @@ int hbp_hash_perm_empty(int64_t n, int64_t a, int64_t b, int64_t c, int64_t d,
  * blocks, and reorder.py:222-225 identity_permutations. */
 int hbp_sort_perm(const uint32_t *len_local, const int32_t *blk_br, int64_t nzb, int64_t rows,
                   int64_t row_height, uint32_t *perm, hbp_stream_t stream);
+/* reorder.py:139-157 _counting_merge_sort: the number of key comparisons the
+ * reference's instrumented top-down merge sort makes on keys[0..n) (split at
+ * len//2, merge with `<=`); *out += that count (sort_permutation(counter=)). */
+int hbp_merge_comparisons(const int64_t *keys, int64_t n, unsigned long long *out,
+                          hbp_stream_t stream);
 /* Gathers nonzero blocks' slices of a dense [ncb*rows] permutation table and
  * checks every block (empty ones too) is a bijection (hbp.py:179-181):
  * *bad = smallest bc-major block index that is not, or -1. */
@@ -329,6 +334,18 @@ typedef struct {
                               in fast mode (deterministic, not the reference's order:
                               within ~1e-14 relative for f64); every other row stays
                               bitwise the reference.  Needs the fast-mode scratch. */
+    /* Stream kernel, competitive pieces (engine.py:137-176 applied to element
+     * slices): with pieces > workers, the first fixed_elems elements are cut
+     * into `workers` equal pieces (warp w starts on piece w, its fixed chunk)
+     * and the rest into pieces - workers equal pieces that warps claim with
+     * an atomic ticket (ticket: u32[2], zero-filled once; the kernel leaves
+     * it zeroed).  slice_lo/slice_g and part_head/part_tail are then sized
+     * by pieces.  0 (or == workers): one static slice per warp. */
+    int64_t pieces;
+    int64_t fixed_elems;
+    uint32_t *ticket;
+    int64_t *warp_ns; /* nullable [2*workers]: %globaltimer at each warp's start
+                         and end (load-balance diagnostics) */
 } hbp_balanced_t;
 
 int hbp_balanced_workers(const hbp_format_t *f, int64_t *workers);

@@ -261,6 +261,33 @@ def sort_permutation(row_nnz):
     return np.argsort(np.asarray(row_nnz), kind="stable").astype(np.uint32)
 
 
+def counting_merge_sort(row_nnz):
+    """reorder.py:139-171 counter path: top-down merge sort split at len//2,
+    merged with `key[left] <= key[right]`, one comparison per step of the
+    merge loop.  Returns (perm u32[n], comparisons)."""
+    key = np.asarray(row_nnz)
+    count = [0]
+
+    def msort(idx):
+        if len(idx) <= 1:
+            return idx
+        mid = len(idx) // 2
+        left, right = msort(idx[:mid]), msort(idx[mid:])
+        out, i, j = [], 0, 0
+        while i < len(left) and j < len(right):
+            count[0] += 1
+            if key[left[i]] <= key[right[j]]:
+                out.append(left[i])
+                i += 1
+            else:
+                out.append(right[j])
+                j += 1
+        return out + left[i:] + right[j:]
+
+    order = msort(list(range(key.size)))
+    return np.asarray(order, dtype=np.uint32), count[0]
+
+
 def sort_permutations(grid: DenseGrid):
     """reorder.py:187-219: per block stable sort by nnz."""
     out = np.empty(grid.ncb * grid.rows, np.uint32)

@@ -4,7 +4,7 @@
 //   make_grid          partition.py:100-127   -> count/emit runs, block heads, fill slots
 //   sample_hash_params reorder.py:69-103       -> sampled counts (the (a, c) arithmetic
 //                                                 stays on the host, same numpy calls)
-//   hash_permutations  reorder.py:174-184 / _kernels.py:62-92 -> bitmap FCFS probing
+//   hash_permutations  reorder.py:174-184 -> hbp_reorder.cu
 //   build_hbp          hbp.py:150-238          -> slot lengths, group sizes, emission
 // The reference's arrays are dense in rows x column-blocks; here every
 // per-slot array is compact over NONZERO blocks and
@@ -185,86 +185,6 @@ __global__ void k_sample_counts(const int64_t *__restrict__ row_ptr,
         int64_t a = lower_bound_col(col, lo, hi, bc * C);
         int64_t b = lower_bound_col(col, a, hi, (bc + 1) * C);
         counts[i] = (int32_t)(b - a);
-    }
-}
-
-// ------------------------------------------------------------- hash perm
-// One thread per nonzero block; the block's occupancy bitmap lives in shared
-// memory, word w of thread t at [w * blockDim + t] (conflict-free).  Rows
-// claim slots in ascending local-row order; the claimed slot is the first
-// free one at or after the preliminary slot, cyclically -- the same slot the
-// reference's +1 probe loop reaches, and the probes
-// it counts are the cyclic distance (slot - preliminary) mod n.
-__device__ __forceinline__ int64_t prelim_slot(uint32_t len, int64_t r, int64_t n, int64_t a,
-                                               int64_t b, int64_t c, int64_t d, int64_t bmax) {
-    int64_t g = a >= 32 ? 0 : (int64_t)(len >> a);
-    if (g > bmax) g = bmax;
-    return (g * b + (r * c) % d) % n;
-}
-
-template <bool EMPTY>
-__global__ void k_hash_perm(const uint32_t *__restrict__ len_local,
-                            const int32_t *__restrict__ blk_br, int64_t nzb, int64_t rows,
-                            int64_t R, int64_t a, int64_t b, int64_t c, int64_t d, int64_t bmax,
-                            uint32_t *__restrict__ perm, unsigned long long *__restrict__ probes) {
-    extern __shared__ uint32_t bm[];
-    const int T = blockDim.x, t = threadIdx.x;
-    int64_t blk = (int64_t)blockIdx.x * T + t;
-    unsigned long long my_probes = 0;
-    if (blk < nzb) {
-        int64_t n = EMPTY ? rows : rows_in_block(rows, R, blk_br[blk]);
-        int nw = (int)((n + 31) >> 5);
-        for (int w = 0; w < nw; ++w) bm[w * T + t] = 0u;
-        if (n & 31) bm[(nw - 1) * T + t] = ~((1u << (n & 31)) - 1u);  // bits >= n: taken
-        const uint32_t *lens = len_local + blk * R;
-        uint32_t *out = perm + blk * R;
-        for (int64_t r = 0; r < n; ++r) {
-            uint32_t len = EMPTY ? 0u : lens[r];
-            int64_t pos = prelim_slot(len, r, n, a, b, c, d, bmax);
-            int w = (int)(pos >> 5);
-            uint32_t word = bm[w * T + t];
-            uint32_t fr = ~word & (0xffffffffu << (pos & 31));
-            while (!fr) {
-                w = (w + 1 == nw) ? 0 : w + 1;
-                word = bm[w * T + t];
-                fr = ~word;
-            }
-            int bit = __ffs(fr) - 1;
-            bm[w * T + t] = word | (1u << bit);
-            int64_t slot = (int64_t)w * 32 + bit;
-            out[slot] = (uint32_t)r;
-            my_probes += (unsigned long long)(slot >= pos ? slot - pos : slot + n - pos);
-        }
-        if (n < R)
-            for (int64_t s = n; s < R && !EMPTY; ++s) out[s] = 0u;
-    }
-    if (probes) {
-        for (int o = 16; o; o >>= 1) my_probes += __shfl_xor_sync(0xffffffffu, my_probes, o);
-        if ((t & 31) == 0 && my_probes) atomicAdd(probes, my_probes);
-    }
-}
-
-// reorder.py:160-171 sort_permutation: stable ascending nnz; warp per block,
-// rank(r) = #{r' : len[r'] < len[r]} + #{r' < r : len[r'] == len[r]}.
-__global__ void k_sort_perm(const uint32_t *__restrict__ len_local,
-                            const int32_t *__restrict__ blk_br, int64_t nzb, int64_t rows,
-                            int64_t R, uint32_t *__restrict__ perm) {
-    int lane = threadIdx.x & 31;
-    int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t blk = warp; blk < nzb; blk += nwarps) {
-        int64_t n = rows_in_block(rows, R, blk_br[blk]);
-        const uint32_t *lens = len_local + blk * R;
-        for (int64_t r = lane; r < n; r += 32) {
-            uint32_t lr = lens[r];
-            int64_t rank = 0;
-            for (int64_t o = 0; o < n; ++o) {
-                uint32_t lo = lens[o];
-                rank += (lo < lr) || (lo == lr && o < r);
-            }
-            perm[blk * R + rank] = (uint32_t)r;
-        }
-        for (int64_t s = n + lane; s < R; s += 32) perm[blk * R + s] = 0u;
     }
 }
 
@@ -796,56 +716,6 @@ int hbp_sample_counts(const int64_t *row_ptr, const int32_t *col_idx, int64_t ro
     if (k <= 0) return HBP_OK;
     k_sample_counts<<<grid_for(k, kThreads), kThreads, 0, as_stream(stream)>>>(
         row_ptr, col_idx, rows, col_width, flat_idx, k, counts);
-    HBP_LAUNCH_CHECK();
-    return HBP_OK;
-}
-
-static int hash_launch_shape(int64_t R, int *threads, size_t *smem) {
-    int64_t nw = (R + 31) / 32;
-    int64_t t = 64;
-    while (t > 1 && nw * 4 * t > 48 * 1024) t >>= 1;
-    if (nw * 4 * t > 48 * 1024) return HBP_E_UNSUPPORTED;
-    *threads = (int)t;
-    *smem = (size_t)(nw * 4 * t);
-    return HBP_OK;
-}
-
-int hbp_hash_perm(const uint32_t *len_local, const int32_t *blk_br, int64_t nzb, int64_t rows,
-                  int64_t row_height, int64_t a, int64_t b, int64_t c, int64_t d,
-                  int64_t bucket_max, uint32_t *perm, unsigned long long *probes,
-                  hbp_stream_t stream) {
-    if (b < 1 || d < 1 || a < 0 || row_height < 1) return HBP_E_ARG;
-    if (nzb <= 0) return HBP_OK;
-    int threads;
-    size_t smem;
-    int st = hash_launch_shape(row_height, &threads, &smem);
-    if (st) return st;
-    unsigned grid = (unsigned)((nzb + threads - 1) / threads);
-    k_hash_perm<false><<<grid, threads, smem, as_stream(stream)>>>(
-        len_local, blk_br, nzb, rows, row_height, a, b, c, d, bucket_max, perm, probes);
-    HBP_LAUNCH_CHECK();
-    return HBP_OK;
-}
-
-int hbp_hash_perm_empty(int64_t n, int64_t a, int64_t b, int64_t c, int64_t d,
-                        int64_t bucket_max, uint32_t *perm, hbp_stream_t stream) {
-    if (n < 1 || b < 1 || d < 1) return HBP_E_ARG;
-    int threads;
-    size_t smem;
-    int st = hash_launch_shape(n, &threads, &smem);
-    if (st) return st;
-    // one thread; `rows` carries n, R = n
-    k_hash_perm<true><<<1, 32, (size_t)((n + 31) / 32) * 4 * 32, as_stream(stream)>>>(
-        nullptr, nullptr, 1, n, n, a, b, c, d, bucket_max, perm, nullptr);
-    HBP_LAUNCH_CHECK();
-    return HBP_OK;
-}
-
-int hbp_sort_perm(const uint32_t *len_local, const int32_t *blk_br, int64_t nzb, int64_t rows,
-                  int64_t row_height, uint32_t *perm, hbp_stream_t stream) {
-    if (nzb <= 0) return HBP_OK;
-    k_sort_perm<<<grid_for(nzb * 32, kThreads), kThreads, 0, as_stream(stream)>>>(
-        len_local, blk_br, nzb, rows, row_height, perm);
     HBP_LAUNCH_CHECK();
     return HBP_OK;
 }

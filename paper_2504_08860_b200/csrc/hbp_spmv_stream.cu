@@ -145,17 +145,28 @@ __device__ __forceinline__ int64_t cut_at(int64_t w, int64_t E, int64_t Nw) {
     return (int64_t)((__int128)w * E / Nw);
 }
 
-// Slice of worker w: equal element ranges [cut(w), cut(w+1)); exact mode
-// rounds both ends up to group boundaries (every row summed by one lane in
-// step order).  g = the first group whose elements the slice touches.
+// Cut v of the slicing: equal ranges of the element array per worker, or,
+// with competitive pieces (np > nw), nw equal pieces of the first F
+// elements (the workers' fixed chunks) followed by np - nw equal pieces of
+// the rest (the ticket pool; engine.py:38-56 plan_execution on elements).
+__device__ __forceinline__ int64_t piece_cut(int64_t v, int64_t E, int64_t nw, int64_t np,
+                                             int64_t F) {
+    if (np <= nw) return cut_at(v, E, nw);
+    if (v <= nw) return (int64_t)((__int128)v * F / nw);
+    return F + (int64_t)((__int128)(v - nw) * (E - F) / (np - nw));
+}
+
+// Slice of worker (or piece) w: [cut(w), cut(w+1)); exact mode rounds both
+// ends up to group boundaries (every row summed by one lane in step order).
+// g = the first group whose elements the slice touches.
 // With hub_min > 0 (exact mode), a cut inside a group longer than hub_min
 // elements stays where it is: that group is split over warps like a
 // fast-mode group (the thresholded hub-row path).
 __device__ __forceinline__ void stream_slice(const int64_t *__restrict__ gs, int64_t ngroups,
                                              int64_t E, int64_t w, int64_t Nw, bool exact,
                                              int64_t hub_min, int64_t *lo, int64_t *hi,
-                                             int64_t *g0) {
-    int64_t c_lo = cut_at(w, E, Nw), c_hi = cut_at(w + 1, E, Nw);
+                                             int64_t *g0, int64_t np = 0, int64_t F = 0) {
+    int64_t c_lo = piece_cut(w, E, Nw, np, F), c_hi = piece_cut(w + 1, E, Nw, np, F);
     if (exact) {
         if (c_lo > 0 && c_lo < E) {
             int64_t g = upper_group(gs, ngroups, c_lo);
@@ -173,16 +184,19 @@ __device__ __forceinline__ void stream_slice(const int64_t *__restrict__ gs, int
     *g0 = g;
 }
 
+// one thread per slice (per piece when np > Nw)
 __global__ void k_stream_slices(const int64_t *__restrict__ gs, int64_t ngroups, int64_t E,
                                 int64_t Nw, bool exact, int64_t hub_min,
-                                int64_t *__restrict__ slice_lo, int64_t *__restrict__ slice_g) {
+                                int64_t *__restrict__ slice_lo, int64_t *__restrict__ slice_g,
+                                int64_t np, int64_t F) {
     const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (w >= Nw) return;
+    const int64_t n = np > Nw ? np : Nw;
+    if (w >= n) return;
     int64_t lo, hi, g;
-    stream_slice(gs, ngroups, E, w, Nw, exact, hub_min, &lo, &hi, &g);
+    stream_slice(gs, ngroups, E, w, Nw, exact, hub_min, &lo, &hi, &g, np, F);
     slice_lo[w] = lo;
     slice_g[w] = g;
-    if (w == Nw - 1) slice_lo[Nw] = hi;
+    if (w == n - 1) slice_lo[n] = hi;
 }
 
 template <typename V, bool EXACT>
@@ -574,9 +588,14 @@ __global__ void __launch_bounds__(NT, MINB)
         for (int32_t i = threadIdx.x; i < nv; i += NT) reinterpret_cast<uint4 *>(hot)[i] = __ldcg(src + i);
         __syncthreads();
     }
-    const int64_t w = (int64_t)blockIdx.x * kWarps + wib;
+    const int64_t w0 = (int64_t)blockIdx.x * kWarps + wib;
     const int64_t Nw = b.workers;
-    if (w >= Nw) return;
+    if (w0 >= Nw) return;
+    if (b.warp_ns && lane == 0) b.warp_ns[2 * w0] = globaltimer_ns();
+    // XM & 8192: competitive pieces -- warp w0 runs piece w0 (its fixed chunk),
+    // then claims pieces Nw.. with the ticket (engine.py:155-165 on slices)
+    constexpr bool TK = (XM & 8192) != 0;
+    const int64_t Np = TK ? b.pieces : Nw;
     const int32_t R = (int32_t)f.row_height, gpb = R / 32;
     const int64_t ngroups = f.nzb * gpb;
     const int64_t E = f.nnz;
@@ -585,6 +604,7 @@ __global__ void __launch_bounds__(NT, MINB)
     const uint2 *__restrict__ phs = (const uint2 *)f.phases;
     const uint32_t *__restrict__ permp = (const uint32_t *)f.perm;
 
+    for (int64_t w = w0, np_done = 0;; ++np_done) {
     int64_t c_lo, c_hi, g;
     if (b.slice_lo) {  // precomputed (hbp_stream_slices): no binary searches here
         c_lo = b.slice_lo[w];
@@ -602,8 +622,14 @@ __global__ void __launch_bounds__(NT, MINB)
     }
     const int32_t len32 = (int32_t)(c_hi - base);
     const int32_t lo_s = (int32_t)(c_lo - base);  // slice start (0..3)
+    if (TK && np_done) {  // the previous piece's ring is drained (every chunk waited)
+        fence_proxy_async();
+        __syncwarp();
+    }
     if (lane == 0) {
         const int32_t nchunks = c_hi > c_lo ? (len32 + CH - 1) / CH : 0;
+        if (TK && np_done)
+            for (int i = 0; i < NB; ++i) mbar_inval(&S.mbar[i]);
         S.colg = (HOT ? f.scol : f.col) + base;
         S.valg = (const V *)f.data + base;
         S.len32 = len32;
@@ -619,7 +645,7 @@ __global__ void __launch_bounds__(NT, MINB)
     }
     __syncwarp();
 
-    const bool last_warp = (w == Nw - 1);
+    const bool last_warp = (w == Np - 1);
     // y written directly is scaled by 1 / sqrt(*b.y_sumsq) when given (the
     // power iteration folds x / ||x|| into the next SpMV); 1.0 is exact
     const double ys = b.y_sumsq ? 1.0 / sqrt(*b.y_sumsq) : 1.0;
@@ -807,13 +833,24 @@ __global__ void __launch_bounds__(NT, MINB)
         done = __shfl_sync(FULL, done, 0);
         if (!done) continue;
         __threadfence();
-        int64_t wa = (int64_t)((__int128)ga0 * Nw / E);
-        while (wa + 1 < Nw && cut_at(wa + 1, E, Nw) <= ga0) ++wa;
-        while (wa > 0 && cut_at(wa, E, Nw) > ga0) --wa;
+        int64_t wa;
+        if constexpr (TK) {  // last piece starting at or before ga0 (slice_lo sorted)
+            int64_t l = 0, h = Np;
+            while (h - l > 1) {
+                const int64_t m = (l + h) >> 1;
+                if (b.slice_lo[m] <= ga0) l = m;
+                else h = m;
+            }
+            wa = l;
+        } else {
+            wa = (int64_t)((__int128)ga0 * Nw / E);
+            while (wa + 1 < Nw && cut_at(wa + 1, E, Nw) <= ga0) ++wa;
+            while (wa > 0 && cut_at(wa, E, Nw) > ga0) --wa;
+        }
         double s = __ldcg(b.part_tail + wa * 32 + lane);
-        for (int64_t v = wa + 1; v < Nw; ++v) {
+        for (int64_t v = wa + 1; v < Np; ++v) {
             s += __ldcg(b.part_head + v * 32 + lane);
-            if (cut_at(v + 1, E, Nw) >= ga1) break;
+            if ((TK ? b.slice_lo[v + 1] : cut_at(v + 1, E, Nw)) >= ga1) break;
         }
         if (valid) {
             if (pb_now) pb_now[row_local] = s;
@@ -823,6 +860,25 @@ __global__ void __launch_bounds__(NT, MINB)
         if (FC && pb_now) group_done(br_now, rows_now);
     }
     if (FC && pend_n) flush_done(pend_br, pend_n, pend_rows);
+    if constexpr (!TK) break;
+    else {
+        int64_t nxt = 0;
+        if (lane == 0) {
+            const uint32_t t = atomicAdd(b.ticket, 1u);
+            nxt = Nw + (int64_t)t;
+            // every warp draws exactly one ticket past the pool; the last such
+            // draw resets the counters for the next launch
+            if (nxt >= Np && atomicAdd(b.ticket + 1, 1u) + 1u == (uint32_t)Nw) {
+                b.ticket[0] = 0u;
+                b.ticket[1] = 0u;
+            }
+        }
+        nxt = __shfl_sync(FULL, nxt, 0);
+        if (nxt >= Np) break;
+        w = nxt;
+    }
+    }
+    if (b.warp_ns && lane == 0) b.warp_ns[2 * w0 + 1] = globaltimer_ns();
 }
 
 // Shared memory per SM is kept to what MINB CTAs need: the rest of the
@@ -939,7 +995,18 @@ bool staged(const hbp_format_t *f) { return f->n_hot > 0 && f->scol && f->hot_co
 // exact mode with the hub-row path (b->hub_min > 0) is its own instantiation
 // (XM | 4096): the fast-mode walk it adds would cost the plain exact kernel
 // registers
-#define HBP_STREAM_DISPATCH(FN, V, EXACT, FUSED, HUB, ...)                                  \
+// competitive pieces (b->pieces > b->workers, XM | 8192) have their own
+// instantiations of the default, warm and unstaged kernels
+#define HBP_STREAM_DISPATCH(FN, V, EXACT, FUSED, HUB, TICKET, ...)                          \
+    if (TICKET && !HUB && !FUSED) {                                                         \
+        if (staged(f) && f->n_warm > 0) {                                                   \
+            HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, kWarmThreads, 1, 53 | 2048 | 8192, __VA_ARGS__); \
+        }                                                                                   \
+        if (staged(f)) {                                                                    \
+            HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, kHotThreads, 1, 21 | 2048 | 8192, __VA_ARGS__); \
+        }                                                                                   \
+        HBP_VARIANT_X(FN, V, EXACT, false, 128, 4, kHotThreads, 1, 21 | 2048 | 8192, __VA_ARGS__); \
+    }                                                                                       \
     if (EXACT && HUB) {                                                                     \
         if (staged(f) && f->n_warm > 0) {                                                   \
             HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, kWarmThreads, 1, 53 | 2048 | 4096, __VA_ARGS__); \
@@ -981,7 +1048,7 @@ int hot_ring_bytes(size_t *out, bool warm) {  // shared memory of the staged lau
 
 template <typename V, bool EXACT>
 int occupancy(const hbp_format_t *f, int *per_sm, int *warps_per_cta) {
-    HBP_STREAM_DISPATCH(occupancy_of, V, EXACT, false, false, f, per_sm, warps_per_cta)
+    HBP_STREAM_DISPATCH(occupancy_of, V, EXACT, false, false, false, f, per_sm, warps_per_cta)
 }
 
 template <typename V>
@@ -1007,8 +1074,8 @@ int run(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y, 
         const int rc = hot_gather<V>(x, f->hot_cols, f->n_hot + f->n_warm, b->x_hot, st);
         if (rc) return rc;
     }
-    HBP_STREAM_DISPATCH(launch, V, EXACT, (b->rb_done != nullptr), (b->hub_min > 0), f, b, x, y,
-                        partial, st)
+    HBP_STREAM_DISPATCH(launch, V, EXACT, (b->rb_done != nullptr), (b->hub_min > 0),
+                        (b->pieces > b->workers), f, b, x, y, partial, st)
 }
 
 }  // namespace
@@ -1075,9 +1142,12 @@ int hbp_stream_slices(const hbp_format_t *f, const hbp_balanced_t *b, hbp_stream
     if (f->warp_size != 32 || f->row_height % 32) return HBP_E_UNSUPPORTED;
     const int64_t ngroups = f->nzb * (f->row_height / 32);
     const bool exact = f->exact != 0 || f->dtype == HBP_F64;
-    k_stream_slices<<<(unsigned)((b->workers + 127) / 128), 128, 0, as_stream(stream)>>>(
+    const int64_t n = b->pieces > b->workers ? b->pieces : b->workers;
+    if (b->pieces > b->workers && (b->fixed_elems < 0 || b->fixed_elems > f->nnz))
+        return HBP_E_ARG;
+    k_stream_slices<<<(unsigned)((n + 127) / 128), 128, 0, as_stream(stream)>>>(
         f->group_start, ngroups, f->nnz, b->workers, exact, exact ? b->hub_min : 0, b->slice_lo,
-        b->slice_g);
+        b->slice_g, b->pieces, b->fixed_elems);
     return (int)cudaGetLastError();
 }
 
@@ -1097,6 +1167,11 @@ int hbp_spmv_stream(const hbp_format_t *f, const hbp_balanced_t *b, const void *
     if ((!exact || b->hub_min > 0) && (!b->part_head || !b->part_tail || !b->counters))
         return HBP_E_ARG;
     if (b->hub_min < 0) return HBP_E_ARG;
+    if (b->pieces > b->workers) {  // competitive pieces
+        if (!b->slice_lo || !b->slice_g || !b->ticket || b->rb_done || b->hub_min > 0)
+            return HBP_E_ARG;
+        if ((f->nnz + b->pieces - 1) / b->pieces > (int64_t)1 << 30) return HBP_E_UNSUPPORTED;
+    }
     if (staged(f)) {
         int64_t cap = 0;
         const int rc = hbp_hot_capacity(f->dtype, f->n_warm > 0, &cap);

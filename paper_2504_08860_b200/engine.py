@@ -186,7 +186,7 @@ class SpmvOperator:
     def __init__(self, hbp: HbpMatrix, workers: int | None = None,
                  fixed_fraction: float | None = None, schedule: str | None = None,
                  hot: bool | int | None = None, warm_bytes: int | None = None,
-                 hub_min: int | str | None = None):
+                 hub_min: int | str | None = None, ticket=None):
         self.hbp = hbp
         dev = hbp.data.device
         if schedule is None:
@@ -235,6 +235,24 @@ class SpmvOperator:
             if self.hub_min < 0:
                 raise ValueError("hub_min must be >= 0")
             self.bal.hub_min = self.hub_min
+            # competitive pieces (stream schedule): (fixed fraction of the
+            # elements as one static piece per warp, competitive pieces per
+            # warp for the rest), e.g. "0.7:2"; off by default
+            if ticket is None:
+                ticket = os.environ.get("HBP_STREAM_TICKET") or None
+            self.pieces = self.workers
+            if ticket and schedule == "stream" and hbp.nzb and not self.hub_min:
+                ff, per = (ticket.split(":") if isinstance(ticket, str) else ticket)
+                ff, per = float(ff), float(per)
+                if not (0.0 <= ff <= 1.0 and per > 0):
+                    raise ValueError("ticket needs a fixed fraction in [0, 1] and pieces > 0")
+                self.pieces = self.workers + max(1, int(per * self.workers + 0.5))
+                self.bal.pieces = self.pieces
+                self.bal.fixed_elems = int(ff * hbp.nnz + 0.5)
+                tk = torch.zeros(2, dtype=torch.int32, device=dev)
+                self._ticket_buf = tk
+                self.bal.ticket = tk.data_ptr()
+            npc = self.pieces
             self.hub_groups, self.hub_share = 0, 0.0
             if self.hub_min:
                 glen = hbp.group_start_c[1:] - hbp.group_start_c[:-1]
@@ -242,8 +260,8 @@ class SpmvOperator:
                 self.hub_groups = int(big.sum().item())
                 self.hub_share = float(glen[big].sum().item()) / max(1, hbp.nnz)
             if not f.exact or self.hub_min:
-                ph = torch.empty(self.workers * 32, dtype=torch.float64, device=dev)
-                pt = torch.empty(self.workers * 32, dtype=torch.float64, device=dev)
+                ph = torch.empty(npc * 32, dtype=torch.float64, device=dev)
+                pt = torch.empty(npc * 32, dtype=torch.float64, device=dev)
                 ce = torch.empty(self.workers, dtype=torch.int64, device=dev)
                 cn = torch.zeros(max(1, hbp.nzb * (hbp.config.row_height // 32)),
                                  dtype=torch.int32, device=dev)
@@ -255,8 +273,8 @@ class SpmvOperator:
                 self._scratch.append(xh)
                 self.bal.x_hot = xh.data_ptr()
             if schedule == "stream" and hbp.nzb:
-                sl = torch.empty(self.workers + 1, dtype=torch.int64, device=dev)
-                sg = torch.empty(self.workers, dtype=torch.int64, device=dev)
+                sl = torch.empty(npc + 1, dtype=torch.int64, device=dev)
+                sg = torch.empty(npc, dtype=torch.int64, device=dev)
                 self._scratch += [sl, sg]
                 self.bal.slice_lo, self.bal.slice_g = sl.data_ptr(), sg.data_ptr()
                 L.call("hbp_stream_slices", ctypes.byref(f), ctypes.byref(self.bal), L.stream())
@@ -405,6 +423,17 @@ class SpmvOperator:
             raise ValueError(f"{name} dtype {v.dtype} != matrix dtype {d.dtype}")
         if not v.is_contiguous() or v.numel() != n:
             raise ValueError(f"{name} length {v.numel()} != {n} (or not contiguous)")
+
+    def warp_clock(self) -> torch.Tensor:
+        """Stream schedule diagnostics: from now on every launch records each
+        persistent warp's %globaltimer at start and end into the returned
+        int64 [workers, 2] tensor (load balance: the spread of the end times)."""
+        if self.schedule != "stream":
+            raise ValueError("warp_clock needs the stream schedule")
+        t = torch.zeros(self.workers, 2, dtype=torch.int64, device=self.hbp.data.device)
+        self._warp_ns = t
+        self.bal.warp_ns = t.data_ptr()
+        return t
 
     def capture(self, x: torch.Tensor, y: torch.Tensor) -> "torch.cuda.CUDAGraph":
         """Capture one SpMV (+combine) on fixed x / y buffers in a CUDA graph."""

@@ -3,8 +3,8 @@
 Mirrors /root/reference/pkg/src/hbp_spmv/reorder.py.  The hash constants
 (a, b, c, d) are chosen on the host with the reference's own numpy calls
 (reorder.py:69-103) from 4096 counts the GPU looks up; every nonzero block's
-permutation is then built by ``hbp_hash_perm`` (FCFS linear probing via an
-occupancy bitmap, bit-exact with _kernels.py:62-92).
+permutation is then built by ``hbp_hash_perm`` (FCFS linear probing, one warp
+per block over a register-resident occupancy bitmap, bit-exact with _kernels.py:62-92).
 
 Permutations are returned as ``BlockPermutations``: compact per nonzero block
 on the device, array-like (``.size``, ``np.asarray``, slicing) over the
@@ -195,7 +195,7 @@ def build_block_permutation(row_nnz, params: HashParams,
 def hash_permutations(grid: BlockGrid, params: HashParams,
                       counter: OpCounter | None = None) -> BlockPermutations:
     """reorder.py:174-184: every nonzero block's hash permutation (one GPU
-    thread per block).  The probe count covers nonzero blocks plus the
+    warp per block, the block's occupancy bitmap in the warp's registers).  The probe count covers nonzero blocks plus the
     implied empty blocks, so it equals the reference's OpCounter.probes."""
     R = grid.config.row_height
     perm = _hash_compact(grid.len_local, grid.blk_br, grid.nzb, grid.rows, R, params, counter)
@@ -229,13 +229,21 @@ def _empty_block_probes(grid: BlockGrid, params: HashParams) -> int:
 
 def sort_permutation(row_nnz, counter: OpCounter | None = None) -> np.ndarray:
     """reorder.py:160-171: ascending nnz, ties by ascending local row (GPU
-    stable rank).  Comparison counting (the merge-sort instrumentation) is
-    host bookkeeping the GPU sort does not perform."""
-    if counter is not None:
-        raise NotImplementedError("comparison counting is not implemented on the GPU path")
+    stable block radix sort).  With a counter attached, ``hbp_merge_comparisons``
+    adds the comparisons the reference's instrumented merge sort
+    (reorder.py:139-157) makes on the same keys; the permutation is the same
+    either way, as in the reference."""
     dev = L.require_cuda()
-    lens = torch.as_tensor(np.asarray(row_nnz, dtype=np.int64).astype(np.int32), device=dev)
+    keys = np.asarray(row_nnz, dtype=np.int64)
+    if keys.size and (keys.min() < 0 or keys.max() >= 2**31):
+        raise ValueError("row nnz counts must lie in [0, 2^31)")
+    lens = torch.as_tensor(keys.astype(np.int32), device=dev)
     n = lens.numel()
+    if counter is not None and n > 1:
+        k64 = torch.as_tensor(keys, device=dev)
+        cmp = torch.zeros(1, dtype=torch.int64, device=dev)
+        L.call("hbp_merge_comparisons", L.P(k64), L.c_i64(n), L.P(cmp), L.stream())
+        counter.comparisons += int(cmp.item())
     if n == 0:
         return np.empty(0, np.uint32)
     perm = torch.empty(n, dtype=torch.int32, device=dev)

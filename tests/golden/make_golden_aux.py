@@ -11,6 +11,9 @@ Writes tests/golden/aux/:
                   the reference's group order for the unordered, hash and
                   sort orderings (metrics.py:53-75), plus mean_group_std and
                   reduction_summary;
+  sortcmp.npz     sort_permutation(row_nnz, counter) of a few key arrays:
+                  the permutation and OpCounter.comparisons of the
+                  instrumented merge sort (reorder.py:139-171);
   mtx.npz         parse_matrix_market of a few texts (formats.py:124-194):
                   canonical triplets, incl. duplicates, pattern and integer
                   fields and a symmetric expansion (formats.py:222-240).
@@ -116,7 +119,24 @@ def main():
             e = h.expand_symmetric(t)
             mtx[f"sym_row_{i}"], mtx[f"sym_col_{i}"], mtx[f"sym_val_{i}"] = e.row, e.col, e.val
     np.savez_compressed(os.path.join(OUT, "mtx.npz"), **mtx)
+    sort_counts(h)
     print("wrote", OUT)
+
+
+def sort_counts(h):
+    rng = np.random.default_rng(5)
+    arrays = [np.array([3]), np.array([1, 0]), np.array([1, 1, 1]),
+              np.array([5, 0, 3, 3, 9, 1, 0, 7]), np.zeros(512, np.int64),
+              np.arange(100)[::-1].copy(), np.arange(64), rng.integers(0, 9, 17),
+              rng.integers(0, 9, 100), rng.integers(0, 40, 512), rng.integers(0, 3, 1000),
+              rng.zipf(1.8, 2048) % 5000, rng.integers(0, 1 << 20, 777)]
+    out = {}
+    for i, a in enumerate(arrays):
+        ctr = h.OpCounter()
+        out[f"keys_{i}"] = np.asarray(a, np.int64)
+        out[f"perm_{i}"] = h.sort_permutation(a, counter=ctr)
+        out[f"cmp_{i}"] = np.array(ctr.comparisons, np.int64)
+    np.savez_compressed(os.path.join(OUT, "sortcmp.npz"), **out)
 
 
 if __name__ == "__main__":
