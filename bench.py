@@ -617,6 +617,8 @@ def run_gpu(args):
                    "nonzero_blocks": hbp.nzb, "col_width": C, "row_height": R,
                    "warp_size": 32, "fixed_fraction": 0.7, "workers": op.workers,
                    "schedule": op.schedule,
+                   "slice_cost": (list(op.slice_cost) if getattr(op, "slice_cost", None)
+                                  else None),
                    "hub_min": getattr(op, "hub_min", 0),
                    "hub_groups": getattr(op, "hub_groups", 0),
                    "hub_element_share": round(getattr(op, "hub_share", 0.0), 4),

@@ -346,6 +346,10 @@ typedef struct {
     uint32_t *ticket;
     int64_t *warp_ns; /* nullable [2*workers]: %globaltimer at each warp's start
                          and end (load-balance diagnostics) */
+    /* nullable [ngroups + 1]: exclusive prefix of per-group costs
+     * (hbp_group_costs); hbp_stream_slices then cuts equal COST instead of
+     * equal elements (a group's fixed cost sits at its start). */
+    const int64_t *cost_prefix;
 } hbp_balanced_t;
 
 int hbp_balanced_workers(const hbp_format_t *f, int64_t *workers);
@@ -360,6 +364,12 @@ int hbp_stream_workers(const hbp_format_t *f, int64_t *workers);
  * (otherwise every warp binary-searches group_start at launch -- ~20
  * dependent loads, visible on small matrices). */
 int hbp_stream_slices(const hbp_format_t *f, const hbp_balanced_t *b, hbp_stream_t stream);
+/* Stream-kernel cost of every group in element units (the per-warp cost
+ * model fitted to measured warp times, tools/warp_cost.py): its elements +
+ * w_group + w_phase * phases + w_modular * modular-pass phases (fewer than 12
+ * live lanes, more than 4 steps).  cost[ngroups]. */
+int hbp_group_costs(const hbp_format_t *f, int64_t w_group, int64_t w_phase, int64_t w_modular,
+                    int64_t *cost, hbp_stream_t stream);
 /* Tuning: kernel variant of hbp_spmv_stream for later calls (0 = default;
  * the others are measured alternatives and diagnostics).
  * Not thread-safe; for benchmarks. */

@@ -162,11 +162,10 @@ __device__ __forceinline__ int64_t piece_cut(int64_t v, int64_t E, int64_t nw, i
 // With hub_min > 0 (exact mode), a cut inside a group longer than hub_min
 // elements stays where it is: that group is split over warps like a
 // fast-mode group (the thresholded hub-row path).
-__device__ __forceinline__ void stream_slice(const int64_t *__restrict__ gs, int64_t ngroups,
-                                             int64_t E, int64_t w, int64_t Nw, bool exact,
-                                             int64_t hub_min, int64_t *lo, int64_t *hi,
-                                             int64_t *g0, int64_t np = 0, int64_t F = 0) {
-    int64_t c_lo = piece_cut(w, E, Nw, np, F), c_hi = piece_cut(w + 1, E, Nw, np, F);
+__device__ __forceinline__ void stream_slice_at(const int64_t *__restrict__ gs, int64_t ngroups,
+                                                int64_t E, int64_t c_lo, int64_t c_hi, bool exact,
+                                                int64_t hub_min, int64_t *lo, int64_t *hi,
+                                                int64_t *g0) {
     if (exact) {
         if (c_lo > 0 && c_lo < E) {
             int64_t g = upper_group(gs, ngroups, c_lo);
@@ -183,20 +182,75 @@ __device__ __forceinline__ void stream_slice(const int64_t *__restrict__ gs, int
     *hi = c_hi;
     *g0 = g;
 }
+__device__ __forceinline__ void stream_slice(const int64_t *__restrict__ gs, int64_t ngroups,
+                                             int64_t E, int64_t w, int64_t Nw, bool exact,
+                                             int64_t hub_min, int64_t *lo, int64_t *hi,
+                                             int64_t *g0, int64_t np = 0, int64_t F = 0) {
+    stream_slice_at(gs, ngroups, E, piece_cut(w, E, Nw, np, F), piece_cut(w + 1, E, Nw, np, F),
+                    exact, hub_min, lo, hi, g0);
+}
 
-// one thread per slice (per piece when np > Nw)
+// Element offset of the cost-balanced cut v of Nw: the cost prefix cp
+// (exclusive, per group; a group's fixed cost sits at its start, then one
+// unit per element) reaches v * total / Nw.
+__device__ __forceinline__ int64_t cost_cut(const int64_t *__restrict__ gs,
+                                            const int64_t *__restrict__ cp, int64_t ngroups,
+                                            int64_t E, int64_t v, int64_t Nw) {
+    if (v <= 0) return 0;
+    if (v >= Nw) return E;
+    const int64_t T = (int64_t)((__int128)v * cp[ngroups] / Nw);
+    int64_t lo = 0, hi = ngroups;  // largest g < ngroups with cp[g] <= T
+    while (hi - lo > 1) {
+        const int64_t m = (lo + hi) >> 1;
+        if (cp[m] <= T) lo = m;
+        else hi = m;
+    }
+    const int64_t len = gs[lo + 1] - gs[lo];
+    const int64_t fixed = (cp[lo + 1] - cp[lo]) - len;
+    int64_t off = T - cp[lo] - fixed;
+    off = off < 0 ? 0 : (off > len ? len : off);
+    return gs[lo] + off;
+}
+
+// one thread per slice (per piece when np > Nw); cost-balanced cuts when a
+// cost prefix is given
 __global__ void k_stream_slices(const int64_t *__restrict__ gs, int64_t ngroups, int64_t E,
                                 int64_t Nw, bool exact, int64_t hub_min,
                                 int64_t *__restrict__ slice_lo, int64_t *__restrict__ slice_g,
-                                int64_t np, int64_t F) {
+                                int64_t np, int64_t F, const int64_t *__restrict__ cp) {
     const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t n = np > Nw ? np : Nw;
     if (w >= n) return;
     int64_t lo, hi, g;
-    stream_slice(gs, ngroups, E, w, Nw, exact, hub_min, &lo, &hi, &g, np, F);
+    if (cp) {
+        const int64_t c_lo = cost_cut(gs, cp, ngroups, E, w, Nw);
+        const int64_t c_hi = cost_cut(gs, cp, ngroups, E, w + 1, Nw);
+        stream_slice_at(gs, ngroups, E, c_lo, c_hi, exact, hub_min, &lo, &hi, &g);
+    } else {
+        stream_slice(gs, ngroups, E, w, Nw, exact, hub_min, &lo, &hi, &g, np, F);
+    }
     slice_lo[w] = lo;
     slice_g[w] = g;
     if (w == n - 1) slice_lo[n] = hi;
+}
+
+// hbp_group_costs: thread per group, over its phases
+__global__ void k_group_costs(const int64_t *__restrict__ gs, const int64_t *__restrict__ pptr,
+                              const uint2 *__restrict__ phs, int64_t ngroups, int64_t wg,
+                              int64_t wp, int64_t wm, int64_t *__restrict__ cost) {
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ngroups;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t len = gs[g + 1] - gs[g];
+        const int64_t p0 = pptr[g], p1 = pptr[g + 1];
+        int64_t nmod = 0;
+        for (int64_t j = p0; j < p1; ++j) {
+            const uint2 ph = phs[j];
+            const int64_t end = j + 1 < p1 ? (int64_t)phs[j + 1].y : len;
+            const int k = __popc(ph.x);
+            nmod += (k < 12 && end - (int64_t)ph.y > 4 * k);
+        }
+        cost[g] = len + wg + wp * (p1 - p0) + wm * nmod;
+    }
 }
 
 template <typename V, bool EXACT>
@@ -834,7 +888,8 @@ __global__ void __launch_bounds__(NT, MINB)
         if (!done) continue;
         __threadfence();
         int64_t wa;
-        if constexpr (TK) {  // last piece starting at or before ga0 (slice_lo sorted)
+        const bool by_table = TK || b.slice_lo != nullptr;  // cuts need not be equal
+        if (by_table) {  // last piece starting at or before ga0 (slice_lo sorted)
             int64_t l = 0, h = Np;
             while (h - l > 1) {
                 const int64_t m = (l + h) >> 1;
@@ -850,7 +905,7 @@ __global__ void __launch_bounds__(NT, MINB)
         double s = __ldcg(b.part_tail + wa * 32 + lane);
         for (int64_t v = wa + 1; v < Np; ++v) {
             s += __ldcg(b.part_head + v * 32 + lane);
-            if ((TK ? b.slice_lo[v + 1] : cut_at(v + 1, E, Nw)) >= ga1) break;
+            if ((by_table ? b.slice_lo[v + 1] : cut_at(v + 1, E, Nw)) >= ga1) break;
         }
         if (valid) {
             if (pb_now) pb_now[row_local] = s;
@@ -1147,7 +1202,21 @@ int hbp_stream_slices(const hbp_format_t *f, const hbp_balanced_t *b, hbp_stream
         return HBP_E_ARG;
     k_stream_slices<<<(unsigned)((n + 127) / 128), 128, 0, as_stream(stream)>>>(
         f->group_start, ngroups, f->nnz, b->workers, exact, exact ? b->hub_min : 0, b->slice_lo,
-        b->slice_g, b->pieces, b->fixed_elems);
+        b->slice_g, b->pieces, b->fixed_elems,
+        b->pieces > b->workers ? nullptr : b->cost_prefix);
+    return (int)cudaGetLastError();
+}
+
+int hbp_group_costs(const hbp_format_t *f, int64_t w_group, int64_t w_phase, int64_t w_modular,
+                    int64_t *cost, hbp_stream_t stream) {
+    if (!f || !cost || w_group < 0 || w_phase < 0 || w_modular < 0) return HBP_E_ARG;
+    if (f->warp_size != 32 || f->row_height % 32) return HBP_E_UNSUPPORTED;
+    if (!f->phases || !f->phase_ptr) return HBP_E_ARG;
+    const int64_t ngroups = f->nzb * (f->row_height / 32);
+    if (ngroups == 0) return HBP_OK;
+    k_group_costs<<<grid_for(ngroups, 256), 256, 0, as_stream(stream)>>>(
+        f->group_start, f->phase_ptr, (const uint2 *)f->phases, ngroups, w_group, w_phase,
+        w_modular, cost);
     return (int)cudaGetLastError();
 }
 

@@ -186,7 +186,7 @@ class SpmvOperator:
     def __init__(self, hbp: HbpMatrix, workers: int | None = None,
                  fixed_fraction: float | None = None, schedule: str | None = None,
                  hot: bool | int | None = None, warm_bytes: int | None = None,
-                 hub_min: int | str | None = None, ticket=None):
+                 hub_min: int | str | None = None, ticket=None, slice_cost=None):
         self.hbp = hbp
         dev = hbp.data.device
         if schedule is None:
@@ -194,6 +194,7 @@ class SpmvOperator:
         if schedule in ("balanced", "stream", "seg") and hbp.config.warp_size != 32:
             raise ValueError(f"the {schedule} schedule needs warp_size == 32")
         self.schedule = schedule
+        self.slice_cost = None
         if schedule == "stream":
             hbp.ensure_phases()
         # private descriptor: hot-column staging is a property of this operator
@@ -276,7 +277,21 @@ class SpmvOperator:
                 sl = torch.empty(npc + 1, dtype=torch.int64, device=dev)
                 sg = torch.empty(npc, dtype=torch.int64, device=dev)
                 self._scratch += [sl, sg]
+                self.slice_lo_t = sl
                 self.bal.slice_lo, self.bal.slice_g = sl.data_ptr(), sg.data_ptr()
+                self.slice_cost = self._cost_weights(f, slice_cost)
+                if self.slice_cost and self.pieces == self.workers:
+                    ng = hbp.nzb * (hbp.config.row_height // 32)
+                    cost = torch.empty(ng + 1, dtype=torch.int64, device=dev)
+                    cost[ng] = 0
+                    L.call("hbp_group_costs", ctypes.byref(f), *map(L.c_i64, self.slice_cost),
+                           L.P(cost), L.stream())
+                    cp = L.exclusive_sum(cost)
+                    if int(cp[-1].item()) // self.workers < (1 << 30):  # 32-bit slice offsets
+                        self._scratch.append(cp)
+                        self.bal.cost_prefix = cp.data_ptr()
+                    else:
+                        self.slice_cost = None
                 L.call("hbp_stream_slices", ctypes.byref(f), ctypes.byref(self.bal), L.stream())
         elif schedule == "seg":
             self.seg = self._seg_setup(hbp, f, workers)
@@ -315,6 +330,34 @@ class SpmvOperator:
             self.direct or self.fused_combine) else 0) + (1 if self.hot is not None else 0))
         self._graph = None
         self._gx = self._gy = None
+
+    # Stream schedule, fast mode: warps get equal predicted COST, not equal
+    # elements.  Per-group cost in element units = elements + 48 + 20 per phase
+    # + 40 per modular-pass phase: the per-warp model fitted to measured warp
+    # times (tools/warp_cost.py; cfg2 R^2 0.97 -- equal-element slices ran
+    # 771..1181 us per warp on R-MAT, short-row groups cost the most).
+    SLICE_COST = (48, 20, 40)
+
+    def _cost_weights(self, f, slice_cost):
+        """(w_group, w_phase, w_modular) or None (equal elements).  Default:
+        the fitted weights in fast mode; exact mode keeps equal elements."""
+        if slice_cost is None:
+            env = os.environ.get("HBP_SLICE_COST")
+            if env is not None:
+                slice_cost = env
+            elif f.exact:
+                return None
+            else:
+                return self.SLICE_COST
+        if isinstance(slice_cost, str):
+            slice_cost = None if slice_cost.strip() in ("", "0", "off") else \
+                tuple(int(v) for v in slice_cost.split(","))
+        if not slice_cost:
+            return None
+        w = tuple(int(v) for v in slice_cost)
+        if len(w) != 3 or min(w) < 0:
+            raise ValueError("slice_cost needs three non-negative weights")
+        return w
 
     def _seg_setup(self, hbp: HbpMatrix, f, workers) -> "L.SegT":
         """Column windows of the nonzero blocks (hbp_seg_windows, cached on

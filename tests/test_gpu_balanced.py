@@ -127,10 +127,10 @@ def test_stream_precomputed_slices(dtype, workers):
     hbp = _hbp(rows, cols, r, c, v.astype(dtype), C=cols)
     x = torch.as_tensor(np.random.default_rng(2).uniform(-1, 1, cols).astype(dtype),
                         device="cuda")
-    op = H.SpmvOperator(hbp, workers=workers, hot=False, schedule="stream")
+    op = H.SpmvOperator(hbp, workers=workers, hot=False, schedule="stream", slice_cost="0")
     assert op.bal.slice_lo and op.bal.slice_g
     y1 = op(x).cpu().numpy()
-    lo = op._scratch[-2].cpu().numpy()
+    lo = op.slice_lo_t.cpu().numpy()
     assert lo[0] == 0 and lo[-1] == hbp.nnz and np.all(np.diff(lo) >= 0)
     op.bal.slice_lo = op.bal.slice_g = 0
     y2 = op(x).cpu().numpy()
@@ -197,3 +197,92 @@ def test_stream_direct_single_row_blocks(dtype, C, monkeypatch):
     routed = H.SpmvOperator(hbp, hot=False, schedule="stream")
     assert not routed._fmt.reserved & 4
     np.testing.assert_array_equal(direct(x).cpu().numpy(), routed(x).cpu().numpy())
+
+
+TICKETS = ["0.7:2", "0.0:3", "1.0:1", "0.5:7"]
+
+
+@pytest.mark.parametrize("name", [n for n in W32 if not n.startswith("kat")][:12])
+@pytest.mark.parametrize("ticket", TICKETS)
+@pytest.mark.parametrize("workers", [1, 5, None])
+def test_stream_ticket_matches_golden(name, ticket, workers):
+    """Competitive pieces (fixed element chunk per warp + atomic ticket): f64
+    bitwise the reference, f32 within 1e-5; the ticket self-resets, so
+    repeated calls give the same y."""
+    g = load_golden(name)
+    val = g["trip_val"].astype(np.float32) if g["fp32"] else g["trip_val"]
+    hbp = _hbp(g["rows"], g["cols"], g["trip_row"], g["trip_col"], val, g["C"], g["R"], g["W"],
+               g["seed"])
+    x = torch.as_tensor(g["x"].astype(np.float32) if g["fp32"] else g["x"], device="cuda")
+    op = H.SpmvOperator(hbp, workers=workers, schedule="stream", ticket=ticket)
+    y = op(x).cpu().numpy()
+    np.testing.assert_array_equal(op(x).cpu().numpy(), y)
+    if g["fp32"]:
+        err = O.componentwise_error(g["rows"], g["trip_row"], g["trip_col"], g["trip_val"],
+                                    g["x"], y.astype(np.float64))
+        assert err <= 1e-5
+    else:
+        np.testing.assert_array_equal(y, g["y"])
+
+
+@pytest.mark.parametrize("ticket", TICKETS)
+@pytest.mark.parametrize("workers", [2, 64, None])
+def test_stream_ticket_f32_hot_rows(ticket, workers):
+    rows, cols, r, c, v = _hot_matrix()
+    v32 = v.astype(np.float32)
+    x = np.random.default_rng(1).uniform(-1, 1, cols).astype(np.float32)
+    hbp = _hbp(rows, cols, r, c, v32, C=cols)
+    op = H.SpmvOperator(hbp, workers=workers, schedule="stream", ticket=ticket)
+    xd = torch.as_tensor(x, device="cuda")
+    y1 = op(xd).cpu().numpy()
+    for _ in range(3):
+        np.testing.assert_array_equal(op(xd).cpu().numpy(), y1)
+    err = O.componentwise_error(rows, r, c, v32.astype(np.float64), x.astype(np.float64),
+                                y1.astype(np.float64))
+    assert err <= 1e-5
+    clk = op.warp_clock()
+    op(xd)
+    t = clk.cpu().numpy()
+    assert (t[:, 1] >= t[:, 0]).all() and (t[:, 0] > 0).all()
+
+
+def test_stream_ticket_rejects_bad_fraction():
+    rows, cols, r, c, v = _hot_matrix()
+    hbp = _hbp(rows, cols, r, c, v.astype(np.float32), C=cols)
+    with pytest.raises(ValueError, match="fixed fraction"):
+        H.SpmvOperator(hbp, schedule="stream", ticket="1.5:2")
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("workers", [1, 7, 333, None])
+@pytest.mark.parametrize("cost", ["48,20,40", "0,0,0", "500,100,0", "1,300,900"])
+def test_stream_cost_balanced_slices(dtype, workers, cost):
+    """Cost-balanced slice cuts (hbp_group_costs + prefix): valid monotone
+    bounds, f64 bitwise the reference (exact mode), f32 within 1e-5 and
+    deterministic; the cut positions move with the weights."""
+    rows, cols, r, c, v = _hot_matrix(seed=5)
+    vv = v.astype(dtype)
+    hbp = _hbp(rows, cols, r, c, vv, C=cols)
+    xh = np.random.default_rng(2).uniform(-1, 1, cols).astype(dtype)
+    x = torch.as_tensor(xh, device="cuda")
+    op = H.SpmvOperator(hbp, workers=workers, schedule="stream", slice_cost=cost)
+    lo = op.slice_lo_t.cpu().numpy()
+    assert lo[0] == 0 and lo[-1] == hbp.nnz and np.all(np.diff(lo) >= 0)
+    y1 = op(x).cpu().numpy()
+    np.testing.assert_array_equal(op(x).cpu().numpy(), y1)
+    err = O.componentwise_error(rows, r, c, vv.astype(np.float64), xh.astype(np.float64),
+                                y1.astype(np.float64))
+    assert err <= (1e-12 if dtype == np.float64 else 1e-5)
+    if dtype == np.float64:  # exact mode: bitwise the equal-element schedule
+        ref = H.SpmvOperator(hbp, workers=workers, schedule="stream", slice_cost="0")
+        np.testing.assert_array_equal(ref(x).cpu().numpy(), y1)
+
+
+def test_stream_cost_weights_default_and_validation():
+    rows, cols, r, c, v = _hot_matrix(seed=5)
+    h32 = _hbp(rows, cols, r, c, v.astype(np.float32), C=cols)
+    h64 = _hbp(rows, cols, r, c, v, C=cols)
+    assert H.SpmvOperator(h32, schedule="stream").slice_cost == H.SpmvOperator.SLICE_COST
+    assert H.SpmvOperator(h64, schedule="stream").slice_cost is None  # exact: equal elements
+    with pytest.raises(ValueError, match="weights"):
+        H.SpmvOperator(h32, schedule="stream", slice_cost="1,2")

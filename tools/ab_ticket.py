@@ -5,7 +5,9 @@ ticket -- engine.py:137-176 applied to element slices) vs more, hardware-
 scheduled warps.  Also prints the per-warp end-time spread of each run
 (%globaltimer, SpmvOperator.warp_clock) -- the most a dynamic schedule can win.
 
-    python tools/ab_ticket.py --config cfg2 --runs static,0.7:2,0.5:4,w2
+    python tools/ab_ticket.py --config cfg2 --runs eq,static,c=48,20,40,0.7:2,w2
+
+(runs are separated by "/" when a cost spec holds commas: --runs "eq/c=48,20,40")
 """
 import argparse
 import os
@@ -34,11 +36,15 @@ grid = H.make_grid(csr, cfg)
 hbp = H.build_hbp(csr, grid, H.hash_permutations(grid, H.sample_hash_params(grid, cfg)),
                   with_add_sign=False, with_zero_row=False)
 del csr, grid, col, val
-runs = a.runs.split(",")
+runs = a.runs.split("/") if "/" in a.runs else a.runs.split(",")
 ops = {}
 for r in runs:
-    if r == "static":
+    if r == "static":  # the default (cost-balanced slices in fast mode)
         ops[r] = H.SpmvOperator(hbp, schedule="stream")
+    elif r == "eq":  # equal-element slices
+        ops[r] = H.SpmvOperator(hbp, schedule="stream", slice_cost="0")
+    elif r.startswith("c="):  # cost weights w_group,w_phase,w_modular
+        ops[r] = H.SpmvOperator(hbp, schedule="stream", slice_cost=r[2:])
     elif r.startswith("w"):  # k x the resident warps, scheduled by the hardware
         base = H.SpmvOperator(hbp, schedule="stream").workers
         ops[r] = H.SpmvOperator(hbp, schedule="stream", workers=int(float(r[1:]) * base))
