@@ -720,7 +720,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-baselines", action="store_true",
                     help="skip the CSR / 2D / cuSPARSE comparison timings")
-    ap.add_argument("--schedule", default=None, choices=[None, "stream", "balanced", "plan", "rowblock", "seg"])
+    ap.add_argument("--schedule", default=None, choices=[None, "stream", "balanced", "plan", "rowblock", "rowstage", "seg"])
     ap.add_argument("--workers", type=int, default=None,
                     help="persistent warps of the SpMV (default: one per resident warp slot)")
     ap.add_argument("--no-overlap", action="store_true",

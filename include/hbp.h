@@ -436,6 +436,20 @@ int hbp_spmv_seg(const hbp_format_t *f, const hbp_seg_t *s, const void *x, void 
 /* A/B tuning selector of the launch shape (HBP_SEG_VARIANT); 0 = default. */
 int hbp_seg_set_variant(int v);
 
+/* Row-block owner with TMA-staged elements (hbp_spmv_rowstage.cu; W = 32):
+ * a persistent CTA per row block bulk-copies the col/data
+ * ranges of all the row block's nonzero blocks into shared memory with one
+ * mbarrier, walks them there (x gathered from global memory) and folds the
+ * block partials in ascending bc -- y bitwise that of hbp_spmv_blocks +
+ * hbp_combine.  hbp_rowstage_plan fills the per-block staging descriptors
+ * desc (i64[2*nzb], rb_blk order) and caps (device u64[2]: largest staged
+ * span of a row block, most nonzero blocks in a row block); pass them as
+ * ecap / kmax (kmax <= 32; shared memory ecap * (4 + sizeof V) +
+ * kmax * R * 8 bytes must fit one CTA). */
+int hbp_rowstage_plan(const hbp_format_t *f, int64_t *desc, unsigned long long *caps,
+                      hbp_stream_t stream);
+int hbp_spmv_rowstage(const hbp_format_t *f, const int64_t *desc, const void *x, void *y,
+                      int64_t ecap, int64_t kmax, hbp_stream_t stream);
 /* engine.py:196-201 combine over nonzero blocks only, ascending bc
  * (bitwise equal to the dense combine); rows of row blocks with
  * no nonzero block get +0.0. */

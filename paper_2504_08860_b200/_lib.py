@@ -95,6 +95,8 @@ _SIGS = {
     "hbp_sort_perm": [c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp],
     "hbp_merge_comparisons": [c_vp, c_i64, c_vp, c_vp],
     "hbp_group_costs": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp],
+    "hbp_rowstage_plan": [c_vp, c_vp, c_vp, c_vp],
+    "hbp_spmv_rowstage": [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp],
     "hbp_gather_dense_perm": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp],
     "hbp_slot_lengths": [c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp,
                          c_vp],

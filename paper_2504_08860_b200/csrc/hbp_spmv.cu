@@ -294,6 +294,31 @@ __global__ void k_combine(const hbp_format_t f, const double *__restrict__ parti
     }
 }
 
+// Row-block-parallel combine for matrices with many nonzero blocks per row
+// block (few row blocks, many column blocks): the scan above gives each warp
+// 32 row blocks in series, so with nrb = 512 only 64 warps would run.  Here
+// one warp task = (row block, 32-row segment), a lane per row, summed in
+// ascending bc by combine_row (bitwise the same).
+template <typename V>
+__global__ void k_combine_rows(const hbp_format_t f, const double *__restrict__ partial,
+                               V *__restrict__ y, int64_t nrb) {
+    const int64_t R = f.row_height;
+    const bool skip_single = (f.reserved & HBP_FLAG_DIRECT_SINGLE) != 0;
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nseg = (R + 31) / 32;
+    for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < nrb * nseg;
+         t += nwarps) {
+        const int64_t rb = t / nseg, seg = t - rb * nseg;
+        const int64_t lo = f.rb_ptr[rb], hi = f.rb_ptr[rb + 1];
+        if (skip_single && hi - lo == 1) continue;
+        int64_t n = f.rows - rb * R;
+        if (n > R) n = R;
+        const int64_t local = seg * 32 + lane;
+        if (local < n) y[rb * R + local] = (V)combine_row<V>(f, partial, lo, hi, R, local);
+    }
+}
+
 template <typename V>
 __global__ void k_zero_empty(const hbp_format_t f, V *__restrict__ y, int64_t nrb) {
     // same warp scan as k_combine: one rb_ptr load + ballot per 32 row blocks
@@ -499,6 +524,17 @@ int hbp_combine(const hbp_format_t *f, const double *partial, void *y, hbp_strea
     const int64_t warps = (nrb + 31) / 32 * ((f->row_height + 127) / 128),
                   cap = (int64_t)sms * 8 * 8;
     const int threads = 256;
+    if (f->nzb >= 4 * nrb) {  // many blocks per row block: a task per (row block, 32 rows)
+        const int64_t tasks = nrb * ((f->row_height + 31) / 32);
+        const unsigned g2 = (unsigned)(((tasks < cap ? tasks : cap) + 7) / 8);
+        if (f->dtype == HBP_F64)
+            k_combine_rows<double><<<g2, threads, 0, st>>>(*f, partial, (double *)y, nrb);
+        else if (f->dtype == HBP_F32)
+            k_combine_rows<float><<<g2, threads, 0, st>>>(*f, partial, (float *)y, nrb);
+        else return HBP_E_ARG;
+        HBP_LAUNCH_CHECK();
+        return HBP_OK;
+    }
     const unsigned grid = (unsigned)(((warps < cap ? warps : cap) + 7) / 8);
     if (f->dtype == HBP_F64)
         k_combine<double><<<grid, threads, 0, st>>>(*f, partial, (double *)y, nrb);

@@ -1,0 +1,288 @@
+// hbp_spmv_rowstage.cu -- row-block-owner HBP SpMV with TMA-staged elements
+// (W = 32; small matrices with several column blocks, e.g. cfg1).
+//
+// Same work split and arithmetic as hbp_spmv_rowblock (one CTA per row
+// block computes the partials of the row block's nonzero blocks, then folds
+// them in ascending bc exactly as combine does, engine.py:196-201), but the
+// dependent global-load chain of each (block, group) task is cut:
+//
+//   1. a per-operator descriptor table (hbp_rowstage_plan) holds every
+//      nonzero block's 16-byte-aligned element span and its offset in the
+//      row block's staging buffer, so thread j of the CTA bulk-copies
+//      (cp.async.bulk) block j's col/data straight away -- one DRAM round
+//      trip for the whole row block, issued in parallel, no registers held;
+//   2. the CTA is persistent; several CTAs per SM overlap one row block's
+//      copies with another's walk (a double-buffered form, row block i+1's
+//      copies in flight while row block i is walked, measured no faster);
+//   3. every lane loads its tasks' slot length, output row and group start
+//      one task ahead (coalesced, independent);
+//   4. the walk reads col/data from shared memory (positions from per-step
+//      ballots of the slot lengths, the closed form of build_hbp's layout);
+//      only the x gathers go to global memory, four steps in flight.
+//
+// Per-slot sums are group_dot's (hbp_spmv.cu): f64 products __dmul_rn, then
+// __dadd_rn in step order -- bitwise the reference; f32 products exact in f64,
+// f64 sums.  So y is bitwise that of hbp_spmv_blocks + hbp_combine.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include "hbp.h"
+#include "hbp_common.cuh"
+
+using namespace hbp;
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int kMaxBlocks = 32;  // nonzero blocks per row block (staging table)
+
+template <typename V, bool EXACT>
+__device__ __forceinline__ double fmadd_rs(double acc, V v, V xv) {
+    if (EXACT) return __dadd_rn(acc, __dmul_rn((double)v, (double)xv));
+    return fma((double)v, (double)xv, acc);
+}
+
+__device__ __forceinline__ void mbar_expect_only(uint64_t *m, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(m)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive1(uint64_t *m) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(m)) : "memory");
+}
+
+__host__ __device__ constexpr int64_t staged_span(int64_t e0, int64_t e1) {
+    return ((e1 - (e0 & ~(int64_t)3)) + 3) & ~(int64_t)3;  // 16-byte granules of u32 / V
+}
+
+// Descriptor of the block at row-block position i (rb_blk order):
+// desc[2i] = a0 (first staged element, e0 rounded down to a multiple of 4),
+// desc[2i+1] = m (staged elements, a multiple of 4) << 32 | offset of a0 in
+// the row block's staging buffer.  caps[0] = largest buffer, caps[1] = most
+// blocks in a row block.
+__global__ void k_rowstage_plan(const hbp_format_t f, int64_t *__restrict__ desc,
+                                unsigned long long *__restrict__ caps) {
+    const int64_t R = f.row_height, gpb = R / 32, nrb = (f.rows + R - 1) / R;
+    for (int64_t br = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; br < nrb;
+         br += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t lo = f.rb_ptr[br], hi = f.rb_ptr[br + 1];
+        int64_t off = 0;
+        for (int64_t i = lo; i < hi; ++i) {
+            const int64_t b = f.rb_blk[i];
+            const int64_t e0 = f.group_start[b * gpb], e1 = f.group_start[(b + 1) * gpb];
+            const int64_t m = staged_span(e0, e1);
+            desc[2 * i] = e0 & ~(int64_t)3;
+            desc[2 * i + 1] = (m << 32) | off;
+            off += m;
+        }
+        atomicMax(caps, (unsigned long long)off);
+        atomicMax(caps + 1, (unsigned long long)(hi - lo));
+    }
+}
+
+template <typename V, bool EXACT, int NT, bool DB>
+__global__ void __launch_bounds__(NT)
+    k_spmv_rowstage(const hbp_format_t f, const int64_t *__restrict__ desc,
+                    const V *__restrict__ x, V *__restrict__ y, int32_t ecap) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    __shared__ __align__(8) uint64_t mbar[2];
+    __shared__ int64_t s_base[2][kMaxBlocks];  // staged index of element 0 of block j
+    const int64_t buf_bytes = (int64_t)ecap * (4 + sizeof(V));
+    double *part = reinterpret_cast<double *>(sm + (DB ? 2 : 1) * buf_bytes);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    constexpr int nwarps = NT / 32;
+    const unsigned lt = (1u << lane) - 1u;
+    const int32_t R = (int32_t)f.row_height, gpb = R / 32;
+    const int64_t nrb = (f.rows + R - 1) / R;
+    const V *__restrict__ data = (const V *)f.data;
+    const uint64_t pe = policy_evict_first(), pl = policy_evict_last();
+    if (threadIdx.x == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    // thread j < cnt stages block j of row block br into buffer `buf`; the
+    // caller syncs, then thread 0 arrives once every expect_tx is posted
+    auto stage = [&](int64_t br, int buf) {
+        const int64_t lo = f.rb_ptr[br], hi = f.rb_ptr[br + 1];
+        const int32_t cnt = (int32_t)(hi - lo);
+        uint32_t *col_s = reinterpret_cast<uint32_t *>(sm + buf * buf_bytes);
+        V *dat_s = reinterpret_cast<V *>(sm + buf * buf_bytes + (int64_t)ecap * 4);
+        if ((int)threadIdx.x < cnt) {
+            const int64_t a0 = desc[2 * (lo + threadIdx.x)];
+            const int64_t mo = desc[2 * (lo + threadIdx.x) + 1];
+            const int32_t m = (int32_t)(mo >> 32), off = (int32_t)(mo & 0xffffffff);
+            s_base[buf][threadIdx.x] = (int64_t)off - a0;
+            if (m > 0) {
+                fence_proxy_async();  // the CTA's generic reads of this buffer (barrier-ordered) first
+                mbar_expect_only(&mbar[buf], (uint32_t)m * (4u + (uint32_t)sizeof(V)));
+                bulk_g2s(col_s + off, f.col + a0, (uint32_t)m * 4u, &mbar[buf], pe);
+                bulk_g2s(dat_s + off, data + a0, (uint32_t)m * (uint32_t)sizeof(V), &mbar[buf], pe);
+            }
+        }
+    };
+
+    uint32_t phase0 = 0u, phase1 = 0u;
+    // DB: double-buffered (row block i+1's copies in flight while row block i
+    // is walked; half the staging capacity per CTA) -- measured no faster on
+    // cfg1 than more single-buffered CTAs per SM, so off by default
+    int buf = 0;
+    if (DB && blockIdx.x < nrb) {
+        stage(blockIdx.x, 0);
+        __syncthreads();
+        if (threadIdx.x == 0) mbar_arrive1(&mbar[0]);
+    }
+    for (int64_t br = blockIdx.x; br < nrb; br += gridDim.x, buf ^= (DB ? 1 : 0)) {
+        const int64_t lo = f.rb_ptr[br], hi = f.rb_ptr[br + 1];
+        const int64_t n64 = f.rows - br * R;
+        const int32_t n = (int32_t)(n64 > R ? R : n64);
+        const int32_t cnt = (int32_t)(hi - lo);
+        const int64_t nx = DB ? br + gridDim.x : br;
+        if (nx < nrb) {
+            stage(nx, DB ? buf ^ 1 : buf);
+            __syncthreads();
+            if (threadIdx.x == 0) mbar_arrive1(&mbar[DB ? buf ^ 1 : buf]);
+        }
+        V *yb = y + br * R;
+        const uint32_t *col_s = reinterpret_cast<const uint32_t *>(sm + buf * buf_bytes);
+        const V *dat_s = reinterpret_cast<const V *>(sm + buf * buf_bytes + (int64_t)ecap * 4);
+        const int32_t ng = (n + 31) >> 5;
+        const int32_t ntask = cnt * ng;
+        uint32_t len_n = 0u, row_n = 0u;
+        int32_t base_n = 0, j_n = 0;
+        auto load = [&](int32_t t) {
+            const int32_t j = t / ng, g = t - j * ng;
+            const int64_t b = f.rb_blk[lo + j];
+            const int32_t slot = g * 32 + lane;
+            len_n = slot < n ? __ldcs(f.slot_len + b * R + slot) : 0u;
+            row_n = slot < n ? __ldcs(f.perm + b * R + slot) : 0u;
+            base_n = (int32_t)(f.group_start[b * gpb + g] + s_base[buf][j]);
+            j_n = j;
+        };
+        if (wid < ntask) load(wid);
+        if (buf == 0) {
+            mbar_wait(&mbar[0], phase0);
+            phase0 ^= 1u;
+        } else {
+            mbar_wait(&mbar[1], phase1);
+            phase1 ^= 1u;
+        }
+        for (int32_t t = wid; t < ntask; t += nwarps) {
+            const uint32_t len = len_n, row = row_n;
+            int32_t base = base_n;
+            const int32_t j = j_n;
+            const bool valid = (t - j * ng) * 32 + lane < n;
+            if (t + nwarps < ntask) load(t + nwarps);
+            double acc = 0.0;
+            uint32_t t0 = 0;
+            bool live = len > 0;
+            unsigned mask = __ballot_sync(FULL, live);
+            while (mask) {
+                const int k = __popc(mask);
+                const uint32_t t1 = __reduce_min_sync(FULL, live ? len : 0xffffffffu);
+                if (live) {
+                    int32_t p = base + __popc(mask & lt);
+                    const uint32_t M = t1 - t0;
+                    uint32_t s = 0;
+                    for (; s + 4 <= M; s += 4) {
+                        const uint32_t c0 = col_s[p], c1 = col_s[p + k], c2 = col_s[p + 2 * k],
+                                       c3 = col_s[p + 3 * k];
+                        const V x0 = ld_x(x + c0, pl), x1 = ld_x(x + c1, pl), x2 = ld_x(x + c2, pl),
+                                x3 = ld_x(x + c3, pl);
+                        acc = fmadd_rs<V, EXACT>(acc, dat_s[p], x0);
+                        acc = fmadd_rs<V, EXACT>(acc, dat_s[p + k], x1);
+                        acc = fmadd_rs<V, EXACT>(acc, dat_s[p + 2 * k], x2);
+                        acc = fmadd_rs<V, EXACT>(acc, dat_s[p + 3 * k], x3);
+                        p += 4 * k;
+                    }
+                    if (s + 2 <= M) {
+                        const uint32_t c0 = col_s[p], c1 = col_s[p + k];
+                        const V x0 = ld_x(x + c0, pl), x1 = ld_x(x + c1, pl);
+                        acc = fmadd_rs<V, EXACT>(acc, dat_s[p], x0);
+                        acc = fmadd_rs<V, EXACT>(acc, dat_s[p + k], x1);
+                        p += 2 * k;
+                        s += 2;
+                    }
+                    if (s < M) acc = fmadd_rs<V, EXACT>(acc, dat_s[p], ld_x(x + col_s[p], pl));
+                }
+                base += (int32_t)(t1 - t0) * k;
+                t0 = t1;
+                live = len > t0;
+                mask = __ballot_sync(FULL, live);
+            }
+            if (valid) part[(int64_t)j * R + row] = acc;
+        }
+        __syncthreads();
+        // fold in ascending bc: s = p_first; s += p_next ... (combine's order);
+        // a row block without nonzero blocks gets +0.0
+        for (int32_t r = threadIdx.x; r < n; r += NT) {
+            double v = cnt ? part[r] : 0.0;
+            for (int32_t j = 1; j < cnt; ++j) v = __dadd_rn(v, part[(int64_t)j * R + r]);
+            __stcs(yb + r, (V)v);
+        }
+        __syncthreads();
+    }
+}
+
+template <typename V, bool EXACT, int NT, bool DB = false>
+int launch_rowstage(const hbp_format_t *f, const int64_t *desc, const void *x, void *y,
+                    int32_t ecap, int32_t kmax, cudaStream_t st) {
+    const size_t smem =
+        (DB ? 2 : 1) * (size_t)ecap * (4 + sizeof(V)) + (size_t)kmax * f->row_height * 8;
+    auto kern = k_spmv_rowstage<V, EXACT, NT, DB>;
+    HBP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int dev = 0, sms = 0, per_sm = 0;
+    HBP_CUDA_TRY(cudaGetDevice(&dev));
+    HBP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    HBP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
+    if (per_sm < 1) return HBP_E_UNSUPPORTED;
+    const int64_t nrb = (f->rows + f->row_height - 1) / f->row_height;
+    const int64_t want = (int64_t)sms * per_sm;
+    const unsigned grid = (unsigned)(nrb < want ? nrb : want);
+    kern<<<grid, NT, smem, st>>>(*f, desc, (const V *)x, (V *)y, ecap);
+    return (int)cudaGetLastError();
+}
+
+}  // namespace
+
+extern "C" {
+
+int hbp_rowstage_plan(const hbp_format_t *f, int64_t *desc, unsigned long long *caps,
+                      hbp_stream_t stream) {
+    if (!f || !caps || !f->rb_ptr || (f->nzb > 0 && (!f->rb_blk || !desc))) return HBP_E_ARG;
+    if (f->warp_size != 32 || f->row_height % 32) return HBP_E_UNSUPPORTED;
+    cudaStream_t st = as_stream(stream);
+    HBP_CUDA_TRY(cudaMemsetAsync(caps, 0, 2 * sizeof(unsigned long long), st));
+    const int64_t nrb = (f->rows + f->row_height - 1) / f->row_height;
+    if (nrb == 0 || f->nzb == 0) return HBP_OK;
+    k_rowstage_plan<<<grid_for(nrb, 256), 256, 0, st>>>(*f, desc, caps);
+    return (int)cudaGetLastError();
+}
+
+int hbp_spmv_rowstage(const hbp_format_t *f, const int64_t *desc, const void *x, void *y,
+                      int64_t ecap, int64_t kmax, hbp_stream_t stream) {
+    if (!f || f->rows < 0 || (f->rows > 0 && !y)) return HBP_E_ARG;
+    if (f->warp_size != 32 || f->row_height % 32) return HBP_E_UNSUPPORTED;
+    if (f->rows == 0) return HBP_OK;
+    if (!f->rb_ptr || (f->nzb > 0 && (!x || !f->rb_blk || !desc))) return HBP_E_ARG;
+    if (ecap < 4 || kmax < 1 || (ecap & 3)) return HBP_E_ARG;
+    if (kmax > kMaxBlocks || ecap > (1 << 24)) return HBP_E_UNSUPPORTED;
+    cudaStream_t st = as_stream(stream);
+    // tuning A/B only: threads per CTA (512 default)
+    static const int nt =
+        getenv("HBP_ROWSTAGE_THREADS") ? atoi(getenv("HBP_ROWSTAGE_THREADS")) : 512;
+    const int32_t e = (int32_t)ecap, k = (int32_t)kmax;
+    if (f->dtype == HBP_F64)
+        return nt == 256   ? launch_rowstage<double, true, 256>(f, desc, x, y, e, k, st)
+               : nt == 2   ? launch_rowstage<double, true, 512, true>(f, desc, x, y, e, k, st)
+                           : launch_rowstage<double, true, 512>(f, desc, x, y, e, k, st);
+    if (f->dtype == HBP_F32)
+        return nt == 256 ? launch_rowstage<float, false, 256>(f, desc, x, y, e, k, st)
+                         : launch_rowstage<float, false, 512>(f, desc, x, y, e, k, st);
+    return HBP_E_ARG;
+}
+
+}  // extern "C"

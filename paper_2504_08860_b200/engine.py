@@ -306,7 +306,13 @@ class SpmvOperator:
             self.seg.ticket = self.ticket.data_ptr()
         self.direct = hbp.num_col_blocks == 1
         R = hbp.config.row_height
-        self.partial = None if self.direct or schedule == "rowblock" else torch.empty(hbp.nzb * R, dtype=torch.float64,
+        if schedule == "rowstage":
+            self.rowstage_caps = self._rowstage_caps(hbp, f)
+            if self.rowstage_caps is None:
+                raise ValueError("the rowstage schedule needs warp_size == 32 and a row block "
+                                 "whose staged elements fit one CTA's shared memory")
+            self._rowstage_desc = hbp._ops["rowstage_desc"]
+        self.partial = None if self.direct or schedule in ("rowblock", "rowstage") else torch.empty(hbp.nzb * R, dtype=torch.float64,
                                                             device=dev)
         self.has_empty_row_blocks = bool((hbp.rb_ptr[1:] == hbp.rb_ptr[:-1]).any())
         # stream schedule with several column blocks: optionally fuse the combine
@@ -326,7 +332,7 @@ class SpmvOperator:
         self.sched.workers = self.workers
         self.sched.fixed_count = self.fixed_count
         self.sched.ticket = self.ticket.data_ptr()
-        self.launches_per_call = 1 if schedule == "rowblock" else (1 + (1 if self.has_empty_row_blocks or not (
+        self.launches_per_call = 1 if schedule in ("rowblock", "rowstage") else (1 + (1 if self.has_empty_row_blocks or not (
             self.direct or self.fused_combine) else 0) + (1 if self.hot is not None else 0))
         self._graph = None
         self._gx = self._gy = None
@@ -359,6 +365,29 @@ class SpmvOperator:
             raise ValueError("slice_cost needs three non-negative weights")
         return w
 
+    ROWSTAGE_SMEM = 200 * 1024  # one CTA's staged elements + partials at most
+
+    @classmethod
+    def _rowstage_caps(cls, hbp: HbpMatrix, f):
+        """(ecap, kmax) of the TMA-staged row-block schedule (hbp_rowstage_caps),
+        cached on the matrix; None when W != 32 or a row block's staged
+        elements and partials exceed ROWSTAGE_SMEM."""
+        if hbp.config.warp_size != 32:
+            return None
+        if "rowstage_caps" not in hbp._ops:
+            dev = hbp.data.device
+            caps = torch.zeros(2, dtype=torch.int64, device=dev)
+            desc = torch.zeros(max(1, 2 * hbp.nzb), dtype=torch.int64, device=dev)
+            L.call("hbp_rowstage_plan", ctypes.byref(f), L.P(desc), L.P(caps), L.stream())
+            ecap, kmax = (int(v) for v in caps.cpu())
+            hbp._ops["rowstage_caps"] = (max(4, ecap), max(1, kmax))
+            hbp._ops["rowstage_desc"] = desc
+        ecap, kmax = hbp._ops["rowstage_caps"]
+        need = ecap * (4 + hbp.data.element_size()) + kmax * hbp.config.row_height * 8
+        if kmax > 32 or need > cls.ROWSTAGE_SMEM:
+            return None
+        return ecap, kmax
+
     def _seg_setup(self, hbp: HbpMatrix, f, workers) -> "L.SegT":
         """Column windows of the nonzero blocks (hbp_seg_windows, cached on
         the matrix) and the CTA count of the column-segment schedule."""
@@ -388,7 +417,8 @@ class SpmvOperator:
         rowblock for small, evenly
         spread matrices with several column blocks and few nonzero blocks
         per row block (one launch instead of SpMV + combine; cfg1: 38.7 vs
-        61 us) unless hot staging was asked about (a stream-schedule
+        61 us) -- rowstage (its TMA-staged form) for f64 when a row block's
+        elements fit one CTA (cfg1 28.7 us) -- unless hot staging was asked about (a stream-schedule
         feature).  With many small blocks per row block (uniform columns,
         C << cols) the stream schedule wins: 0.19 vs 0.30 ms at 4M nnz,
         64 blocks per row block (tools/prof_sched.py)."""
@@ -402,6 +432,12 @@ class SpmvOperator:
             rb = torch.zeros(hbp.num_row_blocks, dtype=torch.int64, device=gs.device)
             rb.index_add_(0, hbp.blk_br.long(), blk_nnz)
             if float(rb.max()) <= cls.ROWBLOCK_MAX_SKEW * hbp.nnz / hbp.num_row_blocks:
+                # f64 with W = 32: the TMA-staged form when a row block's
+                # elements fit a CTA (cfg1 28.7 vs 36.9 us); f32 banded
+                # matrices keep rowblock (0.101 vs 0.109 ms at 35M nnz)
+                if (hbp.dtype == torch.float64 and
+                        cls._rowstage_caps(hbp, L.FormatT.from_buffer_copy(hbp.format_struct()))):
+                    return "rowstage"
                 return "rowblock"
         if (hbp.config.warp_size == 32 and hbp.num_col_blocks > 1 and hbp.nzb
                 and hbp.nnz >= cls.SEG_MIN_BLOCK_NNZ * hbp.nzb
@@ -441,6 +477,11 @@ class SpmvOperator:
             self.bal.y_sumsq = None
         if self.schedule == "rowblock":
             L.call("hbp_spmv_rowblock", ctypes.byref(f), L.P(x), L.P(y), s)
+            return y
+        if self.schedule == "rowstage":
+            ecap, kmax = self.rowstage_caps
+            L.call("hbp_spmv_rowstage", ctypes.byref(f), L.P(self._rowstage_desc), L.P(x),
+                   L.P(y), L.c_i64(ecap), L.c_i64(kmax), s)
             return y
         if self.direct:
             self._blocks(f, x, None, y, s)

@@ -77,8 +77,8 @@ def _full_pipeline_bitwise(rows, cols, rp, ci, v, C, schedules):
 def test_cfg1_full_size_bitwise():
     rows, cols, rp, ci, v = BI.laplacian_csr(1024)
     assert rp[-1] == 5_238_784
-    got = _full_pipeline_bitwise(rows, cols, rp, ci, v, 4096, (None, "stream", "plan"))
-    assert got[None] == "rowblock"  # the auto schedule cfg1 is benchmarked with
+    got = _full_pipeline_bitwise(rows, cols, rp, ci, v, 4096, (None, "rowblock", "stream", "plan"))
+    assert got[None] == "rowstage"  # the auto schedule cfg1 is benchmarked with
     _free()
 
 

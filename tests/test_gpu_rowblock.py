@@ -104,7 +104,9 @@ def test_auto_schedule():
     v = np.ones(r.size)
     hbp = _hbp(n, n, r, c, v, C=512)
     op = H.SpmvOperator(hbp)
-    assert op.schedule == "rowblock" and op.launches_per_call == 1
+    assert op.schedule == "rowstage" and op.launches_per_call == 1  # f64, fits a CTA
+    h32 = _hbp(n, n, r, c, v.astype(np.float32), C=512)
+    assert H.SpmvOperator(h32).schedule == "rowblock"
     assert H.SpmvOperator(hbp, hot=False).schedule == "stream"
     assert H.SpmvOperator(_hbp(n, n, r, c, v, C=n)).schedule == "stream"
     # one dense row block among sparse ones
@@ -113,7 +115,7 @@ def test_auto_schedule():
     key = np.unique(rr * n + cc)
     skew = _hbp(n, n, key // n, key % n, np.ones(key.size), C=512, R=64)
     assert H.SpmvOperator(skew).schedule == "stream"
-    assert H.SpmvOperator(_hbp(n, n, r, c, v, C=512, R=64)).schedule == "rowblock"
+    assert H.SpmvOperator(_hbp(n, n, r, c, v, C=512, R=64)).schedule == "rowstage"
     # uniform columns over many column blocks: many small blocks per row block
     rng = np.random.default_rng(4)
     ru = np.repeat(np.arange(n), 16)
@@ -124,3 +126,77 @@ def test_auto_schedule():
     x = torch.as_tensor(np.random.default_rng(0).uniform(-1, 1, n), device="cuda")
     np.testing.assert_array_equal(op(x).cpu().numpy(),
                                   H.SpmvOperator(hbp, schedule="plan")(x).cpu().numpy())
+
+
+# ---- TMA-staged row-block owner (hbp_spmv_rowstage, W = 32)
+
+@pytest.mark.parametrize("name", [n for n in golden_names() if load_golden(n)["W"] == 32])
+def test_rowstage_matches_golden(name):
+    g = load_golden(name)
+    val = g["trip_val"].astype(np.float32) if g["fp32"] else g["trip_val"]
+    hbp = _hbp(g["rows"], g["cols"], g["trip_row"], g["trip_col"], val, g["C"], g["R"], g["W"],
+               g["seed"])
+    x = g["x"].astype(np.float32) if g["fp32"] else g["x"]
+    op = H.SpmvOperator(hbp, schedule="rowstage")
+    assert op.launches_per_call == 1
+    y = op(torch.as_tensor(x, device="cuda")).cpu().numpy()
+    if g["fp32"]:
+        err = O.componentwise_error(g["rows"], g["trip_row"], g["trip_col"], g["trip_val"],
+                                    g["x"], y.astype(np.float64))
+        assert err <= 1e-5
+    else:
+        np.testing.assert_array_equal(y, g["y"])
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("rows,cols,C,R", [
+    (1000, 3000, 256, 64),      # ragged last row block, 12 column blocks
+    (5000, 5000, 512, 512),     # cfg1 geometry, small
+    (300, 9000, 1000, 32),      # one group per row block
+    (4096, 4096, 4096, 1024),   # one column block
+    (3000, 70000, 2400, 256),   # up to 30 blocks per row block
+    (2000, 2000, 70, 96),       # C not a multiple of 4: unaligned staged ranges
+])
+def test_rowstage_equals_plan_bitwise(dtype, rows, cols, C, R):
+    rng = np.random.default_rng(rows + cols + 1)
+    lens = rng.poisson(7, rows)
+    lens[rng.choice(rows, rows // 10, replace=False)] = 0
+    lens[rows // 3: rows // 3 + 5] = min(cols, 600)
+    r = np.repeat(np.arange(rows), lens)
+    c = np.concatenate([rng.choice(cols, k, replace=False) for k in lens])
+    v = rng.uniform(-1, 1, r.size).astype(dtype)
+    hbp = _hbp(rows, cols, r, c, v, C, R, 32)
+    x = torch.as_tensor(rng.uniform(-1, 1, cols).astype(dtype), device="cuda")
+    op = H.SpmvOperator(hbp, schedule="rowstage")
+    y_st = op(x).cpu().numpy()
+    np.testing.assert_array_equal(op(x).cpu().numpy(), y_st)
+    y_plan = H.SpmvOperator(hbp, schedule="plan")(x).cpu().numpy()
+    np.testing.assert_array_equal(y_st.view(np.uint8), y_plan.view(np.uint8))
+
+
+def test_rowstage_empty_row_blocks_and_matrix():
+    rows, cols, R = 4096, 4096, 256
+    r = np.concatenate([np.arange(0, 256), np.arange(2048, 2100)])
+    c = (r * 7) % cols
+    hbp = _hbp(rows, cols, r, c, np.full(r.size, -1.5), C=512, R=R)
+    x = torch.full((cols,), 2.0, dtype=torch.float64, device="cuda")
+    y = torch.full((rows,), np.nan, dtype=torch.float64, device="cuda")
+    H.SpmvOperator(hbp, schedule="rowstage")(x, y)
+    want = np.zeros(rows)
+    want[r] = -3.0
+    np.testing.assert_array_equal(y.cpu().numpy(), want)
+    empty = _hbp(700, 900, np.zeros(0, np.int64), np.zeros(0, np.int64), np.zeros(0), C=128, R=64)
+    y = H.SpmvOperator(empty, schedule="rowstage")(torch.ones(900, dtype=torch.float64,
+                                                              device="cuda"))
+    assert (y == 0).all()
+
+
+def test_rowstage_rejects_oversized_row_blocks(monkeypatch):
+    rng = np.random.default_rng(0)
+    rows, cols = 512, 4096
+    lens = np.full(rows, 300)
+    r = np.repeat(np.arange(rows), lens)
+    c = np.concatenate([rng.choice(cols, k, replace=False) for k in lens])
+    hbp = _hbp(rows, cols, r, c, rng.uniform(-1, 1, r.size), C=4096, R=512)
+    with pytest.raises(ValueError, match="shared memory"):
+        H.SpmvOperator(hbp, schedule="rowstage")

@@ -3,7 +3,7 @@ with several column blocks (checks SpmvOperator._auto_schedule's threshold).
 
     python tools/prof_sched.py
 
-Each line: matrix, dtype, nnz, auto choice, stream ms, rowblock ms (L2
+Each line: matrix, dtype, nnz, auto choice, stream / rowblock / rowstage ms (L2
 flushed before every timed SpMV, CUDA events, mean of 30).
 """
 import os
@@ -44,9 +44,15 @@ def run(name, rows, cols, rp, col, val, C):
     x = torch.rand(cols, device=dev, dtype=torch.float64).to(val.dtype)
     y = torch.empty(rows, device=dev, dtype=val.dtype)
     auto = H.SpmvOperator._auto_schedule(hbp)
-    t = {s: timed(H.SpmvOperator(hbp, schedule=s), x, y) for s in ("stream", "rowblock")}
+    t = {}
+    for s in ("stream", "rowblock", "rowstage"):
+        try:
+            t[s] = timed(H.SpmvOperator(hbp, schedule=s), x, y)
+        except ValueError:  # rowstage: a row block too large to stage
+            t[s] = float("nan")
     print(f"{name:28s} {str(val.dtype)[6:]:8s} nnz={hbp.nnz:>10d} ncb={hbp.num_col_blocks:>5d} "
-          f"auto={auto:8s} stream={t['stream']:.4f} rowblock={t['rowblock']:.4f}", flush=True)
+          f"auto={auto:8s} stream={t['stream']:.4f} rowblock={t['rowblock']:.4f} "
+          f"rowstage={t['rowstage']:.4f}", flush=True)
 
 
 for dt in (torch.float64, torch.float32):
