@@ -282,6 +282,90 @@ def cpu_reference(cfg_name: str, steps: int, warmup: int, seed: int = 0):
                                    total=(t4 - t0) * 1e3))
 
 
+def _reference_pkg():
+    """The UNMODIFIED reference package (Python + numba), pip-installed into
+    baseline/_ref (git-ignored, travels with the repo): its own public API
+    and stock code path.  None when it is absent or numba is missing."""
+    ref = os.path.join(os.path.dirname(os.path.abspath(__file__)), "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "hbp_spmv")):
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/hbp_numba_cache")
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        import hbp_spmv as ref_pkg
+        return ref_pkg
+    except Exception:  # numba or numpy missing on this host
+        return None
+
+
+def numba_reference(cfg_name: str, steps: int, warmup: int, seed: int = 0):
+    """The reference itself (baseline/_ref: engine.py:228-232 hbp_spmv with
+    numba kernels and Python worker threads, formats.py:266-273 csr_spmv) on
+    the same bounded sample as cpu_reference, at workers = cpu_count / 4 / 1.
+    Returns a dict, or None without the reference package."""
+    h = _reference_pkg()
+    if h is None:
+        return None
+    rows, cols, rp, col, val, C, sample = make_matrix_cpu_sample(cfg_name, seed)
+    cfg = h.PartitionConfig(col_width=C, row_height=512, warp_size=32)
+    csr = h.CsrMatrix(rows, cols, rp, col, val)
+    t0 = time.perf_counter()
+    grid = h.make_grid(csr, cfg)
+    t1 = time.perf_counter()
+    params = h.sample_hash_params(grid, cfg)
+    t2 = time.perf_counter()
+    perms = h.hash_permutations(grid, params)
+    t3 = time.perf_counter()
+    hbp = h.build_hbp(csr, grid, perms, cfg)
+    t4 = time.perf_counter()
+    x = np.random.default_rng(0).uniform(-1.0, 1.0, cols)
+    nnz = int(rp[-1])
+    ncpu = os.cpu_count() or 1
+
+    def timed(fn, n, budget=20.0):
+        for _ in range(max(1, warmup)):
+            fn()
+        ts, deadline = [], time.perf_counter() + budget
+        for i in range(max(1, n)):
+            a = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - a)
+            if time.perf_counter() > deadline and i >= 1:
+                break
+        return statistics.median(ts), len(ts)
+
+    by_workers = {}
+    t_main, n_main = timed(lambda: h.hbp_spmv(hbp, x, workers=ncpu), steps)
+    by_workers[str(ncpu)] = round(2.0 * nnz / t_main / 1e9, 4)
+    for wk in sorted({1, 4} - {ncpu}):
+        tw, _ = timed(lambda: h.hbp_spmv(hbp, x, workers=wk), 3, budget=10.0)
+        by_workers[str(wk)] = round(2.0 * nnz / tw / 1e9, 4)
+    best = max(by_workers, key=lambda k: by_workers[k])
+    t_csr, _ = timed(lambda: h.csr_spmv(csr, x), 3, budget=10.0)
+    return dict(value=by_workers[best], unit=UNIT, cores=int(best), kind="reference",
+                workers_best=int(best), gflops_by_workers=by_workers,
+                csr_spmv_gflops_1thread=round(2.0 * nnz / t_csr / 1e9, 4),
+                sample=(f"{sample}: {rows} rows, {nnz} nnz; the reference package itself "
+                        f"(baseline/_ref, numba), hbp_spmv(workers={best}) = its best worker "
+                        f"count, median of {n_main if best == str(ncpu) else 3}"),
+                ms_per_step=2.0 * nnz / by_workers[best] / 1e6, nnz=nnz, rows=rows,
+                preprocess_ms=dict(grid=(t1 - t0) * 1e3, sample=(t2 - t1) * 1e3,
+                                   hash=(t3 - t2) * 1e3, build=(t4 - t3) * 1e3,
+                                   total=(t4 - t0) * 1e3))
+
+
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 # ------------------------------------------------------------------ GPU arm
 def _dist():
     import torch
@@ -661,11 +745,22 @@ def run_gpu(args):
     if baselines is not None:
         out["baselines_same_gpu"] = baselines
     if world == 1 and not args.no_cpu_baseline:
-        cb = cpu_reference(args.config, steps=5, warmup=1)
+        # the reference package itself when baseline/_ref holds it (numba),
+        # else (and alongside, for comparison) the oracle's C port
+        port = cpu_reference(args.config, steps=5, warmup=1)
+        nb = numba_reference(args.config, steps=3, warmup=1) \
+            if args.config != "cfg1" or os.environ.get("HBP_REF_CFG1") else None
+        cb = nb if nb is not None else port
         out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample",
                                                    "gflops_by_workers")}
         out["cpu_baseline"]["preprocess_ms"] = {k: round(v, 1)
                                                 for k, v in cb["preprocess_ms"].items()}
+        out["cpu_baseline"]["cpu_model"] = _cpu_model()
+        out["cpu_baseline"]["host_threads"] = os.cpu_count()
+        if nb is not None:
+            out["cpu_baseline"]["csr_spmv_gflops_1thread"] = nb["csr_spmv_gflops_1thread"]
+            out["cpu_baseline"]["port"] = {k: port[k] for k in ("value", "cores",
+                                                                "gflops_by_workers")}
         # SURVEY.md §8(d) gate: GPU preprocess vs one CPU reference SpMV of the
         # same sample, and the CPU preprocess on its sample
         out["preprocess_gate"] = {
@@ -692,8 +787,17 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
-    cb = cpu_reference(args.config, steps=args.steps, warmup=args.warmup)
+    nb = numba_reference(args.config, steps=args.steps, warmup=args.warmup) \
+        if args.config != "cfg1" or os.environ.get("HBP_REF_CFG1") else None
+    port = cpu_reference(args.config, steps=args.steps, warmup=args.warmup)
+    cb = nb if nb is not None else port
     desc = CONFIGS[args.config][0]
+    others = {"port": {"value": round(port["value"], 4), "cores": port["cores"],
+                       "gflops_by_workers": port["gflops_by_workers"],
+                       "what": "oracle/ C port of the same path (pthreads)"}}
+    if nb is not None:
+        others["reference_numba"] = {k: nb[k] for k in ("gflops_by_workers",
+                                                         "csr_spmv_gflops_1thread")}
     return {
         "impl": "reference", "metric": METRIC, "value": round(cb["value"], 4), "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -707,6 +811,8 @@ def run_reference(args):
         "e2e": {"value": round(cb["value"], 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "preprocess_ms": {k: round(v, 1) for k, v in cb["preprocess_ms"].items()},
+        "cpu_model": _cpu_model(), "host_threads": os.cpu_count(),
+        "cpu_arms": others,
     }
 
 
