@@ -415,6 +415,8 @@ def run_gpu(args):
     hot_arg = {"auto": None, "off": False, "on": True}.get(args.hot)
     if hot_arg is None and args.hot != "auto":
         hot_arg = int(args.hot)
+    if args.hub is None and args.config == "cfg2d":
+        args.hub = "auto"  # the fp64 R-MAT line is quoted with the hub-row path
     hub_arg = None if args.hub in (None, "off", "0") else (
         "auto" if args.hub == "auto" else int(args.hub))
     op_kwargs = dict(schedule=args.schedule, hot=hot_arg, workers=args.workers, hub_min=hub_arg)
