@@ -11,11 +11,13 @@
 //      row block's staging buffer, so thread j of the CTA bulk-copies
 //      (cp.async.bulk) block j's col/data straight away -- one DRAM round
 //      trip for the whole row block, issued in parallel, no registers held;
-//   2. the CTA is persistent; several CTAs per SM overlap one row block's
-//      copies with another's walk (a double-buffered form, row block i+1's
-//      copies in flight while row block i is walked, measured no faster);
+//   2. the CTA is persistent and loads the next row block's rb_ptr entries
+//      and descriptors into registers behind the current walk; several CTAs
+//      per SM overlap one row block's copies with another's walk (a
+//      double-buffered form -- row block i+1's copies in flight while i is
+//      walked -- halved the CTAs per SM and measured slower, 32.8 vs 28.7 us);
 //   3. every lane loads its tasks' slot length, output row and group start
-//      one task ahead (coalesced, independent);
+//      one task ahead (block indices from shared memory, no division);
 //   4. the walk reads col/data from shared memory (positions from per-step
 //      ballots of the slot lengths, the closed form of build_hbp's layout);
 //      only the x gathers go to global memory, four steps in flight.
@@ -81,15 +83,17 @@ __global__ void k_rowstage_plan(const hbp_format_t f, int64_t *__restrict__ desc
     }
 }
 
-template <typename V, bool EXACT, int NT, bool DB>
+template <typename V, bool EXACT, int NT>
 __global__ void __launch_bounds__(NT)
     k_spmv_rowstage(const hbp_format_t f, const int64_t *__restrict__ desc,
                     const V *__restrict__ x, V *__restrict__ y, int32_t ecap) {
     extern __shared__ __align__(16) unsigned char sm[];
-    __shared__ __align__(8) uint64_t mbar[2];
-    __shared__ int64_t s_base[2][kMaxBlocks];  // staged index of element 0 of block j
-    const int64_t buf_bytes = (int64_t)ecap * (4 + sizeof(V));
-    double *part = reinterpret_cast<double *>(sm + (DB ? 2 : 1) * buf_bytes);
+    __shared__ __align__(8) uint64_t mbar;
+    __shared__ int64_t s_base[kMaxBlocks];  // staged index of element 0 of block j
+    __shared__ int32_t s_blk[kMaxBlocks];   // block j's index (rb_blk order)
+    uint32_t *col_s = reinterpret_cast<uint32_t *>(sm);
+    V *dat_s = reinterpret_cast<V *>(sm + (int64_t)ecap * 4);
+    double *part = reinterpret_cast<double *>(sm + (int64_t)ecap * (4 + sizeof(V)));
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     constexpr int nwarps = NT / 32;
     const unsigned lt = (1u << lane) - 1u;
@@ -98,84 +102,81 @@ __global__ void __launch_bounds__(NT)
     const V *__restrict__ data = (const V *)f.data;
     const uint64_t pe = policy_evict_first(), pl = policy_evict_last();
     if (threadIdx.x == 0) {
-        mbar_init(&mbar[0], 1);
-        mbar_init(&mbar[1], 1);
+        mbar_init(&mbar, 1);
         fence_mbar_init();
     }
     __syncthreads();
 
-    // thread j < cnt stages block j of row block br into buffer `buf`; the
-    // caller syncs, then thread 0 arrives once every expect_tx is posted
-    auto stage = [&](int64_t br, int buf) {
-        const int64_t lo = f.rb_ptr[br], hi = f.rb_ptr[br + 1];
-        const int32_t cnt = (int32_t)(hi - lo);
-        uint32_t *col_s = reinterpret_cast<uint32_t *>(sm + buf * buf_bytes);
-        V *dat_s = reinterpret_cast<V *>(sm + buf * buf_bytes + (int64_t)ecap * 4);
-        if ((int)threadIdx.x < cnt) {
-            const int64_t a0 = desc[2 * (lo + threadIdx.x)];
-            const int64_t mo = desc[2 * (lo + threadIdx.x) + 1];
-            const int32_t m = (int32_t)(mo >> 32), off = (int32_t)(mo & 0xffffffff);
-            s_base[buf][threadIdx.x] = (int64_t)off - a0;
-            if (m > 0) {
-                fence_proxy_async();  // the CTA's generic reads of this buffer (barrier-ordered) first
-                mbar_expect_only(&mbar[buf], (uint32_t)m * (4u + (uint32_t)sizeof(V)));
-                bulk_g2s(col_s + off, f.col + a0, (uint32_t)m * 4u, &mbar[buf], pe);
-                bulk_g2s(dat_s + off, data + a0, (uint32_t)m * (uint32_t)sizeof(V), &mbar[buf], pe);
-            }
+    // The next row block's rb_ptr entries, and (threads j < its block count)
+    // block j's descriptor and index, are loaded into registers while the
+    // current row block is walked, so staging issues without a round trip.
+    int64_t br = blockIdx.x;
+    int64_t lo = 0, hi = 0, d_a0 = 0, d_mo = 0;
+    int32_t d_blk = 0;
+    auto fetch_desc = [&](int64_t l, int64_t h) {
+        if ((int64_t)threadIdx.x < h - l) {
+            d_a0 = desc[2 * (l + threadIdx.x)];
+            d_mo = desc[2 * (l + threadIdx.x) + 1];
+            d_blk = f.rb_blk[l + threadIdx.x];
         }
     };
-
-    uint32_t phase0 = 0u, phase1 = 0u;
-    // DB: double-buffered (row block i+1's copies in flight while row block i
-    // is walked; half the staging capacity per CTA) -- measured no faster on
-    // cfg1 than more single-buffered CTAs per SM, so off by default
-    int buf = 0;
-    if (DB && blockIdx.x < nrb) {
-        stage(blockIdx.x, 0);
-        __syncthreads();
-        if (threadIdx.x == 0) mbar_arrive1(&mbar[0]);
+    if (br < nrb) {
+        lo = f.rb_ptr[br];
+        hi = f.rb_ptr[br + 1];
+        fetch_desc(lo, hi);
     }
-    for (int64_t br = blockIdx.x; br < nrb; br += gridDim.x, buf ^= (DB ? 1 : 0)) {
-        const int64_t lo = f.rb_ptr[br], hi = f.rb_ptr[br + 1];
+    uint32_t phase = 0u;
+    for (; br < nrb; br += gridDim.x) {
         const int64_t n64 = f.rows - br * R;
         const int32_t n = (int32_t)(n64 > R ? R : n64);
         const int32_t cnt = (int32_t)(hi - lo);
-        const int64_t nx = DB ? br + gridDim.x : br;
+        if ((int)threadIdx.x < cnt) {  // thread j stages block j
+            const int32_t m = (int32_t)(d_mo >> 32), off = (int32_t)(d_mo & 0xffffffff);
+            s_base[threadIdx.x] = (int64_t)off - d_a0;
+            s_blk[threadIdx.x] = d_blk;
+            if (m > 0) {
+                fence_proxy_async();  // the CTA's generic reads of the buffer (barrier-ordered) first
+                mbar_expect_only(&mbar, (uint32_t)m * (4u + (uint32_t)sizeof(V)));
+                bulk_g2s(col_s + off, f.col + d_a0, (uint32_t)m * 4u, &mbar, pe);
+                bulk_g2s(dat_s + off, data + d_a0, (uint32_t)m * (uint32_t)sizeof(V), &mbar, pe);
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) mbar_arrive1(&mbar);
+        const int64_t nx = br + gridDim.x;
+        int64_t nlo = 0, nhi = 0;
         if (nx < nrb) {
-            stage(nx, DB ? buf ^ 1 : buf);
-            __syncthreads();
-            if (threadIdx.x == 0) mbar_arrive1(&mbar[DB ? buf ^ 1 : buf]);
+            nlo = f.rb_ptr[nx];
+            nhi = f.rb_ptr[nx + 1];
         }
         V *yb = y + br * R;
-        const uint32_t *col_s = reinterpret_cast<const uint32_t *>(sm + buf * buf_bytes);
-        const V *dat_s = reinterpret_cast<const V *>(sm + buf * buf_bytes + (int64_t)ecap * 4);
         const int32_t ng = (n + 31) >> 5;
         const int32_t ntask = cnt * ng;
+        // task t = (block j, group g), t = j * ng + g; advanced without division
+        int32_t tj = 0, tg = wid;
+        while (tg >= ng && tj < cnt) tg -= ng, ++tj;
         uint32_t len_n = 0u, row_n = 0u;
-        int32_t base_n = 0, j_n = 0;
-        auto load = [&](int32_t t) {
-            const int32_t j = t / ng, g = t - j * ng;
-            const int64_t b = f.rb_blk[lo + j];
-            const int32_t slot = g * 32 + lane;
+        int32_t base_n = 0, j_n = 0, g_n = 0;
+        auto load = [&]() {
+            const int64_t b = s_blk[tj];
+            const int32_t slot = tg * 32 + lane;
             len_n = slot < n ? __ldcs(f.slot_len + b * R + slot) : 0u;
             row_n = slot < n ? __ldcs(f.perm + b * R + slot) : 0u;
-            base_n = (int32_t)(f.group_start[b * gpb + g] + s_base[buf][j]);
-            j_n = j;
+            base_n = (int32_t)(f.group_start[b * gpb + tg] + s_base[tj]);
+            j_n = tj;
+            g_n = tg;
+            tg += nwarps;
+            while (tg >= ng) tg -= ng, ++tj;
         };
-        if (wid < ntask) load(wid);
-        if (buf == 0) {
-            mbar_wait(&mbar[0], phase0);
-            phase0 ^= 1u;
-        } else {
-            mbar_wait(&mbar[1], phase1);
-            phase1 ^= 1u;
-        }
+        if (wid < ntask) load();
+        mbar_wait(&mbar, phase);
+        phase ^= 1u;
         for (int32_t t = wid; t < ntask; t += nwarps) {
             const uint32_t len = len_n, row = row_n;
             int32_t base = base_n;
             const int32_t j = j_n;
-            const bool valid = (t - j * ng) * 32 + lane < n;
-            if (t + nwarps < ntask) load(t + nwarps);
+            const bool valid = g_n * 32 + lane < n;
+            if (t + nwarps < ntask) load();
             double acc = 0.0;
             uint32_t t0 = 0;
             bool live = len > 0;
@@ -215,6 +216,7 @@ __global__ void __launch_bounds__(NT)
             }
             if (valid) part[(int64_t)j * R + row] = acc;
         }
+        fetch_desc(nlo, nhi);  // the next row block's descriptors, behind the walk
         __syncthreads();
         // fold in ascending bc: s = p_first; s += p_next ... (combine's order);
         // a row block without nonzero blocks gets +0.0
@@ -223,16 +225,17 @@ __global__ void __launch_bounds__(NT)
             for (int32_t j = 1; j < cnt; ++j) v = __dadd_rn(v, part[(int64_t)j * R + r]);
             __stcs(yb + r, (V)v);
         }
+        lo = nlo;
+        hi = nhi;
         __syncthreads();
     }
 }
 
-template <typename V, bool EXACT, int NT, bool DB = false>
+template <typename V, bool EXACT, int NT>
 int launch_rowstage(const hbp_format_t *f, const int64_t *desc, const void *x, void *y,
                     int32_t ecap, int32_t kmax, cudaStream_t st) {
-    const size_t smem =
-        (DB ? 2 : 1) * (size_t)ecap * (4 + sizeof(V)) + (size_t)kmax * f->row_height * 8;
-    auto kern = k_spmv_rowstage<V, EXACT, NT, DB>;
+    const size_t smem = (size_t)ecap * (4 + sizeof(V)) + (size_t)kmax * f->row_height * 8;
+    auto kern = k_spmv_rowstage<V, EXACT, NT>;
     HBP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int dev = 0, sms = 0, per_sm = 0;
     HBP_CUDA_TRY(cudaGetDevice(&dev));
@@ -271,14 +274,14 @@ int hbp_spmv_rowstage(const hbp_format_t *f, const int64_t *desc, const void *x,
     if (ecap < 4 || kmax < 1 || (ecap & 3)) return HBP_E_ARG;
     if (kmax > kMaxBlocks || ecap > (1 << 24)) return HBP_E_UNSUPPORTED;
     cudaStream_t st = as_stream(stream);
-    // tuning A/B only: threads per CTA (512 default)
+    // tuning A/B only: threads per CTA (256 default: cfg1 24.1-25.0 us vs 28.2-28.7 at
+    // 512, ncu kernel times, caches flushed)
     static const int nt =
-        getenv("HBP_ROWSTAGE_THREADS") ? atoi(getenv("HBP_ROWSTAGE_THREADS")) : 512;
+        getenv("HBP_ROWSTAGE_THREADS") ? atoi(getenv("HBP_ROWSTAGE_THREADS")) : 256;
     const int32_t e = (int32_t)ecap, k = (int32_t)kmax;
     if (f->dtype == HBP_F64)
-        return nt == 256   ? launch_rowstage<double, true, 256>(f, desc, x, y, e, k, st)
-               : nt == 2   ? launch_rowstage<double, true, 512, true>(f, desc, x, y, e, k, st)
-                           : launch_rowstage<double, true, 512>(f, desc, x, y, e, k, st);
+        return nt == 256 ? launch_rowstage<double, true, 256>(f, desc, x, y, e, k, st)
+                         : launch_rowstage<double, true, 512>(f, desc, x, y, e, k, st);
     if (f->dtype == HBP_F32)
         return nt == 256 ? launch_rowstage<float, false, 256>(f, desc, x, y, e, k, st)
                          : launch_rowstage<float, false, 512>(f, desc, x, y, e, k, st);
