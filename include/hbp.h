@@ -279,6 +279,13 @@ typedef struct {
  * one nonzero block are written to y directly (there is nothing to combine;
  * bitwise the same), and hbp_combine skips those row blocks. */
 #define HBP_FLAG_DIRECT_SINGLE 4
+/* Packed x (hbp_spmv_stream with hot staging): every column the matrix uses
+ * is in hot_cols (heaviest first); scol holds HBP_HOT_FLAG | s for the n_hot
+ * staged ones and the PLAIN index w < n_warm of the packed copy
+ * x_hot[n_hot + w] for the rest, which the kernel gathers instead of x
+ * (degree-ordered: the heavy columns share L2 lines).  n_warm is then the
+ * packed count and no warm tier is used. */
+#define HBP_FLAG_PACKED_X 8
 #define HBP_HOT_FLAG 0x80000000u
 #define HBP_WARM_FLAG 0x40000000u
 
@@ -390,6 +397,8 @@ int hbp_spmv_stream(const hbp_format_t *f, const hbp_balanced_t *b, const void *
  *   hbp_hot_slots:   slot_of[hot_cols[s]] = s (slot_of filled with -1).
  *   hbp_hot_remap:   scol[e] = slot s = slot_of[col[e]]: s < n_hot -> HBP_HOT_FLAG | s,
  *                    n_hot <= s -> HBP_WARM_FLAG | (s - n_hot), none -> col[e].
+ *   hbp_hot_remap_packed: the same with n_hot <= s -> (s - n_hot) (HBP_FLAG_PACKED_X;
+ *                    every column must have a slot).
  *   hbp_hot_gather:  x_hot[s] = x[hot_cols[s]] (run inside hbp_spmv_stream).
  * The warm tier (next-heaviest columns after the hot ones) is a compact copy
  * of x that the kernel gathers with an L2 evict-last policy while the other
@@ -402,6 +411,8 @@ int hbp_hot_slots(const uint32_t *hot_cols, int64_t n_hot, int32_t *slot_of,
                   hbp_stream_t stream);
 int hbp_hot_remap(const uint32_t *col, int64_t nnz, const int32_t *slot_of, int64_t n_hot,
                   uint32_t *scol, hbp_stream_t stream);
+int hbp_hot_remap_packed(const uint32_t *col, int64_t nnz, const int32_t *slot_of, int64_t n_hot,
+                         uint32_t *scol, hbp_stream_t stream);
 int hbp_hot_gather(const void *x, int dtype, const uint32_t *hot_cols, int64_t n_hot,
                    void *x_hot, hbp_stream_t stream);
 int hbp_spmv_balanced(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y,

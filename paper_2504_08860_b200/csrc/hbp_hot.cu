@@ -55,6 +55,7 @@ __global__ void k_hot_slots(const uint32_t *__restrict__ hot_cols, int64_t n_hot
     if (s < n_hot) slot_of[hot_cols[s]] = (int32_t)s;
 }
 
+template <bool PACKED>
 __global__ void k_hot_remap(const uint4 *__restrict__ col4, const uint32_t *__restrict__ col,
                             int64_t nnz, const int32_t *__restrict__ slot_of, int32_t n_hot,
                             uint4 *__restrict__ scol4, uint32_t *__restrict__ scol) {
@@ -62,8 +63,9 @@ __global__ void k_hot_remap(const uint4 *__restrict__ col4, const uint32_t *__re
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     auto map = [&](uint32_t c) -> uint32_t {
         const int32_t s = __ldg(slot_of + c);
-        if (s < 0) return c;
-        return s < n_hot ? (HBP_HOT_FLAG | (uint32_t)s) : (HBP_WARM_FLAG | (uint32_t)(s - n_hot));
+        if (s < 0) return PACKED ? 0u : c;  // (packed: every used column has a slot)
+        if (s < n_hot) return HBP_HOT_FLAG | (uint32_t)s;
+        return PACKED ? (uint32_t)(s - n_hot) : (HBP_WARM_FLAG | (uint32_t)(s - n_hot));
     };
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
         const uint4 c = __ldcs(col4 + i);
@@ -103,7 +105,18 @@ int hbp_hot_remap(const uint32_t *col, int64_t nnz, const int32_t *slot_of, int6
         return HBP_E_ARG;
     if (nnz == 0) return HBP_OK;
     if ((((uintptr_t)col | (uintptr_t)scol) & 15) != 0) return HBP_E_ARG;
-    k_hot_remap<<<grid_for(nnz / 4 + 1, 256), 256, 0, as_stream(stream)>>>(
+    k_hot_remap<false><<<grid_for(nnz / 4 + 1, 256), 256, 0, as_stream(stream)>>>(
+        (const uint4 *)col, col, nnz, slot_of, (int32_t)n_hot, (uint4 *)scol, scol);
+    return (int)cudaGetLastError();
+}
+
+int hbp_hot_remap_packed(const uint32_t *col, int64_t nnz, const int32_t *slot_of, int64_t n_hot,
+                         uint32_t *scol, hbp_stream_t stream) {
+    if (nnz < 0 || n_hot < 0 || n_hot >= (1 << 30) || (nnz > 0 && (!col || !slot_of || !scol)))
+        return HBP_E_ARG;
+    if (nnz == 0) return HBP_OK;
+    if ((((uintptr_t)col | (uintptr_t)scol) & 15) != 0) return HBP_E_ARG;
+    k_hot_remap<true><<<grid_for(nnz / 4 + 1, 256), 256, 0, as_stream(stream)>>>(
         (const uint4 *)col, col, nnz, slot_of, (int32_t)n_hot, (uint4 *)scol, scol);
     return (int)cudaGetLastError();
 }

@@ -1024,6 +1024,10 @@ int variant() {
 }
 
 bool staged(const hbp_format_t *f) { return f->n_hot > 0 && f->scol && f->hot_cols; }
+bool packed(const hbp_format_t *f) { return staged(f) && (f->reserved & HBP_FLAG_PACKED_X); }
+// a warm tier (its own instantiation) -- not with a packed x, whose n_warm
+// counts the packed columns gathered like plain ones
+bool warm(const hbp_format_t *f) { return f->n_warm > 0 && !packed(f); }
 
 // One variant = (chunk CH, ring slots NB, threads NT, CTAs per SM MINB, the
 // XM feature bits).  f64 data always uses CH 128, NB 4.  Every launch is one CTA per SM (staged ones need one shared
@@ -1054,7 +1058,7 @@ bool staged(const hbp_format_t *f) { return f->n_hot > 0 && f->scol && f->hot_co
 // instantiations of the default, warm and unstaged kernels
 #define HBP_STREAM_DISPATCH(FN, V, EXACT, FUSED, HUB, TICKET, ...)                          \
     if (TICKET && !HUB && !FUSED) {                                                         \
-        if (staged(f) && f->n_warm > 0) {                                                   \
+        if (staged(f) && warm(f)) {                                                         \
             HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, kWarmThreads, 1, 53 | 2048 | 8192, __VA_ARGS__); \
         }                                                                                   \
         if (staged(f)) {                                                                    \
@@ -1063,7 +1067,7 @@ bool staged(const hbp_format_t *f) { return f->n_hot > 0 && f->scol && f->hot_co
         HBP_VARIANT_X(FN, V, EXACT, false, 128, 4, kHotThreads, 1, 21 | 2048 | 8192, __VA_ARGS__); \
     }                                                                                       \
     if (EXACT && HUB) {                                                                     \
-        if (staged(f) && f->n_warm > 0) {                                                   \
+        if (staged(f) && warm(f)) {                                                         \
             HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, kWarmThreads, 1, 53 | 2048 | 4096, __VA_ARGS__); \
         }                                                                                   \
         if (staged(f)) {                                                                    \
@@ -1072,13 +1076,13 @@ bool staged(const hbp_format_t *f) { return f->n_hot > 0 && f->scol && f->hot_co
         HBP_VARIANT_X(FN, V, EXACT, false, 128, 4, kHotThreads, 1, 21 | 2048 | 4096, __VA_ARGS__); \
     }                                                                                       \
     if (staged(f)) {                                                                        \
-        if (FUSED && f->n_warm > 0) {                                                       \
+        if (FUSED && warm(f)) {                                                             \
             HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, kWarmThreads, 1, 53 | 512 | 2048, __VA_ARGS__); \
         }                                                                                   \
         if (FUSED) {                                                                        \
             HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, kHotThreads, 1, 21 | 512 | 2048, __VA_ARGS__); \
         }                                                                                   \
-        if (f->n_warm > 0) {                                                                \
+        if (warm(f)) {                                                                      \
             HBP_VARIANT_X(FN, V, EXACT, true, 128, 4, kWarmThreads, 1, 53 | 2048, __VA_ARGS__); \
         }                                                                                   \
         HBP_VARIANTS(FN, V, EXACT, true, kHotThreads, 1, __VA_ARGS__)                       \
@@ -1128,6 +1132,7 @@ int run(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y, 
     if (staged(f)) {
         const int rc = hot_gather<V>(x, f->hot_cols, f->n_hot + f->n_warm, b->x_hot, st);
         if (rc) return rc;
+        if (packed(f)) x = (const V *)b->x_hot + f->n_hot;  // gathers read the packed copy
     }
     HBP_STREAM_DISPATCH(launch, V, EXACT, (b->rb_done != nullptr), (b->hub_min > 0),
                         (b->pieces > b->workers), f, b, x, y, partial, st)
@@ -1243,10 +1248,11 @@ int hbp_spmv_stream(const hbp_format_t *f, const hbp_balanced_t *b, const void *
     }
     if (staged(f)) {
         int64_t cap = 0;
-        const int rc = hbp_hot_capacity(f->dtype, f->n_warm > 0, &cap);
+        const int rc = hbp_hot_capacity(f->dtype, warm(f), &cap);
         if (rc) return rc;
         if (f->n_hot > cap || (f->n_hot & 3) || !b->x_hot) return HBP_E_ARG;
-        if (f->n_warm < 0 || (f->n_warm > 0 && f->cols > (int64_t)1 << 30)) return HBP_E_ARG;
+        if (f->n_warm < 0 || (warm(f) && f->cols > (int64_t)1 << 30)) return HBP_E_ARG;
+        if (packed(f) && (f->n_warm >= (int64_t)1 << 31 || f->n_warm > f->cols)) return HBP_E_ARG;
         if (f->cols >= (int64_t)1 << 31) return HBP_E_ARG;  // bit 31 flags hot columns
     }
     cudaStream_t st = as_stream(stream);

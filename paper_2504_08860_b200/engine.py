@@ -186,7 +186,8 @@ class SpmvOperator:
     def __init__(self, hbp: HbpMatrix, workers: int | None = None,
                  fixed_fraction: float | None = None, schedule: str | None = None,
                  hot: bool | int | None = None, warm_bytes: int | None = None,
-                 hub_min: int | str | None = None, ticket=None, slice_cost=None):
+                 hub_min: int | str | None = None, ticket=None, slice_cost=None,
+                 packed_x: bool | None = None):
         self.hbp = hbp
         dev = hbp.data.device
         if schedule is None:
@@ -212,12 +213,17 @@ class SpmvOperator:
             n = min(cap if n_hot is None else min(n_hot, cap), hbp.cols) & ~3
             if hbp.cols >= (1 << 31):
                 n = 0
+            if packed_x is None:
+                packed_x = os.environ.get("HBP_PACKED_X", "0") == "1"
             if n > 0 and (hot is not None or hbp.column_share(n) >= self.HOT_MIN_SHARE):
-                hc = hbp.hot_columns(n_hot, max(0, wb) // hbp.data.element_size())
+                if packed_x:
+                    hc = hbp.hot_columns(n_hot, packed=True)
+                else:
+                    hc = hbp.hot_columns(n_hot, max(0, wb) // hbp.data.element_size())
                 if hc.n_hot > 0:
                     self.hot = hc
                     hc.apply(f)
-                f.cold_last = int(fits)
+                f.cold_last = int(fits or hc.packed)
         if schedule in ("balanced", "stream"):
             if workers is None:
                 w = L.c_i64(0)

@@ -57,9 +57,14 @@ class HotColumns:
         self.n_hot, self.hot_cols, self.scol, self.share = n_hot, hot_cols, scol, share
         self.n_warm, self.warm_share = n_warm, warm_share
 
+    packed = False  # HBP_FLAG_PACKED_X: n_warm counts the packed copy of x
+
     def apply(self, f: "L.FormatT") -> None:
         f.scol, f.hot_cols = self.scol.data_ptr(), self.hot_cols.data_ptr()
         f.n_hot, f.n_warm = self.n_hot, self.n_warm
+        if self.packed:
+            f.reserved |= 8  # HBP_FLAG_PACKED_X
+            f.cold_last = 1
 
 
 class HbpFormatError(ValueError):
@@ -143,7 +148,31 @@ class HbpMatrix:
             vals = torch.arange(self.cols, dtype=torch.int32, device=dev)
             _, order = L.sort_pairs_u32(keys, vals, 32)
             self._ops["rank"] = (deg, order)
+            self._ops["rank_stride"] = stride
         return self._ops["rank"]
+
+    def packed_order(self):
+        """(order, n_used): every column the matrix uses, heaviest first (by
+        the possibly sampled ranking), then the unused ones; n_used is exact
+        (a full degree pass when the ranking was sampled).  Cached."""
+        if "packed_order" not in self._ops:
+            deg, order = self.column_ranking()
+            if self._ops["rank_stride"] == 1:
+                n_used = int((deg > 0).sum().item())
+            else:
+                dev = self.data.device
+                exact = torch.zeros(self.cols, dtype=torch.int32, device=dev)
+                L.call("hbp_col_degree", L.P(self.col), L.c_i64(self.nnz), L.c_i64(1),
+                       L.P(exact), L.stream())
+                used = exact > 0
+                n_used = int(used.sum().item())
+                imax = torch.iinfo(torch.int32).max
+                keys = torch.where(used, imax - deg, torch.full_like(deg, -1)).contiguous()
+                vals = torch.arange(self.cols, dtype=torch.int32, device=dev)
+                _, order = L.sort_pairs_u32(keys, vals, 32)
+                del exact, used, keys
+            self._ops["packed_order"] = (order, n_used)
+        return self._ops["packed_order"]
 
     def column_share(self, n: int) -> float:
         """Fraction of the (sampled) nonzeros in the n heaviest columns."""
@@ -153,11 +182,16 @@ class HbpMatrix:
         return float(deg[order[:n].long()].to(torch.int64).sum().item()) / max(
             1, int(deg.to(torch.int64).sum().item()))
 
-    def hot_columns(self, n_hot: int | None = None, n_warm: int = 0) -> "HotColumns":
+    def hot_columns(self, n_hot: int | None = None, n_warm: int = 0,
+                    packed: bool = False) -> "HotColumns":
         """Hot-column staging metadata for hbp_spmv_stream (include/hbp.h
         hbp_col_degree .. hbp_hot_remap): the n_hot heaviest columns (capped
         by the kernel's shared-memory capacity), then the n_warm next ones
-        (warm tier), and the staged column stream.  Cached."""
+        (warm tier), and the staged column stream.  packed: every used column
+        after the hot ones goes to the packed copy of x (HBP_FLAG_PACKED_X;
+        n_warm is ignored).  Cached."""
+        if packed:
+            return self._packed_columns(n_hot)
         cap = self.hot_capacity(warm=n_warm > 0)
         n = cap if n_hot is None else min(int(n_hot), cap)
         n = max(0, min(n, self.cols)) & ~3
@@ -180,6 +214,29 @@ class HbpMatrix:
         L.call("hbp_hot_remap", L.P(self.col), L.c_i64(self.nnz), L.P(slot_of), L.c_i64(n),
                L.P(scol), L.stream())
         hc = HotColumns(n, hot_cols, scol, share, nw, warm_share)
+        self._ops[key] = hc
+        return hc
+
+    def _packed_columns(self, n_hot: int | None) -> "HotColumns":
+        cap = self.hot_capacity(warm=False)
+        n = cap if n_hot is None else min(int(n_hot), cap)
+        order, n_used = self.packed_order()
+        n = max(0, min(n, n_used)) & ~3
+        key = ("packed", n)
+        if key in self._ops:
+            return self._ops[key]
+        dev = self.data.device
+        deg, _ = self.column_ranking()
+        hot_cols = order[:n_used].contiguous()
+        total = max(1, int(deg.to(torch.int64).sum().item()))
+        share = float(deg[hot_cols[:n].long()].to(torch.int64).sum().item()) / total if n else 0.0
+        slot_of = torch.full((self.cols,), -1, dtype=torch.int32, device=dev)
+        L.call("hbp_hot_slots", L.P(hot_cols), L.c_i64(n_used), L.P(slot_of), L.stream())
+        scol = _padded(torch.empty(self.nnz, dtype=self.col.dtype, device=dev))
+        L.call("hbp_hot_remap_packed", L.P(self.col), L.c_i64(self.nnz), L.P(slot_of),
+               L.c_i64(n), L.P(scol), L.stream())
+        hc = HotColumns(n, hot_cols, scol, share, n_used - n, 1.0 - share)
+        hc.packed = True
         self._ops[key] = hc
         return hc
 
