@@ -213,3 +213,57 @@ def test_staging_empty_matrix():
     op = H.SpmvOperator(hbp, hot=True)
     y = op(torch.ones(50, dtype=torch.float64, device="cuda"))
     assert torch.equal(y, torch.zeros(100, dtype=torch.float64, device="cuda"))
+
+
+# ---- packed x (HBP_FLAG_PACKED_X): every used column after the hot ones in a
+# degree-ordered compact copy of x
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("n_hot", [4, 1000, None])
+@pytest.mark.parametrize("workers", [1, 37, None])
+def test_packed_bitwise_equals_unstaged(mat, dtype, n_hot, workers):
+    rows, cols, r, c, v = mat
+    vv = v.astype(np.float32) if dtype == "f32" else v
+    hbp = _hbp(rows, cols, r, c, vv)
+    x = np.random.default_rng(6).uniform(-1, 1, cols)
+    xd = torch.as_tensor(x.astype(vv.dtype), device="cuda")
+    plain = H.SpmvOperator(hbp, workers=workers, hot=False)
+    packed = H.SpmvOperator(hbp, workers=workers, hot=True if n_hot is None else n_hot,
+                            packed_x=True)
+    assert packed.hot is not None and packed.hot.packed
+    y0 = plain(xd).cpu().numpy()
+    y1 = packed(xd).cpu().numpy()
+    np.testing.assert_array_equal(y1, y0)
+    np.testing.assert_array_equal(packed(xd).cpu().numpy(), y1)
+
+
+@pytest.mark.parametrize("sample", [None, 1000])
+def test_packed_metadata(mat, monkeypatch, sample):
+    """hot_cols lists exactly the used columns (heaviest first by the -- maybe
+    sampled -- ranking); scol decodes back to col."""
+    rows, cols, r, c, v = mat
+    if sample is not None:  # force the sampled ranking + exact presence pass
+        monkeypatch.setattr(H.HbpMatrix, "RANK_SAMPLE", sample)
+    hbp = _hbp(rows, cols, r, c, v.astype(np.float32))
+    hc = hbp.hot_columns(64, packed=True)
+    used = np.unique(c)
+    n_used = hc.n_hot + hc.n_warm
+    hot_cols = hc.hot_cols.cpu().numpy().astype(np.int64)
+    assert n_used == used.size == hot_cols.size
+    np.testing.assert_array_equal(np.sort(hot_cols), used)
+    col = hbp.col.cpu().numpy().astype(np.int64)
+    sc = hc.scol[:hbp.nnz].cpu().numpy().astype(np.uint32).astype(np.int64)
+    hot = (sc & FLAG) != 0
+    dec = np.where(hot, hot_cols[sc & (FLAG - 1)], hot_cols[np.minimum(hc.n_hot + sc, n_used - 1)])
+    np.testing.assert_array_equal(dec, col)
+    if sample is None:
+        deg = np.bincount(c, minlength=cols)
+        assert np.all(np.diff(deg[hot_cols]) <= 0)  # degree order
+
+
+def test_packed_is_the_default_when_x_fits_l2(mat):
+    rows, cols, r, c, v = mat
+    hbp = _hbp(rows, cols, r, c, v.astype(np.float32))
+    op = H.SpmvOperator(hbp)
+    assert op.hot is not None and op.hot.packed
+    assert not H.SpmvOperator(hbp, packed_x=False).hot.packed

@@ -41,6 +41,8 @@ ops = {}
 for r in runs:
     if r == "static":  # the default (cost-balanced slices in fast mode)
         ops[r] = H.SpmvOperator(hbp, schedule="stream")
+    elif r == "px":  # packed x: degree-ordered compact copy of the used columns
+        ops[r] = H.SpmvOperator(hbp, schedule="stream", packed_x=True)
     elif r == "eq":  # equal-element slices
         ops[r] = H.SpmvOperator(hbp, schedule="stream", slice_cost="0")
     elif r.startswith("c="):  # cost weights w_group,w_phase,w_modular
