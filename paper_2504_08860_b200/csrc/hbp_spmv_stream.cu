@@ -1110,19 +1110,31 @@ int occupancy(const hbp_format_t *f, int *per_sm, int *warps_per_cta) {
     HBP_STREAM_DISPATCH(occupancy_of, V, EXACT, false, false, false, f, per_sm, warps_per_cta)
 }
 
+// x_hot[s] = x[hot_cols[s]]: four slots per thread (one 16-byte load of
+// hot_cols, four independent gathers in flight); hot_cols / x_hot are
+// 16-byte aligned (torch allocations), a tail of < 4 slots is done singly
 template <typename V>
 __global__ void k_hot_gather(const V *__restrict__ x, const uint32_t *__restrict__ hot_cols,
                              int64_t n_hot, V *__restrict__ x_hot) {
-    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s < n_hot) x_hot[s] = __ldg(x + hot_cols[s]);
+    const int64_t n4 = n_hot >> 2;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+        const uint4 c = __ldcs(reinterpret_cast<const uint4 *>(hot_cols) + i);
+        const V v0 = __ldg(x + c.x), v1 = __ldg(x + c.y), v2 = __ldg(x + c.z), v3 = __ldg(x + c.w);
+        V *o = x_hot + 4 * i;
+        o[0] = v0, o[1] = v1, o[2] = v2, o[3] = v3;
+    }
+    const int64_t t = (n4 << 2) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n_hot && t < (n4 << 2) + 4) x_hot[t] = __ldg(x + hot_cols[t]);
 }
 
 template <typename V>
 int hot_gather(const void *x, const uint32_t *hot_cols, int64_t n_hot, void *x_hot,
                cudaStream_t st) {
     if (n_hot == 0) return HBP_OK;
-    k_hot_gather<V><<<(unsigned)((n_hot + 255) / 256), 256, 0, st>>>(
-        (const V *)x, hot_cols, n_hot, (V *)x_hot);
+    if (((uintptr_t)hot_cols & 15) || ((uintptr_t)x_hot & 15)) return HBP_E_ARG;
+    k_hot_gather<V><<<grid_for((n_hot + 3) / 4, 256), 256, 0, st>>>((const V *)x, hot_cols,
+                                                                    n_hot, (V *)x_hot);
     return (int)cudaGetLastError();
 }
 

@@ -239,8 +239,9 @@ def test_packed_bitwise_equals_unstaged(mat, dtype, n_hot, workers):
 
 @pytest.mark.parametrize("sample", [None, 1000])
 def test_packed_metadata(mat, monkeypatch, sample):
-    """hot_cols lists exactly the used columns (heaviest first by the -- maybe
-    sampled -- ranking); scol decodes back to col."""
+    """hot_cols = the n_hot heaviest columns (the ranking's order), then every
+    other used column ascending -- exactly the used ones, from exact
+    presence even when the ranking is sampled; scol decodes back to col."""
     rows, cols, r, c, v = mat
     if sample is not None:  # force the sampled ranking + exact presence pass
         monkeypatch.setattr(H.HbpMatrix, "RANK_SAMPLE", sample)
@@ -249,16 +250,16 @@ def test_packed_metadata(mat, monkeypatch, sample):
     used = np.unique(c)
     n_used = hc.n_hot + hc.n_warm
     hot_cols = hc.hot_cols.cpu().numpy().astype(np.int64)
-    assert n_used == used.size == hot_cols.size
+    assert hc.n_hot == 64 and n_used == used.size == hot_cols.size
     np.testing.assert_array_equal(np.sort(hot_cols), used)
+    _, order = hbp.column_ranking()
+    np.testing.assert_array_equal(hot_cols[:64], order[:64].cpu().numpy())
+    assert np.all(np.diff(hot_cols[64:]) > 0)
     col = hbp.col.cpu().numpy().astype(np.int64)
     sc = hc.scol[:hbp.nnz].cpu().numpy().astype(np.uint32).astype(np.int64)
     hot = (sc & FLAG) != 0
     dec = np.where(hot, hot_cols[sc & (FLAG - 1)], hot_cols[np.minimum(hc.n_hot + sc, n_used - 1)])
     np.testing.assert_array_equal(dec, col)
-    if sample is None:
-        deg = np.bincount(c, minlength=cols)
-        assert np.all(np.diff(deg[hot_cols]) <= 0)  # degree order
 
 
 def test_packed_is_the_default_when_x_fits_l2(mat):
