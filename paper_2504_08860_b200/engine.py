@@ -213,14 +213,15 @@ class SpmvOperator:
             n = min(cap if n_hot is None else min(n_hot, cap), hbp.cols) & ~3
             if hbp.cols >= (1 << 31):
                 n = 0
-            # packed x (x within the L2 budget): every used column after the
-            # hot ones read from a degree-ordered compact copy, so the heavy
-            # columns share L2 lines (cfg2 1.100 -> 1.027 ms, bitwise equal);
-            # past L2 the warm tier (already degree-ordered) stays
+            # packed x: the non-hot gathers read a compact copy of the USED
+            # columns (cfg2: 29 MB instead of 64) when x fits the L2 budget;
+            # past it the warm tier stays (cfg5 4.94 vs 5.23 ms packed; cfg2d,
+            # f64: 1.52 vs 1.71 ms packed) -- DESIGN.md §4
+            stage = n > 0 and (hot is not None or hbp.column_share(n) >= self.HOT_MIN_SHARE)
             if packed_x is None:
                 env = os.environ.get("HBP_PACKED_X")
                 packed_x = (env == "1") if env is not None else (fits and wb == 0)
-            if n > 0 and (hot is not None or hbp.column_share(n) >= self.HOT_MIN_SHARE):
+            if stage:
                 if packed_x:
                     hc = hbp.hot_columns(n_hot, packed=True)
                 else:
