@@ -637,6 +637,9 @@ __global__ void __launch_bounds__(NT, MINB)
     Smem &S = reinterpret_cast<Smem *>(smem_raw)[wib];
     V *const hot = reinterpret_cast<V *>(smem_raw + sizeof(Smem) * kWarps);
     if constexpr (HOT) {  // stage x at the hot columns (b.x_hot, hbp_hot_gather)
+        // launched as a programmatic dependent of k_hot_gather: everything
+        // above ran while the gather finished; its x_hot is visible after this
+        asm volatile("griddepcontrol.wait;" ::: "memory");
         const int32_t nv = (int32_t)(f.n_hot * (int64_t)sizeof(V) / 16);
         const uint4 *src = (const uint4 *)b.x_hot;
         for (int32_t i = threadIdx.x; i < nv; i += NT) reinterpret_cast<uint4 *>(hot)[i] = __ldcg(src + i);
@@ -987,6 +990,23 @@ int launch(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *
     const int ra = ensure_attributes<V, EXACT, CH, NB, MINB, XM, KT, LMIN, NT, HOT>(smem);
     if (ra) return ra;
     unsigned grid = (unsigned)((b->workers + NT / 32 - 1) / (NT / 32));
+    if (HOT) {
+        // programmatic dependent launch after k_hot_gather (which triggers its
+        // dependents on entry): this kernel's launch and CTA setup overlap the
+        // gather's tail; griddepcontrol.wait orders the x_hot reads
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(NT);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return (int)cudaLaunchKernelEx(&cfg, k_spmv_stream<V, EXACT, CH, NB, MINB, XM, KT, LMIN, NT, HOT>,
+                                       *f, *b, (const V *)x, (V *)y, partial);
+    }
     k_spmv_stream<V, EXACT, CH, NB, MINB, XM, KT, LMIN, NT, HOT><<<grid, NT, smem, st>>>(
         *f, *b, (const V *)x, (V *)y, partial);
     return (int)cudaGetLastError();
@@ -1116,6 +1136,9 @@ int occupancy(const hbp_format_t *f, int *per_sm, int *warps_per_cta) {
 template <typename V>
 __global__ void k_hot_gather(const V *__restrict__ x, const uint32_t *__restrict__ hot_cols,
                              int64_t n_hot, V *__restrict__ x_hot) {
+    // the stream kernel (a programmatic dependent) may launch now; it waits
+    // for this grid's completion before reading x_hot
+    asm volatile("griddepcontrol.launch_dependents;");
     const int64_t n4 = n_hot >> 2;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
