@@ -373,9 +373,17 @@ def _dist():
     if ws > 1:
         import torch.distributed as dist
         lr = int(os.environ.get("LOCAL_RANK", "0"))
-        torch.cuda.set_device(lr)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
-        return dist, dist.get_rank(), ws, lr
+        # HBP_DIST_BACKEND=gloo: a functional run of the multi-process path
+        # when fewer GPUs than ranks are visible (ranks share devices round
+        # robin; the numbers are then not a scaling measurement)
+        backend = os.environ.get("HBP_DIST_BACKEND", "nccl")
+        dev = lr % max(1, torch.cuda.device_count()) if backend == "gloo" else lr
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
+        return dist, dist.get_rank(), ws, dev
     torch.cuda.set_device(0)
     return None, 0, 1, 0
 
