@@ -357,6 +357,10 @@ typedef struct {
      * (hbp_group_costs); hbp_stream_slices then cuts equal COST instead of
      * equal elements (a group's fixed cost sits at its start). */
     const int64_t *cost_prefix;
+    /* 0: CTA c runs slices c*warps_per_cta .. (contiguous ranges per SM);
+     * 1: slice w runs on CTA w % ctas (each SM gets slices from all over the
+     * element array).  Results do not depend on it. */
+    int64_t warp_map;
 } hbp_balanced_t;
 
 int hbp_balanced_workers(const hbp_format_t *f, int64_t *workers);
@@ -448,19 +452,22 @@ int hbp_spmv_seg(const hbp_format_t *f, const hbp_seg_t *s, const void *x, void 
 int hbp_seg_set_variant(int v);
 
 /* Row-block owner with TMA-staged elements (hbp_spmv_rowstage.cu; W = 32):
- * a persistent CTA per row block bulk-copies the col/data
- * ranges of all the row block's nonzero blocks into shared memory with one
- * mbarrier, walks them there (x gathered from global memory) and folds the
- * block partials in ascending bc -- y bitwise that of hbp_spmv_blocks +
+ * a persistent CTA per row block bulk-copies the col/data ranges of all the
+ * row block's nonzero blocks -- and, with windows, each block's touched x
+ * window -- into shared memory with one mbarrier, walks them there and folds
+ * the block partials in ascending bc: y bitwise that of hbp_spmv_blocks +
  * hbp_combine.  hbp_rowstage_plan fills the per-block staging descriptors
- * desc (i64[2*nzb], rb_blk order) and caps (device u64[2]: largest staged
- * span of a row block, most nonzero blocks in a row block); pass them as
- * ecap / kmax (kmax <= 32; shared memory ecap * (4 + sizeof V) +
- * kmax * R * 8 bytes must fit one CTA). */
-int hbp_rowstage_plan(const hbp_format_t *f, int64_t *desc, unsigned long long *caps,
-                      hbp_stream_t stream);
+ * desc (i64[4*nzb], rb_blk order) and caps (device u64[3]: largest staged
+ * element span of a row block, most nonzero blocks in a row block, largest
+ * staged x span); win_lo / win_hi are hbp_seg_windows' per-block column
+ * windows (nullable: no x staging).  Pass ecap / kmax / xcap (xcap 0: x
+ * gathered from global memory; > 0 needs a 16-byte aligned x); kmax <= 32,
+ * shared memory ecap * (4 + sizeof V) + kmax * R * 8 + xcap * sizeof V must
+ * fit one CTA. */
+int hbp_rowstage_plan(const hbp_format_t *f, const int32_t *win_lo, const int32_t *win_hi,
+                      int64_t *desc, unsigned long long *caps, hbp_stream_t stream);
 int hbp_spmv_rowstage(const hbp_format_t *f, const int64_t *desc, const void *x, void *y,
-                      int64_t ecap, int64_t kmax, hbp_stream_t stream);
+                      int64_t ecap, int64_t kmax, int64_t xcap, hbp_stream_t stream);
 /* engine.py:196-201 combine over nonzero blocks only, ascending bc
  * (bitwise equal to the dense combine); rows of row blocks with
  * no nonzero block get +0.0. */

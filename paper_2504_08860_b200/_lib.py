@@ -64,7 +64,8 @@ class BalancedT(ctypes.Structure):
                 ("cut_end", c_vp), ("counters", c_vp), ("x_hot", c_vp),
                 ("slice_lo", c_vp), ("slice_g", c_vp), ("rb_done", c_vp), ("y_sumsq", c_vp),
                 ("hub_min", c_i64), ("pieces", c_i64), ("fixed_elems", c_i64),
-                ("ticket", c_vp), ("warp_ns", c_vp), ("cost_prefix", c_vp)]
+                ("ticket", c_vp), ("warp_ns", c_vp), ("cost_prefix", c_vp),
+                ("warp_map", c_i64)]
 
 
 # name -> argtypes (all return int status)
@@ -95,9 +96,9 @@ _SIGS = {
     "hbp_sort_perm": [c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp],
     "hbp_merge_comparisons": [c_vp, c_i64, c_vp, c_vp],
     "hbp_group_costs": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp],
-    "hbp_rowstage_plan": [c_vp, c_vp, c_vp, c_vp],
+    "hbp_rowstage_plan": [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
     "hbp_hot_remap_packed": [c_vp, c_i64, c_vp, c_i64, c_vp, c_vp],
-    "hbp_spmv_rowstage": [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp],
+    "hbp_spmv_rowstage": [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp],
     "hbp_gather_dense_perm": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp],
     "hbp_slot_lengths": [c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp,
                          c_vp],

@@ -645,7 +645,8 @@ __global__ void __launch_bounds__(NT, MINB)
         for (int32_t i = threadIdx.x; i < nv; i += NT) reinterpret_cast<uint4 *>(hot)[i] = __ldcg(src + i);
         __syncthreads();
     }
-    const int64_t w0 = (int64_t)blockIdx.x * kWarps + wib;
+    const int64_t w0 = b.warp_map ? (int64_t)wib * gridDim.x + blockIdx.x
+                                  : (int64_t)blockIdx.x * kWarps + wib;
     const int64_t Nw = b.workers;
     if (w0 >= Nw) return;
     if (b.warp_ns && lane == 0) b.warp_ns[2 * w0] = globaltimer_ns();

@@ -248,6 +248,7 @@ class SpmvOperator:
             if self.hub_min < 0:
                 raise ValueError("hub_min must be >= 0")
             self.bal.hub_min = self.hub_min
+            self.bal.warp_map = int(os.environ.get("HBP_WARP_MAP", "0"))
             # competitive pieces (stream schedule): (fixed fraction of the
             # elements as one static piece per warp, competitive pieces per
             # warp for the rest), e.g. "0.7:2"; off by default
@@ -377,28 +378,45 @@ class SpmvOperator:
             raise ValueError("slice_cost needs three non-negative weights")
         return w
 
-    ROWSTAGE_SMEM = 200 * 1024  # one CTA's staged elements + partials at most
+    ROWSTAGE_SMEM = 200 * 1024  # one CTA's staged elements + partials (+ x windows) at most
+    ROWSTAGE_X_SMEM = 72 * 1024  # x windows staged only while the CTA stays this small
 
     @classmethod
     def _rowstage_caps(cls, hbp: HbpMatrix, f):
-        """(ecap, kmax) of the TMA-staged row-block schedule (hbp_rowstage_caps),
-        cached on the matrix; None when W != 32 or a row block's staged
-        elements and partials exceed ROWSTAGE_SMEM."""
+        """(ecap, kmax, xcap) of the TMA-staged row-block schedule
+        (hbp_rowstage_plan over hbp_seg_windows' column windows), cached on
+        the matrix; xcap = 0 (x gathered from global memory) when staging
+        the windows would grow the CTA past ROWSTAGE_X_SMEM; None when
+        W != 32 or a row block exceeds ROWSTAGE_SMEM."""
         if hbp.config.warp_size != 32:
             return None
         if "rowstage_caps" not in hbp._ops:
             dev = hbp.data.device
-            caps = torch.zeros(2, dtype=torch.int64, device=dev)
-            desc = torch.zeros(max(1, 2 * hbp.nzb), dtype=torch.int64, device=dev)
-            L.call("hbp_rowstage_plan", ctypes.byref(f), L.P(desc), L.P(caps), L.stream())
-            ecap, kmax = (int(v) for v in caps.cpu())
-            hbp._ops["rowstage_caps"] = (max(4, ecap), max(1, kmax))
+            lo = hi = None
+            if hbp.nzb:
+                lo = torch.empty(hbp.nzb, dtype=torch.int32, device=dev)
+                hi = torch.empty(hbp.nzb, dtype=torch.int32, device=dev)
+                cap = torch.zeros(1, dtype=torch.int64, device=dev)
+                L.call("hbp_seg_windows", ctypes.byref(f), L.P(lo), L.P(hi), L.P(cap),
+                       L.stream())
+            caps = torch.zeros(3, dtype=torch.int64, device=dev)
+            desc = torch.zeros(max(1, 4 * hbp.nzb), dtype=torch.int64, device=dev)
+            L.call("hbp_rowstage_plan", ctypes.byref(f), L.P(lo) if lo is not None else None,
+                   L.P(hi) if hi is not None else None, L.P(desc), L.P(caps), L.stream())
+            ecap, kmax, xcap = (int(v) for v in caps.cpu())
+            hbp._ops["rowstage_caps"] = (max(4, ecap), max(1, kmax), xcap)
             hbp._ops["rowstage_desc"] = desc
-        ecap, kmax = hbp._ops["rowstage_caps"]
-        need = ecap * (4 + hbp.data.element_size()) + kmax * hbp.config.row_height * 8
+        ecap, kmax, xcap = hbp._ops["rowstage_caps"]
+        esz = hbp.data.element_size()
+        need = ecap * (4 + esz) + kmax * hbp.config.row_height * 8
         if kmax > 32 or need > cls.ROWSTAGE_SMEM:
             return None
-        return ecap, kmax
+        # x windows staged too: measured slower on cfg1 (27.4 vs 24.1 us: the
+        # windows hold 2.5x the columns the walk reads and cost CTAs per SM),
+        # so opt-in (HBP_ROWSTAGE_X=1)
+        if os.environ.get("HBP_ROWSTAGE_X", "0") != "1" or need + xcap * esz > cls.ROWSTAGE_X_SMEM:
+            xcap = 0
+        return ecap, kmax, xcap
 
     def _seg_setup(self, hbp: HbpMatrix, f, workers) -> "L.SegT":
         """Column windows of the nonzero blocks (hbp_seg_windows, cached on
@@ -491,9 +509,11 @@ class SpmvOperator:
             L.call("hbp_spmv_rowblock", ctypes.byref(f), L.P(x), L.P(y), s)
             return y
         if self.schedule == "rowstage":
-            ecap, kmax = self.rowstage_caps
+            ecap, kmax, xcap = self.rowstage_caps
+            if x.data_ptr() % 16:
+                xcap = 0  # the x windows' bulk copies need a 16-byte aligned x
             L.call("hbp_spmv_rowstage", ctypes.byref(f), L.P(self._rowstage_desc), L.P(x),
-                   L.P(y), L.c_i64(ecap), L.c_i64(kmax), s)
+                   L.P(y), L.c_i64(ecap), L.c_i64(kmax), L.c_i64(xcap), s)
             return y
         if self.direct:
             self._blocks(f, x, None, y, s)

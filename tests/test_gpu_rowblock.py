@@ -200,3 +200,29 @@ def test_rowstage_rejects_oversized_row_blocks(monkeypatch):
     hbp = _hbp(rows, cols, r, c, rng.uniform(-1, 1, r.size), C=4096, R=512)
     with pytest.raises(ValueError, match="shared memory"):
         H.SpmvOperator(hbp, schedule="rowstage")
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("rows,cols,C,R", [(5000, 5000, 512, 512), (2000, 2000, 70, 96),
+                                          (3001, 9000, 1000, 64)])
+def test_rowstage_x_windows_bitwise(dtype, rows, cols, C, R, monkeypatch):
+    """hbp_spmv_rowstage with each block's x window staged by TMA (opt-in,
+    HBP_ROWSTAGE_X=1; unaligned window ends copied by hand) == plan bitwise."""
+    monkeypatch.setenv("HBP_ROWSTAGE_X", "1")
+    monkeypatch.setattr(H.SpmvOperator, "ROWSTAGE_X_SMEM", 200 * 1024)
+    rng = np.random.default_rng(rows + 7)
+    lens = rng.poisson(6, rows)
+    r = np.repeat(np.arange(rows), lens)
+    c = np.concatenate([rng.choice(cols, k, replace=False) for k in lens])
+    v = rng.uniform(-1, 1, r.size).astype(dtype)
+    hbp = _hbp(rows, cols, r, c, v, C, R, 32)
+    x = torch.as_tensor(rng.uniform(-1, 1, cols).astype(dtype), device="cuda")
+    op = H.SpmvOperator(hbp, schedule="rowstage")
+    assert op.rowstage_caps[2] > 0
+    y = op(x).cpu().numpy()
+    y_plan = H.SpmvOperator(hbp, schedule="plan")(x).cpu().numpy()
+    np.testing.assert_array_equal(y.view(np.uint8), y_plan.view(np.uint8))
+    # an x view at an odd offset falls back to global gathers (same bits)
+    xb = torch.empty(cols + 1, dtype=x.dtype, device="cuda")
+    xb[1:] = x
+    np.testing.assert_array_equal(op(xb[1:]).cpu().numpy(), y)
