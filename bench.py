@@ -355,6 +355,30 @@ def numba_reference(cfg_name: str, steps: int, warmup: int, seed: int = 0):
                                    total=(t4 - t0) * 1e3))
 
 
+def format_bytes(op, hbp, esz: int) -> dict:
+    """SURVEY §8(d) "format bytes": what this schedule must move per SpMV on
+    top of the elements -- slot / group metadata, the phase stream, x
+    staging copies and the partial round trip -- as an estimate next to the
+    algorithmic bytes (x once, y once)."""
+    R = hbp.config.row_height
+    ngroups = hbp.nzb * (R // 32)
+    slots = hbp.nzb * R
+    elements = hbp.nnz * (4 + esz)
+    if op.schedule == "stream":
+        nph = int(hbp.phase_ptr[-1].item()) if hbp.phases is not None else 0
+        meta = ngroups * 16 + slots * 4 + nph * 8  # group_start + phase_ptr, perm, phases
+    else:
+        meta = ngroups * 8 + slots * 8  # group_start, slot_len + perm
+    staging = 0
+    if getattr(op, "hot", None) is not None:
+        n = op.hot.n_hot + op.hot.n_warm
+        staging = n * (4 + 2 * esz)  # hot_cols + gathered x read + copy written
+    partial = 0 if op.partial is None else op.partial.numel() * 8 * 2
+    total = elements + meta + staging + partial + (hbp.cols + hbp.rows) * esz
+    return {"elements": elements, "metadata": meta, "x_staging": staging,
+            "partial_round_trip": partial, "total": total}
+
+
 def _cpu_model() -> str:
     try:
         with open("/proc/cpuinfo") as fh:
@@ -690,6 +714,7 @@ def run_gpu(args):
     if os.path.exists(prof):
         with open(prof) as fh:
             traffic = json.load(fh).get(args.config, {}).get("dram_bytes_per_launch")
+    fmt_bytes = format_bytes(op, hbp, esz)
     launches_step = sop.launches_per_call + (2 if iterated else 0)  # + sumsq (2 launches)
     groof = None
     if hbp.num_col_blocks == 1:  # random columns over all of x: gather-bound, not HBM-bound
@@ -734,7 +759,8 @@ def run_gpu(args):
         "roofline": {"bound": "hbm", "binding": "l1_gather" if groof else "hbm",
                      "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "algorithmic_bytes": b_alg, "peak_source": peak_src,
+                     "algorithmic_bytes": b_alg, "format_bytes": fmt_bytes,
+                     "peak_source": peak_src,
                      "kernel_ms": round(spmv_ms, 5),
                      "kernel": f"k_spmv_{op.schedule}" + (" (+ hot-column gather)" if op.hot is not None else "")
                      + ("" if op.launches_per_call == 1 + (op.hot is not None) else " (+ combine/zero launch)")},
