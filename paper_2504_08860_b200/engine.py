@@ -379,6 +379,7 @@ class SpmvOperator:
         return w
 
     ROWSTAGE_SMEM = 200 * 1024  # one CTA's staged elements + partials (+ x windows) at most
+    ROWSTAGE_AUTO_SMEM = 64 * 1024  # auto choice only where >= 3 CTAs fit an SM (cfg1: 44 KB)
     ROWSTAGE_X_SMEM = 72 * 1024  # x windows staged only while the CTA stays this small
 
     @classmethod
@@ -465,8 +466,9 @@ class SpmvOperator:
                 # f64 with W = 32: the TMA-staged form when a row block's
                 # elements fit a CTA (cfg1 28.7 vs 36.9 us); f32 banded
                 # matrices keep rowblock (0.101 vs 0.109 ms at 35M nnz)
-                if (hbp.dtype == torch.float64 and
-                        cls._rowstage_caps(hbp, L.FormatT.from_buffer_copy(hbp.format_struct()))):
+                caps = (cls._rowstage_caps(hbp, L.FormatT.from_buffer_copy(hbp.format_struct()))
+                        if hbp.dtype == torch.float64 else None)
+                if caps is not None and (caps[0] * 12 + caps[1] * R * 8 <= cls.ROWSTAGE_AUTO_SMEM):
                     return "rowstage"
                 return "rowblock"
         if (hbp.config.warp_size == 32 and hbp.num_col_blocks > 1 and hbp.nzb
