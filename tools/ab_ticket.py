@@ -41,6 +41,9 @@ ops = {}
 for r in runs:
     if r == "static":  # the default (cost-balanced slices in fast mode)
         ops[r] = H.SpmvOperator(hbp, schedule="stream")
+    elif r.startswith("hub"):  # f64 hub-row path, optional cost weights: hub or hub:48,20,40
+        ops[r] = H.SpmvOperator(hbp, schedule="stream", hub_min="auto",
+                                slice_cost=r[4:] if ":" in r else None)
     elif r == "px":  # packed x: degree-ordered compact copy of the used columns
         ops[r] = H.SpmvOperator(hbp, schedule="stream", packed_x=True)
     elif r == "eq":  # equal-element slices
