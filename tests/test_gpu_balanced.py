@@ -284,5 +284,7 @@ def test_stream_cost_weights_default_and_validation():
     h64 = _hbp(rows, cols, r, c, v, C=cols)
     assert H.SpmvOperator(h32, schedule="stream").slice_cost == H.SpmvOperator.SLICE_COST
     assert H.SpmvOperator(h64, schedule="stream").slice_cost is None  # exact: equal elements
+    assert H.SpmvOperator(h64, schedule="stream", hub_min=1000).slice_cost == \
+        H.SpmvOperator.SLICE_COST  # the hub-row path balances by cost too
     with pytest.raises(ValueError, match="weights"):
         H.SpmvOperator(h32, schedule="stream", slice_cost="1,2")
