@@ -397,7 +397,9 @@ int hbp_spmv_stream(const hbp_format_t *f, const hbp_balanced_t *b, const void *
  *   hbp_col_degree:  deg[c] += #{e = i * stride : col[e] == c} (deg zero-filled;
  *                    stride 1 = exact degrees, larger = a deterministic sample).
  *   hbp_hot_capacity: largest n_hot the stream kernel can stage for dtype
- *                    (warm != 0: for a launch that also has a warm tier).
+ *                    (mode 0: hot tier only; 1: with a warm tier; 2: with a
+ *                    packed x, HBP_FLAG_PACKED_X -- its L2-resident gathers
+ *                    leave L1 room for a larger tier).
  *   hbp_hot_slots:   slot_of[hot_cols[s]] = s (slot_of filled with -1).
  *   hbp_hot_remap:   scol[e] = slot s = slot_of[col[e]]: s < n_hot -> HBP_HOT_FLAG | s,
  *                    n_hot <= s -> HBP_WARM_FLAG | (s - n_hot), none -> col[e].
@@ -410,7 +412,7 @@ int hbp_spmv_stream(const hbp_format_t *f, const hbp_balanced_t *b, const void *
  * (cfg5: 256 MB) the heavy columns stay L2-resident in a dense array. */
 int hbp_col_degree(const uint32_t *col, int64_t nnz, int64_t stride, uint32_t *deg,
                    hbp_stream_t stream);
-int hbp_hot_capacity(int dtype, int warm, int64_t *n_hot_max);
+int hbp_hot_capacity(int dtype, int mode, int64_t *n_hot_max);
 int hbp_hot_slots(const uint32_t *hot_cols, int64_t n_hot, int32_t *slot_of,
                   hbp_stream_t stream);
 int hbp_hot_remap(const uint32_t *col, int64_t nnz, const int32_t *slot_of, int64_t n_hot,

@@ -62,6 +62,7 @@ constexpr int kHotThreads = 896;   // 28 warps at 72 registers (measured best, D
 constexpr int kWarmThreads = 768;  // warm-tier launches (x beyond L2): 24 warps measured best
 constexpr size_t kHotBudgetDefault = 155 * 1024;   // hot tier only -> 164 KB carveout
 constexpr size_t kWarmBudgetDefault = 131 * 1024;  // with a warm tier -> 132 KB carveout
+constexpr size_t kPackedBudgetDefault = 185 * 1024;  // packed x -> 196 KB carveout
 
 // Column slots: a chunk's columns are needed only until its gathers are
 // issued; while chunk ready+1 is started, chunks up to ready+NB-2 are in
@@ -1200,20 +1201,26 @@ int hbp_stream_workers(const hbp_format_t *f, int64_t *workers) {
     return HBP_OK;
 }
 
-int hbp_hot_capacity(int dtype, int warm, int64_t *n_hot_max) {
-    if (!n_hot_max || (dtype != HBP_F32 && dtype != HBP_F64)) return HBP_E_ARG;
-    // f32: 155 KB (hot tier only) / 131 KB (with a warm tier) of shared memory
-    // per SM (sweeps); f64 rings are twice as large, so its
-    // staged launch takes a larger carveout
-    size_t budget = dtype == HBP_F64 ? 187 * 1024 : (warm ? kWarmBudgetDefault : kHotBudgetDefault);
+int hbp_hot_capacity(int dtype, int mode, int64_t *n_hot_max) {
+    if (!n_hot_max || (dtype != HBP_F32 && dtype != HBP_F64) || mode < 0 || mode > 2)
+        return HBP_E_ARG;
+    const bool warm = mode == 1;
+    // f32: 155 KB (hot tier only) / 131 KB (with a warm tier) / 185 KB (packed
+    // x: its gathers hit L2, so L1 needs less room -- cfg2 0.990 vs 1.007 ms,
+    // while an unpacked launch at 185 KB takes 1.40 ms) of shared memory per
+    // SM (sweeps); f64 rings are twice as large, so its staged
+    // launch takes a larger carveout
+    size_t budget = dtype == HBP_F64 ? 187 * 1024
+                    : (warm ? kWarmBudgetDefault : mode == 2 ? kPackedBudgetDefault
+                                                              : kHotBudgetDefault);
     if (const char *e = getenv("HBP_HOT_BUDGET_KB")) budget = (size_t)atoi(e) * 1024;
     int dev = 0, optin = 0;
     HBP_CUDA_TRY(cudaGetDevice(&dev));
     HBP_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     if (budget > (size_t)optin) budget = (size_t)optin;
     size_t ring = 0;
-    if (dtype == HBP_F64) hot_ring_bytes<double>(&ring, warm != 0);
-    else hot_ring_bytes<float>(&ring, warm != 0);
+    if (dtype == HBP_F64) hot_ring_bytes<double>(&ring, warm);
+    else hot_ring_bytes<float>(&ring, warm);
     const size_t sv = dtype == HBP_F64 ? 8 : 4;
     *n_hot_max = budget > ring ? (int64_t)(((budget - ring) / sv) & ~(size_t)1023) : 0;
     return HBP_OK;
@@ -1284,7 +1291,7 @@ int hbp_spmv_stream(const hbp_format_t *f, const hbp_balanced_t *b, const void *
     }
     if (staged(f)) {
         int64_t cap = 0;
-        const int rc = hbp_hot_capacity(f->dtype, warm(f), &cap);
+        const int rc = hbp_hot_capacity(f->dtype, packed(f) ? 2 : warm(f) ? 1 : 0, &cap);
         if (rc) return rc;
         if (f->n_hot > cap || (f->n_hot & 3) || !b->x_hot) return HBP_E_ARG;
         if (f->n_warm < 0 || (warm(f) && f->cols > (int64_t)1 << 30)) return HBP_E_ARG;

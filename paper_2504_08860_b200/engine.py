@@ -209,7 +209,10 @@ class SpmvOperator:
             fits = hbp.cols * hbp.data.element_size() <= L.l2_bytes() * 0.6
             wb = (0 if fits else int(os.environ.get("HBP_WARM_BYTES", self.WARM_BYTES))) \
                 if warm_bytes is None else int(warm_bytes)
-            cap = hbp.hot_capacity(warm=wb > 0 and hbp.cols <= (1 << 30))
+            if packed_x is None:
+                env = os.environ.get("HBP_PACKED_X")
+                packed_x = (env == "1") if env is not None else (fits and wb == 0)
+            cap = hbp.hot_capacity(warm=wb > 0 and hbp.cols <= (1 << 30), packed=bool(packed_x))
             n = min(cap if n_hot is None else min(n_hot, cap), hbp.cols) & ~3
             if hbp.cols >= (1 << 31):
                 n = 0
@@ -218,9 +221,6 @@ class SpmvOperator:
             # past it the warm tier stays (cfg5 4.94 vs 5.23 ms packed; cfg2d,
             # f64: 1.52 vs 1.71 ms packed) -- DESIGN.md §4
             stage = n > 0 and (hot is not None or hbp.column_share(n) >= self.HOT_MIN_SHARE)
-            if packed_x is None:
-                env = os.environ.get("HBP_PACKED_X")
-                packed_x = (env == "1") if env is not None else (fits and wb == 0)
             if stage:
                 if packed_x:
                     hc = hbp.hot_columns(n_hot, packed=True)

@@ -121,11 +121,12 @@ class HbpMatrix:
             self._fmt.phase_ptr = ptr.data_ptr()
             self._fmt.phases = phases.data_ptr()
 
-    def hot_capacity(self, warm: bool = False) -> int:
+    def hot_capacity(self, warm: bool = False, packed: bool = False) -> int:
         """Largest hot set the stream kernel can stage for this dtype (with or
         without a warm tier in the same launch)."""
         cap = L.c_i64(0)
-        L.call("hbp_hot_capacity", L.c_int(L.dtype_code(self.data.dtype)), L.c_int(int(warm)),
+        L.call("hbp_hot_capacity", L.c_int(L.dtype_code(self.data.dtype)),
+               L.c_int(2 if packed else int(warm)),
                ctypes.byref(cap))
         return int(cap.value)
 
@@ -214,7 +215,7 @@ class HbpMatrix:
         only the columns the matrix touches (cfg2: 7.36M of 16.8M, 29 MB), so
         it stays L2-resident where x thrashed; ascending order makes the
         per-SpMV refresh one coalesced sweep over x."""
-        cap = self.hot_capacity(warm=False)
+        cap = self.hot_capacity(packed=True)
         n = cap if n_hot is None else min(int(n_hot), cap)
         used, n_used = self.used_columns()
         deg, order = self.column_ranking()

@@ -144,11 +144,15 @@ def test_staged_multi_col_block(mat):
 
 def test_hot_gather_and_capacity():
     cap = L.c_i64(0)
-    for warm in (0, 1):
-        L.call("hbp_hot_capacity", L.c_int(L.HBP_F32), L.c_int(warm), ctypes.byref(cap))
-        cap32 = int(cap.value)
-        L.call("hbp_hot_capacity", L.c_int(L.HBP_F64), L.c_int(warm), ctypes.byref(cap))
+    caps = {}
+    for mode in (0, 1, 2):  # hot only, warm tier, packed x
+        L.call("hbp_hot_capacity", L.c_int(L.HBP_F32), L.c_int(mode), ctypes.byref(cap))
+        cap32 = caps[mode] = int(cap.value)
+        L.call("hbp_hot_capacity", L.c_int(L.HBP_F64), L.c_int(mode), ctypes.byref(cap))
         assert cap32 >= 4096 and int(cap.value) >= 1024 and cap32 % 1024 == 0
+    assert caps[1] < caps[0] < caps[2]
+    with pytest.raises(ValueError):
+        L.call("hbp_hot_capacity", L.c_int(L.HBP_F32), L.c_int(3), ctypes.byref(cap))
     x = torch.randn(100000, device="cuda", dtype=torch.float64)
     hot = torch.randint(0, 100000, (4096,), device="cuda", dtype=torch.int32)
     out = torch.empty(4096, device="cuda", dtype=torch.float64)

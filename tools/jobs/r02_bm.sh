@@ -1,0 +1,6 @@
+for kb in 155 185; do
+HBP_PACKED_X=0 HBP_HOT_BUDGET_KB=$kb timeout 600 python tools/ab_ticket.py --config cfg2 --runs "static" --rounds 3 --iters 10 2>&1 | tail -1 | cut -c1-120 | sed "s/^/unpacked kb=$kb /"
+done
+for kb in 155 185; do
+HBP_HOT_BUDGET_KB=$kb timeout 600 python tools/ab_ticket.py --config cfg2 --runs "static" --rounds 3 --iters 10 2>&1 | tail -1 | cut -c1-120 | sed "s/^/packed kb=$kb /"
+done
