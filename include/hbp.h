@@ -361,6 +361,16 @@ typedef struct {
      * 1: slice w runs on CTA w % ctas (each SM gets slices from all over the
      * element array).  Results do not depend on it. */
     int64_t warp_map;
+    /* Tail pieces (with pieces > workers): instead of a ticket, pieces
+     * workers..pieces-1 run as a second launch of the static kernel (one warp
+     * per piece) that depends programmatically on the first: its CTAs take
+     * SMs as the first launch's CTAs finish, so the imbalance of the static
+     * slices is filled in by the hardware's CTA scheduler.  With a cost
+     * prefix, fixed_elems is then a cost (the first fixed_elems cost units
+     * form the `workers` static pieces).  piece_base: first piece of this
+     * launch (set by the library for the second launch; 0 for callers). */
+    int64_t tail;
+    int64_t piece_base;
 } hbp_balanced_t;
 
 int hbp_balanced_workers(const hbp_format_t *f, int64_t *workers);

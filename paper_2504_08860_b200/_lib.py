@@ -65,7 +65,7 @@ class BalancedT(ctypes.Structure):
                 ("slice_lo", c_vp), ("slice_g", c_vp), ("rb_done", c_vp), ("y_sumsq", c_vp),
                 ("hub_min", c_i64), ("pieces", c_i64), ("fixed_elems", c_i64),
                 ("ticket", c_vp), ("warp_ns", c_vp), ("cost_prefix", c_vp),
-                ("warp_map", c_i64)]
+                ("warp_map", c_i64), ("tail", c_i64), ("piece_base", c_i64)]
 
 
 # name -> argtypes (all return int status)

@@ -196,10 +196,20 @@ __device__ __forceinline__ void stream_slice(const int64_t *__restrict__ gs, int
 // unit per element) reaches v * total / Nw.
 __device__ __forceinline__ int64_t cost_cut(const int64_t *__restrict__ gs,
                                             const int64_t *__restrict__ cp, int64_t ngroups,
-                                            int64_t E, int64_t v, int64_t Nw) {
+                                            int64_t E, int64_t v, int64_t Nw, int64_t np = 0,
+                                            int64_t Fc = 0) {
+    const int64_t n = np > Nw ? np : Nw;
     if (v <= 0) return 0;
-    if (v >= Nw) return E;
-    const int64_t T = (int64_t)((__int128)v * cp[ngroups] / Nw);
+    if (v >= n) return E;
+    const int64_t tot = cp[ngroups];
+    int64_t T;
+    if (np > Nw) {  // Nw pieces of the first Fc cost units, then np - Nw of the rest
+        const int64_t F = Fc < 0 ? 0 : (Fc > tot ? tot : Fc);
+        T = v <= Nw ? (int64_t)((__int128)v * F / Nw)
+                    : F + (int64_t)((__int128)(v - Nw) * (tot - F) / (np - Nw));
+    } else {
+        T = (int64_t)((__int128)v * tot / Nw);
+    }
     int64_t lo = 0, hi = ngroups;  // largest g < ngroups with cp[g] <= T
     while (hi - lo > 1) {
         const int64_t m = (lo + hi) >> 1;
@@ -224,8 +234,8 @@ __global__ void k_stream_slices(const int64_t *__restrict__ gs, int64_t ngroups,
     if (w >= n) return;
     int64_t lo, hi, g;
     if (cp) {
-        const int64_t c_lo = cost_cut(gs, cp, ngroups, E, w, Nw);
-        const int64_t c_hi = cost_cut(gs, cp, ngroups, E, w + 1, Nw);
+        const int64_t c_lo = cost_cut(gs, cp, ngroups, E, w, Nw, np, F);
+        const int64_t c_hi = cost_cut(gs, cp, ngroups, E, w + 1, Nw, np, F);
         stream_slice_at(gs, ngroups, E, c_lo, c_hi, exact, hub_min, &lo, &hi, &g);
     } else {
         stream_slice(gs, ngroups, E, w, Nw, exact, hub_min, &lo, &hi, &g, np, F);
@@ -640,12 +650,17 @@ __global__ void __launch_bounds__(NT, MINB)
     if constexpr (HOT) {  // stage x at the hot columns (b.x_hot, hbp_hot_gather)
         // launched as a programmatic dependent of k_hot_gather: everything
         // above ran while the gather finished; its x_hot is visible after this
-        asm volatile("griddepcontrol.wait;" ::: "memory");
+        // (a tail launch, piece_base > 0, depends on the main launch, which only
+        // triggers it after this wait -- so it must not wait for that launch)
+        if (b.piece_base == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
         const int32_t nv = (int32_t)(f.n_hot * (int64_t)sizeof(V) / 16);
         const uint4 *src = (const uint4 *)b.x_hot;
         for (int32_t i = threadIdx.x; i < nv; i += NT) reinterpret_cast<uint4 *>(hot)[i] = __ldcg(src + i);
         __syncthreads();
     }
+    // the tail launch (if any) may be scheduled now: its CTAs take the SMs
+    // this launch's CTAs free
+    if (b.tail && b.piece_base == 0) asm volatile("griddepcontrol.launch_dependents;");
     const int64_t w0 = b.warp_map ? (int64_t)wib * gridDim.x + blockIdx.x
                                   : (int64_t)blockIdx.x * kWarps + wib;
     const int64_t Nw = b.workers;
@@ -654,7 +669,8 @@ __global__ void __launch_bounds__(NT, MINB)
     // XM & 8192: competitive pieces -- warp w0 runs piece w0 (its fixed chunk),
     // then claims pieces Nw.. with the ticket (engine.py:155-165 on slices)
     constexpr bool TK = (XM & 8192) != 0;
-    const int64_t Np = TK ? b.pieces : Nw;
+    // total pieces (the slice table's size): competitive (TK) or tail pieces
+    const int64_t Np = (TK || b.pieces > Nw) ? b.pieces : Nw;
     const int32_t R = (int32_t)f.row_height, gpb = R / 32;
     const int64_t ngroups = f.nzb * gpb;
     const int64_t E = f.nnz;
@@ -663,7 +679,7 @@ __global__ void __launch_bounds__(NT, MINB)
     const uint2 *__restrict__ phs = (const uint2 *)f.phases;
     const uint32_t *__restrict__ permp = (const uint32_t *)f.perm;
 
-    for (int64_t w = w0, np_done = 0;; ++np_done) {
+    for (int64_t w = w0 + (TK ? 0 : b.piece_base), np_done = 0;; ++np_done) {
     int64_t c_lo, c_hi, g;
     if (b.slice_lo) {  // precomputed (hbp_stream_slices): no binary searches here
         c_lo = b.slice_lo[w];
@@ -986,16 +1002,40 @@ int ensure_attributes(size_t smem) {
 
 template <typename V, bool EXACT, int CH, int NB, int MINB, int XM, int KT, int LMIN, int NT,
           bool HOT>
+int launch_one(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y,
+               double *partial, cudaStream_t st, bool pdl);
+
+template <typename V, bool EXACT, int CH, int NB, int MINB, int XM, int KT, int LMIN, int NT,
+          bool HOT>
 int launch(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y,
            double *partial, cudaStream_t st) {
+    // staged launches follow k_hot_gather as programmatic dependents
+    const int r = launch_one<V, EXACT, CH, NB, MINB, XM, KT, LMIN, NT, HOT>(f, b, x, y, partial,
+                                                                           st, HOT);
+    if (r || !(b->tail && b->pieces > b->workers)) return r;
+    // tail pieces: a second launch, one warp per piece, depending on the main
+    // one programmatically (it triggers once its own dependencies are met)
+    hbp_balanced_t b2 = *b;
+    b2.piece_base = b->workers;
+    b2.workers = b->pieces - b->workers;
+    b2.warp_ns = nullptr;
+    return launch_one<V, EXACT, CH, NB, MINB, XM, KT, LMIN, NT, HOT>(f, &b2, x, y, partial, st,
+                                                                     true);
+}
+
+template <typename V, bool EXACT, int CH, int NB, int MINB, int XM, int KT, int LMIN, int NT,
+          bool HOT>
+int launch_one(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y,
+               double *partial, cudaStream_t st, bool pdl) {
     const size_t smem = ring_smem<V, CH, NB, NT>() + (HOT ? (size_t)f->n_hot * sizeof(V) : 0);
     const int ra = ensure_attributes<V, EXACT, CH, NB, MINB, XM, KT, LMIN, NT, HOT>(smem);
     if (ra) return ra;
     unsigned grid = (unsigned)((b->workers + NT / 32 - 1) / (NT / 32));
-    if (HOT) {
+    if (pdl) {
         // programmatic dependent launch after k_hot_gather (which triggers its
         // dependents on entry): this kernel's launch and CTA setup overlap the
-        // gather's tail; griddepcontrol.wait orders the x_hot reads
+        // gather's tail; griddepcontrol.wait orders the x_hot reads (a tail
+        // launch depends on the main launch the same way)
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(grid);
         cfg.blockDim = dim3(NT);
@@ -1172,7 +1212,7 @@ int run(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y, 
         if (packed(f)) x = (const V *)b->x_hot + f->n_hot;  // gathers read the packed copy
     }
     HBP_STREAM_DISPATCH(launch, V, EXACT, (b->rb_done != nullptr), (b->hub_min > 0),
-                        (b->pieces > b->workers), f, b, x, y, partial, st)
+                        (b->pieces > b->workers && !b->tail), f, b, x, y, partial, st)
 }
 
 }  // namespace
@@ -1246,12 +1286,12 @@ int hbp_stream_slices(const hbp_format_t *f, const hbp_balanced_t *b, hbp_stream
     const int64_t ngroups = f->nzb * (f->row_height / 32);
     const bool exact = f->exact != 0 || f->dtype == HBP_F64;
     const int64_t n = b->pieces > b->workers ? b->pieces : b->workers;
-    if (b->pieces > b->workers && (b->fixed_elems < 0 || b->fixed_elems > f->nnz))
+    if (b->pieces > b->workers && (b->fixed_elems < 0 ||
+                                   (!b->cost_prefix && b->fixed_elems > f->nnz)))
         return HBP_E_ARG;
     k_stream_slices<<<(unsigned)((n + 127) / 128), 128, 0, as_stream(stream)>>>(
         f->group_start, ngroups, f->nnz, b->workers, exact, exact ? b->hub_min : 0, b->slice_lo,
-        b->slice_g, b->pieces, b->fixed_elems,
-        b->pieces > b->workers ? nullptr : b->cost_prefix);
+        b->slice_g, b->pieces, b->fixed_elems, b->cost_prefix);
     return (int)cudaGetLastError();
 }
 
@@ -1284,9 +1324,11 @@ int hbp_spmv_stream(const hbp_format_t *f, const hbp_balanced_t *b, const void *
     if ((!exact || b->hub_min > 0) && (!b->part_head || !b->part_tail || !b->counters))
         return HBP_E_ARG;
     if (b->hub_min < 0) return HBP_E_ARG;
-    if (b->pieces > b->workers) {  // competitive pieces
-        if (!b->slice_lo || !b->slice_g || !b->ticket || b->rb_done || b->hub_min > 0)
+    if (b->piece_base != 0) return HBP_E_ARG;  // set by the library only
+    if (b->pieces > b->workers) {  // competitive or tail pieces
+        if (!b->slice_lo || !b->slice_g || (!b->tail && !b->ticket) || b->rb_done)
             return HBP_E_ARG;
+        if (!b->tail && b->hub_min > 0) return HBP_E_ARG;
         if ((f->nnz + b->pieces - 1) / b->pieces > (int64_t)1 << 30) return HBP_E_UNSUPPORTED;
     }
     if (staged(f)) {

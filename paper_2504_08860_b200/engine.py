@@ -187,7 +187,7 @@ class SpmvOperator:
                  fixed_fraction: float | None = None, schedule: str | None = None,
                  hot: bool | int | None = None, warm_bytes: int | None = None,
                  hub_min: int | str | None = None, ticket=None, slice_cost=None,
-                 packed_x: bool | None = None):
+                 packed_x: bool | None = None, tail=None):
         self.hbp = hbp
         dev = hbp.data.device
         if schedule is None:
@@ -196,6 +196,7 @@ class SpmvOperator:
             raise ValueError(f"the {schedule} schedule needs warp_size == 32")
         self.schedule = schedule
         self.slice_cost = None
+        self.tail = None
         if schedule == "stream":
             hbp.ensure_phases()
         # private descriptor: hot-column staging is a property of this operator
@@ -255,6 +256,22 @@ class SpmvOperator:
             if ticket is None:
                 ticket = os.environ.get("HBP_STREAM_TICKET") or None
             self.pieces = self.workers
+            # tail pieces (stream schedule): "f:m" -- the first f of the cost as
+            # one static slice per warp, the rest as m * workers pieces run by a
+            # second, programmatically dependent launch whose CTAs fill the SMs
+            # the first launch frees
+            if tail is None:
+                tail = os.environ.get("HBP_STREAM_TAIL") or None
+            self.tail = None
+            if tail and schedule == "stream" and hbp.nzb and not ticket:
+                tf, tm = (tail.split(":") if isinstance(tail, str) else tail)
+                tf, tm = float(tf), float(tm)
+                if not (0.0 < tf <= 1.0 and tm > 0):
+                    raise ValueError("tail needs a fixed fraction in (0, 1] and pieces > 0")
+                self.tail = (tf, tm)
+                self.pieces = self.workers + max(1, int(tm * self.workers + 0.5))
+                self.bal.pieces = self.pieces
+                self.bal.tail = 1
             if ticket and schedule == "stream" and hbp.nzb and not self.hub_min:
                 ff, per = (ticket.split(":") if isinstance(ticket, str) else ticket)
                 ff, per = float(ff), float(per)
@@ -293,18 +310,23 @@ class SpmvOperator:
                 self.slice_lo_t = sl
                 self.bal.slice_lo, self.bal.slice_g = sl.data_ptr(), sg.data_ptr()
                 self.slice_cost = self._cost_weights(f, slice_cost)
-                if self.slice_cost and self.pieces == self.workers:
+                if self.slice_cost and (self.pieces == self.workers or self.tail):
                     ng = hbp.nzb * (hbp.config.row_height // 32)
                     cost = torch.empty(ng + 1, dtype=torch.int64, device=dev)
                     cost[ng] = 0
                     L.call("hbp_group_costs", ctypes.byref(f), *map(L.c_i64, self.slice_cost),
                            L.P(cost), L.stream())
                     cp = L.exclusive_sum(cost)
-                    if int(cp[-1].item()) // self.workers < (1 << 30):  # 32-bit slice offsets
+                    total = int(cp[-1].item())
+                    if total // self.workers < (1 << 30):  # 32-bit slice offsets
                         self._scratch.append(cp)
                         self.bal.cost_prefix = cp.data_ptr()
+                        if self.tail:  # the static part in cost units
+                            self.bal.fixed_elems = int(self.tail[0] * total + 0.5)
                     else:
                         self.slice_cost = None
+                if self.tail and not self.bal.cost_prefix:  # equal elements
+                    self.bal.fixed_elems = int(self.tail[0] * hbp.nnz + 0.5)
                 L.call("hbp_stream_slices", ctypes.byref(f), ctypes.byref(self.bal), L.stream())
         elif schedule == "seg":
             self.seg = self._seg_setup(hbp, f, workers)
@@ -347,6 +369,8 @@ class SpmvOperator:
         self.sched.ticket = self.ticket.data_ptr()
         self.launches_per_call = 1 if schedule in ("rowblock", "rowstage") else (1 + (1 if self.has_empty_row_blocks or not (
             self.direct or self.fused_combine) else 0) + (1 if self.hot is not None else 0))
+        if self.tail:
+            self.launches_per_call += 1  # the tail pieces' dependent launch
         self._graph = None
         self._gx = self._gy = None
 

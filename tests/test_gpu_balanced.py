@@ -288,3 +288,52 @@ def test_stream_cost_weights_default_and_validation():
         H.SpmvOperator.SLICE_COST  # the hub-row path balances by cost too
     with pytest.raises(ValueError, match="weights"):
         H.SpmvOperator(h32, schedule="stream", slice_cost="1,2")
+
+
+TAILS = ["0.95:1", "0.8:2", "0.5:4", "1.0:1"]
+
+
+@pytest.mark.parametrize("name", [n for n in W32 if not n.startswith("kat")][:10])
+@pytest.mark.parametrize("tail", TAILS)
+@pytest.mark.parametrize("workers", [1, 5, None])
+def test_stream_tail_matches_golden(name, tail, workers):
+    """Tail pieces (a second, programmatically dependent launch over the last
+    pieces): f64 bitwise the reference, f32 within 1e-5, repeat calls equal."""
+    g = load_golden(name)
+    val = g["trip_val"].astype(np.float32) if g["fp32"] else g["trip_val"]
+    hbp = _hbp(g["rows"], g["cols"], g["trip_row"], g["trip_col"], val, g["C"], g["R"], g["W"],
+               g["seed"])
+    x = torch.as_tensor(g["x"].astype(np.float32) if g["fp32"] else g["x"], device="cuda")
+    op = H.SpmvOperator(hbp, workers=workers, schedule="stream", tail=tail)
+    assert op.launches_per_call >= 2
+    y = op(x).cpu().numpy()
+    for _ in range(3):
+        np.testing.assert_array_equal(op(x).cpu().numpy(), y)
+    if g["fp32"]:
+        err = O.componentwise_error(g["rows"], g["trip_row"], g["trip_col"], g["trip_val"],
+                                    g["x"], y.astype(np.float64))
+        assert err <= 1e-5
+    else:
+        np.testing.assert_array_equal(y, g["y"])
+
+
+@pytest.mark.parametrize("tail", TAILS)
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("hub", [None, 2000])
+def test_stream_tail_hot_rows(tail, dtype, hub):
+    rows, cols, r, c, v = _hot_matrix()
+    vv = v.astype(dtype)
+    x = np.random.default_rng(1).uniform(-1, 1, cols).astype(dtype)
+    hbp = _hbp(rows, cols, r, c, vv, C=cols)
+    xd = torch.as_tensor(x, device="cuda")
+    op = H.SpmvOperator(hbp, schedule="stream", tail=tail, hub_min=hub)
+    y1 = op(xd).cpu().numpy()
+    for _ in range(5):  # back to back: the dependent launch must not overtake later work
+        y2 = op(xd)
+    np.testing.assert_array_equal(y2.cpu().numpy(), y1)
+    err = O.componentwise_error(rows, r, c, vv.astype(np.float64), x.astype(np.float64),
+                                y1.astype(np.float64))
+    assert err <= (1e-12 if dtype == np.float64 else 1e-5)
+    if dtype == np.float64 and hub is None:  # exact: bitwise the static schedule
+        ref = H.SpmvOperator(hbp, schedule="stream")(xd).cpu().numpy()
+        np.testing.assert_array_equal(y1, ref)

@@ -44,6 +44,10 @@ for r in runs:
     elif r.startswith("hub"):  # f64 hub-row path, optional cost weights: hub or hub:48,20,40
         ops[r] = H.SpmvOperator(hbp, schedule="stream", hub_min="auto",
                                 slice_cost=r[4:] if ":" in r else None)
+    elif r.startswith("t="):  # tail pieces: t=0.95:1
+        ops[r] = H.SpmvOperator(hbp, schedule="stream", tail=r[2:])
+    elif r.startswith("hubt="):  # hub path + tail pieces
+        ops[r] = H.SpmvOperator(hbp, schedule="stream", hub_min="auto", tail=r[5:])
     elif r == "px":  # packed x: degree-ordered compact copy of the used columns
         ops[r] = H.SpmvOperator(hbp, schedule="stream", packed_x=True)
     elif r == "eq":  # equal-element slices
