@@ -386,11 +386,13 @@ int hbp_stream_workers(const hbp_format_t *f, int64_t *workers);
  * dependent loads, visible on small matrices). */
 int hbp_stream_slices(const hbp_format_t *f, const hbp_balanced_t *b, hbp_stream_t stream);
 /* Stream-kernel cost of every group in element units (the per-warp cost
- * model fitted to measured warp times, tools/warp_cost.py): its elements +
- * w_group + w_phase * phases + w_modular * modular-pass phases (fewer than 12
- * live lanes, more than 4 steps).  cost[ngroups]. */
-int hbp_group_costs(const hbp_format_t *f, int64_t w_group, int64_t w_phase, int64_t w_modular,
-                    int64_t *cost, hbp_stream_t stream);
+ * model fitted to measured warp times, tools/warp_cost.py): its elements -
+ * (w_hot / 64) per element staged in shared memory (HBP_HOT_FLAG in scol;
+ * cheaper gathers) + w_group + w_short per one- / two-step phase + w_step
+ * per step-loop phase + w_modular per modular-pass phase (fewer than 12 live
+ * lanes, more than 4 steps).  cost[ngroups]. */
+int hbp_group_costs(const hbp_format_t *f, int64_t w_group, int64_t w_short, int64_t w_step,
+                    int64_t w_modular, int64_t w_hot, int64_t *cost, hbp_stream_t stream);
 /* Tuning: kernel variant of hbp_spmv_stream for later calls (0 = default;
  * the others are measured alternatives and diagnostics).
  * Not thread-safe; for benchmarks. */

@@ -95,7 +95,7 @@ _SIGS = {
     "hbp_hash_perm_empty": [c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp],
     "hbp_sort_perm": [c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp],
     "hbp_merge_comparisons": [c_vp, c_i64, c_vp, c_vp],
-    "hbp_group_costs": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp],
+    "hbp_group_costs": [c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp],
     "hbp_rowstage_plan": [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
     "hbp_hot_remap_packed": [c_vp, c_i64, c_vp, c_i64, c_vp, c_vp],
     "hbp_spmv_rowstage": [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp],

@@ -245,22 +245,36 @@ __global__ void k_stream_slices(const int64_t *__restrict__ gs, int64_t ngroups,
     if (w == n - 1) slice_lo[n] = hi;
 }
 
-// hbp_group_costs: thread per group, over its phases
+// hbp_group_costs: one warp per group -- lanes count the group's staged (hot)
+// elements, lane 0 classifies its phases as the walk does (one- / two-step,
+// modular passes for k < 12 live lanes over more than 4 steps, step loop)
 __global__ void k_group_costs(const int64_t *__restrict__ gs, const int64_t *__restrict__ pptr,
-                              const uint2 *__restrict__ phs, int64_t ngroups, int64_t wg,
-                              int64_t wp, int64_t wm, int64_t *__restrict__ cost) {
-    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ngroups;
-         g += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t len = gs[g + 1] - gs[g];
-        const int64_t p0 = pptr[g], p1 = pptr[g + 1];
-        int64_t nmod = 0;
-        for (int64_t j = p0; j < p1; ++j) {
-            const uint2 ph = phs[j];
-            const int64_t end = j + 1 < p1 ? (int64_t)phs[j + 1].y : len;
-            const int k = __popc(ph.x);
-            nmod += (k < 12 && end - (int64_t)ph.y > 4 * k);
+                              const uint2 *__restrict__ phs, const uint32_t *__restrict__ scol,
+                              int64_t ngroups, int64_t wg, int64_t ws, int64_t wt, int64_t wm,
+                              int64_t wh, int64_t *__restrict__ cost) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < ngroups;
+         g += nwarps) {
+        const int64_t e0 = gs[g], len = gs[g + 1] - e0;
+        int64_t hot = 0;
+        if (scol && wh)
+            for (int64_t e = lane; e < len; e += 32) hot += (__ldcs(scol + e0 + e) & HBP_HOT_FLAG) != 0;
+        for (int o = 16; o; o >>= 1) hot += __shfl_xor_sync(0xffffffffu, hot, o);
+        if (lane == 0) {
+            const int64_t p0 = pptr[g], p1 = pptr[g + 1];
+            int64_t nshort = 0, nstep = 0, nmod = 0;
+            for (int64_t j = p0; j < p1; ++j) {
+                const uint2 ph = phs[j];
+                const int64_t end = j + 1 < p1 ? (int64_t)phs[j + 1].y : len;
+                const int k = __popc(ph.x);
+                const int64_t n = end - (int64_t)ph.y;
+                if (n <= 2 * k) ++nshort;
+                else if (k < 12 && n > 4 * k) ++nmod;
+                else ++nstep;
+            }
+            cost[g] = len - ((hot * wh) >> 6) + wg + ws * nshort + wt * nstep + wm * nmod;
         }
-        cost[g] = len + wg + wp * (p1 - p0) + wm * nmod;
     }
 }
 
@@ -1295,16 +1309,18 @@ int hbp_stream_slices(const hbp_format_t *f, const hbp_balanced_t *b, hbp_stream
     return (int)cudaGetLastError();
 }
 
-int hbp_group_costs(const hbp_format_t *f, int64_t w_group, int64_t w_phase, int64_t w_modular,
-                    int64_t *cost, hbp_stream_t stream) {
-    if (!f || !cost || w_group < 0 || w_phase < 0 || w_modular < 0) return HBP_E_ARG;
+int hbp_group_costs(const hbp_format_t *f, int64_t w_group, int64_t w_short, int64_t w_step,
+                    int64_t w_modular, int64_t w_hot, int64_t *cost, hbp_stream_t stream) {
+    if (!f || !cost || w_group < 0 || w_short < 0 || w_step < 0 || w_modular < 0 || w_hot < 0 ||
+        w_hot > 64)
+        return HBP_E_ARG;
     if (f->warp_size != 32 || f->row_height % 32) return HBP_E_UNSUPPORTED;
     if (!f->phases || !f->phase_ptr) return HBP_E_ARG;
     const int64_t ngroups = f->nzb * (f->row_height / 32);
     if (ngroups == 0) return HBP_OK;
-    k_group_costs<<<grid_for(ngroups, 256), 256, 0, as_stream(stream)>>>(
-        f->group_start, f->phase_ptr, (const uint2 *)f->phases, ngroups, w_group, w_phase,
-        w_modular, cost);
+    k_group_costs<<<grid_for(ngroups * 32, 256), 256, 0, as_stream(stream)>>>(
+        f->group_start, f->phase_ptr, (const uint2 *)f->phases, f->n_hot > 0 ? f->scol : nullptr,
+        ngroups, w_group, w_short, w_step, w_modular, w_hot, cost);
     return (int)cudaGetLastError();
 }
 

@@ -376,10 +376,14 @@ class SpmvOperator:
 
     # Stream schedule, fast mode: warps get equal predicted COST, not equal
     # elements.  Per-group cost in element units = elements + 48 + 20 per phase
-    # + 40 per modular-pass phase: the per-warp model fitted to measured warp
-    # times (tools/warp_cost.py; cfg2 R^2 0.97 -- equal-element slices ran
-    # 771..1181 us per warp on R-MAT, short-row groups cost the most).
-    SLICE_COST = (48, 20, 40)
+    # + 40 more per modular-pass phase: the per-warp model fitted to measured
+    # warp times (tools/warp_cost.py; cfg2 R^2 0.97 on equal-element slices,
+    # which ran 771..1181 us per warp on R-MAT -- short-row groups cost the
+    # most).  A refit on its residual -- (49, 26, 33, 76) by phase kind and a
+    # 17/64 discount per hot element -- narrowed the per-warp spread but not
+    # the kernel time (cfg2 1.022 vs 1.024 ms, cfg5 +1 %): the end is set by
+    # aggregate throughput once the gross imbalance is gone.
+    SLICE_COST = (48, 20, 20, 60, 0)
 
     def _cost_weights(self, f, slice_cost):
         """(w_group, w_phase, w_modular) or None (equal elements).  Default:
@@ -400,8 +404,11 @@ class SpmvOperator:
         if not slice_cost:
             return None
         w = tuple(int(v) for v in slice_cost)
-        if len(w) != 3 or min(w) < 0:
-            raise ValueError("slice_cost needs three non-negative weights")
+        if len(w) == 3:  # (group, phase, modular extra): the first model's form
+            w = (w[0], w[1], w[1], w[1] + w[2], 0)
+        if len(w) != 5 or min(w) < 0 or w[4] > 64:
+            raise ValueError("slice_cost needs 3 or 5 non-negative weights "
+                             "(group, short, step, modular phase, hot/64)")
         return w
 
     ROWSTAGE_SMEM = 200 * 1024  # one CTA's staged elements + partials (+ x windows) at most

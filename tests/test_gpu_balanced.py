@@ -255,7 +255,8 @@ def test_stream_ticket_rejects_bad_fraction():
 
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
 @pytest.mark.parametrize("workers", [1, 7, 333, None])
-@pytest.mark.parametrize("cost", ["48,20,40", "0,0,0", "500,100,0", "1,300,900"])
+@pytest.mark.parametrize("cost", ["48,20,40", "0,0,0", "500,100,0", "1,300,900",
+                                  "49,26,33,76,17", "0,0,0,0,64"])
 def test_stream_cost_balanced_slices(dtype, workers, cost):
     """Cost-balanced slice cuts (hbp_group_costs + prefix): valid monotone
     bounds, f64 bitwise the reference (exact mode), f32 within 1e-5 and
@@ -288,6 +289,8 @@ def test_stream_cost_weights_default_and_validation():
         H.SpmvOperator.SLICE_COST  # the hub-row path balances by cost too
     with pytest.raises(ValueError, match="weights"):
         H.SpmvOperator(h32, schedule="stream", slice_cost="1,2")
+    with pytest.raises(ValueError, match="weights"):
+        H.SpmvOperator(h32, schedule="stream", slice_cost="1,2,3,4,99")
 
 
 TAILS = ["0.95:1", "0.8:2", "0.5:4", "1.0:1"]
