@@ -274,6 +274,12 @@ typedef struct {
     int64_t n_warm;              /* warm tier: scol = HBP_WARM_FLAG | w (cols < 2^30) */
     int32_t cold_last;           /* 1: cold columns gathered L2 evict-last too (x fits L2) */
     int32_t reserved;            /* flags: HBP_FLAG_DIRECT_SINGLE */
+    /* nullable: the staged slots in ascending column order (refresh_cols[i] =
+     * hot_cols[refresh_slots[i]]) -- hbp_spmv_stream then refreshes x_hot by
+     * reading x in column order and scattering into the slots, instead of
+     * gathering it in slot (degree) order */
+    const uint32_t *refresh_cols;
+    const uint32_t *refresh_slots;
 } hbp_format_t;
 /* hbp_spmv_stream with a partial AND y: rows of row blocks that have exactly
  * one nonzero block are written to y directly (there is nothing to combine;

@@ -41,6 +41,7 @@ class FormatT(ctypes.Structure):
         ("phase_ptr", c_vp), ("phases", c_vp),
         ("scol", c_vp), ("hot_cols", c_vp), ("n_hot", c_i64), ("n_warm", c_i64),
         ("cold_last", ctypes.c_int32), ("reserved", ctypes.c_int32),
+        ("refresh_cols", c_vp), ("refresh_slots", c_vp),
     ]
 
 

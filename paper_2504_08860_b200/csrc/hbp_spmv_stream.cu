@@ -1207,6 +1207,35 @@ __global__ void k_hot_gather(const V *__restrict__ x, const uint32_t *__restrict
     if (t < n_hot && t < (n4 << 2) + 4) x_hot[t] = __ldg(x + hot_cols[t]);
 }
 
+// x_hot[slots[i]] = x[cols[i]] with cols ascending: x is read in column
+// order (coalesced runs) and the copy written by scatter (it is L2-resident)
+template <typename V>
+__global__ void k_hot_refresh(const V *__restrict__ x, const uint32_t *__restrict__ cols,
+                              const uint32_t *__restrict__ slots, int64_t n,
+                              V *__restrict__ x_hot) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    const int64_t n4 = n >> 2;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+        const uint4 c = __ldcs(reinterpret_cast<const uint4 *>(cols) + i);
+        const uint4 s = __ldcs(reinterpret_cast<const uint4 *>(slots) + i);
+        const V v0 = __ldg(x + c.x), v1 = __ldg(x + c.y), v2 = __ldg(x + c.z), v3 = __ldg(x + c.w);
+        x_hot[s.x] = v0, x_hot[s.y] = v1, x_hot[s.z] = v2, x_hot[s.w] = v3;
+    }
+    const int64_t t = (n4 << 2) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n && t < (n4 << 2) + 4) x_hot[slots[t]] = __ldg(x + cols[t]);
+}
+
+template <typename V>
+int hot_refresh(const void *x, const uint32_t *cols, const uint32_t *slots, int64_t n,
+                void *x_hot, cudaStream_t st) {
+    if (n == 0) return HBP_OK;
+    if (((uintptr_t)cols & 15) || ((uintptr_t)slots & 15)) return HBP_E_ARG;
+    k_hot_refresh<V><<<grid_for((n + 3) / 4, 256), 256, 0, st>>>((const V *)x, cols, slots, n,
+                                                                  (V *)x_hot);
+    return (int)cudaGetLastError();
+}
+
 template <typename V>
 int hot_gather(const void *x, const uint32_t *hot_cols, int64_t n_hot, void *x_hot,
                cudaStream_t st) {
@@ -1221,7 +1250,11 @@ template <typename V, bool EXACT>
 int run(const hbp_format_t *f, const hbp_balanced_t *b, const void *x, void *y, double *partial,
         cudaStream_t st) {
     if (staged(f)) {
-        const int rc = hot_gather<V>(x, f->hot_cols, f->n_hot + f->n_warm, b->x_hot, st);
+        const int rc =
+            f->refresh_cols
+                ? hot_refresh<V>(x, f->refresh_cols, f->refresh_slots, f->n_hot + f->n_warm,
+                                 b->x_hot, st)
+                : hot_gather<V>(x, f->hot_cols, f->n_hot + f->n_warm, b->x_hot, st);
         if (rc) return rc;
         if (packed(f)) x = (const V *)b->x_hot + f->n_hot;  // gathers read the packed copy
     }

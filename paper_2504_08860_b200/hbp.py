@@ -60,9 +60,24 @@ class HotColumns:
 
     packed = False  # HBP_FLAG_PACKED_X: n_warm counts the packed copy of x
 
+    def refresh_order(self):
+        """(cols, slots): the staged slots in ascending column order, for the
+        per-SpMV refresh of x_hot (reads x in column order).  Cached."""
+        if self._refresh is None:
+            n = self.hot_cols.numel()
+            slots = torch.arange(n, dtype=torch.int32, device=self.hot_cols.device)
+            cols, slots = L.sort_pairs_u32(self.hot_cols.contiguous(), slots, 32)
+            self._refresh = (cols, slots)
+        return self._refresh
+
+    _refresh = None
+
     def apply(self, f: "L.FormatT") -> None:
         f.scol, f.hot_cols = self.scol.data_ptr(), self.hot_cols.data_ptr()
         f.n_hot, f.n_warm = self.n_hot, self.n_warm
+        if os.environ.get("HBP_HOT_REFRESH", "1") != "0" and self.hot_cols.numel():
+            cols, slots = self.refresh_order()
+            f.refresh_cols, f.refresh_slots = cols.data_ptr(), slots.data_ptr()
         if self.packed:
             f.reserved |= 8  # HBP_FLAG_PACKED_X
             f.cold_last = 1
