@@ -8,15 +8,17 @@
 // order, each at the first free slot at or after its preliminary slot,
 // cyclically (the slot the reference's +1 probe loop reaches); its probe count
 // is the cyclic distance (slot - preliminary) mod n.  The claim chain is
-// sequential by definition, so the B200 form keeps that chain as short as
-// possible: one WARP per block, the block's occupancy bitmap held in the
-// warp's registers (word w in lane w, R <= 1024), the preliminary slots of 32
-// rows computed in parallel and broadcast by shuffle, and each claim one
-// ballot over the lanes' masked free words -- no memory access on the chain.
-// Claimed slots go to a per-warp shared table and leave as coalesced stores.
+// sequential by definition.  Two forms: with few blocks (fewer than a wave of
+// warps) one WARP per block keeps the chain short -- the block's occupancy
+// bitmap in the warp's registers (word w in lane w, R <= 1024), the
+// preliminary slots of 32 rows computed in parallel and broadcast by shuffle,
+// each claim one ballot over the lanes' masked free words, claimed slots to
+// a per-warp shared table and out as coalesced stores; with many blocks one
+// THREAD per block (shared-memory bitmap), 32 chains per warp instruction.
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "hbp.h"
 #include "hbp_common.cuh"
@@ -110,7 +112,7 @@ k_hash_perm_warp(const uint32_t *__restrict__ len_local, const int32_t *__restri
     }
 }
 
-// ---------------------------------------- hash: one thread per block (R > 1024)
+// ------------------------------ hash: one thread per block (many blocks, R > 1024)
 // The occupancy bitmap of thread t lives in shared memory, word w at
 // [w * blockDim + t] (conflict-free); find-next-free scans words.
 template <bool EMPTY>
@@ -282,7 +284,25 @@ int hash_launch(const uint32_t *len_local, const int32_t *blk_br, int64_t nzb, i
                 int64_t R, int64_t a, int64_t b, int64_t c, int64_t d, int64_t bmax,
                 uint32_t *perm, unsigned long long *probes, bool empty, cudaStream_t s) {
     const int small = small_hash_math(R, b, c, d, bmax) ? 1 : 0;
-    if (R <= 1024) {
+    // The claim chain is serial per block either way.  A warp per block keeps
+    // it in registers but leaves 31 lanes idle on it, so it only wins while
+    // the blocks alone cannot fill the GPU: up to one resident wave of warps
+    // (cfg1, 3,068 blocks: 0.116 vs 0.28 ms); beyond that a thread per block
+    // runs 32 chains per warp instruction (cfg2 0.36 vs 0.80 ms, cfg3 0.50 vs
+    // 2.07 ms; ncu).  A thread-per-block form with its slot table in shared
+    // memory and coalesced table stores was slower still (cfg3 1.12 ms: the
+    // tables cap it at 6 CTAs of 32 threads per SM).  HBP_HASH_THREAD=0/1
+    // forces the warp / thread form (A/B).
+    int64_t wave = 148 * 64;
+    {
+        int dev = 0, sms = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+            wave = (int64_t)sms * 64;
+    }
+    const char *force = getenv("HBP_HASH_THREAD");
+    const int form = force ? atoi(force) : (nzb <= wave ? 0 : 1);  // 0 warp, 1 thread
+    if (R <= 1024 && form == 0) {
         const int warps = 4;
         const unsigned grid = (unsigned)((nzb + warps - 1) / warps);
         const size_t smem = (size_t)warps * R * sizeof(uint16_t);
