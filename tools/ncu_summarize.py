@@ -1,6 +1,6 @@
 """Summarise `ncu --set full` captures of the SpMV kernel into profiles/.
 
-    python tools/ncu_summarize.py CONFIG REPORT.ncu-rep [ROUND_TAG]
+    python tools/ncu_summarize.py CONFIG REPORT.ncu-rep|RAW.csv [ROUND_TAG]
 
 Writes profiles/<tag>_ncu_<config>.csv (the key metrics, one row per
 kernel) and merges {config: {...}} into profiles/ncu_summary.json, which
@@ -33,8 +33,11 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
 def main():
     cfg, rep = sys.argv[1], sys.argv[2]
     tag = sys.argv[3] if len(sys.argv) > 3 else "r01"
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout
+    if rep.endswith(".csv"):  # `ncu -i REP --page raw --csv` exported on the GPU box
+        raw = open(rep).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units, data = rows[0], rows[1], rows[2:]
     out_rows = []
