@@ -299,15 +299,59 @@ def _reference_pkg():
         return None
 
 
-def numba_reference(cfg_name: str, steps: int, warmup: int, seed: int = 0):
+# the reference at FULL scale for these configs in `bench.py --impl reference`
+# (its dense layout makes cfg3 / cfg5 infeasible on the host: bounded samples)
+REF_FULL = {"cfg1", "cfg2", "cfg2d", "cfg4", "H"}
+
+
+def make_matrix_full_host(cfg_name: str, seed: int = 0):
+    """The benchmarked matrix itself on the host: generated on the GPU when
+    one is visible (generation is not timed; numpy's R-MAT at scale 24 takes
+    minutes), else with the host generators; values rounded to the config's
+    dtype, as the GPU arm sees them."""
+    import bench_inputs as BI
+    desc, gen, dt, C = CONFIGS[cfg_name]
+    try:
+        import torch
+        if torch.cuda.is_available():
+            _, rows, cols, rp, col, val, C2, _ = make_matrix_gpu(cfg_name, seed,
+                                                                 torch.device("cuda", 0))
+            out = (rows, cols, rp.cpu().numpy().astype(np.int64),
+                   col.cpu().numpy().astype(np.int64), val.double().cpu().numpy(), C2)
+            del rp, col, val
+            torch.cuda.empty_cache()
+            return out + (f"the benchmarked matrix itself ({desc})",)
+    except Exception:  # no usable GPU: host generators below
+        pass
+    if gen["kind"] == "rmat":
+        rows, cols, rp, col, val = BI.rmat_csr_numpy(gen["scale"], gen["edge_factor"], seed)
+    elif gen["kind"] == "laplacian":
+        rows, cols, rp, col, val = BI.laplacian_csr(gen["n"])
+    else:
+        from paper_2504_08860_b200.synth import SyntheticSpec, generate_arrays
+        r, c, val = generate_arrays(SyntheticSpec(gen["rows"], gen["cols"], "uniform",
+                                                  gen["mean"], seed=seed))
+        rows, cols = gen["rows"], gen["cols"]
+        rp = np.concatenate(([0], np.cumsum(np.bincount(r, minlength=rows)))).astype(np.int64)
+        col = c
+    if dt == "f32":
+        val = val.astype(np.float32).astype(np.float64)
+    return rows, cols, rp, col, val, (C or cols), f"the benchmarked matrix itself ({desc})"
+
+
+def numba_reference(cfg_name: str, steps: int, warmup: int, seed: int = 0, full: bool = False):
     """The reference itself (baseline/_ref: engine.py:228-232 hbp_spmv with
-    numba kernels and Python worker threads, formats.py:266-273 csr_spmv) on
-    the same bounded sample as cpu_reference, at workers = cpu_count / 4 / 1.
-    Returns a dict, or None without the reference package."""
+    numba kernels and Python worker threads, formats.py:266-273 csr_spmv) at
+    workers = cpu_count / 4 / 1, on the same bounded sample as cpu_reference
+    or (full, REF_FULL configs) on the benchmarked matrix itself.  Returns a
+    dict, or None without the reference package."""
     h = _reference_pkg()
     if h is None:
         return None
-    rows, cols, rp, col, val, C, sample = make_matrix_cpu_sample(cfg_name, seed)
+    if full and cfg_name in REF_FULL:
+        rows, cols, rp, col, val, C, sample = make_matrix_full_host(cfg_name, seed)
+    else:
+        rows, cols, rp, col, val, C, sample = make_matrix_cpu_sample(cfg_name, seed)
     cfg = h.PartitionConfig(col_width=C, row_height=512, warp_size=32)
     csr = h.CsrMatrix(rows, cols, rp, col, val)
     t0 = time.perf_counter()
@@ -823,8 +867,10 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
-    nb = numba_reference(args.config, steps=args.steps, warmup=args.warmup) \
-        if args.config != "cfg1" or os.environ.get("HBP_REF_CFG1") else None
+    # the reference package on the benchmarked matrix itself where its dense
+    # layout fits the host (REF_FULL; HBP_REF_SAMPLE=1: the bounded sample)
+    full = os.environ.get("HBP_REF_SAMPLE", "0") != "1"
+    nb = numba_reference(args.config, steps=args.steps, warmup=args.warmup, full=full)
     port = cpu_reference(args.config, steps=args.steps, warmup=args.warmup)
     cb = nb if nb is not None else port
     desc = CONFIGS[args.config][0]
