@@ -12,7 +12,8 @@ import os
 import torch
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libhbp.so")
+# HBP_LIB_PATH: an alternative build of the same library (A/B measurements)
+LIB_PATH = os.environ.get("HBP_LIB_PATH") or os.path.join(PKG, "libhbp.so")
 
 HBP_OK = 0
 HBP_E_ARG = 1001
