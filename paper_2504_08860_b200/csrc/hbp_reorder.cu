@@ -45,65 +45,76 @@ __device__ __forceinline__ uint32_t prelim_slot(uint32_t len, int64_t r, int64_t
     return (uint32_t)((g * b + (r * c) % d) % n);
 }
 
-// ------------------------------------------------ hash: one warp per block
-// Lane L owns bitmap word L (slots 32L .. 32L+31); words past the block's
-// rows are all-taken.  For a row with preliminary slot p (word w, bit q):
-//   m_L = free bits of lane L at or after p (L == w: bits >= q; L > w: all;
-//         L < w: none); the winner is the lowest lane with m_L != 0, else
-//         (wraparound) the lowest lane with any free bit.
+// ------------------------------------- hash: a lane group (L lanes) per block
+// L = 8, 16 or 32 lanes own one block (32/L blocks per warp, in lockstep);
+// lane l of a group owns bitmap word l (slots 32l .. 32l+31, R <= 32L); words
+// past the block's rows are all-taken.  For a row with preliminary slot p
+// (word w, bit q):
+//   m_l = free bits of lane l at or after p (l == w: bits >= q; l > w: all;
+//         l < w: none); the winner is the group's lowest lane with m_l != 0,
+//         else (wraparound) its lowest lane with any free bit.
 // The winner sets its bit and records slot -> row in shared memory.
-template <bool EMPTY>
+template <bool EMPTY, int L>
 __global__ void __launch_bounds__(128)
 k_hash_perm_warp(const uint32_t *__restrict__ len_local, const int32_t *__restrict__ blk_br,
                  int64_t nzb, int64_t rows, int64_t R, int64_t a, int64_t b, int64_t c, int64_t d,
                  int64_t bmax, int small, uint32_t *__restrict__ perm,
                  unsigned long long *__restrict__ probes) {
-    extern __shared__ uint16_t slot_row[];  // [warps][R]
+    constexpr int S = 32 / L;  // blocks per warp
+    constexpr unsigned GMASK = L == 32 ? 0xffffffffu : ((1u << L) - 1u);
+    extern __shared__ uint16_t slot_row[];  // [warps * S][R]
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    uint16_t *tab = slot_row + (int64_t)wid * R;
-    const int64_t blk = (int64_t)blockIdx.x * (blockDim.x >> 5) + wid;
+    const int sub = lane / L, sl = lane - sub * L, shift = sub * L;
+    uint16_t *tab = slot_row + ((int64_t)wid * S + sub) * R;
+    const int64_t blk = ((int64_t)blockIdx.x * (blockDim.x >> 5) + wid) * S + sub;
+    const bool have = blk < nzb;
     unsigned long long my_probes = 0;
-    if (blk < nzb) {
-        const int64_t n = EMPTY ? rows : rows_in_block(rows, R, blk_br[blk]);
-        const int nn = (int)n;
-        uint32_t word;
-        if (lane * 32 >= nn) word = FULL;
-        else if (lane * 32 + 32 > nn) word = ~((1u << (nn & 31)) - 1u);
-        else word = 0u;
-        const uint32_t *lens = EMPTY ? nullptr : len_local + blk * R;
-        uint32_t next_len = (!EMPTY && lane < nn) ? __ldg(lens + lane) : 0u;
-        for (int base = 0; base < nn; base += 32) {
-            const int r = base + lane;
-            const uint32_t len = next_len;
-            if (!EMPTY && r + 32 < nn) next_len = __ldg(lens + r + 32);
-            const uint32_t pre = r < nn ? prelim_slot(len, r, n, a, b, c, d, bmax, small) : 0u;
-            const int cnt = nn - base < 32 ? nn - base : 32;
-#pragma unroll 8
-            for (int j = 0; j < cnt; ++j) {
-                const uint32_t home = __shfl_sync(FULL, pre, j);
-                const int w = (int)(home >> 5);
-                const uint32_t fr = ~word;
-                uint32_t m = lane == w ? fr & (FULL << (home & 31)) : (lane > w ? fr : 0u);
-                uint32_t bal = __ballot_sync(FULL, m != 0u);
-                if (bal == 0u) {  // wraparound: first free slot from slot 0
+    const int64_t n = !have ? 0 : EMPTY ? rows : rows_in_block(rows, R, blk_br[blk]);
+    const int nn = (int)n;
+    uint32_t word;
+    if (sl * 32 >= nn) word = FULL;
+    else if (sl * 32 + 32 > nn) word = ~((1u << (nn & 31)) - 1u);
+    else word = 0u;
+    const uint32_t *lens = (EMPTY || !have) ? nullptr : len_local + blk * R;
+    const int nmax = __reduce_max_sync(FULL, (unsigned)nn);
+    uint32_t next_len = (!EMPTY && sl < nn) ? __ldg(lens + sl) : 0u;
+    for (int base = 0; base < nmax; base += L) {
+        const int r = base + sl;
+        const uint32_t len = next_len;
+        if (!EMPTY && r + L < nn) next_len = __ldg(lens + r + L);
+        const uint32_t pre = r < nn ? prelim_slot(len, r, n, a, b, c, d, bmax, small) : 0u;
+#pragma unroll 4
+        for (int j = 0; j < L; ++j) {
+            const bool valid = base + j < nn;
+            const uint32_t home = __shfl_sync(FULL, pre, shift + j);
+            const int w = (int)(home >> 5);
+            const uint32_t fr = ~word;
+            uint32_t m = !valid ? 0u : sl == w ? fr & (FULL << (home & 31)) : (sl > w ? fr : 0u);
+            uint32_t bal = (__ballot_sync(FULL, m != 0u) >> shift) & GMASK;
+            const bool wrap = valid && bal == 0u;  // first free slot from slot 0
+            if (__any_sync(FULL, wrap)) {
+                const uint32_t b2 = (__ballot_sync(FULL, fr != 0u) >> shift) & GMASK;
+                if (wrap) {
                     m = fr;
-                    bal = __ballot_sync(FULL, fr != 0u);
-                }
-                if (lane == __ffs(bal) - 1) {
-                    const int bit = __ffs(m) - 1;
-                    word |= 1u << bit;
-                    const uint32_t slot = (uint32_t)(lane * 32 + bit);
-                    tab[slot] = (uint16_t)(base + j);
-                    my_probes += slot >= home ? slot - home : slot + (uint32_t)nn - home;
+                    bal = b2;
                 }
             }
+            if (valid && sl == __ffs(bal) - 1) {
+                const int bit = __ffs(m) - 1;
+                word |= 1u << bit;
+                const uint32_t slot = (uint32_t)(sl * 32 + bit);
+                tab[slot] = (uint16_t)(base + j);
+                my_probes += slot >= home ? slot - home : slot + (uint32_t)nn - home;
+            }
         }
-        __syncwarp();
+    }
+    __syncwarp();
+    if (have) {
         uint32_t *out = perm + blk * R;
-        for (int s = lane; s < (int)R; s += 32) {
-            if (s < nn) out[s] = tab[s];
-            else if (!EMPTY) out[s] = 0u;
+        for (int s2 = sl; s2 < (int)R; s2 += L) {
+            if (s2 < nn) out[s2] = tab[s2];
+            else if (!EMPTY) out[s2] = 0u;
         }
     }
     if (probes) {
@@ -284,12 +295,12 @@ int hash_launch(const uint32_t *len_local, const int32_t *blk_br, int64_t nzb, i
                 int64_t R, int64_t a, int64_t b, int64_t c, int64_t d, int64_t bmax,
                 uint32_t *perm, unsigned long long *probes, bool empty, cudaStream_t s) {
     const int small = small_hash_math(R, b, c, d, bmax) ? 1 : 0;
-    // The claim chain is serial per block either way.  A warp per block keeps
-    // it in registers but leaves 31 lanes idle on it, so it only wins while
-    // the blocks alone cannot fill the GPU: up to one resident wave of warps
-    // (cfg1, 3,068 blocks: 0.116 vs 0.28 ms); beyond that a thread per block
-    // runs 32 chains per warp instruction (cfg2 0.36 vs 0.80 ms, cfg3 0.50 vs
-    // 2.07 ms; ncu).  A thread-per-block form with its slot table in shared
+    // The claim chain is serial per block either way.  A lane group per block
+    // (8-32 lanes, 1-4 blocks per warp) keeps it in registers but leaves most
+    // lanes idle on it, so it only wins while the blocks alone cannot fill the
+    // GPU (cfg1, 3,068 blocks: 0.105 vs 0.28 ms); beyond that a thread per
+    // block runs 32 chains per warp instruction (cfg2 0.36 vs 0.59 ms, cfg3
+    // 0.51 vs 1.42 ms; ncu).  A thread-per-block form with its slot table in shared
     // memory and coalesced table stores was slower still (cfg3 1.12 ms: the
     // tables cap it at 6 CTAs of 32 threads per SM).  HBP_HASH_THREAD=0/1
     // forces the warp / thread form (A/B).
@@ -301,17 +312,29 @@ int hash_launch(const uint32_t *len_local, const int32_t *blk_br, int64_t nzb, i
             wave = (int64_t)sms * 64;
     }
     const char *force = getenv("HBP_HASH_THREAD");
-    const int form = force ? atoi(force) : (nzb <= wave ? 0 : 1);  // 0 warp, 1 thread
+    // lane-group form up to ~3/4 of a wave of its groups (H, 12,208 blocks of
+    // R = 512: 0.259 vs 0.308 ms; cfg4, 16,384: 0.320 vs 0.302)
+    const int64_t lanes = R <= 256 ? 8 : R <= 512 ? 16 : 32;
+    const int form = force ? atoi(force) : (nzb * lanes * 4 <= wave * 32 * 3 ? 0 : 1);
     if (R <= 1024 && form == 0) {
-        const int warps = 4;
-        const unsigned grid = (unsigned)((nzb + warps - 1) / warps);
-        const size_t smem = (size_t)warps * R * sizeof(uint16_t);
-        if (empty)
-            k_hash_perm_warp<true><<<grid, warps * 32, smem, s>>>(
-                nullptr, nullptr, nzb, rows, R, a, b, c, d, bmax, small, perm, probes);
-        else
-            k_hash_perm_warp<false><<<grid, warps * 32, smem, s>>>(
-                len_local, blk_br, nzb, rows, R, a, b, c, d, bmax, small, perm, probes);
+        // lanes per block: the fewest (>= 8) whose bitmap words cover R slots
+        const int L = R <= 256 ? 8 : R <= 512 ? 16 : 32;
+        const int warps = 4, per_cta = warps * (32 / L);
+        const unsigned grid = (unsigned)((nzb + per_cta - 1) / per_cta);
+        const size_t smem = (size_t)per_cta * R * sizeof(uint16_t);
+#define HBP_HASH_WARP(LL)                                                                     \
+    do {                                                                                      \
+        if (empty)                                                                            \
+            k_hash_perm_warp<true, LL><<<grid, warps * 32, smem, s>>>(                        \
+                nullptr, nullptr, nzb, rows, R, a, b, c, d, bmax, small, perm, probes);       \
+        else                                                                                  \
+            k_hash_perm_warp<false, LL><<<grid, warps * 32, smem, s>>>(                       \
+                len_local, blk_br, nzb, rows, R, a, b, c, d, bmax, small, perm, probes);      \
+    } while (0)
+        if (L == 8) HBP_HASH_WARP(8);
+        else if (L == 16) HBP_HASH_WARP(16);
+        else HBP_HASH_WARP(32);
+#undef HBP_HASH_WARP
         HBP_LAUNCH_CHECK();
         return HBP_OK;
     }
