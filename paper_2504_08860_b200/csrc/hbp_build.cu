@@ -29,28 +29,56 @@ __device__ __forceinline__ int64_t rows_in_block(int64_t rows, int64_t R, int64_
 }
 
 // ------------------------------------------------------------- make_grid
-// One warp per CSR row: a run head is the row's first element or an element
-// whose column block differs from its predecessor's (partition.py:109-112).
+// A run head is the row's first element or an element whose column block
+// differs from its predecessor's (partition.py:109-112).  A warp takes 32
+// consecutive rows: each lane walks its own row when it is short (<= kShortRow
+// elements: a row then costs one lane, not a warp with a dependent row_ptr
+// load per row -- cfg3's 33.5M rows of 33 elements), and
+// rows longer than that are walked by the whole warp, 32 elements per step.
+// Column blocks by 32-bit division: C < cols < 2^31 off the single-block path.
+constexpr int64_t kShortRow = 64;
+
 __global__ void k_count_runs(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                              int64_t rows, int64_t C, int single_block,
                              int64_t *__restrict__ out) {
-    int lane = threadIdx.x & 31;
-    int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t r = warp; r < rows; r += nwarps) {
-        int64_t lo = row_ptr[r], hi = row_ptr[r + 1];
+    const uint32_t Cu = (uint32_t)(C < 0xffffffffLL ? C : 0xffffffffLL);
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t base = warp * 32; base < rows; base += nwarps * 32) {
+        const int64_t r = base + lane;
+        int64_t lo = 0, hi = 0;
+        if (r < rows) lo = row_ptr[r], hi = row_ptr[r + 1];
         if (single_block) {
-            if (lane == 0) out[r] = hi > lo ? 1 : 0;
+            if (r < rows) out[r] = hi > lo ? 1 : 0;
             continue;
         }
-        int64_t cnt = 0;
-        for (int64_t b = lo; b < hi; b += 32) {
-            int64_t j = b + lane;
-            bool head = false;
-            if (j < hi) head = (j == lo) || (col[j] / C != col[j - 1] / C);
-            cnt += __popc(__ballot_sync(0xffffffffu, head));
+        const bool shortr = hi - lo <= kShortRow;
+        if (r < rows && shortr) {
+            int64_t cnt = 0;
+            uint32_t prev = 0xffffffffu;
+            for (int64_t j = lo; j < hi; ++j) {
+                const uint32_t bc = (uint32_t)col[j] / Cu;
+                cnt += bc != prev;
+                prev = bc;
+            }
+            out[r] = cnt;
         }
-        if (lane == 0) out[r] = cnt;
+        unsigned longm = __ballot_sync(0xffffffffu, r < rows && !shortr);
+        while (longm) {
+            const int l = __ffs(longm) - 1;
+            longm &= longm - 1;
+            const int64_t lo_l = __shfl_sync(0xffffffffu, lo, l), hi_l = __shfl_sync(0xffffffffu, hi, l);
+            int64_t cnt = 0;
+            for (int64_t b = lo_l; b < hi_l; b += 32) {
+                const int64_t j = b + lane;
+                bool head = false;
+                if (j < hi_l)
+                    head = (j == lo_l) || ((uint32_t)col[j] / Cu != (uint32_t)col[j - 1] / Cu);
+                cnt += __popc(__ballot_sync(0xffffffffu, head));
+            }
+            if (lane == l) out[r] = cnt;
+        }
     }
 }
 
@@ -58,37 +86,61 @@ __global__ void k_emit_runs(const int64_t *__restrict__ row_ptr, const int32_t *
                             int64_t rows, int64_t C, int single_block,
                             const int64_t *__restrict__ run_offset, uint32_t *__restrict__ run_bc,
                             uint32_t *__restrict__ run_row, int64_t *__restrict__ run_start) {
-    int lane = threadIdx.x & 31;
-    int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    unsigned lt = (1u << lane) - 1u;
-    for (int64_t r = warp; r < rows; r += nwarps) {
-        int64_t lo = row_ptr[r], hi = row_ptr[r + 1];
-        int64_t off = run_offset[r];
+    const uint32_t Cu = (uint32_t)(C < 0xffffffffLL ? C : 0xffffffffLL);
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int64_t base = warp * 32; base < rows; base += nwarps * 32) {
+        const int64_t r = base + lane;
+        int64_t lo = 0, hi = 0, off = 0;
+        if (r < rows) lo = row_ptr[r], hi = row_ptr[r + 1], off = run_offset[r];
         if (single_block) {
-            if (lane == 0 && hi > lo) {
+            if (r < rows && hi > lo) {
                 run_bc[off] = 0;
                 run_row[off] = (uint32_t)r;
                 run_start[off] = lo;
             }
             continue;
         }
-        for (int64_t b = lo; b < hi; b += 32) {
-            int64_t j = b + lane;
-            bool head = false;
-            int32_t bc = 0;
-            if (j < hi) {
-                bc = col[j] / C;
-                head = (j == lo) || (bc != col[j - 1] / C);
+        const bool shortr = hi - lo <= kShortRow;
+        if (r < rows && shortr) {
+            uint32_t prev = 0xffffffffu;
+            for (int64_t j = lo; j < hi; ++j) {
+                const uint32_t bc = (uint32_t)col[j] / Cu;
+                if (bc != prev) {
+                    run_bc[off] = bc;
+                    run_row[off] = (uint32_t)r;
+                    run_start[off] = j;
+                    ++off;
+                }
+                prev = bc;
             }
-            unsigned m = __ballot_sync(0xffffffffu, head);
-            if (head) {
-                int64_t i = off + __popc(m & lt);
-                run_bc[i] = (uint32_t)bc;
-                run_row[i] = (uint32_t)r;
-                run_start[i] = j;
+        }
+        unsigned longm = __ballot_sync(0xffffffffu, r < rows && !shortr);
+        while (longm) {
+            const int l = __ffs(longm) - 1;
+            longm &= longm - 1;
+            const int64_t lo_l = __shfl_sync(0xffffffffu, lo, l), hi_l = __shfl_sync(0xffffffffu, hi, l);
+            int64_t off_l = __shfl_sync(0xffffffffu, off, l);
+            const int64_t r_l = base + l;
+            for (int64_t b = lo_l; b < hi_l; b += 32) {
+                const int64_t j = b + lane;
+                bool head = false;
+                uint32_t bc = 0;
+                if (j < hi_l) {
+                    bc = (uint32_t)col[j] / Cu;
+                    head = (j == lo_l) || (bc != (uint32_t)col[j - 1] / Cu);
+                }
+                const unsigned m = __ballot_sync(0xffffffffu, head);
+                if (head) {
+                    const int64_t i = off_l + __popc(m & lt);
+                    run_bc[i] = bc;
+                    run_row[i] = (uint32_t)r_l;
+                    run_start[i] = j;
+                }
+                off_l += __popc(m);
             }
-            off += __popc(m);
         }
     }
 }
