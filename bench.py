@@ -15,8 +15,11 @@ timed steps (untimed), otherwise the inputs exceed L2 and x stays
 cache-resident by design.
 Multi-GPU (torchrun): every config but cfg1 is strong -- one global matrix
 split into nnz-balanced row stripes (stripes.plan_stripes / StripedOperator),
-x replicated; a single SpMV has no collective, cfg5's power iteration
-all-gathers the y stripes (overlapped with the next step's own-column part).
+x replicated; a single SpMV has no collective.  cfg5's power iteration
+by default has the SpMV kernel store its y rows straight into every rank's
+next x (CUDA IPC mappings over NVLink; `--collective fused`), leaving only
+an 8-byte all-reduce; `--collective gather` all-gathers the y stripes with
+NCCL instead (overlapped with the next step's own-column part).
 cfg1 (5M nnz) runs an independent full instance per rank (weak).
 """
 from __future__ import annotations
@@ -496,7 +499,11 @@ def run_gpu(args):
     hub_arg = None if args.hub in (None, "off", "0") else (
         "auto" if args.hub == "auto" else int(args.hub))
     op_kwargs = dict(schedule=args.schedule, hot=hot_arg, workers=args.workers, hub_min=hub_arg)
-    split = iterated and world > 1 and not args.no_overlap
+    # cfg5 at N > 1: "fused" = the SpMV kernel stores y into every rank's next x
+    # (CUDA IPC over NVLink, stripes.PowerIteration(fused=True)), no all-gather;
+    # "gather" = NCCL all-gather, overlapped with the own-column split
+    fused = iterated and world > 1 and args.collective == "fused"
+    split = iterated and world > 1 and not args.no_overlap and not fused
 
     # ---- preprocessing (timed like cli.py:150-158, GPU stages; the global
     # hash-parameter draw is part of "sample" at N > 1)
@@ -545,7 +552,18 @@ def run_gpu(args):
         # an 8-byte all-reduce and an in-place all-gather of the y stripes into the
         # next x (padded layout); at N > 1 the gather overlaps the next step's
         # own-column part
-        pit = PowerIteration(sop, torch.as_tensor(x_host, device=dev))
+        collective = None
+        if fused:
+            try:
+                pit = PowerIteration(sop, torch.as_tensor(x_host, device=dev), fused=True)
+                collective = "fused-p2p-stores"
+            except Exception as e:  # no IPC between these processes: NCCL all-gather
+                print(f"fused power iteration unavailable ({e}); all-gather instead",
+                      file=sys.stderr)
+        if collective is None:
+            pit = PowerIteration(sop, torch.as_tensor(x_host, device=dev))
+            collective = ("nccl-all-gather" + ("+own-column-overlap" if split else "")
+                          if world > 1 else None)
         step = pit.step
         x_res = pit.x_global
     else:
@@ -734,7 +752,8 @@ def run_gpu(args):
         c0.record(stream)
         for _ in range(K):
             dist.all_reduce(pit.sq)
-            dist.all_gather_into_tensor(nxt, nxt[rank * sop.pad:(rank + 1) * sop.pad])
+            if not pit.fused:  # fused: the y exchange is inside the SpMV's stores
+                dist.all_gather_into_tensor(nxt, nxt[rank * sop.pad:(rank + 1) * sop.pad])
         c1.record(stream)
         torch.cuda.synchronize()
         cm = torch.tensor([c0.elapsed_time(c1) / K], dtype=torch.float64, device=dev)
@@ -790,12 +809,15 @@ def run_gpu(args):
                    "warm_columns": op.hot.n_warm if op.hot is not None else 0,
                    "warm_share": round(op.hot.warm_share, 4) if op.hot is not None else 0.0,
                    "hash_params": [params.a, params.b, params.c, params.d],
-                   "step": ("power iteration: SpMV + ||y|| all-reduce + y all-gather"
+                   "step": (("power iteration: SpMV storing y into every rank's next x "
+                             "(CUDA IPC) + ||y|| all-reduce" if pit.fused else
+                             "power iteration: SpMV + ||y|| all-reduce + y all-gather")
                             if iterated else "SpMV (+ combine when ncb > 1)"),
                    "parallelism": (f"row stripes x{world} of one matrix (strong)" if strong
                                    else f"independent instances x{world} (weak)"),
                    "stripes": stripe_info,
                    "own_column_split": sop.split,
+                   "collective": collective if iterated else None,
                    "own_column_share_rank0": round(sop.own_share, 4),
                    "comm_ms_per_step": comm_ms,
                    "l2": ("working set < 2x L2: L2 flushed between timed steps" if flush
@@ -911,6 +933,9 @@ def main():
     ap.add_argument("--schedule", default=None, choices=[None, "stream", "balanced", "plan", "rowblock", "rowstage", "seg"])
     ap.add_argument("--workers", type=int, default=None,
                     help="persistent warps of the SpMV (default: one per resident warp slot)")
+    ap.add_argument("--collective", default="fused", choices=["fused", "gather"],
+                    help="cfg5 at N > 1: y stored into the peers' x by the SpMV kernel "
+                         "(CUDA IPC), or an NCCL all-gather")
     ap.add_argument("--no-overlap", action="store_true",
                     help="cfg5 at N > 1: no own-column split, all-gather then SpMV")
     ap.add_argument("--hub", default=None,

@@ -60,6 +60,9 @@ const char *hbp_status_string(int status);
  * read (cudaGetLastError) -- for tests that check no call left one behind. */
 int hbp_last_error(void);
 int hbp_abi_version(void);
+/* sizeof hbp_format_t, hbp_schedule_t, hbp_balanced_t, hbp_seg_t (bindings
+ * check their struct mirrors against it); no device needed. */
+int hbp_struct_sizes(int64_t *sizes);
 
 /* Device facts for sizing persistent grids (replaces the worker-count
  * argument of engine.py:96 / cli.py:59-60 with a device-derived default). */
@@ -294,6 +297,8 @@ typedef struct {
 #define HBP_FLAG_PACKED_X 8
 #define HBP_HOT_FLAG 0x80000000u
 #define HBP_WARM_FLAG 0x40000000u
+/* peer copies of y a stream launch can write (hbp_balanced_t.y_peer): 8 GPUs */
+#define HBP_MAX_PEERS 7
 
 /* Phase stream (runtime index used by hbp_spmv_stream, W = 32): a group's
  * phases are its maximal step ranges with a fixed live-lane set; phase j is
@@ -377,6 +382,14 @@ typedef struct {
      * launch (set by the library for the second launch; 0 for callers). */
     int64_t tail;
     int64_t piece_base;
+    /* Peer copies of y (SURVEY §8(e) fused variant: the iterated SpMV's
+     * all-gather folded into its stores).  Every value the stream kernel
+     * writes to y[r] (one column block, no partial) is also written to
+     * y_peer[p][r] for p < n_peers: device pointers, normally other GPUs'
+     * next-x buffers mapped with hbp_ipc_open, stored over NVLink as the
+     * rows finish; each warp ends with a system-scope fence.  0: off. */
+    int64_t n_peers;
+    void *y_peer[HBP_MAX_PEERS];
 } hbp_balanced_t;
 
 int hbp_balanced_workers(const hbp_format_t *f, int64_t *workers);
@@ -528,6 +541,19 @@ int hbp_add(void *y, const void *a, int dtype, int64_t n, hbp_stream_t stream);
 int hbp_sumsq_scratch(int64_t *doubles);
 int hbp_scale(const void *y, int dtype, int64_t n, const double *sumsq, void *out,
               hbp_stream_t stream);
+
+/* Peer mappings for the fused power iteration (hbp_balanced_t.y_peer): one
+ * process per GPU exports the device buffer its next x lives in and maps the
+ * other ranks' (CUDA IPC over NVLink / NVSwitch; the handles travel through
+ * torch.distributed).  hbp_ipc_export: handle[HBP_IPC_HANDLE_BYTES] of the
+ * allocation holding ptr and ptr's byte offset in it (device allocations
+ * from a caching allocator start below ptr).  hbp_ipc_open: the exporter's
+ * allocation mapped into this process, plus offset (*ptr is then the
+ * exporter's ptr).  hbp_ipc_close: unmap (ptr as returned minus offset). */
+#define HBP_IPC_HANDLE_BYTES 64
+int hbp_ipc_export(const void *ptr, void *handle, int64_t *offset);
+int hbp_ipc_open(const void *handle, int64_t offset, void **ptr);
+int hbp_ipc_close(void *base);
 #ifdef __cplusplus
 }
 #endif

@@ -60,6 +60,10 @@ class SegT(ctypes.Structure):
                 ("win_hi", c_vp), ("win_cap", c_i64)]
 
 
+MAX_PEERS = 7  # HBP_MAX_PEERS
+IPC_HANDLE_BYTES = 64  # HBP_IPC_HANDLE_BYTES
+
+
 class BalancedT(ctypes.Structure):
     """Mirror of hbp_balanced_t."""
     _fields_ = [("workers", c_i64), ("part_head", c_vp), ("part_tail", c_vp),
@@ -67,12 +71,14 @@ class BalancedT(ctypes.Structure):
                 ("slice_lo", c_vp), ("slice_g", c_vp), ("rb_done", c_vp), ("y_sumsq", c_vp),
                 ("hub_min", c_i64), ("pieces", c_i64), ("fixed_elems", c_i64),
                 ("ticket", c_vp), ("warp_ns", c_vp), ("cost_prefix", c_vp),
-                ("warp_map", c_i64), ("tail", c_i64), ("piece_base", c_i64)]
+                ("warp_map", c_i64), ("tail", c_i64), ("piece_base", c_i64),
+                ("n_peers", c_i64), ("y_peer", c_vp * MAX_PEERS)]
 
 
 # name -> argtypes (all return int status)
 _SIGS = {
     "hbp_abi_version": [],
+    "hbp_struct_sizes": [c_vp],
     "hbp_last_error": [],
     "hbp_device_sm_count": [ctypes.POINTER(c_int)],
     "hbp_spmv_default_workers": [c_int, c_i64, ctypes.POINTER(c_i64)],
@@ -138,6 +144,9 @@ _SIGS = {
     "hbp_sumsq": [c_vp, c_int, c_i64, c_vp, c_vp, c_vp],
     "hbp_sumsq_scratch": [ctypes.POINTER(c_i64)],
     "hbp_add": [c_vp, c_vp, c_int, c_i64, c_vp],
+    "hbp_ipc_export": [c_vp, c_vp, ctypes.POINTER(c_i64)],
+    "hbp_ipc_open": [c_vp, c_i64, ctypes.POINTER(c_vp)],
+    "hbp_ipc_close": [c_vp],
     "hbp_scale": [c_vp, c_int, c_i64, c_vp, c_vp, c_vp],
     "hbp_l2_persist": [c_vp, ctypes.c_size_t, ctypes.c_float, c_vp],
     "hbp_l2_persist_reset": [c_vp],

@@ -655,6 +655,16 @@ __global__ void __launch_bounds__(NT, MINB)
         if constexpr (MS) __stcs(p, v);
         else *p = v;
     };
+    // a row of y, and its copies in the peers' buffers (hbp_balanced_t.y_peer:
+    // the fused power iteration's all-gather; plain stores over NVLink)
+    auto sty = [&](V *yrow, int64_t r, V v) {
+        stm(yrow, v);
+        if (b.n_peers) {
+#pragma unroll
+            for (int p = 0; p < HBP_MAX_PEERS; ++p)
+                if (p < b.n_peers) stm(static_cast<V *>(b.y_peer[p]) + r, v);
+        }
+    };
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
@@ -902,7 +912,7 @@ __global__ void __launch_bounds__(NT, MINB)
         if (!piece) {
             if (valid) {
                 if (pb_now) pb_now[row_local] = acc;
-                else stm(yb_now + row_local, (V)(acc * ys));
+                else sty(yb_now + row_local, (int64_t)br_now * R + row_local, (V)(acc * ys));
             }
             if (FC && pb_now) group_done(br_now, rows_now);
             continue;
@@ -944,7 +954,7 @@ __global__ void __launch_bounds__(NT, MINB)
         }
         if (valid) {
             if (pb_now) pb_now[row_local] = s;
-            else stm(yb_now + row_local, (V)(s * ys));
+            else sty(yb_now + row_local, (int64_t)br_now * R + row_local, (V)(s * ys));
         }
         if (lane == 0) b.counters[gq] = 0u;
         if (FC && pb_now) group_done(br_now, rows_now);
@@ -968,6 +978,7 @@ __global__ void __launch_bounds__(NT, MINB)
         w = nxt;
     }
     }
+    if (b.n_peers) __threadfence_system();  // peer stores before the next collective
     if (b.warp_ns && lane == 0) b.warp_ns[2 * w0 + 1] = globaltimer_ns();
 }
 

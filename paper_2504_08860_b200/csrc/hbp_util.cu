@@ -133,7 +133,16 @@ const char *hbp_status_string(int status) {
     }
 }
 
-int hbp_abi_version(void) { return 2; }
+int hbp_abi_version(void) { return 3; }
+
+int hbp_struct_sizes(int64_t *sizes) {
+    if (!sizes) return HBP_E_ARG;
+    sizes[0] = (int64_t)sizeof(hbp_format_t);
+    sizes[1] = (int64_t)sizeof(hbp_schedule_t);
+    sizes[2] = (int64_t)sizeof(hbp_balanced_t);
+    sizes[3] = (int64_t)sizeof(hbp_seg_t);
+    return HBP_OK;
+}
 
 int hbp_last_error(void) { return (int)cudaGetLastError(); }
 

@@ -8,6 +8,7 @@
 //               device after an optional all-reduce: no host round trip).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <string.h>
 
 #include "hbp.h"
 #include "hbp_common.cuh"
@@ -117,6 +118,46 @@ int hbp_add(void *y, const void *a, int dtype, int64_t n, hbp_stream_t stream) {
     else if (dtype == HBP_F64) k_add<double><<<grid, 256, 0, st>>>((double *)y, (const double *)a, n);
     else return HBP_E_ARG;
     return (int)cudaGetLastError();
+}
+
+// ---- peer mappings (CUDA IPC) for the fused power iteration
+// cuMemGetAddressRange through the runtime's driver entry point (no libcuda
+// link dependency: the library still loads on a host without a driver).
+typedef int (*hbp_get_range_fn)(unsigned long long *, size_t *, unsigned long long);
+
+int hbp_ipc_export(const void *ptr, void *handle, int64_t *offset) {
+    if (!ptr || !handle || !offset) return HBP_E_ARG;
+    static_assert(sizeof(cudaIpcMemHandle_t) == HBP_IPC_HANDLE_BYTES, "IPC handle size");
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    HBP_CUDA_TRY(cudaGetDriverEntryPointByVersion("cuMemGetAddressRange", &fn, 12000,
+                                                  cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !fn) return HBP_E_UNSUPPORTED;
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (((hbp_get_range_fn)fn)(&base, &size, (unsigned long long)(uintptr_t)ptr) != 0)
+        return HBP_E_ARG;
+    cudaIpcMemHandle_t h;
+    HBP_CUDA_TRY(cudaIpcGetMemHandle(&h, (void *)(uintptr_t)base));
+    memcpy(handle, &h, sizeof h);
+    *offset = (int64_t)((uintptr_t)ptr - (uintptr_t)base);
+    return HBP_OK;
+}
+
+int hbp_ipc_open(const void *handle, int64_t offset, void **ptr) {
+    if (!handle || !ptr || offset < 0) return HBP_E_ARG;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof h);
+    void *base = nullptr;
+    HBP_CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    *ptr = (char *)base + offset;
+    return HBP_OK;
+}
+
+int hbp_ipc_close(void *base) {
+    if (!base) return HBP_E_ARG;
+    HBP_CUDA_TRY(cudaIpcCloseMemHandle(base));
+    return HBP_OK;
 }
 
 }  // extern "C"

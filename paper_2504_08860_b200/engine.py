@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+from collections.abc import Sequence
 from dataclasses import dataclass
 
 import numpy as np
@@ -522,10 +523,13 @@ class SpmvOperator:
                    L.P(partial), L.P(y), s)
 
     def __call__(self, x: torch.Tensor, y: torch.Tensor | None = None,
-                 x_sumsq: torch.Tensor | None = None) -> torch.Tensor:
+                 x_sumsq: torch.Tensor | None = None,
+                 y_peers: Sequence[int] = ()) -> torch.Tensor:
         """y = A x, or y = A (x / sqrt(x_sumsq[0])) when x_sumsq (a float64
         device scalar) is given -- the power-iteration step without a separate
-        scaling pass (stream schedule, one column block)."""
+        scaling pass (stream schedule, one column block).  y_peers: device
+        addresses (e.g. other GPUs' buffers mapped by hbp_ipc_open) that get
+        a copy of y from the same stores."""
         hbp = self.hbp
         self._check_vec(x, hbp.cols, "x")
         if y is None:
@@ -534,12 +538,15 @@ class SpmvOperator:
             self._check_vec(y, hbp.rows, "y")
         f = self._fmt
         s = L.stream()
-        if x_sumsq is not None:
-            if self.schedule != "stream" or not self.direct:
-                raise ValueError("x_sumsq needs the stream schedule and one column block")
-            self.bal.y_sumsq = x_sumsq.data_ptr()
-        elif self.schedule == "stream":
-            self.bal.y_sumsq = None
+        if (x_sumsq is not None or y_peers) and (self.schedule != "stream" or not self.direct):
+            raise ValueError("x_sumsq / y_peers need the stream schedule and one column block")
+        if len(y_peers) > L.MAX_PEERS:
+            raise ValueError(f"at most {L.MAX_PEERS} y_peers")
+        if self.schedule == "stream":
+            self.bal.y_sumsq = x_sumsq.data_ptr() if x_sumsq is not None else None
+            self.bal.n_peers = len(y_peers)
+            for i, a in enumerate(y_peers):
+                self.bal.y_peer[i] = int(a)
         if self.schedule == "rowblock":
             L.call("hbp_spmv_rowblock", ctypes.byref(f), L.P(x), L.P(y), s)
             return y
@@ -553,7 +560,8 @@ class SpmvOperator:
         if self.direct:
             self._blocks(f, x, None, y, s)
             if self.has_empty_row_blocks:
-                L.call("hbp_zero_empty_rows", ctypes.byref(f), L.P(y), s)
+                for a in (y.data_ptr(), *y_peers):
+                    L.call("hbp_zero_empty_rows", ctypes.byref(f), L.c_vp(a), s)
         elif self.fused_combine:
             self._blocks(f, x, self.partial, y, s)
             if self.has_empty_row_blocks:

@@ -290,10 +290,13 @@ class StripedOperator:
         return sum(o.launches_per_call for o in self.ops) + (1 if self.split else 0)
 
     def __call__(self, x: torch.Tensor, y: torch.Tensor, x_sumsq: torch.Tensor | None = None,
-                 before_remote=None) -> torch.Tensor:
+                 before_remote=None, y_peers=()) -> torch.Tensor:
         """y (this stripe's rows) = A_stripe x.  With the own-column split,
         before_remote() (e.g. waiting for the all-gather) runs between the
-        own-column part and the rest."""
+        own-column part and the rest.  y_peers: addresses that receive a copy
+        of y from the kernel's own stores (unsplit operator only)."""
+        if y_peers and self.split:
+            raise ValueError("y_peers needs an operator without the own-column split")
         if self.split:
             self.op_own(x, self.y_own, x_sumsq=x_sumsq)
             if before_remote is not None:
@@ -305,7 +308,7 @@ class StripedOperator:
             return y
         if before_remote is not None:
             before_remote()
-        return self.op(x, y, x_sumsq=x_sumsq)
+        return self.op(x, y, x_sumsq=x_sumsq, y_peers=y_peers)
 
 
 class PowerIteration:
@@ -314,16 +317,30 @@ class PowerIteration:
     8-byte all-reduce of ||y||^2 and an in-place all-gather of the y
     stripes straight into the next x buffer (padded layout, no copy).  With
     overlap, the gather runs asynchronously and the next step's own-column
-    part (StripedOperator split_own) computes while it is in flight."""
+    part (StripedOperator split_own) computes while it is in flight.
 
-    def __init__(self, op: StripedOperator, x0: torch.Tensor, group=None, overlap: bool = True):
+    fused=True (SURVEY §8(e)'s fused variant): there is no all-gather.  The
+    ranks map each other's two x buffers once (CUDA IPC, handles exchanged
+    through torch.distributed), and the SpMV kernel stores every y row into
+    its own next-x buffer AND into every peer's at the same offset, over
+    NVLink, as the rows finish -- the transfer overlaps the SpMV row by row.
+    The 8-byte all-reduce that follows orders the steps: a rank's next SpMV
+    starts after every rank's current one has finished (and fenced its peer
+    stores), so x is complete, and no rank writes a peer's x while the peer
+    still reads it (the two buffers alternate)."""
+
+    def __init__(self, op: StripedOperator, x0: torch.Tensor, group=None, overlap: bool = True,
+                 fused: bool = False):
         import torch.distributed as dist
         from . import engine as E
         if op.x_layout != "padded":
             raise ValueError("PowerIteration needs a padded-layout StripedOperator")
+        if fused and op.split:
+            raise ValueError("the fused power iteration needs an operator without split_own")
         self.op, self.group = op, group
         self.dist = dist if op.world > 1 else None
-        self.overlap = overlap and op.world > 1
+        self.fused = bool(fused and op.world > 1)
+        self.overlap = overlap and op.world > 1 and not self.fused
         dev = x0.device
         n = op.world * op.pad
         self.xs = [torch.zeros(n, dtype=op.dtype, device=dev) for _ in range(2)]
@@ -337,6 +354,44 @@ class PowerIteration:
         self.cur = 0
         self.pending = None
         self._sumsq = E.sumsq
+        self._mapped = []            # (base address) of every peer mapping opened here
+        self.peer_x = [[], []]       # peer_x[k]: the other ranks' xs[k] addresses
+        if self.fused:
+            self._map_peers()
+        self.sync_host = self.dist is not None and dist.get_backend(group) != "nccl"
+
+    def _map_peers(self) -> None:
+        from . import _lib as L
+        import ctypes
+        mine = []
+        for buf in self.xs:
+            h = (ctypes.c_char * L.IPC_HANDLE_BYTES)()
+            off = L.c_i64(0)
+            L.call("hbp_ipc_export", L.P(buf), h, ctypes.byref(off))
+            mine.append((bytes(h), off.value))
+        allh = [None] * self.op.world
+        self.dist.all_gather_object(allh, mine, group=self.group)
+        for p in range(self.op.world):
+            if p == self.op.rank:
+                continue
+            for k in range(2):
+                hb, off = allh[p][k]
+                ptr = L.c_vp()
+                L.call("hbp_ipc_open", ctypes.create_string_buffer(hb, len(hb)), L.c_i64(off),
+                       ctypes.byref(ptr))
+                self._mapped.append(ptr.value - off)
+                self.peer_x[k].append(ptr.value)
+
+    def close(self) -> None:
+        """Unmap the peers' buffers (fused); the object is unusable after."""
+        from . import _lib as L
+        self.finish()
+        if self._mapped:
+            torch.cuda.synchronize()
+            for base in self._mapped:
+                L.call("hbp_ipc_close", L.c_vp(base))
+            self._mapped = []
+            self.peer_x = [[], []]
 
     def _own(self, buf: torch.Tensor) -> torch.Tensor:
         o = self.op
@@ -346,6 +401,15 @@ class PowerIteration:
         o = self.op
         x, nxt = self.xs[self.cur], self.xs[1 - self.cur]
         y = self._own(nxt)[:o.stripe.rows]
+        if self.fused:
+            off = o.rank * o.pad * nxt.element_size()
+            o(x, y, x_sumsq=self.sq, y_peers=[a + off for a in self.peer_x[1 - self.cur]])
+            self._sumsq(y, self.sq, self.scratch)
+            if self.sync_host:
+                torch.cuda.synchronize()  # gloo: the peer stores are done before we meet
+            self.dist.all_reduce(self.sq, group=self.group)
+            self.cur = 1 - self.cur
+            return
 
         def wait_gather():
             if self.pending is not None:

@@ -45,7 +45,7 @@ def test_ctypes_binding_covers_header(libpath):
     for name in _declared():
         assert hasattr(lib, name), name
     assert set(_declared()) <= set(L.EXPORTED)
-    assert lib.hbp_abi_version() == 2
+    assert lib.hbp_abi_version() == 3
     assert lib.hbp_status_string(1002).decode().startswith("permutation")
 
 
@@ -107,3 +107,14 @@ def test_product_never_imports_oracle():
             if f.endswith(".py"):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", src, re.M), f
+
+
+def test_struct_mirrors_match_the_header(libpath):
+    """The ctypes mirrors have the C structs' sizes (a field added on one
+    side only would shift every later field)."""
+    import ctypes
+    from paper_2504_08860_b200 import _lib as L
+    lib = L.load_library(libpath)
+    out = (ctypes.c_int64 * 4)()
+    assert lib.hbp_struct_sizes(out) == 0
+    assert list(out) == [ctypes.sizeof(t) for t in (L.FormatT, L.ScheduleT, L.BalancedT, L.SegT)]

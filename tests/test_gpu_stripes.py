@@ -10,7 +10,10 @@ second GPU.
   (f64 bitwise; exact mode);
 - the power iteration over two stripes -- with and without the own-column
   split that overlaps the all-gather -- matches the single-process power
-  iteration (f32: within 1e-5; f64 unsplit: bitwise).
+  iteration (f32: within 1e-5; f64 unsplit: bitwise);
+- the fused power iteration (the SpMV kernel stores y into the peer's x
+  buffer through a CUDA IPC mapping; no all-gather) equals the all-gather
+  one bitwise.
 """
 from __future__ import annotations
 
@@ -81,6 +84,15 @@ def _worker(rank, world, port, n, dtype_name, split, out):
     for _ in range(5):
         pit.step()
     res["x"] = pit.x_global().cpu().numpy()
+    if not split:
+        # fused: y rows stored into the peer's x buffer (CUDA IPC) by the SpMV
+        # kernel itself, no all-gather
+        fz = PowerIteration(p, torch.as_tensor(x, device=dev), fused=True)
+        for _ in range(5):
+            fz.step()
+        res["x_fused"] = fz.x_global().cpu().numpy()
+        res["fused"] = fz.fused
+        fz.close()
     torch.cuda.synchronize()
     out[rank] = res
     dist.destroy_process_group()
@@ -134,6 +146,9 @@ def test_two_stripes_on_one_gpu(dtype_name, split):
     else:
         np.testing.assert_allclose(y, y_ref, rtol=0, atol=1e-5 * np.abs(y_ref).max())
     for k in range(2):
+        if not split:  # the fused step computes the same values: bitwise
+            assert out[k]["fused"]
+            np.testing.assert_array_equal(out[k]["x_fused"], out[k]["x"])
         if dtype == np.float64 and not split:
             np.testing.assert_allclose(out[k]["x"], x_ref, rtol=1e-13, atol=1e-15)
         else:
