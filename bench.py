@@ -490,6 +490,8 @@ def run_gpu(args):
         me = rank
     else:
         stripes, me = [Stripe(0, 0, -(-rows_g // R), 0, rows_g)], 0
+    if args.col_width:
+        C = int(args.col_width)  # geometry experiment (SURVEY §8(d) fixes C only for cfg1-4)
     cfg = H.PartitionConfig(col_width=C, row_height=R, warp_size=32, fixed_fraction=0.7)
     hot_arg = {"auto": None, "off": False, "on": True}.get(args.hot)
     if hot_arg is None and args.hot != "auto":
@@ -931,6 +933,8 @@ def main():
     ap.add_argument("--no-baselines", action="store_true",
                     help="skip the CSR / 2D / cuSPARSE comparison timings")
     ap.add_argument("--schedule", default=None, choices=[None, "stream", "balanced", "plan", "rowblock", "rowstage", "seg"])
+    ap.add_argument("--col-width", type=int, default=None,
+                    help="override the config's column-block width C (geometry experiments)")
     ap.add_argument("--workers", type=int, default=None,
                     help="persistent warps of the SpMV (default: one per resident warp slot)")
     ap.add_argument("--collective", default="fused", choices=["fused", "gather"],
