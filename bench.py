@@ -83,11 +83,12 @@ def _peaks():
 def gather_roofline(nnz: int, hot_share: float, warm_share: float, x_fits_l2: bool,
                     kernel_ms: float, sm_mhz, sms: int):
     """Random-column SpMV bound by the measured gather rates
-    (profiles/gather_peaks.json, tools/gather_peaks.cu): every element's x
-    gather costs one L1 line request -- ~0.93 per SM-cycle while x is
-    L2-resident, ~0.24 beyond L2 -- and a hot-tier gather one shared-memory
-    load (~2 per SM-cycle).  t_min = sum(n_tier / (rate_tier * SMs * clock));
-    frac = t_min / kernel time."""
+    (profiles/gather_peaks.json, tools/gather_peaks.cu, tools/gather_mix.cu):
+    every element's x gather through global memory costs one L1 line request
+    -- ~0.93 per SM-cycle while x is L2-resident, ~0.24 beyond L2 -- and a
+    hot-tier gather one shared-memory load (~4 per SM-cycle).  The two paths
+    overlap (gather_mix: time follows the L2 share alone), so
+    t_min = max(t_l1_miss_path, t_shared); frac = t_min / kernel time."""
     p = os.path.join(ROOT, "profiles", "gather_peaks.json")
     if not os.path.exists(p) or not sm_mhz:
         return None
@@ -96,15 +97,18 @@ def gather_roofline(nnz: int, hot_share: float, warm_share: float, x_fits_l2: bo
     hz = float(sm_mhz) * 1e6 * sms
     r_l2 = g["ldg_l2_resident"]["per_sm_cycle"]
     r_far = g["ldg_beyond_l2"]["per_sm_cycle"]
-    r_lds = g["lds_random_128KB"]["per_sm_cycle"]
+    r_lds = g["lds_mix"]["per_sm_cycle_pure_lds"]
     cold = 1.0 - hot_share - warm_share
-    t = nnz * (hot_share / r_lds + warm_share / r_l2 + cold / (r_l2 if x_fits_l2 else r_far)) / hz
+    t_miss = nnz * (warm_share / r_l2 + cold / (r_l2 if x_fits_l2 else r_far)) / hz
+    t_lds = nnz * hot_share / r_lds / hz
+    t = max(t_miss, t_lds)
     return {"bound": "l1_gather", "unit": "Ggathers/s", "achieved": round(nnz / (kernel_ms * 1e-3) / 1e9, 2),
             "peak": round(nnz / t / 1e9, 2), "frac": round(t * 1e3 / kernel_ms, 4),
-            "min_ms": round(t * 1e3, 5), "sm_mhz": sm_mhz,
+            "min_ms": round(t * 1e3, 5), "sm_mhz": sm_mhz, "model": "max(l1_miss_path, shared)",
             "tiers": {"hot_lds": round(hot_share, 4), "warm_l2": round(warm_share, 4),
                       "cold": round(cold, 4), "cold_rate": "l2_resident" if x_fits_l2 else "beyond_l2"},
-            "source": "profiles/gather_peaks.json (measured on B200: random 4-byte gathers per SM-cycle)"}
+            "source": "profiles/gather_peaks.json (measured on B200: random 4-byte gathers per SM-cycle; "
+                      "lds_mix: shared-memory gathers overlap the L1 miss path)"}
 
 
 class ClockSampler:

@@ -18,14 +18,17 @@ def test_gather_roofline_arithmetic():
     nnz, ms, mhz, sms = 100_000_000, 0.5, 1965.0, 148
     r = bench.gather_roofline(nnz, 0.25, 0.0, True, ms, mhz, sms)
     hz = mhz * 1e6 * sms
-    t = nnz * (0.25 / g["lds_random_128KB"]["per_sm_cycle"]
-               + 0.75 / g["ldg_l2_resident"]["per_sm_cycle"]) / hz
+    t = nnz * max(0.25 / g["lds_mix"]["per_sm_cycle_pure_lds"],
+                  0.75 / g["ldg_l2_resident"]["per_sm_cycle"]) / hz  # the paths overlap
     assert r["min_ms"] == pytest.approx(t * 1e3, rel=1e-4)
     assert r["frac"] == pytest.approx(t * 1e3 / ms, rel=1e-3)
     assert r["tiers"]["cold"] == pytest.approx(0.75)
     far = bench.gather_roofline(nnz, 0.0, 0.0, False, ms, mhz, sms)
     assert far["min_ms"] > r["min_ms"]  # beyond L2 is slower per gather
     assert bench.gather_roofline(nnz, 0.0, 0.0, True, ms, None, sms) is None
+    # all-shared: bound by the shared-memory rate alone
+    lds = bench.gather_roofline(nnz, 1.0, 0.0, True, ms, mhz, sms)
+    assert lds["min_ms"] == pytest.approx(nnz / g["lds_mix"]["per_sm_cycle_pure_lds"] / hz * 1e3, rel=1e-4)
 
 
 def _fake(schedule, nzb=10, R=512, nnz=100_000, rows=5000, cols=7000, esz=4, hot=None,
