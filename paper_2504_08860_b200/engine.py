@@ -618,7 +618,7 @@ class HostPipeline:
     work that read it finished (SpMV_{i-depth} for x, D2H_{i-depth} for y)."""
 
     def __init__(self, hbp: HbpMatrix | None, depth: int = 2, operator=None,
-                 x_len: int | None = None, **op_kwargs):
+                 x_len: int | None = None, chunks: int | None = None, **op_kwargs):
         """operator: any y = op(x, y) callable on device buffers (e.g. a
         StripedOperator) instead of a SpmvOperator of hbp; x_len its x
         length (default hbp.cols)."""
@@ -632,11 +632,20 @@ class HostPipeline:
         self.op = operator if operator is not None else SpmvOperator(hbp, **op_kwargs)
         nx = x_len if x_len is not None else src.cols
         self.xd = [torch.empty(nx, dtype=src.dtype, device=dev) for _ in range(self.depth)]
+        # each copy as `chunks` consecutive pieces (the two directions interleave
+        # at piece granularity instead of whole vectors)
+        self.chunks = max(1, int(os.environ.get("HBP_PIPE_CHUNKS", "1")) if chunks is None
+                          else int(chunks))
         self.yd = [torch.empty(src.rows, dtype=src.dtype, device=dev) for _ in range(self.depth)]
 
     @property
     def launches_per_call(self) -> int:
         return getattr(self.op, "launches_per_call", 1)
+
+    def _pieces(self, n: int):
+        k = min(self.chunks, max(1, n))
+        step = -(-n // k)
+        return [(a, min(n, a + step)) for a in range(0, n, step)]
 
     def run(self, xs_host, ys_host) -> None:
         """Enqueue every (x_i -> y_i); ordered after the current stream's work.
@@ -652,7 +661,8 @@ class HostPipeline:
             if x_free[j] is not None:
                 self.s_in.wait_event(x_free[j])
             with torch.cuda.stream(self.s_in):
-                self.xd[j].copy_(xh, non_blocking=True)
+                for a, b in self._pieces(xh.numel()):
+                    self.xd[j][a:b].copy_(xh[a:b], non_blocking=True)
             x_ready = torch.cuda.Event()
             x_ready.record(self.s_in)
             self.s_comp.wait_event(x_ready)
@@ -665,7 +675,8 @@ class HostPipeline:
             x_free[j] = done
             self.s_out.wait_event(done)
             with torch.cuda.stream(self.s_out):
-                yh.copy_(self.yd[j], non_blocking=True)
+                for a, b in self._pieces(yh.numel()):
+                    yh[a:b].copy_(self.yd[j][a:b], non_blocking=True)
             out = torch.cuda.Event()
             out.record(self.s_out)
             y_free[j] = out

@@ -62,3 +62,16 @@ def test_config_table_and_reference_scope():
     assert "cfg3" not in bench.REF_FULL and "cfg5" not in bench.REF_FULL  # host-infeasible
     for name, (desc, gen, dt, C) in bench.CONFIGS.items():
         assert dt in ("f32", "f64") and isinstance(desc, str) and "kind" in gen
+
+
+def test_pipeline_pieces_cover_the_vector():
+    """HostPipeline copies each vector as `chunks` consecutive pieces."""
+    from paper_2504_08860_b200.engine import HostPipeline
+    p = HostPipeline.__new__(HostPipeline)
+    for n in (1, 7, 1000, 1 << 20):
+        for k in (1, 2, 3, 8, 16):
+            p.chunks = k
+            pcs = p._pieces(n)
+            assert pcs[0][0] == 0 and pcs[-1][1] == n
+            assert all(a < b for a, b in pcs) and len(pcs) <= k
+            assert all(pcs[i][1] == pcs[i + 1][0] for i in range(len(pcs) - 1))

@@ -14,9 +14,9 @@ if has_gpu():
     import paper_2504_08860_b200 as H
 
 
-@pytest.mark.parametrize("depth", [1, 2, 3])
+@pytest.mark.parametrize("depth,chunks", [(1, 1), (2, 1), (3, 1), (2, 3), (3, 8)])
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
-def test_pipeline_matches_device_spmv(depth, dtype):
+def test_pipeline_matches_device_spmv(depth, chunks, dtype):
     rng = np.random.default_rng(depth)
     rows, cols = 5000, 7000
     lens = rng.poisson(9, rows)
@@ -33,7 +33,7 @@ def test_pipeline_matches_device_spmv(depth, dtype):
     tdt = torch.float32 if dtype == "f32" else torch.float64
     xs = [torch.as_tensor(rng.uniform(-1, 1, cols)).to(tdt).pin_memory() for _ in range(7)]
     ys = [torch.empty(rows, dtype=tdt).pin_memory() for _ in range(7)]
-    pipe = H.HostPipeline(hbp, depth=depth)
+    pipe = H.HostPipeline(hbp, depth=depth, chunks=chunks)
     pipe.run(xs, ys)
     torch.cuda.synchronize()
     op = H.SpmvOperator(hbp)
