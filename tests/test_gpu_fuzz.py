@@ -111,3 +111,34 @@ def test_random_geometry_every_schedule_fp64(seed):
         assert np.array_equal(y, y_ref), sched
         ran.append(sched)
     assert {"stream", "balanced", "plan", "rowblock"} <= set(ran)
+
+
+@pytest.mark.parametrize("seed", range(1, N_CASES, 5))
+def test_random_geometry_codec_and_walk(seed):
+    """hbp.py:241-391 on random geometries: the .hbp codec round-trips to the
+    same bytes and the same six arrays, and the inverse walk
+    (hbp_to_triplets) gives back exactly the canonical input triplets."""
+    import io
+    rows, cols, r, c, v, x, C, R, W, f32 = _case(seed)
+    cfg = H.PartitionConfig(col_width=C, row_height=R, warp_size=W)
+    csr = H.coo_to_csr(H.TripletMatrix(rows, cols, r, c, v))
+    grid = H.make_grid(csr, cfg)
+    hbp = H.build_hbp(csr, grid, H.hash_permutations(grid, H.sample_hash_params(grid, cfg)))
+    buf = io.BytesIO()
+    H.serialize_hbp(hbp, buf)
+    raw = buf.getvalue()
+    back = H.deserialize_hbp(io.BytesIO(raw))
+    buf2 = io.BytesIO()
+    H.serialize_hbp(back, buf2)
+    assert buf2.getvalue() == raw
+    a, b = hbp.to_reference(), back.to_reference()
+    for k in ("col", "add_sign", "zero_row", "group_start", "output_hash"):
+        assert np.array_equal(a[k], b[k]), k
+    t = H.hbp_to_triplets(hbp)
+    tr = np.asarray(t.row.cpu() if hasattr(t.row, "cpu") else t.row, np.int64)
+    tc = np.asarray(t.col.cpu() if hasattr(t.col, "cpu") else t.col, np.int64)
+    tv = np.asarray(t.val.cpu() if hasattr(t.val, "cpu") else t.val, np.float64)
+    order = np.lexsort((tc, tr))
+    ref_order = np.lexsort((c, r))
+    assert np.array_equal(tr[order], r[ref_order]) and np.array_equal(tc[order], c[ref_order])
+    assert np.array_equal(tv[order], np.asarray(v, np.float64)[ref_order])
