@@ -142,3 +142,40 @@ def test_random_geometry_codec_and_walk(seed):
     ref_order = np.lexsort((c, r))
     assert np.array_equal(tr[order], r[ref_order]) and np.array_equal(tc[order], c[ref_order])
     assert np.array_equal(tv[order], np.asarray(v, np.float64)[ref_order])
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_rmat_fp32_fast_paths(seed):
+    """Skewed R-MAT graphs (2^12 .. 2^17 vertices, the bench generator) in
+    fp32 through the stream schedule with randomly drawn knobs -- hot-column
+    staging on / off, packed x on / off, persistent-warp count, competitive
+    pieces (ticket) or tail pieces -- every result within 1e-5 of (|A||x|)_i
+    against the oracle, and repeat calls identical (deterministic)."""
+    import bench_inputs
+    rng = np.random.default_rng(500 + seed)
+    scale = int(rng.integers(12, 18))
+    n, _, rp, col, val = bench_inputs.rmat_csr_torch(scale, int(rng.integers(4, 17)), seed,
+                                                     torch.device("cuda"), torch.float32)
+    rows_t = torch.repeat_interleave(torch.arange(n, device="cuda"), rp[1:] - rp[:-1])
+    r, c = rows_t.cpu().numpy(), col.cpu().numpy().astype(np.int64)
+    v = val.cpu().numpy()
+    x = rng.uniform(-1, 1, n).astype(np.float32)
+    cfg = H.PartitionConfig(col_width=n)
+    csr = H.CsrMatrix(n, n, rp, col, val)
+    grid = H.make_grid(csr, cfg)
+    hbp = H.build_hbp(csr, grid, H.hash_permutations(grid, H.sample_hash_params(grid, cfg)))
+    knobs = dict(hot=[None, False][int(rng.integers(0, 2))],
+                 packed_x=[None, True, False][int(rng.integers(0, 3))],
+                 workers=[None, int(rng.integers(1, 5000))][int(rng.integers(0, 2))])
+    extra = int(rng.integers(0, 3))
+    if extra == 1:
+        knobs["ticket"] = ["0.7:2", "0.3:5"][int(rng.integers(0, 2))]
+    elif extra == 2:
+        knobs["tail"] = ["0.9:2", "0.6:4"][int(rng.integers(0, 2))]
+    op = H.SpmvOperator(hbp, schedule="stream", **knobs)
+    xd = torch.as_tensor(x, device="cuda")
+    y = op(xd).cpu().numpy()
+    np.testing.assert_array_equal(op(xd).cpu().numpy(), y)
+    err = O.componentwise_error(n, r, c, v.astype(np.float64), x.astype(np.float64),
+                                y.astype(np.float64))
+    assert err <= 1e-5, (knobs, err)
